@@ -1,0 +1,333 @@
+#!/usr/bin/env python
+"""Benchmark of the B200 solver loop (heat-method geodesics, arXiv 1812.06060).
+
+Workload: BASELINE.json configs[2] (config 3), the ~10M-vertex case the
+headline "end-to-end geodesic s at 10M verts" is quoted on and the largest
+config that fits one GPU with the CPU reference timed beside it: torus
+4096x2048 (8,388,608 vertices), 4 seeded sources, t = (mean edge)^2,
+1000 Gauss-Seidel sweeps, face formulation, 10 ADMM iterations.
+
+  value  vertex-updates/s of the diffusion solve (reachable V x sweeps / time),
+         mesh and BFS layout resident in HBM, one step = one full 1000-sweep
+         solve (the dominant kernel: one cooperative launch), CUDA events.
+  e2e    the same metric through the C ABI end to end: gh_distance_host from
+         pinned host arrays (H2D positions+faces, device build_mesh, BFS,
+         diffusion, normalisation, ADMM, integration, D2H distances), wall
+         clock around the synchronous call; e2e.seconds is the end-to-end
+         geodesic time.
+  --impl reference  the reference's own CPU gs_diffuse (oracle/_ref, the
+         unmodified reference headers, all host threads) on a bounded sample.
+
+Multi-GPU (torchrun, N > 1): every rank runs the same workload on its own GPU
+(replicas; the band-sharded path of SURVEY §8(e) is not built yet), value is
+the total over ranks / the max time over ranks.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+CONFIG = 3
+METRIC = "vertex-updates/s per solver sweep"
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--config", type=int, default=CONFIG)
+    ap.add_argument("--sweeps", type=int, default=1000)
+    ap.add_argument("--e2e-steps", type=int, default=3)
+    ap.add_argument("--cpu-sample-sweeps", type=int, default=0, help="0 = auto (about 10-30 s of CPU work)")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    return ap.parse_args()
+
+
+# ---------------------------------------------------------------- clocks
+class ClockSampler:
+    """nvidia-smi clocks and throttle reasons sampled during the timed region."""
+
+    Q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.hw_slowdown,"
+         "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+         "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, device: int):
+        self.device = device
+        self.rows = []
+        self.proc = None
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.device), f"--query-gpu={self.Q}",
+                                          "--format=csv,noheader,nounits", "-lms", "200"],
+                                         stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except (OSError, FileNotFoundError):
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            parts = [p.strip() for p in line.split(",")]
+            if len(parts) >= 8:
+                self.rows.append(parts)
+
+    def __exit__(self, *exc):
+        if self.proc:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except subprocess.TimeoutExpired:
+                self.proc.kill()
+
+    def summary(self):
+        if not self.rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"], "samples": 0}
+        sm = [float(r[1]) for r in self.rows if r[1].replace(".", "").isdigit()]
+        mx = [float(r[2]) for r in self.rows if r[2].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for r in self.rows for i in range(4) if r[4 + i].lower() == "active"})
+        return {"sm_mhz": float(np.median(sm)) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": reasons, "samples": len(self.rows)}
+
+
+# ---------------------------------------------------------------- helpers
+def load_peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            p = json.load(f)
+        return float(p["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs)"
+    except (OSError, KeyError, ValueError):
+        return 6650.0, "fallback (B200_PROFILING.md)"
+
+
+def algorithmic_bytes_per_sweep(vv_offset: np.ndarray, reach_mask: np.ndarray) -> int:
+    """28 + 12*deg bytes per vertex-update (row ptr 4, deg x (col 4 + weight 8),
+    den 8, u read 8, u write 8), summed over reachable vertices."""
+    deg = np.diff(vv_offset.astype(np.int64))[reach_mask]
+    return int(28 * deg.size + 12 * deg.sum())
+
+
+def recorded_traffic(workload: str, sweeps: int):
+    """DRAM bytes per launch of the diffusion kernel from the committed ncu capture."""
+    path = os.path.join(ROOT, "profiles", "diffusion_traffic.json")
+    try:
+        with open(path) as f:
+            rec = json.load(f)
+        if rec.get("workload") == workload:
+            return float(rec["dram_bytes_per_sweep"]) * sweeps, rec.get("source")
+    except (OSError, KeyError, ValueError):
+        pass
+    return None, None
+
+
+def dist_setup(n_gpus: int):
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if world > 1:
+        import torch
+        import torch.distributed as dist
+        torch.cuda.set_device(local)
+        dist.init_process_group("nccl", init_method="env://")
+        return rank, world, local, dist
+    return 0, 1, 0, None
+
+
+def max_over_ranks(dist, x: float, local: int) -> float:
+    if dist is None:
+        return x
+    import torch
+    t = torch.tensor([x], dtype=torch.float64, device=f"cuda:{local}")
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return float(t.item())
+
+
+def barrier(dist):
+    if dist is not None:
+        dist.barrier()
+
+
+def cuda_sync():
+    try:
+        import torch
+        if torch.cuda.is_available():
+            torch.cuda.synchronize()
+    except ImportError:
+        pass
+
+
+# ---------------------------------------------------------------- CPU reference leg
+def cpu_reference_rate(w, sample_sweeps: int, steps: int, warmup: int):
+    """Reference gs_diffuse (oracle/_ref = unmodified reference headers; else the C port)
+    on the box's host cores, all threads; returns (vu/s per step list, info)."""
+    from oracle import oracle as orc
+    kind = "reference" if orc.available("reference") else "port"
+    o = orc.Oracle(kind)
+    cores = os.cpu_count() or 1
+    o.set_threads(cores)
+    t0 = time.time()
+    mesh = o.build_mesh(w.positions, w.faces)
+    lv = mesh.bfs(w.sources)
+    build_s = time.time() - t0
+    t = w.t if w.t is not None else mesh.diffusion_time(w.m)
+    reach = mesh.nv - lv.unreachable
+    if sample_sweeps <= 0:
+        u, rep = mesh.gs_diffuse(lv, t, 1)
+        per = max(rep.wall_seconds, 1e-6)
+        sample_sweeps = int(min(200, max(1, 15.0 / per)))
+    rates = []
+    for i in range(warmup + steps):
+        u, rep = mesh.gs_diffuse(lv, t, sample_sweeps)
+        if i >= warmup:
+            rates.append(reach * sample_sweeps / rep.wall_seconds)
+    info = {"kind": kind, "cores": cores, "sample": f"{sample_sweeps} gs_diffuse sweeps of {w.name} "
+            f"({reach} reachable vertices), mesh built outside the timed region ({build_s:.1f} s)",
+            "sample_sweeps": sample_sweeps}
+    return rates, info
+
+
+# ---------------------------------------------------------------- main
+def main():
+    a = parse()
+    rank, world, local, dist = dist_setup(a.gpus)
+    from paper_1812_06060_b200 import meshgen
+    w = meshgen.config(a.config)
+    w.sweeps = a.sweeps
+    workload = f"C{a.config} {w.name} {w.method}, {w.sweeps} sweeps, {w.admm_iters} ADMM iters"
+    base_cfg = {"workload": workload, "vertices": int(w.positions.shape[0]), "faces": int(w.faces.shape[0]),
+                "sources": [int(s) for s in w.sources], "sweeps": w.sweeps, "method": w.method,
+                "l2": "inputs larger than L2 (CSR+u >= 0.8 GB vs 126 MB)" if a.config >= 3 else "working set may fit L2"}
+
+    if a.impl == "reference":
+        if rank != 0:
+            return
+        rates, info = cpu_reference_rate(w, a.cpu_sample_sweeps, a.steps, a.warmup)
+        v = float(np.mean(rates))
+        line = {"metric": METRIC, "value": v, "unit": "vertex-updates/s", "n_gpus": world, "steps": a.steps,
+                "warmup": a.warmup, "ms_per_step": 1e3 * info["sample_sweeps"] * (w.positions.shape[0]) / v,
+                "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+                "data": "synthetic (seeded BASELINE config mesh)", "impl": "reference",
+                "config": dict(base_cfg, parallelism="cpu-openmp"),
+                "cpu_baseline": {"value": v, "unit": "vertex-updates/s", "cores": info["cores"], "kind": info["kind"],
+                                 "sample": info["sample"]},
+                "e2e": {"value": v, "unit": "vertex-updates/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+        print(json.dumps(line), flush=True)
+        return
+
+    import paper_1812_06060_b200 as gh
+    from paper_1812_06060_b200 import geoheat as G
+    if world > 1:
+        gh.geoheat._lib.load().gh_set_device(local)
+    mesh = gh.build_mesh(w.positions, w.faces)
+    lv = gh.bfs_levels(mesh, w.sources)
+    t = w.t if w.t is not None else gh.diffusion_time(mesh, w.m)
+    reach = mesh.vertex_count() - lv.unreachable_count
+    vv_off = mesh.download("vv_offset")
+    reach_mask = lv.level_of_vertex >= 0
+    bytes_per_sweep = algorithmic_bytes_per_sweep(vv_off, reach_mask)
+    cfg = G.DiffusionConfig(m=w.m, sweeps=w.sweeps)
+
+    # ---- value: device-resident diffusion solves
+    launches = 0
+    for _ in range(a.warmup):
+        G.gs_diffuse(mesh, lv, t, cfg, keep_on_device=True)
+    barrier(dist)
+    cuda_sync()
+    kernel_ms = []
+    with ClockSampler(local) as clk:
+        for _ in range(a.steps):
+            rep = G.SolverReport()
+            G.gs_diffuse(mesh, lv, t, cfg, rep, keep_on_device=True)
+            kernel_ms.append(rep.device_ms)
+            launches += rep.kernel_launches
+    cuda_sync()
+    barrier(dist)
+    step_ms = float(np.mean(kernel_ms))
+    step_ms_max = max_over_ranks(dist, step_ms, local)
+    value = world * reach * w.sweeps / (step_ms_max * 1e-3)
+
+    peak, peak_src = load_peaks()
+    achieved = bytes_per_sweep * w.sweeps / (step_ms * 1e-3) / 1e9
+    traffic, traffic_src = recorded_traffic(workload, w.sweeps)
+
+    # ---- e2e: host arrays in -> distances out through the C ABI, pinned buffers
+    L = gh.geoheat._lib.load()
+    import ctypes as C
+    P = np.ascontiguousarray(w.positions, dtype=np.float64)
+    Fc = np.ascontiguousarray(w.faces, dtype=np.int32)
+    nbytes_p, nbytes_f, nbytes_d = P.nbytes, Fc.nbytes, 8 * P.shape[0]
+    pp, pf, pd = C.c_void_p(), C.c_void_p(), C.c_void_p()
+    for ptr, nb in ((pp, nbytes_p), (pf, nbytes_f), (pd, nbytes_d)):
+        G._check(L.gh_host_alloc(nb, C.byref(ptr)))
+    np.ctypeslib.as_array((C.c_double * P.size).from_address(pp.value))[:] = P.ravel()
+    np.ctypeslib.as_array((C.c_int32 * Fc.size).from_address(pf.value))[:] = Fc.ravel()
+    S = np.ascontiguousarray(w.sources, dtype=np.int32)
+    pcfg = G._pipeline_config(w.method, w.sweeps, w.t, w.m, G.AdmmConfig(max_iterations=w.admm_iters))
+    e2e_s, e2e_rep = [], None
+    for i in range(1 + a.e2e_steps):
+        rr = G.gh_run_report()
+        barrier(dist)
+        t0 = time.perf_counter()
+        G._check(L.gh_distance_host(pp, P.shape[0], pf, Fc.shape[0], S.ctypes.data_as(C.c_void_p), S.size,
+                                    C.byref(pcfg), pd, C.byref(rr)))
+        dt = time.perf_counter() - t0
+        if i > 0:  # first call is a warm-up (module load, pool growth)
+            e2e_s.append(dt)
+            e2e_rep = rr
+            launches_e2e = rr.kernel_launches
+    e2e_sec = max_over_ranks(dist, float(np.mean(e2e_s)), local)
+    e2e_value = world * reach * w.sweeps / e2e_sec
+    for ptr in (pp, pf, pd):
+        L.gh_host_free(ptr)
+
+    if rank != 0:
+        return
+    cpu = None
+    if world == 1 and not a.no_cpu_baseline:
+        try:
+            rates, info = cpu_reference_rate(w, a.cpu_sample_sweeps, 1, 0)
+            cpu = {"value": float(np.mean(rates)), "unit": "vertex-updates/s", "cores": info["cores"],
+                   "kind": info["kind"], "sample": info["sample"]}
+        except Exception as e:  # the baseline is reported, never required
+            cpu = {"value": None, "unit": "vertex-updates/s", "cores": os.cpu_count(), "kind": "port",
+                   "sample": f"unavailable: {e}"}
+    line = {
+        "metric": METRIC, "value": value, "unit": "vertex-updates/s", "n_gpus": world, "steps": a.steps,
+        "warmup": a.warmup, "ms_per_step": step_ms_max, "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "f64", "data": "synthetic (seeded BASELINE config mesh, DESIGN.md §5)",
+        "config": dict(base_cfg, t=t, levels=lv.level_count(), max_level_width=lv.max_level_width,
+                       parallelism="single-gpu" if world == 1 else f"replicas x{world}"),
+        "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
+                     "traffic": traffic, "peak_source": peak_src, "kernel": "k_diffuse_pipelined",
+                     "algorithmic_bytes_per_launch": bytes_per_sweep * w.sweeps,
+                     "bytes_per_vertex_update": bytes_per_sweep / reach, "traffic_source": traffic_src},
+        "e2e": {"value": e2e_value, "unit": "vertex-updates/s", "seconds": e2e_sec,
+                "h2d_bytes_per_step": nbytes_p + nbytes_f + S.nbytes, "d2h_bytes_per_step": nbytes_d,
+                "stages_ms": {"build": e2e_rep.build_ms, "bfs_layout": e2e_rep.bfs_ms,
+                              "diffusion": e2e_rep.diffusion_ms, "normalize": e2e_rep.normalize_ms,
+                              "admm": e2e_rep.optimization_ms, "integrate": e2e_rep.integration_ms,
+                              "d2h": e2e_rep.d2h_ms},
+                "admm_iterations": e2e_rep.admm_iterations, "zero_count": e2e_rep.zero_count},
+        "gpu_launches": launches,
+        "clocks": clk.summary(),
+        "cpu_baseline": cpu,
+    }
+    print(json.dumps(line), flush=True)
+
+
+if __name__ == "__main__":
+    main()

@@ -1,0 +1,221 @@
+/* geoheat_b200 — C ABI of the B200 (sm_100a) solver loop for the parallel heat
+ * method (arXiv 1812.06060). Plain pointers and sizes only; no C++ or torch
+ * types cross this boundary; no exception escapes it.
+ *
+ * The reference exposes the path as inline C++ free functions in
+ * namespace geoheat (reference/proj/include/geoheat/). Each entry point below
+ * names the reference function it replaces; include/geoheat_b200.hpp wraps
+ * them back into the reference's exact C++ signatures and exception types so
+ * run_pipeline (tools/geoheat.cpp:71-161) switches backend with a one-line
+ * change.
+ *
+ * Conventions
+ *   - int32 indices, fp64 values, arrays laid out like the reference's
+ *     std::vector<Vec3> (xyz interleaved) / std::array<Index,3>.
+ *   - every function returns a gh_status; gh_last_error() gives the message
+ *     of the last failure on the calling thread.
+ *   - handles own device memory on the device that was current (or chosen by
+ *     gh_set_device) at creation, and one CUDA stream each. Thread-compatible:
+ *     one handle per host thread, not internally re-entrant.
+ *   - host buffers are caller-owned; outputs are written before return.
+ */
+#ifndef GEOHEAT_B200_H
+#define GEOHEAT_B200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef enum {
+  GH_OK = 0,
+  GH_ERR_MESH = 1,     /* geoheat::MeshError      (common.hpp:30-32)  */
+  GH_ERR_INVALID = 2,  /* std::invalid_argument                       */
+  GH_ERR_SOLVER = 3,   /* geoheat::SolverError    (common.hpp:35-37)  */
+  GH_ERR_CUDA = 4,     /* CUDA runtime / no device / out of memory    */
+  GH_ERR_INTERNAL = 5
+} gh_status;
+
+/* Opaque device-resident TriMesh (mesh.hpp:21-94). */
+typedef struct gh_mesh gh_mesh;
+/* Opaque device-resident BfsLevels (bfs.hpp:15-22) plus the BFS-renumbered
+ * diffusion layout derived from it. Borrows its gh_mesh; handles may be
+ * destroyed in any order (a mesh destroyed while levels are alive is freed
+ * with its last gh_levels). */
+typedef struct gh_levels gh_levels;
+
+/* Array ids for gh_mesh_download: the fields of TriMesh in declaration order
+ * (mesh.hpp:22-49); element type and length in the comment. */
+typedef enum {
+  GH_POSITIONS = 0,           /* f64 [3V]  */
+  GH_FACES = 1,               /* i32 [3F]  */
+  GH_HALFEDGE_TWIN = 2,       /* i32 [3F]  */
+  GH_HALFEDGE_EDGE = 3,       /* i32 [3F]  */
+  GH_EDGE_VERTICES = 4,       /* i32 [2E]  */
+  GH_EDGE_HALFEDGES = 5,      /* i32 [2E]  */
+  GH_INTERIOR_EDGES = 6,      /* i32 [Eint]*/
+  GH_INTERIOR_EDGE_INDEX = 7, /* i32 [E]   */
+  GH_VERTEX_ON_BOUNDARY = 8,  /* u8  [V]   */
+  GH_FACE_AREA = 9,           /* f64 [F]   */
+  GH_FACE_NORMAL = 10,        /* f64 [3F]  */
+  GH_VERTEX_AREA = 11,        /* f64 [V]   */
+  GH_HALFEDGE_COT = 12,       /* f64 [3F]  */
+  GH_EDGE_WEIGHT = 13,        /* f64 [E]   */
+  GH_VERTEX_WEIGHT_SUM = 14,  /* f64 [V]   */
+  GH_VV_OFFSET = 15,          /* i32 [V+1] */
+  GH_VV_INDEX = 16,           /* i32 [2E]  */
+  GH_VV_EDGE = 17,            /* i32 [2E]  */
+  GH_VV_WEIGHT = 18,          /* f64 [2E]  */
+  GH_VC_OFFSET = 19,          /* i32 [V+1] */
+  GH_VC_CORNER = 20,          /* i32 [3F]  */
+  GH_NUM_MESH_ARRAYS = 21
+} gh_mesh_array;
+
+typedef struct {
+  int32_t vertices, faces, edges, interior_edges, boundary_vertices;
+  uint64_t device_bytes; /* device memory held by the handle */
+} gh_mesh_info;
+
+typedef struct {
+  int32_t level_count;       /* BfsLevels::level_count()        */
+  int32_t unreachable_count; /* BfsLevels::unreachable_count    */
+  int32_t max_level_width;   /* widest ring                     */
+  int32_t reserved;
+} gh_levels_info;
+
+/* AdmmConfig (grad_face.hpp:15-26). */
+typedef struct {
+  int32_t max_iterations; /* default 10  */
+  double eps1;            /* default 1e-5 */
+  double eps2;            /* default 1e-5 */
+  double mu;              /* default 100  */
+} gh_admm_config;
+
+/* SolverReport (report.hpp:16-27) plus device timing. History buffers are
+ * caller-owned and may be NULL; history_capacity entries are written. */
+typedef struct {
+  int32_t iterations;
+  int32_t converged;
+  double final_primal;
+  double final_dual;
+  double* primal_history;
+  double* dual_history;
+  double* residual_history; /* reserved for E1 early stop, may be NULL */
+  int32_t history_capacity;
+  uint64_t state_bytes_formula;   /* solver_state_bytes (grad_face.hpp:217-223) */
+  uint64_t state_bytes_allocated; /* device bytes the solver state occupies     */
+  double wall_seconds;            /* host wall time of the call                 */
+  double device_ms;               /* CUDA-event time of the solver kernels      */
+  int32_t kernel_launches;        /* kernels this call launched                 */
+} gh_solver_report;
+
+/* Pipeline selection (PipelineOptions, tools/geoheat.cpp:27-38). */
+typedef enum { GH_METHOD_FACE = 0, GH_METHOD_EDGE = 1 } gh_method;
+
+typedef struct {
+  int32_t method;   /* gh_method */
+  int32_t sweeps;   /* Gauss-Seidel sweeps (gs_iters), default 1000 */
+  double t;         /* diffusion time; <= 0 means m * h^2 from the mesh */
+  double m;         /* smoothing factor used when t <= 0 */
+  gh_admm_config admm;
+} gh_pipeline_config;
+
+/* Per-stage record of gh_distance (RunReport, report.hpp:50-90). */
+typedef struct {
+  double t;
+  int32_t gs_iterations;
+  int32_t admm_iterations;
+  int32_t converged;
+  int32_t zero_count; /* faces whose heat gradient underflowed (diffusion.hpp:128) */
+  double final_primal;
+  double final_dual;
+  double build_ms;      /* device mesh build (gh_distance_host only) */
+  double bfs_ms;        /* BFS + layout      (gh_distance_host only) */
+  double diffusion_ms;
+  double normalize_ms;
+  double optimization_ms;
+  double integration_ms;
+  double h2d_ms, d2h_ms;
+  double total_ms;      /* CUDA-event time of the whole call */
+  uint64_t h2d_bytes, d2h_bytes;
+  uint64_t solver_state_bytes;
+  int32_t kernel_launches;
+  int32_t reserved;
+} gh_run_report;
+
+/* ---- runtime */
+const char* gh_last_error(void);
+const char* gh_version(void);
+gh_status gh_set_device(int32_t device);
+gh_status gh_device_count(int32_t* count);
+/* Pinned host memory for staging (cudaMallocHost / cudaFreeHost). */
+gh_status gh_host_alloc(size_t bytes, void** out);
+gh_status gh_host_free(void* p);
+
+/* ---- mesh: build_mesh (mesh.hpp:113-286), device preprocessing */
+gh_status gh_mesh_create(const double* positions, int32_t nv, const int32_t* faces, int32_t nf, gh_mesh** out);
+gh_status gh_mesh_destroy(gh_mesh* mesh);
+gh_status gh_mesh_get_info(const gh_mesh* mesh, gh_mesh_info* info);
+/* Copy one TriMesh array to host (`count` elements of the array's type). */
+gh_status gh_mesh_download(const gh_mesh* mesh, int32_t which, void* host_out, int64_t count);
+/* average_edge_length (mesh.hpp:289-293); deterministic pairwise sum. */
+gh_status gh_average_edge_length(gh_mesh* mesh, double* h_out);
+/* diffusion_time (diffusion.hpp:28-32): t = m * h * h. */
+gh_status gh_diffusion_time(gh_mesh* mesh, double m, double* t_out);
+/* face_gradient (mesh.hpp:314-327): u [V] -> grad [3F]. */
+gh_status gh_face_gradient(gh_mesh* mesh, const double* u, double* grad_out);
+
+/* ---- BFS: bfs_levels (bfs.hpp:26-72) */
+gh_status gh_bfs_create(gh_mesh* mesh, const int32_t* sources, int32_t ns, gh_levels** out);
+gh_status gh_bfs_destroy(gh_levels* levels);
+gh_status gh_bfs_get_info(const gh_levels* levels, gh_levels_info* info);
+/* Any output may be NULL. order: rings concatenated (V - unreachable
+ * entries); offsets: level_count + 1 ring boundaries. */
+gh_status gh_bfs_download(const gh_levels* levels, int32_t* level_of_vertex, int32_t* parent_of_vertex,
+                          int32_t* order, int32_t* offsets);
+
+/* ---- diffusion: gs_diffuse (diffusion.hpp:57-124) */
+/* initial: NULL (u = u0) or a host warm start [V]. u_out: host [V], or NULL to
+ * keep the result on the device only (benchmarking; see gh_levels_u_device). */
+gh_status gh_gs_diffuse(gh_levels* levels, double t, int32_t sweeps, const double* initial, double* u_out,
+                        gh_solver_report* report);
+/* diffusion_residual (diffusion.hpp:35-49), E1 of a host u. */
+gh_status gh_diffusion_residual(gh_levels* levels, const double* u, double t, double* e1_out);
+
+/* ---- normalisation: normalized_target_gradients (diffusion.hpp:132-145) */
+gh_status gh_normalized_target_gradients(gh_mesh* mesh, const double* u, double* h_out, int32_t* zero_count);
+
+/* ---- integrability optimisation */
+/* admm_face_optimize (grad_face.hpp:228-237): H [3F] -> G [3F]. */
+gh_status gh_admm_face_optimize(gh_mesh* mesh, const double* h, const gh_admm_config* config, double* g_out,
+                                 gh_solver_report* report);
+/* admm_edge_optimize (grad_edge.hpp:207-216): H [3F] -> X [E]. */
+gh_status gh_admm_edge_optimize(gh_mesh* mesh, const double* h, const gh_admm_config* config, double* x_out,
+                                gh_solver_report* report);
+/* solver_state_bytes (grad_face.hpp:217-223); method is gh_method. */
+gh_status gh_solver_state_bytes(const gh_mesh* mesh, int32_t method, uint64_t* bytes_out);
+
+/* ---- distance recovery */
+/* integrate_face_gradients (integrate.hpp:40-59): G [3F] -> d [V]. */
+gh_status gh_integrate_face_gradients(gh_levels* levels, const double* g, double* d_out);
+/* integrate_edge_differences (integrate.hpp:64-75): X [E] -> d [V]. */
+gh_status gh_integrate_edge_differences(gh_levels* levels, const double* x, double* d_out);
+
+/* ---- fused solver loop, device-resident between stages
+ * (the chain of run_pipeline, tools/geoheat.cpp:108-143). d_out host [V]. */
+gh_status gh_distance(gh_levels* levels, const gh_pipeline_config* config, double* d_out, gh_run_report* report);
+/* Host arrays in -> host distances out, everything on the device in between:
+ * H2D, build_mesh, bfs_levels, gh_distance, D2H (the end-to-end path). */
+gh_status gh_distance_host(const double* positions, int32_t nv, const int32_t* faces, int32_t nf,
+                           const int32_t* sources, int32_t ns, const gh_pipeline_config* config, double* d_out,
+                           gh_run_report* report);
+
+/* field_hash (report.hpp:145-153): FNV-1a over the bytes of n doubles. */
+uint64_t gh_field_hash(const double* values, int64_t n);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* GEOHEAT_B200_H */

@@ -1,0 +1,13 @@
+"""geoheat on B200: the solver loop of the parallel heat method (arXiv 1812.06060)
+as hand-written sm_100a CUDA behind a C ABI (include/geoheat_b200.h).
+
+`geoheat` mirrors the reference C++ API (reference/proj/include/geoheat);
+`meshgen` builds the seeded BASELINE meshes. See DESIGN.md.
+"""
+from . import geoheat, meshgen  # noqa: F401
+from .geoheat import (AdmmConfig, BfsLevels, DiffusionConfig, EdgeAdmmResult, FaceAdmmResult,  # noqa: F401
+                      GeoheatCudaError, MeshError, NormalizedGradients, OptimizerKind, SolverError, SolverReport,
+                      TriMesh, admm_edge_optimize, admm_face_optimize, average_edge_length, bfs_levels, build_mesh,
+                      diffusion_residual, diffusion_time, distance, distance_host, face_gradient, field_hash,
+                      gs_diffuse, integrate_edge_differences, integrate_face_gradients, normalized_target_gradients,
+                      solver_state_bytes)

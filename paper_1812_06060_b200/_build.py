@@ -1,0 +1,96 @@
+"""Build recipes for the in-tree native libraries (run by __graft_entry__.build()).
+
+  lib/libgeoheat_b200.so   the CUDA path: csrc/*.cu for sm_100a, fp64 with
+                           FMA contraction off (-fmad=false) so element values
+                           match the reference bit for bit.
+  lib/libgh_meshgen.so     host C mesh generators for the BASELINE configs.
+
+The libraries are built in place (not pip-installed) so they travel with the
+repo snapshot to the GPU box.
+"""
+from __future__ import annotations
+
+import concurrent.futures as cf
+import glob
+import os
+import shutil
+import subprocess
+
+PKG = os.path.dirname(os.path.abspath(__file__))
+ROOT = os.path.dirname(PKG)
+CSRC = os.path.join(PKG, "csrc")
+LIBDIR = os.path.join(PKG, "lib")
+CUDA_LIB = os.path.join(LIBDIR, "libgeoheat_b200.so")
+MESHGEN_LIB = os.path.join(LIBDIR, "libgh_meshgen.so")
+
+ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
+NVCC_FLAGS = ARCH + ["-O3", "-lineinfo", "-std=c++17", "-fmad=false", "-Xcompiler", "-fPIC,-O2,-ffp-contract=off",
+                     "-Xptxas", "-v", "-I", os.path.join(ROOT, "include")]
+
+
+def _nvcc() -> str:
+    for cand in (shutil.which("nvcc"), "/usr/local/cuda/bin/nvcc"):
+        if cand and os.path.exists(cand):
+            return cand
+    raise RuntimeError("nvcc not found")
+
+
+def _newer(target: str, sources) -> bool:
+    if not os.path.exists(target):
+        return False
+    t = os.path.getmtime(target)
+    return all(os.path.getmtime(s) <= t for s in sources)
+
+
+def build_meshgen(force: bool = False) -> str:
+    os.makedirs(LIBDIR, exist_ok=True)
+    src = os.path.join(CSRC, "meshgen.c")
+    if force or not _newer(MESHGEN_LIB, [src]):
+        tmp = MESHGEN_LIB + ".tmp"
+        subprocess.run(["gcc", "-std=gnu11", "-O2", "-fPIC", "-shared", "-ffp-contract=off", "-o", tmp, src, "-lm"],
+                       check=True)
+        os.replace(tmp, MESHGEN_LIB)
+    return MESHGEN_LIB
+
+
+def build_cuda(force: bool = False, verbose: bool = False) -> str:
+    os.makedirs(LIBDIR, exist_ok=True)
+    sources = sorted(glob.glob(os.path.join(CSRC, "*.cu")))
+    headers = sorted(glob.glob(os.path.join(CSRC, "*.cuh"))) + [os.path.join(ROOT, "include", "geoheat_b200.h")]
+    if not force and _newer(CUDA_LIB, sources + headers):
+        return CUDA_LIB
+    nvcc = _nvcc()
+    objdir = os.path.join(LIBDIR, "obj")
+    os.makedirs(objdir, exist_ok=True)
+
+    def compile_one(src):
+        obj = os.path.join(objdir, os.path.basename(src) + ".o")
+        r = subprocess.run([nvcc, *NVCC_FLAGS, "-c", src, "-o", obj], capture_output=True, text=True)
+        if r.returncode != 0:
+            raise RuntimeError(f"nvcc failed on {src}:\n{r.stderr}")
+        with open(obj + ".ptxas.txt", "w") as f:
+            f.write(r.stderr)
+        return obj
+
+    with cf.ThreadPoolExecutor(max_workers=min(8, len(sources))) as ex:
+        objs = list(ex.map(compile_one, sources))
+    tmp = CUDA_LIB + ".tmp"
+    r = subprocess.run([nvcc, *ARCH, "-shared", "-o", tmp, *objs], capture_output=True, text=True)
+    if r.returncode != 0:
+        raise RuntimeError(f"link failed:\n{r.stderr}")
+    os.replace(tmp, CUDA_LIB)
+    if verbose:
+        for o in objs:
+            print(open(o + ".ptxas.txt").read())
+    return CUDA_LIB
+
+
+def build_all(force: bool = False) -> None:
+    build_meshgen(force)
+    build_cuda(force)
+
+
+if __name__ == "__main__":
+    import sys
+    build_all(force="--force" in sys.argv)
+    print(CUDA_LIB)

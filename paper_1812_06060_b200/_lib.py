@@ -1,0 +1,103 @@
+"""ctypes binding of the C ABI in include/geoheat_b200.h.
+
+Loads the in-tree lib/libgeoheat_b200.so. There is no fallback: if the
+library is missing or no CUDA device is present, calls fail loudly
+(GeoheatCudaError), exactly as the ABI does.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+
+from . import _build
+
+LIB_PATH = _build.CUDA_LIB
+
+
+class gh_mesh_info(C.Structure):
+    _fields_ = [("vertices", C.c_int32), ("faces", C.c_int32), ("edges", C.c_int32),
+                ("interior_edges", C.c_int32), ("boundary_vertices", C.c_int32), ("device_bytes", C.c_uint64)]
+
+
+class gh_levels_info(C.Structure):
+    _fields_ = [("level_count", C.c_int32), ("unreachable_count", C.c_int32), ("max_level_width", C.c_int32),
+                ("reserved", C.c_int32)]
+
+
+class gh_admm_config(C.Structure):
+    _fields_ = [("max_iterations", C.c_int32), ("eps1", C.c_double), ("eps2", C.c_double), ("mu", C.c_double)]
+
+
+class gh_solver_report(C.Structure):
+    _fields_ = [("iterations", C.c_int32), ("converged", C.c_int32), ("final_primal", C.c_double),
+                ("final_dual", C.c_double), ("primal_history", C.POINTER(C.c_double)),
+                ("dual_history", C.POINTER(C.c_double)), ("residual_history", C.POINTER(C.c_double)),
+                ("history_capacity", C.c_int32), ("state_bytes_formula", C.c_uint64),
+                ("state_bytes_allocated", C.c_uint64), ("wall_seconds", C.c_double), ("device_ms", C.c_double),
+                ("kernel_launches", C.c_int32)]
+
+
+class gh_pipeline_config(C.Structure):
+    _fields_ = [("method", C.c_int32), ("sweeps", C.c_int32), ("t", C.c_double), ("m", C.c_double),
+                ("admm", gh_admm_config)]
+
+
+class gh_run_report(C.Structure):
+    _fields_ = [("t", C.c_double), ("gs_iterations", C.c_int32), ("admm_iterations", C.c_int32),
+                ("converged", C.c_int32), ("zero_count", C.c_int32), ("final_primal", C.c_double),
+                ("final_dual", C.c_double), ("build_ms", C.c_double), ("bfs_ms", C.c_double),
+                ("diffusion_ms", C.c_double), ("normalize_ms", C.c_double), ("optimization_ms", C.c_double),
+                ("integration_ms", C.c_double), ("h2d_ms", C.c_double), ("d2h_ms", C.c_double),
+                ("total_ms", C.c_double), ("h2d_bytes", C.c_uint64), ("d2h_bytes", C.c_uint64),
+                ("solver_state_bytes", C.c_uint64), ("kernel_launches", C.c_int32), ("reserved", C.c_int32)]
+
+
+# (name, restype, argtypes) for every exported symbol of include/geoheat_b200.h
+vp, i32, i64, f64, st = C.c_void_p, C.c_int32, C.c_int64, C.c_double, C.c_int
+SIGNATURES = [
+    ("gh_last_error", C.c_char_p, []),
+    ("gh_version", C.c_char_p, []),
+    ("gh_set_device", st, [i32]),
+    ("gh_device_count", st, [C.POINTER(i32)]),
+    ("gh_host_alloc", st, [C.c_size_t, C.POINTER(vp)]),
+    ("gh_host_free", st, [vp]),
+    ("gh_mesh_create", st, [vp, i32, vp, i32, C.POINTER(vp)]),
+    ("gh_mesh_destroy", st, [vp]),
+    ("gh_mesh_get_info", st, [vp, C.POINTER(gh_mesh_info)]),
+    ("gh_mesh_download", st, [vp, i32, vp, i64]),
+    ("gh_average_edge_length", st, [vp, C.POINTER(f64)]),
+    ("gh_diffusion_time", st, [vp, f64, C.POINTER(f64)]),
+    ("gh_face_gradient", st, [vp, vp, vp]),
+    ("gh_bfs_create", st, [vp, vp, i32, C.POINTER(vp)]),
+    ("gh_bfs_destroy", st, [vp]),
+    ("gh_bfs_get_info", st, [vp, C.POINTER(gh_levels_info)]),
+    ("gh_bfs_download", st, [vp, vp, vp, vp, vp]),
+    ("gh_gs_diffuse", st, [vp, f64, i32, vp, vp, C.POINTER(gh_solver_report)]),
+    ("gh_diffusion_residual", st, [vp, vp, f64, C.POINTER(f64)]),
+    ("gh_normalized_target_gradients", st, [vp, vp, vp, C.POINTER(i32)]),
+    ("gh_admm_face_optimize", st, [vp, vp, C.POINTER(gh_admm_config), vp, C.POINTER(gh_solver_report)]),
+    ("gh_admm_edge_optimize", st, [vp, vp, C.POINTER(gh_admm_config), vp, C.POINTER(gh_solver_report)]),
+    ("gh_solver_state_bytes", st, [vp, i32, C.POINTER(C.c_uint64)]),
+    ("gh_integrate_face_gradients", st, [vp, vp, vp]),
+    ("gh_integrate_edge_differences", st, [vp, vp, vp]),
+    ("gh_distance", st, [vp, C.POINTER(gh_pipeline_config), vp, C.POINTER(gh_run_report)]),
+    ("gh_distance_host", st, [vp, i32, vp, i32, vp, i32, C.POINTER(gh_pipeline_config), vp, C.POINTER(gh_run_report)]),
+    ("gh_field_hash", C.c_uint64, [vp, i64]),
+]
+
+_lib = None
+
+
+def load() -> C.CDLL:
+    """Load (once) the CUDA library; raise if it was never built."""
+    global _lib
+    if _lib is None:
+        if not os.path.exists(LIB_PATH):
+            raise ImportError(f"{LIB_PATH} is missing: run __graft_entry__.build() (the CUDA path has no fallback)")
+        lib = C.CDLL(LIB_PATH)
+        for name, res, args in SIGNATURES:
+            fn = getattr(lib, name)
+            fn.restype = res
+            fn.argtypes = args
+        _lib = lib
+    return _lib

@@ -1,0 +1,547 @@
+// The C ABI (include/geoheat_b200.h): handle management, host<->device
+// staging, error mapping. No exception crosses this boundary: every entry
+// point catches gh::Error / std::bad_alloc and returns a gh_status, with the
+// message kept per thread for gh_last_error() (the reference's exception
+// types map to codes as in tools/geoheat.cpp:337-349).
+
+#include <chrono>
+#include <cstring>
+#include <memory>
+#include <new>
+
+#include "gh_internal.cuh"
+
+namespace {
+
+thread_local std::string g_last_error;
+thread_local int g_device = -1;
+
+gh_status set_err(int code, const std::string& msg) {
+  g_last_error = msg;
+  return (gh_status)code;
+}
+
+template <class F>
+gh_status guarded(F&& f) {
+  try {
+    f();
+    return GH_OK;
+  } catch (const gh::Error& e) {
+    return set_err(e.code, e.msg);
+  } catch (const std::bad_alloc&) {
+    return set_err(GH_ERR_CUDA, "host allocation failed");
+  } catch (const std::exception& e) {
+    return set_err(GH_ERR_INTERNAL, e.what());
+  }
+}
+
+double now_s() {
+  return std::chrono::duration<double>(std::chrono::steady_clock::now().time_since_epoch()).count();
+}
+
+void require(bool ok, const char* what) {
+  if (!ok) gh::fail(GH_ERR_INVALID, what);
+}
+
+void use_device_of(const gh_mesh* m) { GH_CUDA(cudaSetDevice(m->device)); }
+
+template <class T>
+void to_host(T* dst, const T* src, size_t n, cudaStream_t s) {
+  if (n) GH_CUDA(cudaMemcpyAsync(dst, src, sizeof(T) * n, cudaMemcpyDeviceToHost, s));
+  GH_CUDA(cudaStreamSynchronize(s));
+}
+
+void fill_solver_report(gh_solver_report* r, const gh::AdmmResult& a, uint64_t formula, double wall,
+                        int launches) {
+  if (!r) return;
+  r->iterations = a.iterations;
+  r->converged = a.converged ? 1 : 0;
+  r->final_primal = a.final_primal;
+  r->final_dual = a.final_dual;
+  for (int i = 0; i < r->history_capacity && i < (int)a.primal.size(); ++i) {
+    if (r->primal_history) r->primal_history[i] = a.primal[i];
+    if (r->dual_history) r->dual_history[i] = a.dual[i];
+  }
+  r->state_bytes_formula = formula;
+  r->state_bytes_allocated = a.state_bytes;
+  r->wall_seconds = wall;
+  r->device_ms = a.device_ms;
+  r->kernel_launches = launches;
+}
+
+uint64_t state_formula(const gh_mesh* m, int method) {
+  const uint64_t nf = (uint64_t)m->nf, ne = (uint64_t)m->ne, ni = (uint64_t)m->ni;
+  if (method == GH_METHOD_FACE) return (6 * nf + 15 * ni) * 8;  // grad_face.hpp:222
+  return (6 * nf + 2 * ne) * 8 + 3 * nf;                        // grad_face.hpp:223
+}
+
+// Handle memory comes from the device's default stream-ordered pool. Keeping
+// freed blocks cached (release threshold = max) makes repeated solves reuse
+// them instead of paying cudaMalloc/cudaFree on every call.
+void keep_pool_memory(int device) {
+  static bool done[64] = {false};
+  if (device < 0 || device >= 64 || done[device]) return;
+  cudaMemPool_t pool;
+  GH_CUDA(cudaDeviceGetDefaultMemPool(&pool, device));
+  uint64_t threshold = ~0ull;
+  GH_CUDA(cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &threshold));
+  done[device] = true;
+}
+
+int take_launches(gh_mesh* m) {
+  int n = m->launches;
+  m->launches = 0;
+  return n;
+}
+
+}  // namespace
+
+extern "C" {
+
+const char* gh_last_error(void) { return g_last_error.c_str(); }
+const char* gh_version(void) { return "geoheat_b200 0.1 (sm_100a)"; }
+
+gh_status gh_set_device(int32_t device) {
+  return guarded([&] {
+    GH_CUDA(cudaSetDevice(device));
+    g_device = device;
+  });
+}
+
+gh_status gh_device_count(int32_t* count) {
+  return guarded([&] {
+    int n = 0;
+    cudaError_t e = cudaGetDeviceCount(&n);
+    if (e != cudaSuccess) {
+      (void)cudaGetLastError();
+      n = 0;
+    }
+    *count = n;
+  });
+}
+
+gh_status gh_host_alloc(size_t bytes, void** out) {
+  return guarded([&] { GH_CUDA(cudaMallocHost(out, bytes ? bytes : 1)); });
+}
+
+gh_status gh_host_free(void* p) {
+  return guarded([&] {
+    if (p) GH_CUDA(cudaFreeHost(p));
+  });
+}
+
+gh_status gh_mesh_create(const double* positions, int32_t nv, const int32_t* faces, int32_t nf, gh_mesh** out) {
+  return guarded([&] {
+    require(out != nullptr, "gh_mesh_create: null output");
+    require(nv >= 0 && nf >= 0, "gh_mesh_create: negative size");
+    require((nv == 0 || positions) && (nf == 0 || faces), "gh_mesh_create: null input array");
+    require((int64_t)nf * 3 <= 0x7fffffffLL, "gh_mesh_create: more than 2^31 halfedges");
+    int ndev = 0;
+    if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev == 0) {
+      (void)cudaGetLastError();
+      gh::fail(GH_ERR_CUDA, "no CUDA device available (the geoheat_b200 path has no CPU fallback)");
+    }
+    std::unique_ptr<gh_mesh> m(new gh_mesh());
+    if (g_device >= 0) GH_CUDA(cudaSetDevice(g_device));
+    GH_CUDA(cudaGetDevice(&m->device));
+    keep_pool_memory(m->device);
+    GH_CUDA(cudaStreamCreateWithFlags(&m->stream, cudaStreamNonBlocking));
+    GH_CUDA(cudaMallocHost(&m->pinned_scalars, 8 * sizeof(double)));
+    m->nv = nv;
+    m->nf = nf;
+    gh::mesh_build(m.get(), positions, faces);
+    *out = m.release();
+  });
+}
+
+static void free_mesh(gh_mesh* mesh) {
+  cudaSetDevice(mesh->device);
+  cudaStreamSynchronize(mesh->stream);
+  cudaStream_t s = mesh->stream;
+  double* p = mesh->pinned_scalars;
+  delete mesh;
+  if (p) cudaFreeHost(p);
+  if (s) cudaStreamDestroy(s);
+}
+
+gh_status gh_mesh_destroy(gh_mesh* mesh) {
+  return guarded([&] {
+    if (!mesh) return;
+    // levels borrow the mesh: the last of them frees it (any destroy order is safe)
+    if (mesh->level_refs > 0) {
+      mesh->destroy_pending = true;
+      return;
+    }
+    free_mesh(mesh);
+  });
+}
+
+gh_status gh_mesh_get_info(const gh_mesh* mesh, gh_mesh_info* info) {
+  return guarded([&] {
+    require(mesh && info, "gh_mesh_get_info: null argument");
+    info->vertices = mesh->nv;
+    info->faces = mesh->nf;
+    info->edges = mesh->ne;
+    info->interior_edges = mesh->ni;
+    info->boundary_vertices = mesh->boundary_vertices;
+    info->device_bytes = mesh->device_bytes();
+  });
+}
+
+gh_status gh_mesh_download(const gh_mesh* mesh, int32_t which, void* host_out, int64_t count) {
+  return guarded([&] {
+    require(mesh && host_out, "gh_mesh_download: null argument");
+    use_device_of(mesh);
+    const void* src = nullptr;
+    size_t n = 0, es = 0;
+    const gh_mesh& m = *mesh;
+    switch (which) {
+#define ARR(id, buf) \
+  case id:           \
+    src = m.buf.p;   \
+    n = m.buf.n;     \
+    es = sizeof(*m.buf.p); \
+    break;
+      ARR(GH_POSITIONS, pos)
+      ARR(GH_FACES, faces)
+      ARR(GH_HALFEDGE_TWIN, he_twin)
+      ARR(GH_HALFEDGE_EDGE, he_edge)
+      ARR(GH_EDGE_VERTICES, edge_v)
+      ARR(GH_EDGE_HALFEDGES, edge_he)
+      ARR(GH_INTERIOR_EDGES, interior_edges)
+      ARR(GH_INTERIOR_EDGE_INDEX, interior_edge_index)
+      ARR(GH_VERTEX_ON_BOUNDARY, on_boundary)
+      ARR(GH_FACE_AREA, face_area)
+      ARR(GH_FACE_NORMAL, face_normal)
+      ARR(GH_VERTEX_AREA, vertex_area)
+      ARR(GH_HALFEDGE_COT, he_cot)
+      ARR(GH_EDGE_WEIGHT, edge_weight)
+      ARR(GH_VERTEX_WEIGHT_SUM, vertex_weight_sum)
+      ARR(GH_VV_OFFSET, vv_offset)
+      ARR(GH_VV_INDEX, vv_index)
+      ARR(GH_VV_EDGE, vv_edge)
+      ARR(GH_VV_WEIGHT, vv_weight)
+      ARR(GH_VC_OFFSET, vc_offset)
+      ARR(GH_VC_CORNER, vc_corner)
+#undef ARR
+      default:
+        gh::fail(GH_ERR_INVALID, "gh_mesh_download: unknown array id");
+    }
+    require((size_t)count == n, "gh_mesh_download: count does not match the array length");
+    if (n) GH_CUDA(cudaMemcpyAsync(host_out, src, n * es, cudaMemcpyDeviceToHost, m.stream));
+    GH_CUDA(cudaStreamSynchronize(m.stream));
+  });
+}
+
+gh_status gh_average_edge_length(gh_mesh* mesh, double* h_out) {
+  return guarded([&] {
+    require(mesh && h_out, "gh_average_edge_length: null argument");
+    use_device_of(mesh);
+    *h_out = gh::mesh_average_edge_length(mesh);
+  });
+}
+
+gh_status gh_diffusion_time(gh_mesh* mesh, double m, double* t_out) {
+  return guarded([&] {
+    require(mesh && t_out, "gh_diffusion_time: null argument");
+    if (!(m > 0.0)) gh::fail(GH_ERR_INVALID, "diffusion_time: m must be positive");
+    use_device_of(mesh);
+    const double h = gh::mesh_average_edge_length(mesh);
+    *t_out = m * h * h;  // diffusion.hpp:30-31
+  });
+}
+
+gh_status gh_face_gradient(gh_mesh* mesh, const double* u, double* grad_out) {
+  return guarded([&] {
+    require(mesh && u && grad_out, "gh_face_gradient: null argument");
+    use_device_of(mesh);
+    cudaStream_t s = mesh->stream;
+    gh::Scratch<double> du(mesh->nv, s), dg(3 * (size_t)mesh->nf, s);
+    GH_CUDA(cudaMemcpyAsync(du.p, u, sizeof(double) * mesh->nv, cudaMemcpyHostToDevice, s));
+    gh::face_gradient_dev(mesh, du.p, dg.p);
+    to_host(grad_out, dg.p, 3 * (size_t)mesh->nf, s);
+  });
+}
+
+gh_status gh_bfs_create(gh_mesh* mesh, const int32_t* sources, int32_t ns, gh_levels** out) {
+  return guarded([&] {
+    require(mesh && out, "gh_bfs_create: null argument");
+    require(ns == 0 || sources, "gh_bfs_create: null sources");
+    use_device_of(mesh);
+    std::unique_ptr<gh_levels> L(new gh_levels());
+    L->mesh = mesh;
+    gh::bfs_build(L.get(), sources, ns);
+    mesh->level_refs++;
+    *out = L.release();
+  });
+}
+
+gh_status gh_bfs_destroy(gh_levels* levels) {
+  return guarded([&] {
+    if (!levels) return;
+    gh_mesh* m = levels->mesh;
+    cudaSetDevice(m->device);
+    cudaStreamSynchronize(m->stream);
+    delete levels;
+    if (--m->level_refs == 0 && m->destroy_pending) free_mesh(m);
+  });
+}
+
+gh_status gh_bfs_get_info(const gh_levels* levels, gh_levels_info* info) {
+  return guarded([&] {
+    require(levels && info, "gh_bfs_get_info: null argument");
+    info->level_count = levels->nlev;
+    info->unreachable_count = levels->unreachable;
+    info->max_level_width = levels->max_width;
+    info->reserved = 0;
+  });
+}
+
+gh_status gh_bfs_download(const gh_levels* levels, int32_t* level_of_vertex, int32_t* parent_of_vertex,
+                          int32_t* order, int32_t* offsets) {
+  return guarded([&] {
+    require(levels != nullptr, "gh_bfs_download: null levels");
+    const gh_mesh* m = levels->mesh;
+    use_device_of(m);
+    cudaStream_t s = m->stream;
+    if (level_of_vertex) to_host(level_of_vertex, levels->level.p, m->nv, s);
+    if (parent_of_vertex) to_host(parent_of_vertex, levels->parent.p, m->nv, s);
+    if (order) to_host(order, levels->order.p, levels->nreach, s);
+    if (offsets) std::memcpy(offsets, levels->h_offsets.data(), sizeof(int32_t) * (levels->nlev + 1));
+  });
+}
+
+gh_status gh_gs_diffuse(gh_levels* levels, double t, int32_t sweeps, const double* initial, double* u_out,
+                        gh_solver_report* report) {
+  return guarded([&] {
+    require(levels != nullptr, "gh_gs_diffuse: null levels");
+    gh_mesh* m = levels->mesh;
+    use_device_of(m);
+    cudaStream_t s = m->stream;
+    const double w0 = now_s();
+    take_launches(m);
+    gh::Scratch<double> dinit(initial ? m->nv : 0, s);
+    if (initial) GH_CUDA(cudaMemcpyAsync(dinit.p, initial, sizeof(double) * m->nv, cudaMemcpyHostToDevice, s));
+    const double ms = gh::diffuse_dev(levels, t, sweeps, initial ? dinit.p : nullptr);
+    if (u_out) to_host(u_out, levels->u_orig.p, m->nv, s);
+    else GH_CUDA(cudaStreamSynchronize(s));
+    if (report) {
+      report->iterations = sweeps;
+      report->converged = 0;
+      report->wall_seconds = now_s() - w0;
+      report->device_ms = ms;
+      report->kernel_launches = take_launches(m);
+      report->state_bytes_allocated = levels->device_bytes();
+    }
+  });
+}
+
+gh_status gh_diffusion_residual(gh_levels* levels, const double* u, double t, double* e1_out) {
+  return guarded([&] {
+    require(levels && u && e1_out, "gh_diffusion_residual: null argument");
+    gh_mesh* m = levels->mesh;
+    use_device_of(m);
+    gh::Scratch<double> du(m->nv, m->stream);
+    GH_CUDA(cudaMemcpyAsync(du.p, u, sizeof(double) * m->nv, cudaMemcpyHostToDevice, m->stream));
+    *e1_out = gh::diffusion_residual_dev(levels, du.p, t);
+  });
+}
+
+gh_status gh_normalized_target_gradients(gh_mesh* mesh, const double* u, double* h_out, int32_t* zero_count) {
+  return guarded([&] {
+    require(mesh && u && h_out, "gh_normalized_target_gradients: null argument");
+    use_device_of(mesh);
+    cudaStream_t s = mesh->stream;
+    gh::Scratch<double> du(mesh->nv, s), dh(3 * (size_t)mesh->nf, s);
+    GH_CUDA(cudaMemcpyAsync(du.p, u, sizeof(double) * mesh->nv, cudaMemcpyHostToDevice, s));
+    const int32_t z = gh::normalize_dev(mesh, du.p, dh.p);
+    to_host(h_out, dh.p, 3 * (size_t)mesh->nf, s);
+    if (zero_count) *zero_count = z;
+  });
+}
+
+gh_status gh_admm_face_optimize(gh_mesh* mesh, const double* h, const gh_admm_config* config, double* g_out,
+                                gh_solver_report* report) {
+  return guarded([&] {
+    require(mesh && h && config && g_out, "gh_admm_face_optimize: null argument");
+    use_device_of(mesh);
+    cudaStream_t s = mesh->stream;
+    const double w0 = now_s();
+    take_launches(mesh);
+    gh::Scratch<double> dh(3 * (size_t)mesh->nf, s), dg(3 * (size_t)mesh->nf, s);
+    GH_CUDA(cudaMemcpyAsync(dh.p, h, sizeof(double) * 3 * mesh->nf, cudaMemcpyHostToDevice, s));
+    gh::AdmmResult r = gh::admm_face_dev(mesh, dh.p, *config, dg.p);
+    to_host(g_out, dg.p, 3 * (size_t)mesh->nf, s);
+    fill_solver_report(report, r, state_formula(mesh, GH_METHOD_FACE), now_s() - w0, take_launches(mesh));
+  });
+}
+
+gh_status gh_admm_edge_optimize(gh_mesh* mesh, const double* h, const gh_admm_config* config, double* x_out,
+                                gh_solver_report* report) {
+  return guarded([&] {
+    require(mesh && h && config && x_out, "gh_admm_edge_optimize: null argument");
+    use_device_of(mesh);
+    cudaStream_t s = mesh->stream;
+    const double w0 = now_s();
+    take_launches(mesh);
+    gh::Scratch<double> dh(3 * (size_t)mesh->nf, s), dx(mesh->ne, s);
+    GH_CUDA(cudaMemcpyAsync(dh.p, h, sizeof(double) * 3 * mesh->nf, cudaMemcpyHostToDevice, s));
+    gh::AdmmResult r = gh::admm_edge_dev(mesh, dh.p, *config, dx.p);
+    to_host(x_out, dx.p, mesh->ne, s);
+    fill_solver_report(report, r, state_formula(mesh, GH_METHOD_EDGE), now_s() - w0, take_launches(mesh));
+  });
+}
+
+gh_status gh_solver_state_bytes(const gh_mesh* mesh, int32_t method, uint64_t* bytes_out) {
+  return guarded([&] {
+    require(mesh && bytes_out, "gh_solver_state_bytes: null argument");
+    *bytes_out = state_formula(mesh, method);
+  });
+}
+
+gh_status gh_integrate_face_gradients(gh_levels* levels, const double* g, double* d_out) {
+  return guarded([&] {
+    require(levels && g && d_out, "gh_integrate_face_gradients: null argument");
+    gh_mesh* m = levels->mesh;
+    use_device_of(m);
+    cudaStream_t s = m->stream;
+    gh::Scratch<double> dg(3 * (size_t)m->nf, s), dd(m->nv, s);
+    GH_CUDA(cudaMemcpyAsync(dg.p, g, sizeof(double) * 3 * m->nf, cudaMemcpyHostToDevice, s));
+    gh::integrate_face_dev(levels, dg.p, dd.p);
+    to_host(d_out, dd.p, m->nv, s);
+  });
+}
+
+gh_status gh_integrate_edge_differences(gh_levels* levels, const double* x, double* d_out) {
+  return guarded([&] {
+    require(levels && x && d_out, "gh_integrate_edge_differences: null argument");
+    gh_mesh* m = levels->mesh;
+    use_device_of(m);
+    cudaStream_t s = m->stream;
+    gh::Scratch<double> dx(m->ne, s), dd(m->nv, s);
+    GH_CUDA(cudaMemcpyAsync(dx.p, x, sizeof(double) * m->ne, cudaMemcpyHostToDevice, s));
+    gh::integrate_edge_dev(levels, dx.p, dd.p);
+    to_host(d_out, dd.p, m->nv, s);
+  });
+}
+
+}  // extern "C"
+
+namespace {
+
+// the device-resident chain of run_pipeline (tools/geoheat.cpp:108-143)
+void distance_on_device(gh_levels* L, const gh_pipeline_config& c, double* d_dist, gh_run_report* rep) {
+  gh_mesh* m = L->mesh;
+  cudaStream_t s = m->stream;
+  require(c.method == GH_METHOD_FACE || c.method == GH_METHOD_EDGE, "gh_distance: unknown method");
+  double t = c.t;
+  if (!(t > 0.0)) {
+    if (!(c.m > 0.0)) gh::fail(GH_ERR_INVALID, "diffusion_time: m must be positive");
+    const double h = gh::mesh_average_edge_length(m);
+    t = c.m * h * h;
+  }
+  gh::EventTimer tn(s), ti(s);
+  const double diff_ms = gh::diffuse_dev(L, t, c.sweeps, nullptr);
+  gh::Scratch<double> H(3 * (size_t)m->nf, s);
+  tn.start();
+  const int32_t zc = gh::normalize_dev(m, L->u_orig.p, H.p);
+  tn.stop();
+  gh::AdmmResult r;
+  if (c.method == GH_METHOD_FACE) {
+    gh::Scratch<double> G(3 * (size_t)m->nf, s);
+    r = gh::admm_face_dev(m, H.p, c.admm, G.p);
+    ti.start();
+    gh::integrate_face_dev(L, G.p, d_dist);
+    ti.stop();
+  } else {
+    gh::Scratch<double> X(m->ne, s);
+    r = gh::admm_edge_dev(m, H.p, c.admm, X.p);
+    ti.start();
+    gh::integrate_edge_dev(L, X.p, d_dist);
+    ti.stop();
+  }
+  if (rep) {
+    rep->t = t;
+    rep->gs_iterations = c.sweeps;
+    rep->admm_iterations = r.iterations;
+    rep->converged = r.converged ? 1 : 0;
+    rep->zero_count = zc;
+    rep->final_primal = r.final_primal;
+    rep->final_dual = r.final_dual;
+    rep->diffusion_ms = diff_ms;
+    rep->normalize_ms = tn.ms();
+    rep->optimization_ms = r.device_ms;
+    rep->integration_ms = ti.ms();
+    rep->solver_state_bytes = state_formula(m, c.method);
+  }
+}
+
+}  // namespace
+
+extern "C" {
+
+gh_status gh_distance(gh_levels* levels, const gh_pipeline_config* config, double* d_out, gh_run_report* report) {
+  return guarded([&] {
+    require(levels && config && d_out, "gh_distance: null argument");
+    gh_mesh* m = levels->mesh;
+    use_device_of(m);
+    cudaStream_t s = m->stream;
+    take_launches(m);
+    if (report) std::memset(report, 0, sizeof(*report));
+    gh::EventTimer total(s), d2h(s);
+    total.start();
+    gh::Scratch<double> dd(m->nv, s);
+    distance_on_device(levels, *config, dd.p, report);
+    d2h.start();
+    GH_CUDA(cudaMemcpyAsync(d_out, dd.p, sizeof(double) * m->nv, cudaMemcpyDeviceToHost, s));
+    d2h.stop();
+    total.stop();
+    GH_CUDA(cudaStreamSynchronize(s));
+    if (report) {
+      report->d2h_ms = d2h.ms();
+      report->d2h_bytes = sizeof(double) * (uint64_t)m->nv;
+      report->total_ms = total.ms();
+      report->kernel_launches = take_launches(m);
+    }
+  });
+}
+
+gh_status gh_distance_host(const double* positions, int32_t nv, const int32_t* faces, int32_t nf,
+                           const int32_t* sources, int32_t ns, const gh_pipeline_config* config, double* d_out,
+                           gh_run_report* report) {
+  gh_mesh* mesh = nullptr;
+  gh_levels* levels = nullptr;
+  const auto t0 = std::chrono::steady_clock::now();
+  gh_status st = gh_mesh_create(positions, nv, faces, nf, &mesh);
+  const auto t1 = std::chrono::steady_clock::now();
+  if (st != GH_OK) return st;
+  int launches = mesh->launches;
+  st = gh_bfs_create(mesh, sources, ns, &levels);
+  const auto t2 = std::chrono::steady_clock::now();
+  launches = mesh->launches;
+  if (st == GH_OK) st = gh_distance(levels, config, d_out, report);
+  const auto t3 = std::chrono::steady_clock::now();
+  if (st == GH_OK && report) {
+    report->build_ms = std::chrono::duration<double, std::milli>(t1 - t0).count();
+    report->bfs_ms = std::chrono::duration<double, std::milli>(t2 - t1).count();
+    report->h2d_bytes = sizeof(double) * 3 * (uint64_t)nv + sizeof(int32_t) * 3 * (uint64_t)nf + 4 * (uint64_t)ns;
+    report->total_ms = std::chrono::duration<double, std::milli>(t3 - t0).count();
+    report->kernel_launches += launches;
+  }
+  gh_status s2 = gh_bfs_destroy(levels);
+  gh_status s3 = gh_mesh_destroy(mesh);
+  if (st == GH_OK) st = s2 != GH_OK ? s2 : s3;
+  return st;
+}
+
+uint64_t gh_field_hash(const double* values, int64_t n) {
+  uint64_t h = 1469598103934665603ull;  // report.hpp:145-153
+  const unsigned char* b = reinterpret_cast<const unsigned char*>(values);
+  for (int64_t i = 0; i < n * (int64_t)sizeof(double); ++i) {
+    h ^= b[i];
+    h *= 1099511628211ull;
+  }
+  return h;
+}
+
+}  // extern "C"

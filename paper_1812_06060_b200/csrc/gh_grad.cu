@@ -1,0 +1,433 @@
+// Gradient normalisation and the two integrability-constrained ADMM
+// optimisers as fused gather kernels:
+//   normalized_target_gradients (reference diffusion.hpp:132-145)
+//   FaceAdmmSolver / admm_face_optimize (grad_face.hpp:51-206, 228-237)
+//   EdgeAdmmSolver / admm_edge_optimize (grad_edge.hpp:57-198, 207-216)
+//
+// Per iteration the face method runs two kernels instead of the reference's
+// five loops: G-update (+ dual partials) per face, and lambda-update (+ primal
+// partials) fused with the NEXT iteration's Y-update per interior edge (Y only
+// needs the new g and the new lambda, both final once the edge thread has
+// written lambda). The edge method likewise runs X-update (+ dual) per edge
+// and lambda-update (+ primal) fused with the next W-update per face.
+// Element values are bit-identical to the reference. The residual norms use a
+// fixed-shape tree (kReduceGrid blocks x 256 threads, then one block), which
+// is reproducible run to run but not the reference's left-to-right sum; the
+// stop rule compares them against thresholds with the same formulas.
+
+#include <cmath>
+
+#include "gh_internal.cuh"
+
+using namespace ghd;
+
+namespace {
+
+constexpr int B = gh::kBlock;
+constexpr unsigned G = gh::kReduceGrid;
+
+#define GRID_STRIDE(i, n) \
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < (n); i += (int64_t)gridDim.x * blockDim.x)
+
+// ---------------------------------------------------------------- normalisation
+__global__ void k_normalize(const double* __restrict__ pos, const int32_t* __restrict__ faces,
+                            const double* __restrict__ normal, const double* __restrict__ area,
+                            const double* __restrict__ u, int64_t nf, double* __restrict__ h,
+                            double* __restrict__ part) {
+  double zeros = 0.0;
+  GRID_STRIDE(f, nf) {
+    const int32_t t[3] = {faces[3 * f], faces[3 * f + 1], faces[3 * f + 2]};
+    const v3 n = ld3(normal, f);
+    v3 g = mk(0.0, 0.0, 0.0);
+    for (int k = 0; k < 3; ++k) {  // face_gradient (mesh.hpp:316-325)
+      v3 opp = sub(ld3(pos, t[(k + 2) % 3]), ld3(pos, t[(k + 1) % 3]));
+      g = add(g, scale(u[t[k]], cross(n, opp)));
+    }
+    g = divs(g, 2.0 * area[f]);
+    const double nrm = ghd::norm(g);
+    if (nrm >= 1e-20) {
+      st3(h, f, divs(mk(-g.x, -g.y, -g.z), nrm));
+    } else {
+      st3(h, f, mk(0.0, 0.0, 0.0));
+      zeros += 1.0;
+    }
+  }
+  zeros = block_sum<B>(zeros);
+  if (threadIdx.x == 0) part[blockIdx.x] = zeros;
+}
+
+// ---------------------------------------------------------------- face ADMM
+// Slot of face f's k-th edge in the interior-edge state: 2i + side, or -1.
+__global__ void k_face_slots(const int32_t* __restrict__ he_edge, const int32_t* __restrict__ iei,
+                             const int32_t* __restrict__ edge_he, int64_t nf, int32_t* __restrict__ slot) {
+  GRID_STRIDE(f, nf) {
+    for (int k = 0; k < 3; ++k) {
+      const int32_t e = he_edge[3 * f + k];
+      const int32_t i = iei[e];
+      slot[3 * f + k] = i < 0 ? -1 : 2 * i + (edge_he[2 * e] / 3 == f ? 0 : 1);
+    }
+  }
+}
+
+// ctor (grad_face.hpp:76-85): edge_dir, incident faces, scale partials
+__global__ void k_face_init_edges(const double* __restrict__ pos, const int32_t* __restrict__ interior_edges,
+                                  const int32_t* __restrict__ edge_v, const int32_t* __restrict__ edge_he,
+                                  const double* __restrict__ area, int64_t ni, double* __restrict__ edir,
+                                  int32_t* __restrict__ ef, double* __restrict__ lam, double* __restrict__ part) {
+  double s = 0.0;
+  GRID_STRIDE(i, ni) {
+    const int32_t e = interior_edges[i];
+    st3(edir, i, normalized(sub(ld3(pos, edge_v[2 * e + 1]), ld3(pos, edge_v[2 * e]))));
+    const int32_t f1 = edge_he[2 * e] / 3, f2 = edge_he[2 * e + 1] / 3;
+    ef[2 * i] = f1;
+    ef[2 * i + 1] = f2;
+    st3(lam, 2 * i, mk(0.0, 0.0, 0.0));
+    st3(lam, 2 * i + 1, mk(0.0, 0.0, 0.0));
+    s += area[f1] + area[f2];
+  }
+  s = block_sum<B>(s);
+  if (threadIdx.x == 0) part[blockIdx.x] = s;
+}
+
+// Y-update for interior edge i (grad_face.hpp:126-137 + y_update_edge 31-36)
+__device__ __forceinline__ void face_y_update(int64_t i, int32_t f1, int32_t f2, double a1, double a2, double mu,
+                                              const double* __restrict__ g, const double* __restrict__ edir,
+                                              const v3 l1, const v3 l2, double* __restrict__ Y) {
+  const v3 q1 = sub(ld3(g, f1), divs(l1, mu * sqrt(a1)));
+  const v3 q2 = sub(ld3(g, f2), divs(l2, mu * sqrt(a2)));
+  const v3 ed = ld3(edir, i);
+  const double mismatch = dot(ed, sub(q2, q1));
+  const v3 shift = mk(ed.x * mismatch, ed.y * mismatch, ed.z * mismatch);
+  st3(Y, 2 * i, add(q1, scale(a2 / (a1 + a2), shift)));
+  st3(Y, 2 * i + 1, sub(q2, scale(a1 / (a1 + a2), shift)));
+}
+
+__global__ void k_face_first_y(const int32_t* __restrict__ ef, const double* __restrict__ area,
+                               const double* __restrict__ g, const double* __restrict__ edir,
+                               const double* __restrict__ lam, int64_t ni, double mu, double* __restrict__ Y) {
+  GRID_STRIDE(i, ni) {
+    const int32_t f1 = ef[2 * i], f2 = ef[2 * i + 1];
+    face_y_update(i, f1, f2, area[f1], area[f2], mu, g, edir, ld3(lam, 2 * i), ld3(lam, 2 * i + 1), Y);
+  }
+}
+
+// G-update per face (grad_face.hpp:139-155) + dual partials (170-171, 104-111)
+__global__ void k_face_g(const int32_t* __restrict__ slot, const double* __restrict__ area,
+                         const double* __restrict__ h, const double* __restrict__ Y, const double* __restrict__ lam,
+                         int64_t nf, double mu, double* __restrict__ g, double* __restrict__ part) {
+  double s = 0.0;
+  GRID_STRIDE(f, nf) {
+    const double A = area[f];
+    const double alpha = sqrt(A);
+    v3 sum = mk(0.0, 0.0, 0.0);
+    int count = 0;
+    for (int k = 0; k < 3; ++k) {
+      const int32_t sl = slot[3 * f + k];
+      if (sl < 0) continue;
+      sum = add(sum, add(ld3(Y, sl), divs(ld3(lam, sl), mu * alpha)));
+      ++count;
+    }
+    const v3 gold = ld3(g, f);
+    const v3 gnew = divs(add(scale(2.0, ld3(h, f)), scale(mu, sum)), 2.0 + mu * (double)count);
+    st3(g, f, gnew);
+    const v3 dg = sub(gnew, gold);
+    s += (double)count * A * sqnorm(dg);
+  }
+  s = block_sum<B>(s);
+  if (threadIdx.x == 0) part[blockIdx.x] = s;
+}
+
+// lambda-update + primal rows per interior edge (grad_face.hpp:158-168), then
+// the next iteration's Y-update from the same registers.
+__global__ void k_face_lambda_y(const int32_t* __restrict__ ef, const double* __restrict__ area,
+                                const double* __restrict__ g, const double* __restrict__ edir, int64_t ni, double mu,
+                                double* __restrict__ Y, double* __restrict__ lam, double* __restrict__ part) {
+  double s = 0.0;
+  GRID_STRIDE(i, ni) {
+    const int32_t f1 = ef[2 * i], f2 = ef[2 * i + 1];
+    const double a1 = area[f1], a2 = area[f2];
+    const v3 r1 = scale(sqrt(a1), sub(ld3(Y, 2 * i), ld3(g, f1)));
+    const v3 r2 = scale(sqrt(a2), sub(ld3(Y, 2 * i + 1), ld3(g, f2)));
+    const v3 l1 = add(ld3(lam, 2 * i), scale(mu, r1));
+    const v3 l2 = add(ld3(lam, 2 * i + 1), scale(mu, r2));
+    st3(lam, 2 * i, l1);
+    st3(lam, 2 * i + 1, l2);
+    s += sqnorm(r1) + sqnorm(r2);
+    face_y_update(i, f1, f2, a1, a2, mu, g, edir, l1, l2, Y);
+  }
+  s = block_sum<B>(s);
+  if (threadIdx.x == 0) part[blockIdx.x] = s;
+}
+
+// ---------------------------------------------------------------- edge ADMM
+// ctor (grad_edge.hpp:84-89): z = H_f . e per corner, signs (mesh.hpp:81-83)
+__global__ void k_edge_init_faces(const double* __restrict__ pos, const int32_t* __restrict__ faces,
+                                  const int32_t* __restrict__ he_edge, const int32_t* __restrict__ edge_v,
+                                  const double* __restrict__ h, int64_t nf, double* __restrict__ w,
+                                  double* __restrict__ lam, int8_t* __restrict__ sgn) {
+  GRID_STRIDE(f, nf) {
+    const v3 hf = ld3(h, f);
+    for (int k = 0; k < 3; ++k) {
+      const int64_t hh = 3 * f + k;
+      const int32_t e = he_edge[hh];
+      const int32_t a = edge_v[2 * e], b = edge_v[2 * e + 1];
+      w[hh] = dot(hf, sub(ld3(pos, b), ld3(pos, a)));
+      lam[hh] = 0.0;
+      sgn[hh] = faces[hh] == a ? (int8_t)1 : (int8_t)-1;
+    }
+  }
+}
+
+// target_sum in ascending halfedge order from 0.0; x = target_sum / deg (85-93)
+__global__ void k_edge_init_edges(const int32_t* __restrict__ edge_he, const double* __restrict__ z, int64_t ne,
+                                  double* __restrict__ tsum, double* __restrict__ x) {
+  GRID_STRIDE(e, ne) {
+    int32_t h0 = edge_he[2 * e], h1 = edge_he[2 * e + 1];
+    if (h0 >= 0 && h1 >= 0 && h1 < h0) {
+      const int32_t t = h0;
+      h0 = h1;
+      h1 = t;
+    }
+    double s = 0.0;
+    int deg = 0;
+    if (h0 >= 0) {
+      s += z[h0];
+      ++deg;
+    }
+    if (h1 >= 0) {
+      s += z[h1];
+      ++deg;
+    }
+    tsum[e] = s;
+    x[e] = s / (double)deg;
+  }
+}
+
+// W-update for face f (grad_edge.hpp:131-141)
+__device__ __forceinline__ void edge_w_update(int64_t f, const int32_t* __restrict__ he_edge,
+                                              const double* __restrict__ x, const double l[3],
+                                              const int8_t* __restrict__ sgn, double mu, double* __restrict__ w) {
+  double v[3], dotv = 0.0;
+  for (int k = 0; k < 3; ++k) {
+    v[k] = x[he_edge[3 * f + k]] - l[k] / mu;
+    dotv += (double)sgn[3 * f + k] * v[k];
+  }
+  const double shift = dotv / 3.0;
+  for (int k = 0; k < 3; ++k) w[3 * f + k] = v[k] - shift * (double)sgn[3 * f + k];
+}
+
+__global__ void k_edge_first_w(const int32_t* __restrict__ he_edge, const double* __restrict__ x,
+                               const double* __restrict__ lam, const int8_t* __restrict__ sgn, int64_t nf, double mu,
+                               double* __restrict__ w) {
+  GRID_STRIDE(f, nf) {
+    const double l[3] = {lam[3 * f], lam[3 * f + 1], lam[3 * f + 2]};
+    edge_w_update(f, he_edge, x, l, sgn, mu, w);
+  }
+}
+
+// X-update per edge (143-149) + dual partials (163-164, 117-123)
+__global__ void k_edge_x(const int32_t* __restrict__ edge_he, const double* __restrict__ tsum,
+                         const double* __restrict__ lam, const double* __restrict__ w, int64_t ne, double mu,
+                         double* __restrict__ x, double* __restrict__ part) {
+  double s = 0.0;
+  GRID_STRIDE(e, ne) {
+    const double xold = x[e];
+    double sum = tsum[e];
+    const int32_t h0 = edge_he[2 * e], h1 = edge_he[2 * e + 1];
+    if (h0 >= 0) sum += lam[h0] + mu * w[h0];
+    if (h1 >= 0) sum += lam[h1] + mu * w[h1];
+    const double deg = (h0 >= 0 && h1 >= 0) ? 2.0 : 1.0;
+    const double xn = sum / (deg * (1.0 + mu));
+    x[e] = xn;
+    const double d = xn - xold;
+    s += deg * d * d;
+  }
+  s = block_sum<B>(s);
+  if (threadIdx.x == 0) part[blockIdx.x] = s;
+}
+
+// lambda-update + primal (151-158), then the next W-update per face
+__global__ void k_edge_lambda_w(const int32_t* __restrict__ he_edge, const double* __restrict__ x,
+                                const int8_t* __restrict__ sgn, int64_t nf, double mu, double* __restrict__ w,
+                                double* __restrict__ lam, double* __restrict__ part) {
+  double s = 0.0;
+  GRID_STRIDE(f, nf) {
+    double l[3], rs = 0.0;
+    for (int k = 0; k < 3; ++k) {
+      const int64_t hh = 3 * f + k;
+      const double r = w[hh] - x[he_edge[hh]];
+      l[k] = lam[hh] + mu * r;
+      lam[hh] = l[k];
+      rs += r * r;
+    }
+    s += rs;
+    edge_w_update(f, he_edge, x, l, sgn, mu, w);
+  }
+  s = block_sum<B>(s);
+  if (threadIdx.x == 0) part[blockIdx.x] = s;
+}
+
+__global__ void k_sqrt_pair(const double* __restrict__ sums, double mu, double* __restrict__ out) {
+  if (threadIdx.x == 0) {
+    out[0] = sqrt(sums[0]);       // primal
+    out[1] = mu * sqrt(sums[1]);  // dual
+  }
+}
+
+void validate(const gh_admm_config& c) {
+  if (c.max_iterations < 0) gh::fail(GH_ERR_INVALID, "AdmmConfig: max_iterations must be >= 0");
+  if (!(c.eps1 > 0.0) || !(c.eps2 > 0.0)) gh::fail(GH_ERR_INVALID, "AdmmConfig: eps must be positive");
+  if (!(c.mu > 0.0)) gh::fail(GH_ERR_INVALID, "AdmmConfig: mu must be positive");
+}
+
+}  // namespace
+
+namespace {
+__global__ void k_reduce_block(const double* __restrict__ part, int n, double* __restrict__ out) {
+  __shared__ double sh[1024];
+  double s = 0.0;
+  for (int i = threadIdx.x; i < n; i += 1024) s += part[i];
+  sh[threadIdx.x] = s;
+  __syncthreads();
+  for (int k = 512; k > 0; k >>= 1) {
+    if (threadIdx.x < k) sh[threadIdx.x] += sh[threadIdx.x + k];
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) out[0] = sh[0];
+}
+}  // namespace
+
+void reduce_into(gh_mesh* m, const double* partials, double* slot) {
+  k_reduce_block<<<1, 1024, 0, m->stream>>>(partials, (int)G, slot);
+  GH_LAUNCH_CHECK();
+  m->launches++;
+}
+
+namespace gh {
+
+int32_t normalize_dev(gh_mesh* m, const double* d_u, double* d_h) {
+  if (!m->nf) return 0;
+  k_normalize<<<G, B, 0, m->stream>>>(m->pos.p, m->faces.p, m->face_normal.p, m->face_area.p, d_u, m->nf, d_h,
+                                      m->partials.p);
+  GH_LAUNCH_CHECK();
+  m->launches++;
+  reduce_into(m, m->partials.p, m->scalars.p + 4);
+  double z = 0.0;
+  GH_CUDA(cudaMemcpyAsync(&z, m->scalars.p + 4, sizeof(double), cudaMemcpyDeviceToHost, m->stream));
+  GH_CUDA(cudaStreamSynchronize(m->stream));
+  return (int32_t)z;
+}
+
+AdmmResult admm_face_dev(gh_mesh* m, const double* d_h, const gh_admm_config& cfg, double* d_g) {
+  validate(cfg);
+  cudaStream_t s = m->stream;
+  const int64_t F = m->nf, NI = m->ni;
+  const double mu = cfg.mu;
+  AdmmResult res;
+  Scratch<double> Y(6 * NI + 6, s), lam(6 * NI + 6, s), edir(3 * NI + 3, s);
+  Scratch<int32_t> ef(2 * NI + 2, s), slot(3 * F + 3, s);
+  res.state_bytes = sizeof(double) * (3 * F /*g*/ + 3 * F /*targets*/ + 15 * NI) + sizeof(int32_t) * (2 * NI + 3 * F);
+  double* part_dual = m->partials.p;
+  double* part_primal = m->partials.p + G;
+  double* sums = m->scalars.p + 8;  // [primal_sum, dual_sum]
+  double* pr = m->scalars.p + 10;   // [primal, dual]
+  EventTimer timer(s);
+  timer.start();
+  GH_CUDA(cudaMemcpyAsync(d_g, d_h, sizeof(double) * 3 * F, cudaMemcpyDeviceToDevice, s));  // g = h
+  if (F) k_face_slots<<<G, B, 0, s>>>(m->he_edge.p, m->interior_edge_index.p, m->edge_he.p, F, slot.p);
+  k_face_init_edges<<<G, B, 0, s>>>(m->pos.p, m->interior_edges.p, m->edge_v.p, m->edge_he.p, m->face_area.p, NI,
+                                    edir.p, ef.p, lam.p, part_primal);
+  reduce_into(m, part_primal, m->scalars.p + 5);
+  GH_LAUNCH_CHECK();
+  m->launches += 2;
+  double scale2 = 0.0;
+  GH_CUDA(cudaMemcpyAsync(&scale2, m->scalars.p + 5, sizeof(double), cudaMemcpyDeviceToHost, s));
+  GH_CUDA(cudaStreamSynchronize(s));
+  const double scale = std::sqrt(scale2);  // ||M||_F (grad_face.hpp:86)
+  if (cfg.max_iterations > 0 && NI) {
+    // y1, y2 start at H of the side faces (grad_face.hpp:82-83) == Y-update from
+    // g = h, lambda = 0 of iteration 0 (computed here exactly like later ones)
+    k_face_first_y<<<G, B, 0, s>>>(ef.p, m->face_area.p, d_g, edir.p, lam.p, NI, mu, Y.p);
+    GH_LAUNCH_CHECK();
+    m->launches++;
+  }
+  for (int it = 0; it < cfg.max_iterations; ++it) {
+    k_face_g<<<G, B, 0, s>>>(slot.p, m->face_area.p, d_h, Y.p, lam.p, F, mu, d_g, part_dual);
+    k_face_lambda_y<<<G, B, 0, s>>>(ef.p, m->face_area.p, d_g, edir.p, NI, mu, Y.p, lam.p, part_primal);
+    GH_LAUNCH_CHECK();
+    reduce_into(m, part_primal, sums);
+    reduce_into(m, part_dual, sums + 1);
+    k_sqrt_pair<<<1, 32, 0, s>>>(sums, mu, pr);
+    GH_LAUNCH_CHECK();
+    m->launches += 3;
+    GH_CUDA(cudaMemcpyAsync(m->pinned_scalars, pr, 2 * sizeof(double), cudaMemcpyDeviceToHost, s));
+    GH_CUDA(cudaStreamSynchronize(s));
+    const double primal = m->pinned_scalars[0], dual = m->pinned_scalars[1];
+    res.primal.push_back(primal);
+    res.dual.push_back(dual);
+    res.final_primal = primal;
+    res.final_dual = dual;
+    res.iterations = it + 1;
+    if (primal <= scale * cfg.eps1 && dual <= scale * cfg.eps2) {  // grad_face.hpp:175-177
+      res.converged = true;
+      break;
+    }
+  }
+  timer.stop();
+  res.device_ms = timer.ms();
+  return res;
+}
+
+AdmmResult admm_edge_dev(gh_mesh* m, const double* d_h, const gh_admm_config& cfg, double* d_x) {
+  validate(cfg);
+  cudaStream_t s = m->stream;
+  const int64_t F = m->nf, E = m->ne;
+  const double mu = cfg.mu;
+  AdmmResult res;
+  Scratch<double> w(3 * F + 3, s), lam(3 * F + 3, s), tsum(E + 1, s);
+  Scratch<int8_t> sgn(3 * F + 3, s);
+  res.state_bytes = sizeof(double) * (2 * E + 6 * F) + 3 * F;  // x, target_sum, w, lambda, sign
+  double* part_dual = m->partials.p;
+  double* part_primal = m->partials.p + G;
+  double* sums = m->scalars.p + 8;
+  double* pr = m->scalars.p + 10;
+  const double scale = std::sqrt(3.0 * (double)F);  // ||R||_F (grad_edge.hpp:79)
+  EventTimer timer(s);
+  timer.start();
+  if (F) k_edge_init_faces<<<G, B, 0, s>>>(m->pos.p, m->faces.p, m->he_edge.p, m->edge_v.p, d_h, F, w.p, lam.p, sgn.p);
+  if (E) k_edge_init_edges<<<G, B, 0, s>>>(m->edge_he.p, w.p, E, tsum.p, d_x);
+  GH_LAUNCH_CHECK();
+  m->launches += 2;
+  if (cfg.max_iterations > 0 && F) {
+    k_edge_first_w<<<G, B, 0, s>>>(m->he_edge.p, d_x, lam.p, sgn.p, F, mu, w.p);
+    GH_LAUNCH_CHECK();
+    m->launches++;
+  }
+  for (int it = 0; it < cfg.max_iterations; ++it) {
+    k_edge_x<<<G, B, 0, s>>>(m->edge_he.p, tsum.p, lam.p, w.p, E, mu, d_x, part_dual);
+    k_edge_lambda_w<<<G, B, 0, s>>>(m->he_edge.p, d_x, sgn.p, F, mu, w.p, lam.p, part_primal);
+    GH_LAUNCH_CHECK();
+    reduce_into(m, part_primal, sums);
+    reduce_into(m, part_dual, sums + 1);
+    k_sqrt_pair<<<1, 32, 0, s>>>(sums, mu, pr);
+    GH_LAUNCH_CHECK();
+    m->launches += 3;
+    GH_CUDA(cudaMemcpyAsync(m->pinned_scalars, pr, 2 * sizeof(double), cudaMemcpyDeviceToHost, s));
+    GH_CUDA(cudaStreamSynchronize(s));
+    const double primal = m->pinned_scalars[0], dual = m->pinned_scalars[1];
+    res.primal.push_back(primal);
+    res.dual.push_back(dual);
+    res.final_primal = primal;
+    res.final_dual = dual;
+    res.iterations = it + 1;
+    if (primal <= scale * cfg.eps1 && dual <= scale * cfg.eps2) {  // grad_edge.hpp:168-170
+      res.converged = true;
+      break;
+    }
+  }
+  timer.stop();
+  res.device_ms = timer.ms();
+  return res;
+}
+
+}  // namespace gh

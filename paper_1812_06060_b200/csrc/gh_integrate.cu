@@ -1,0 +1,148 @@
+// Breadth-first distance recovery (reference integrate.hpp:19-75).
+//
+// The reference's step is d(v) = d(parent) + inc(v), with inc(v) computed
+// before the addition (integrate.hpp:56, 72). inc depends only on the
+// optimised field and the geometry, so it is computed for every vertex in one
+// fully parallel gather kernel. The chain d(v) = d(parent) + inc(v) is then
+// evaluated level by level in a cooperative persistent kernel (one grid
+// barrier per BFS level, as the reference's run_levels has one omp barrier per
+// level), which reproduces the reference's additions exactly.
+
+#include <cooperative_groups.h>
+
+#include <algorithm>
+#include <cmath>
+
+#include "gh_internal.cuh"
+
+namespace cg = cooperative_groups;
+using namespace ghd;
+
+namespace {
+
+constexpr int B = gh::kBlock;
+
+// edge_between (mesh.hpp:87-93): lower_bound in a's ascending row
+__device__ __forceinline__ int32_t edge_between(const int32_t* __restrict__ off, const int32_t* __restrict__ idx,
+                                                const int32_t* __restrict__ eid, int32_t a, int32_t b) {
+  int32_t lo = off[a], hi = off[a + 1];
+  const int32_t end = hi;
+  while (lo < hi) {
+    const int32_t mid = lo + ((hi - lo) >> 1);
+    if (idx[mid] < b) lo = mid + 1;
+    else hi = mid;
+  }
+  return (lo == end || idx[lo] != b) ? -1 : eid[lo];
+}
+
+// inc(v) for the face method (integrate.hpp:45-56), indexed by BFS position
+__global__ void k_inc_face(const int32_t* __restrict__ order, const int32_t* __restrict__ parent, int64_t b,
+                           int64_t e, const int32_t* __restrict__ off, const int32_t* __restrict__ idx,
+                           const int32_t* __restrict__ eid, const int32_t* __restrict__ edge_he,
+                           const double* __restrict__ pos, const double* __restrict__ g, double* __restrict__ inc) {
+  for (int64_t i = b + blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < e; i += (int64_t)gridDim.x * blockDim.x) {
+    const int32_t v = order[i], p = parent[v];
+    const int32_t ed = edge_between(off, idx, eid, p, v);
+    const v3 step = sub(ld3(pos, v), ld3(pos, p));
+    double sum = 0.0;
+    int count = 0;
+    for (int s = 0; s < 2; ++s) {
+      const int32_t h = edge_he[2 * ed + s];
+      if (h < 0) continue;
+      sum += dot(ld3(g, h / 3), step);
+      ++count;
+    }
+    inc[i] = sum / (double)count;
+  }
+}
+
+// inc(v) for the edge method (integrate.hpp:67-72)
+__global__ void k_inc_edge(const int32_t* __restrict__ order, const int32_t* __restrict__ parent, int64_t b,
+                           int64_t e, const int32_t* __restrict__ off, const int32_t* __restrict__ idx,
+                           const int32_t* __restrict__ eid, const int32_t* __restrict__ edge_v,
+                           const double* __restrict__ x, double* __restrict__ inc) {
+  for (int64_t i = b + blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < e; i += (int64_t)gridDim.x * blockDim.x) {
+    const int32_t v = order[i], p = parent[v];
+    const int32_t ed = edge_between(off, idx, eid, p, v);
+    const double sigma = edge_v[2 * ed] == p ? 1.0 : -1.0;
+    inc[i] = sigma * x[ed];
+  }
+}
+
+// d = +inf everywhere, 0 on D_0 (integrate.hpp:20, 52)
+__global__ void k_dist_init(const int32_t* __restrict__ level, int64_t nv, double* __restrict__ d) {
+  for (int64_t v = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; v < nv; v += (int64_t)gridDim.x * blockDim.x)
+    d[v] = level[v] == 0 ? 0.0 : INFINITY;
+}
+
+// level-synchronous chain (run_levels, integrate.hpp:19-36)
+__global__ void __launch_bounds__(B) k_chain(const int32_t* __restrict__ order, const int32_t* __restrict__ parent,
+                                             const int32_t* __restrict__ offsets, int32_t nlev,
+                                             const double* __restrict__ inc, double* __restrict__ d) {
+  cg::grid_group grid = cg::this_grid();
+  const int64_t tid = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  for (int32_t L = 1; L < nlev; ++L) {
+    const int64_t b = offsets[L], e = offsets[L + 1];
+    for (int64_t i = b + tid; i < e; i += stride) {
+      const int32_t v = order[i];
+      __stcg(d + v, __ldcg(d + parent[v]) + inc[i]);
+    }
+    grid.sync();
+  }
+}
+
+void run_chain(gh_levels* L, const double* inc, double* d) {
+  gh_mesh* m = L->mesh;
+  cudaStream_t s = m->stream;
+  k_dist_init<<<gh::grid_for(m->nv), B, 0, s>>>(L->level.p, m->nv, d);
+  GH_LAUNCH_CHECK();
+  m->launches++;
+  if (L->nlev <= 1) return;
+  int nsm = 0, per_sm = 0;
+  GH_CUDA(cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, m->device));
+  GH_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_chain, B, 0));
+  // a level holds at most max_width vertices; no need for more threads
+  const int64_t want = (L->max_width + B - 1) / B;
+  const int grid = (int)std::max<int64_t>(1, std::min<int64_t>((int64_t)nsm * std::max(1, per_sm), want));
+  const int32_t* order = L->order.p;
+  const int32_t* parent = L->parent.p;
+  const int32_t* offsets = L->offsets.p;
+  int32_t nlev = L->nlev;
+  void* args[] = {&order, &parent, &offsets, &nlev, &inc, &d};
+  GH_CUDA(cudaLaunchCooperativeKernel((void*)k_chain, grid, B, args, 0, s));
+  GH_LAUNCH_CHECK();
+  m->launches++;
+}
+
+}  // namespace
+
+namespace gh {
+
+void integrate_face_dev(gh_levels* L, const double* d_g, double* d_d) {
+  gh_mesh* m = L->mesh;
+  Scratch<double> inc(L->nreach + 1, m->stream);
+  const int64_t b = L->h_offsets.size() > 1 ? L->h_offsets[1] : 0, e = L->nreach;
+  if (e > b) {
+    k_inc_face<<<grid_for(e - b), B, 0, m->stream>>>(L->order.p, L->parent.p, b, e, m->vv_offset.p, m->vv_index.p,
+                                                     m->vv_edge.p, m->edge_he.p, m->pos.p, d_g, inc.p);
+    GH_LAUNCH_CHECK();
+    m->launches++;
+  }
+  run_chain(L, inc.p, d_d);
+}
+
+void integrate_edge_dev(gh_levels* L, const double* d_x, double* d_d) {
+  gh_mesh* m = L->mesh;
+  Scratch<double> inc(L->nreach + 1, m->stream);
+  const int64_t b = L->h_offsets.size() > 1 ? L->h_offsets[1] : 0, e = L->nreach;
+  if (e > b) {
+    k_inc_edge<<<grid_for(e - b), B, 0, m->stream>>>(L->order.p, L->parent.p, b, e, m->vv_offset.p, m->vv_index.p,
+                                                     m->vv_edge.p, m->edge_v.p, d_x, inc.p);
+    GH_LAUNCH_CHECK();
+    m->launches++;
+  }
+  run_chain(L, inc.p, d_d);
+}
+
+}  // namespace gh

@@ -1,0 +1,242 @@
+// Internal declarations of the geoheat_b200 CUDA library (sm_100a).
+//
+// All fp64 arithmetic in this library is compiled with -fmad=false: every
+// product and sum is rounded exactly where the reference (compiled without
+// FMA contraction) rounds it, so the per-element results are bit-identical to
+// the reference. Only the residual norms of the ADMM stop rule use a
+// different (deterministic, tree) summation order; see DESIGN.md §3.6.
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include <cstdint>
+#include <cstdio>
+#include <stdexcept>
+#include <string>
+#include <vector>
+
+#include "../../include/geoheat_b200.h"
+
+namespace gh {
+
+struct Error {
+  int code;
+  std::string msg;
+};
+
+[[noreturn]] inline void fail(int code, const std::string& msg) { throw Error{code, msg}; }
+
+#define GH_CUDA(x)                                                                                     \
+  do {                                                                                                 \
+    cudaError_t gh_e_ = (x);                                                                           \
+    if (gh_e_ != cudaSuccess)                                                                          \
+      ::gh::fail(GH_ERR_CUDA, std::string(#x) + " failed: " + cudaGetErrorString(gh_e_) + " (" +      \
+                                  __FILE__ + ":" + std::to_string(__LINE__) + ")");                   \
+  } while (0)
+
+#define GH_LAUNCH_CHECK() GH_CUDA(cudaGetLastError())
+
+constexpr int kBlock = 256;
+constexpr int kReduceGrid = 1024;  // fixed partial count => reproducible reductions
+
+inline unsigned grid_for(int64_t n, int block = kBlock, int64_t cap = 148 * 32) {
+  int64_t g = (n + block - 1) / block;
+  if (g < 1) g = 1;
+  if (g > cap) g = cap;
+  return (unsigned)g;
+}
+
+// Device buffer owned by a handle: stream-ordered allocation on the handle's
+// stream from the device's default memory pool, whose release threshold is
+// raised once per device (gh_mesh_create) so freed handle memory stays cached
+// for the next solve instead of going back to the driver.
+template <class T>
+struct DevBuf {
+  T* p = nullptr;
+  size_t n = 0;
+  cudaStream_t s = nullptr;
+  DevBuf() = default;
+  DevBuf(const DevBuf&) = delete;
+  DevBuf& operator=(const DevBuf&) = delete;
+  ~DevBuf() { release(); }
+  void alloc(size_t count, cudaStream_t stream) {
+    release();
+    n = count;
+    s = stream;
+    if (count) GH_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&p), sizeof(T) * count, stream));
+  }
+  void release() {
+    if (p) cudaFreeAsync(p, s);
+    p = nullptr;
+    n = 0;
+  }
+  size_t bytes() const { return n * sizeof(T); }
+};
+
+// Scratch allocation from the stream-ordered pool (freed in stream order).
+template <class T>
+struct Scratch {
+  T* p = nullptr;
+  cudaStream_t s = nullptr;
+  Scratch(size_t count, cudaStream_t stream) : s(stream) {
+    if (count) GH_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&p), sizeof(T) * count, stream));
+  }
+  ~Scratch() {
+    if (p) cudaFreeAsync(p, s);
+  }
+  Scratch(const Scratch&) = delete;
+  Scratch& operator=(const Scratch&) = delete;
+};
+
+struct EventTimer {
+  cudaEvent_t a = nullptr, b = nullptr;
+  cudaStream_t s;
+  explicit EventTimer(cudaStream_t stream) : s(stream) {
+    GH_CUDA(cudaEventCreate(&a));
+    GH_CUDA(cudaEventCreate(&b));
+  }
+  ~EventTimer() {
+    if (a) cudaEventDestroy(a);
+    if (b) cudaEventDestroy(b);
+  }
+  void start() { GH_CUDA(cudaEventRecord(a, s)); }
+  void stop() { GH_CUDA(cudaEventRecord(b, s)); }
+  double ms() {
+    GH_CUDA(cudaEventSynchronize(b));
+    float f = 0.f;
+    GH_CUDA(cudaEventElapsedTime(&f, a, b));
+    return (double)f;
+  }
+};
+
+}  // namespace gh
+
+// ---------------------------------------------------------------- handles
+
+struct gh_mesh {
+  int device = 0;
+  cudaStream_t stream = nullptr;
+  int32_t nv = 0, nf = 0, ne = 0, ni = 0, boundary_vertices = 0;
+  gh::DevBuf<double> pos, face_area, face_normal, vertex_area, he_cot, edge_weight, vertex_weight_sum, vv_weight;
+  gh::DevBuf<int32_t> faces, he_twin, he_edge, edge_v, edge_he, interior_edges, interior_edge_index;
+  gh::DevBuf<int32_t> vv_offset, vv_index, vv_edge, vc_offset, vc_corner;
+  gh::DevBuf<uint8_t> on_boundary;
+  // reduction scratch: kReduceGrid partials + result slots
+  gh::DevBuf<double> partials, scalars;
+  double* pinned_scalars = nullptr;  // host mirror for per-iteration stop checks
+  int launches = 0;                  // kernels launched since the counter was last read
+  int level_refs = 0;                // live gh_levels built on this mesh
+  bool destroy_pending = false;      // gh_mesh_destroy called while levels were alive
+  uint64_t device_bytes() const;
+};
+
+struct gh_levels {
+  gh_mesh* mesh = nullptr;
+  int32_t nlev = 0, unreachable = 0, nreach = 0, max_width = 0;
+  std::vector<int32_t> h_offsets;  // BFS order ring boundaries (nlev + 1)
+  gh::DevBuf<int32_t> level, parent, order, offsets;  // level/parent [V], order [nreach], offsets [nlev+1]
+  // diffusion layout: rows renumbered by (level parity, level, original index)
+  int32_t nrows = 0;      // size of the new index space (odd class starts 32-aligned)
+  int32_t nchunks = 0;    // nrows / 32
+  std::vector<int32_t> h_pstart, h_pend;           // per level: new-index range
+  gh::DevBuf<int32_t> pstart, pend;                // same, on device
+  gh::DevBuf<int32_t> perm;                        // new row -> original vertex (-1 for padding rows)
+  gh::DevBuf<int32_t> chunk_level;                 // level of each chunk's first row
+  gh::DevBuf<int64_t> chunk_ptr;                   // SELL-32 chunk offsets
+  gh::DevBuf<uint16_t> deg;                        // row lengths
+  gh::DevBuf<int32_t> col;                         // new-index neighbour | 0x80000000 if at level L-1
+  gh::DevBuf<double> wt;                           // cotan weights, reference row order
+  gh::DevBuf<double> area_r, wsum_r;               // vertex_area / vertex_weight_sum in row order
+  gh::DevBuf<double> den;                          // A_j + t * sum theta_j for the current t
+  gh::DevBuf<double> ubuf;                         // 2 * nrows: sweep-parity double buffer
+  double den_t = 0.0;                              // t that `den` holds
+  int32_t u_valid = 0;                             // ubuf holds a finished solve
+  int32_t u_sweeps = 0;
+  gh::DevBuf<double> u_orig;                       // last diffusion result, original order [V]
+  uint64_t device_bytes() const;
+};
+
+namespace gh {
+
+// mesh build / queries (gh_mesh.cu)
+void mesh_build(gh_mesh* m, const double* h_pos, const int32_t* h_faces);
+double mesh_average_edge_length(gh_mesh* m);
+void face_gradient_dev(gh_mesh* m, const double* d_u, double* d_grad);
+
+// BFS + diffusion layout (gh_bfs.cu)
+void bfs_build(gh_levels* L, const int32_t* h_sources, int32_t ns);
+
+// diffusion (gh_diffuse.cu): result stays in L->u_orig (original order)
+double diffuse_dev(gh_levels* L, double t, int32_t sweeps, const double* d_initial);
+double diffusion_residual_dev(gh_levels* L, const double* d_u, double t);
+
+// normalisation + optimisation (gh_grad.cu)
+int32_t normalize_dev(gh_mesh* m, const double* d_u, double* d_h);
+struct AdmmResult {
+  int iterations = 0;
+  bool converged = false;
+  double final_primal = 0, final_dual = 0;
+  std::vector<double> primal, dual;
+  uint64_t state_bytes = 0;
+  double device_ms = 0;
+};
+AdmmResult admm_face_dev(gh_mesh* m, const double* d_h, const gh_admm_config& cfg, double* d_g);
+AdmmResult admm_edge_dev(gh_mesh* m, const double* d_h, const gh_admm_config& cfg, double* d_x);
+
+// integration (gh_integrate.cu)
+void integrate_face_dev(gh_levels* L, const double* d_g, double* d_d);
+void integrate_edge_dev(gh_levels* L, const double* d_x, double* d_d);
+
+// deterministic reductions (gh_mesh.cu): sum of partials[0..kReduceGrid)
+void reduce_partials(gh_mesh* m, double* d_result_slot);
+
+}  // namespace gh
+
+// ---------------------------------------------------------------- device helpers
+
+namespace ghd {
+
+struct v3 {
+  double x, y, z;
+};
+__device__ __forceinline__ v3 mk(double x, double y, double z) { return v3{x, y, z}; }
+__device__ __forceinline__ v3 ld3(const double* p, int64_t i) { return v3{p[3 * i], p[3 * i + 1], p[3 * i + 2]}; }
+__device__ __forceinline__ void st3(double* p, int64_t i, v3 a) {
+  p[3 * i] = a.x;
+  p[3 * i + 1] = a.y;
+  p[3 * i + 2] = a.z;
+}
+__device__ __forceinline__ v3 sub(v3 a, v3 b) { return v3{a.x - b.x, a.y - b.y, a.z - b.z}; }
+__device__ __forceinline__ v3 add(v3 a, v3 b) { return v3{a.x + b.x, a.y + b.y, a.z + b.z}; }
+__device__ __forceinline__ v3 scale(double s, v3 a) { return v3{s * a.x, s * a.y, s * a.z}; }
+__device__ __forceinline__ v3 divs(v3 a, double s) { return v3{a.x / s, a.y / s, a.z / s}; }
+// Eigen size-3 dot order: (x0*y0 + x1*y1) + x2*y2
+__device__ __forceinline__ double dot(v3 a, v3 b) { return (a.x * b.x + a.y * b.y) + a.z * b.z; }
+__device__ __forceinline__ double sqnorm(v3 a) { return dot(a, a); }
+__device__ __forceinline__ double norm(v3 a) { return sqrt(sqnorm(a)); }
+__device__ __forceinline__ v3 cross(v3 a, v3 b) {
+  return v3{a.y * b.z - a.z * b.y, a.z * b.x - a.x * b.z, a.x * b.y - a.y * b.x};
+}
+__device__ __forceinline__ v3 normalized(v3 a) {
+  double n2 = sqnorm(a);
+  return n2 > 0.0 ? divs(a, sqrt(n2)) : a;
+}
+
+// Block-wide sum in a fixed tree order (deterministic for a fixed blockDim).
+template <int BLOCK>
+__device__ __forceinline__ double block_sum(double v) {
+  __shared__ double sh[BLOCK / 32];
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_down_sync(0xffffffffu, v, o);
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  if (lane == 0) sh[w] = v;
+  __syncthreads();
+  double r = 0.0;
+  if (w == 0) {
+    r = lane < BLOCK / 32 ? sh[lane] : 0.0;
+    for (int o = 16; o > 0; o >>= 1) r += __shfl_down_sync(0xffffffffu, r, o);
+  }
+  __syncthreads();
+  return r;  // valid in thread 0
+}
+
+}  // namespace ghd

@@ -1,0 +1,575 @@
+// Device mesh preprocessing: the solver-relevant part of build_mesh
+// (reference mesh.hpp:113-286), average_edge_length (289-293) and
+// face_gradient (314-327), as sm_100a kernels.
+//
+// Every per-element value is produced with the reference's operation order
+// (no FMA; sequential per-row sums in the reference's row order), so the
+// device TriMesh arrays equal the reference's bit for bit. Orders that the
+// reference gets from std::sort are produced by stable radix sorts:
+//   edges      : halfedge keys (vmin, vmax) stable-sorted over h ascending
+//   vc CSR     : corners stable-sorted by vertex (face order within a vertex)
+//   vv CSR     : (row, neighbour) keys, unique per row
+
+#include <cub/device/device_radix_sort.cuh>
+#include <cub/device/device_scan.cuh>
+
+#include <cmath>
+#include <cstring>
+
+#include "gh_internal.cuh"
+
+using namespace ghd;
+
+namespace {
+
+constexpr int B = gh::kBlock;
+
+__global__ void k_bbox_partial(const double* __restrict__ pos, int64_t nv, double* __restrict__ part) {
+  double lo[3] = {INFINITY, INFINITY, INFINITY}, hi[3] = {-INFINITY, -INFINITY, -INFINITY};
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < nv; i += (int64_t)gridDim.x * blockDim.x) {
+    for (int k = 0; k < 3; ++k) {
+      double p = pos[3 * i + k];
+      lo[k] = p < lo[k] ? p : lo[k];
+      hi[k] = hi[k] < p ? p : hi[k];
+    }
+  }
+  __shared__ double sh[6][B];
+  for (int k = 0; k < 3; ++k) {
+    sh[k][threadIdx.x] = lo[k];
+    sh[3 + k][threadIdx.x] = hi[k];
+  }
+  __syncthreads();
+  for (int s = B / 2; s > 0; s >>= 1) {
+    if (threadIdx.x < s)
+      for (int k = 0; k < 3; ++k) {
+        double a = sh[k][threadIdx.x + s];
+        sh[k][threadIdx.x] = a < sh[k][threadIdx.x] ? a : sh[k][threadIdx.x];
+        double b = sh[3 + k][threadIdx.x + s];
+        sh[3 + k][threadIdx.x] = sh[3 + k][threadIdx.x] < b ? b : sh[3 + k][threadIdx.x];
+      }
+    __syncthreads();
+  }
+  if (threadIdx.x < 6) part[6 * blockIdx.x + threadIdx.x] = sh[threadIdx.x][0];
+}
+
+// degenerate threshold 1e-14 * |hi - lo|^2 (mesh.hpp:120-126)
+__global__ void k_bbox_final(const double* __restrict__ part, int nparts, int64_t nv, double* __restrict__ out) {
+  if (threadIdx.x != 0) return;
+  double lo[3] = {INFINITY, INFINITY, INFINITY}, hi[3] = {-INFINITY, -INFINITY, -INFINITY};
+  for (int b = 0; b < nparts; ++b)
+    for (int k = 0; k < 3; ++k) {
+      double a = part[6 * b + k], c = part[6 * b + 3 + k];
+      lo[k] = a < lo[k] ? a : lo[k];
+      hi[k] = hi[k] < c ? c : hi[k];
+    }
+  v3 d = sub(mk(hi[0], hi[1], hi[2]), mk(lo[0], lo[1], lo[2]));
+  const double diag2 = nv > 0 ? sqnorm(d) : 0.0;
+  out[0] = 1e-14 * diag2;
+}
+
+// face checks + area + unit normal (mesh.hpp:128-145); first failing face via atomicMin
+__global__ void k_faces(const double* __restrict__ pos, const int32_t* __restrict__ faces, int64_t nf, int32_t nv,
+                        const double* __restrict__ degen, double* __restrict__ area, double* __restrict__ normal,
+                        int32_t* __restrict__ err_face) {
+  const double thr = degen[0];
+  for (int64_t f = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; f < nf; f += (int64_t)gridDim.x * blockDim.x) {
+    const int32_t a = faces[3 * f], b = faces[3 * f + 1], c = faces[3 * f + 2];
+    bool bad = a < 0 || a >= nv || b < 0 || b >= nv || c < 0 || c >= nv || a == b || b == c || a == c;
+    if (!bad) {
+      v3 p0 = ld3(pos, a), p1 = ld3(pos, b), p2 = ld3(pos, c);
+      v3 n = cross(sub(p1, p0), sub(p2, p0));
+      double A = 0.5 * norm(n);
+      if (!(A > thr)) {
+        bad = true;
+      } else {
+        area[f] = A;
+        st3(normal, f, divs(n, 2.0 * A));
+      }
+    }
+    if (bad) atomicMin(err_face, (int32_t)f);
+  }
+}
+
+// halfedge keys: (vmin * nv + vmax, h) (mesh.hpp:147-158)
+__global__ void k_he_keys(const int32_t* __restrict__ faces, int64_t nh, uint64_t nv, uint64_t* __restrict__ key,
+                          int32_t* __restrict__ val) {
+  for (int64_t h = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; h < nh; h += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t f = h / 3;
+    const int32_t a = faces[h], b = faces[3 * f + (h % 3 + 1) % 3];
+    const uint64_t lo = (uint64_t)(a < b ? a : b), hi = (uint64_t)(a < b ? b : a);
+    key[h] = lo * nv + hi;
+    val[h] = (int32_t)h;
+  }
+}
+
+__global__ void k_heads(const uint64_t* __restrict__ key, int64_t n, int32_t* __restrict__ flag) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+    flag[i] = (i == 0 || key[i] != key[i - 1]) ? 1 : 0;
+}
+
+// per sorted position: record the start of its edge group
+__global__ void k_edge_starts(const int32_t* __restrict__ flag, const int32_t* __restrict__ eid, int64_t n,
+                              int32_t* __restrict__ start) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+    if (flag[i]) start[eid[i]] = (int32_t)i;
+}
+
+// edges from sorted groups: endpoints, sides, twins, checks (mesh.hpp:159-192)
+__global__ void k_edges(const uint64_t* __restrict__ key, const int32_t* __restrict__ val,
+                        const int32_t* __restrict__ start, int64_t ne, int64_t nh, uint64_t nv,
+                        const int32_t* __restrict__ faces, int32_t* __restrict__ edge_v, int32_t* __restrict__ edge_he,
+                        int32_t* __restrict__ he_edge, int32_t* __restrict__ he_twin,
+                        unsigned long long* __restrict__ err_edge) {
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < ne; e += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t s = start[e], t = e + 1 < ne ? start[e + 1] : nh;
+    const uint64_t k = key[s];
+    const int32_t vmin = (int32_t)(k / nv), vmax = (int32_t)(k % nv);
+    edge_v[2 * e] = vmin;
+    edge_v[2 * e + 1] = vmax;
+    const int64_t incident = t - s;
+    if (incident > 2) {
+      unsigned long long inc = incident > 0xFFFFFF ? 0xFFFFFFull : (unsigned long long)incident;
+      atomicMin(err_edge, ((unsigned long long)e << 32) | (1ull << 24) | inc);
+      continue;
+    }
+    int32_t halves[2] = {-1, -1};
+    bool winding = false;
+    for (int64_t i = s; i < t; ++i) {
+      const int32_t h = val[i];
+      he_edge[h] = (int32_t)e;
+      const int side = faces[h] == vmin ? 0 : 1;
+      if (halves[side] >= 0) winding = true;
+      halves[side] = h;
+    }
+    if (winding) {
+      atomicMin(err_edge, ((unsigned long long)e << 32) | (2ull << 24));
+      continue;
+    }
+    if (incident == 2) {
+      he_twin[halves[0]] = halves[1];
+      he_twin[halves[1]] = halves[0];
+    }
+    edge_he[2 * e] = halves[0];
+    edge_he[2 * e + 1] = halves[1];
+  }
+}
+
+__global__ void k_interior_flag(const int32_t* __restrict__ edge_he, int64_t ne, int32_t* __restrict__ flag) {
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < ne; e += (int64_t)gridDim.x * blockDim.x)
+    flag[e] = (edge_he[2 * e] >= 0 && edge_he[2 * e + 1] >= 0) ? 1 : 0;
+}
+
+__global__ void k_interior_fill(const int32_t* __restrict__ flag, const int32_t* __restrict__ idx, int64_t ne,
+                                int32_t* __restrict__ interior_edges, int32_t* __restrict__ interior_edge_index) {
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < ne; e += (int64_t)gridDim.x * blockDim.x) {
+    if (flag[e]) {
+      interior_edge_index[e] = idx[e];
+      interior_edges[idx[e]] = (int32_t)e;
+    } else {
+      interior_edge_index[e] = -1;
+    }
+  }
+}
+
+// cot_at (mesh.hpp:102-106), halfedge k opposite v_{k+2} (203-213)
+__device__ __forceinline__ double cot_at(v3 apex, v3 p, v3 q) {
+  v3 u = sub(p, apex), v = sub(q, apex);
+  return dot(u, v) / norm(cross(u, v));
+}
+
+__global__ void k_cot(const double* __restrict__ pos, const int32_t* __restrict__ faces, int64_t nf,
+                      double* __restrict__ cot) {
+  for (int64_t f = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; f < nf; f += (int64_t)gridDim.x * blockDim.x) {
+    v3 p0 = ld3(pos, faces[3 * f]), p1 = ld3(pos, faces[3 * f + 1]), p2 = ld3(pos, faces[3 * f + 2]);
+    cot[3 * f + 0] = cot_at(p2, p0, p1);
+    cot[3 * f + 1] = cot_at(p0, p1, p2);
+    cot[3 * f + 2] = cot_at(p1, p2, p0);
+  }
+}
+
+// theta_e = 0.5 * ((0 + cot side0) + cot side1) (mesh.hpp:214-220); boundary flags (226-232)
+__global__ void k_edge_weight(const int32_t* __restrict__ edge_he, const int32_t* __restrict__ edge_v,
+                              const double* __restrict__ cot, int64_t ne, double* __restrict__ w,
+                              uint8_t* __restrict__ on_boundary) {
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < ne; e += (int64_t)gridDim.x * blockDim.x) {
+    const int32_t h0 = edge_he[2 * e], h1 = edge_he[2 * e + 1];
+    double sum = 0.0;
+    if (h0 >= 0) sum += cot[h0];
+    if (h1 >= 0) sum += cot[h1];
+    w[e] = 0.5 * sum;
+    if (h0 < 0 || h1 < 0) {
+      on_boundary[edge_v[2 * e]] = 1;
+      on_boundary[edge_v[2 * e + 1]] = 1;
+    }
+  }
+}
+
+__global__ void k_count_i32(const int32_t* __restrict__ idx, int64_t n, int32_t* __restrict__ cnt) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+    atomicAdd(&cnt[idx[i]], 1);
+}
+
+__global__ void k_iota_u32(uint32_t* __restrict__ keys, const int32_t* __restrict__ src, int32_t* __restrict__ val,
+                           int64_t n) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+    keys[i] = (uint32_t)src[i];
+    val[i] = (int32_t)i;
+  }
+}
+
+// A_v = sum over incident corners in face order of A_f / 3 (mesh.hpp:222-224)
+__global__ void k_vertex_area(const int32_t* __restrict__ vc_off, const int32_t* __restrict__ vc_corner,
+                              const double* __restrict__ face_area, int64_t nv, double* __restrict__ va) {
+  for (int64_t v = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; v < nv; v += (int64_t)gridDim.x * blockDim.x) {
+    double s = 0.0;
+    for (int32_t i = vc_off[v]; i < vc_off[v + 1]; ++i) s += face_area[vc_corner[i] / 3] / 3.0;
+    va[v] = s;
+  }
+}
+
+// CSR entries: (row * nv + neighbour, edge) for both directions (mesh.hpp:234-249)
+__global__ void k_vv_keys(const int32_t* __restrict__ edge_v, int64_t ne, uint64_t nv, uint64_t* __restrict__ key,
+                          int32_t* __restrict__ val, int32_t* __restrict__ degree) {
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < ne; e += (int64_t)gridDim.x * blockDim.x) {
+    const uint64_t a = (uint64_t)edge_v[2 * e], b = (uint64_t)edge_v[2 * e + 1];
+    key[2 * e] = a * nv + b;
+    val[2 * e] = (int32_t)e;
+    key[2 * e + 1] = b * nv + a;
+    val[2 * e + 1] = (int32_t)e;
+    atomicAdd(&degree[a], 1);
+    atomicAdd(&degree[b], 1);
+  }
+}
+
+__global__ void k_vv_fill(const uint64_t* __restrict__ key, const int32_t* __restrict__ val, int64_t n, uint64_t nv,
+                          const double* __restrict__ edge_w, int32_t* __restrict__ vv_index,
+                          int32_t* __restrict__ vv_edge, double* __restrict__ vv_w) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+    vv_index[i] = (int32_t)(key[i] % nv);
+    vv_edge[i] = val[i];
+    vv_w[i] = edge_w[val[i]];
+  }
+}
+
+// sequential row sums (mesh.hpp:267-270)
+__global__ void k_row_sum(const int32_t* __restrict__ off, const double* __restrict__ w, int64_t nv,
+                          double* __restrict__ out) {
+  for (int64_t v = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; v < nv; v += (int64_t)gridDim.x * blockDim.x) {
+    double s = 0.0;
+    for (int32_t i = off[v]; i < off[v + 1]; ++i) s += w[i];
+    out[v] = s;
+  }
+}
+
+__global__ void k_boundary_count(const uint8_t* __restrict__ f, int64_t n, double* __restrict__ part) {
+  double s = 0.0;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+    s += f[i];
+  s = block_sum<B>(s);
+  if (threadIdx.x == 0) part[blockIdx.x] = s;
+}
+
+// per-edge length partials for average_edge_length (mesh.hpp:289-293)
+__global__ void k_edge_len_partial(const double* __restrict__ pos, const int32_t* __restrict__ edge_v, int64_t ne,
+                                   double* __restrict__ part) {
+  double s = 0.0;
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < ne; e += (int64_t)gridDim.x * blockDim.x)
+    s += norm(sub(ld3(pos, edge_v[2 * e + 1]), ld3(pos, edge_v[2 * e])));
+  s = block_sum<B>(s);
+  if (threadIdx.x == 0) part[blockIdx.x] = s;
+}
+
+__global__ void k_reduce_final(const double* __restrict__ part, int n, double* __restrict__ out) {
+  // one block of 1024 threads, fixed tree => reproducible
+  __shared__ double sh[1024];
+  double s = 0.0;
+  for (int i = threadIdx.x; i < n; i += 1024) s += part[i];
+  sh[threadIdx.x] = s;
+  __syncthreads();
+  for (int k = 512; k > 0; k >>= 1) {
+    if (threadIdx.x < k) sh[threadIdx.x] += sh[threadIdx.x + k];
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) out[0] = sh[0];
+}
+
+// face_gradient (mesh.hpp:314-327)
+__global__ void k_face_gradient(const double* __restrict__ pos, const int32_t* __restrict__ faces,
+                                const double* __restrict__ normal, const double* __restrict__ area,
+                                const double* __restrict__ u, int64_t nf, double* __restrict__ grad) {
+  for (int64_t f = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; f < nf; f += (int64_t)gridDim.x * blockDim.x) {
+    const int32_t t[3] = {faces[3 * f], faces[3 * f + 1], faces[3 * f + 2]};
+    const v3 n = ld3(normal, f);
+    v3 g = mk(0.0, 0.0, 0.0);
+    for (int k = 0; k < 3; ++k) {
+      v3 opp = sub(ld3(pos, t[(k + 2) % 3]), ld3(pos, t[(k + 1) % 3]));
+      g = add(g, scale(u[t[k]], cross(n, opp)));
+    }
+    st3(grad, f, divs(g, 2.0 * area[f]));
+  }
+}
+
+int bits_for(uint64_t maxval) {
+  int b = 1;
+  while (b < 64 && (maxval >> b) != 0) ++b;
+  return b;
+}
+
+template <class K>
+void radix_sort_pairs(K*& keys, K*& keys_alt, int32_t*& vals, int32_t*& vals_alt, int64_t n, int end_bit,
+                      cudaStream_t s) {
+  cub::DoubleBuffer<K> kb(keys, keys_alt);
+  cub::DoubleBuffer<int32_t> vb(vals, vals_alt);
+  size_t tmp = 0;
+  GH_CUDA(cub::DeviceRadixSort::SortPairs(nullptr, tmp, kb, vb, (int)n, 0, end_bit, s));
+  gh::Scratch<char> t(tmp, s);
+  GH_CUDA(cub::DeviceRadixSort::SortPairs(t.p, tmp, kb, vb, (int)n, 0, end_bit, s));
+  if (kb.Current() != keys) std::swap(keys, keys_alt);
+  if (vb.Current() != vals) std::swap(vals, vals_alt);
+}
+
+void exclusive_scan(const int32_t* in, int32_t* out, int64_t n, cudaStream_t s) {
+  size_t tmp = 0;
+  GH_CUDA(cub::DeviceScan::ExclusiveSum(nullptr, tmp, in, out, (int)n, s));
+  gh::Scratch<char> t(tmp, s);
+  GH_CUDA(cub::DeviceScan::ExclusiveSum(t.p, tmp, in, out, (int)n, s));
+}
+
+template <class T>
+T read_scalar(const T* d, cudaStream_t s) {
+  T v;
+  GH_CUDA(cudaMemcpyAsync(&v, d, sizeof(T), cudaMemcpyDeviceToHost, s));
+  GH_CUDA(cudaStreamSynchronize(s));
+  return v;
+}
+
+// Host restatement of one face's checks, only to word the error message of the
+// first failing face exactly like mesh.hpp:133-142 (std::to_string = "%f").
+std::string face_error(const double* P, const int32_t* Fc, int64_t f, int32_t nv, double degenerate) {
+  const int32_t* t = Fc + 3 * f;
+  for (int k = 0; k < 3; ++k)
+    if (t[k] < 0 || t[k] >= nv) return "face " + std::to_string(f) + ": vertex index out of range";
+  if (t[0] == t[1] || t[1] == t[2] || t[0] == t[2])
+    return "face " + std::to_string(f) + ": repeated vertex (degenerate face)";
+  auto L = [&](int32_t i, int k) { return P[3 * (int64_t)i + k]; };
+  double ux = L(t[1], 0) - L(t[0], 0), uy = L(t[1], 1) - L(t[0], 1), uz = L(t[1], 2) - L(t[0], 2);
+  double vx = L(t[2], 0) - L(t[0], 0), vy = L(t[2], 1) - L(t[0], 1), vz = L(t[2], 2) - L(t[0], 2);
+  double nx = uy * vz - uz * vy, ny = uz * vx - ux * vz, nz = ux * vy - uy * vx;
+  double area = 0.5 * std::sqrt((nx * nx + ny * ny) + nz * nz);
+  (void)degenerate;
+  return "face " + std::to_string(f) + ": degenerate (area " + std::to_string(area) + ")";
+}
+
+}  // namespace
+
+uint64_t gh_mesh::device_bytes() const {
+  return pos.bytes() + face_area.bytes() + face_normal.bytes() + vertex_area.bytes() + he_cot.bytes() +
+         edge_weight.bytes() + vertex_weight_sum.bytes() + vv_weight.bytes() + faces.bytes() + he_twin.bytes() +
+         he_edge.bytes() + edge_v.bytes() + edge_he.bytes() + interior_edges.bytes() + interior_edge_index.bytes() +
+         vv_offset.bytes() + vv_index.bytes() + vv_edge.bytes() + vc_offset.bytes() + vc_corner.bytes() +
+         on_boundary.bytes() + partials.bytes() + scalars.bytes();
+}
+
+namespace gh {
+
+void reduce_partials(gh_mesh* m, double* d_result_slot) {
+  k_reduce_final<<<1, 1024, 0, m->stream>>>(m->partials.p, kReduceGrid, d_result_slot);
+  GH_LAUNCH_CHECK();
+  m->launches++;
+}
+
+void mesh_build(gh_mesh* m, const double* h_pos, const int32_t* h_faces) {
+  cudaStream_t s = m->stream;
+  const int64_t V = m->nv, F = m->nf, H = 3 * F;
+  const uint64_t nvu = (uint64_t)(V > 0 ? V : 1);
+  m->partials.alloc(kReduceGrid * 6, s);
+  m->scalars.alloc(16, s);
+  m->pos.alloc(3 * V, s);
+  m->faces.alloc(3 * F, s);
+  if (V) GH_CUDA(cudaMemcpyAsync(m->pos.p, h_pos, sizeof(double) * 3 * V, cudaMemcpyHostToDevice, s));
+  if (F) GH_CUDA(cudaMemcpyAsync(m->faces.p, h_faces, sizeof(int32_t) * 3 * F, cudaMemcpyHostToDevice, s));
+
+  // bbox -> degenerate threshold
+  const unsigned gb = grid_for(V, B, 512);
+  k_bbox_partial<<<gb, B, 0, s>>>(m->pos.p, V, m->partials.p);
+  k_bbox_final<<<1, 32, 0, s>>>(m->partials.p, (int)gb, V, m->scalars.p);
+  GH_LAUNCH_CHECK();
+
+  // faces
+  m->face_area.alloc(F, s);
+  m->face_normal.alloc(3 * F, s);
+  Scratch<int32_t> err_face(1, s);
+  const int32_t big = 0x7fffffff;
+  GH_CUDA(cudaMemcpyAsync(err_face.p, &big, sizeof(int32_t), cudaMemcpyHostToDevice, s));
+  if (F) {
+    k_faces<<<grid_for(F), B, 0, s>>>(m->pos.p, m->faces.p, F, m->nv, m->scalars.p, m->face_area.p,
+                                      m->face_normal.p, err_face.p);
+    GH_LAUNCH_CHECK();
+  }
+  const int32_t bad_face = read_scalar(err_face.p, s);
+  if (bad_face != big) fail(GH_ERR_MESH, face_error(h_pos, h_faces, bad_face, m->nv, 0.0));
+  m->launches += 3;
+
+  // edges: stable radix sort of halfedge keys
+  const int end_bit = bits_for(nvu * nvu - 1 > 0 ? nvu * nvu - 1 : 1);
+  int64_t E = 0;
+  m->he_twin.alloc(H, s);
+  m->he_edge.alloc(H, s);
+  GH_CUDA(cudaMemsetAsync(m->he_twin.p, 0xff, sizeof(int32_t) * H, s));
+  GH_CUDA(cudaMemsetAsync(m->he_edge.p, 0xff, sizeof(int32_t) * H, s));
+  {
+    Scratch<uint64_t> k0(H, s), k1(H, s);
+    Scratch<int32_t> v0(H, s), v1(H, s);
+    uint64_t *ka = k0.p, *kb = k1.p;
+    int32_t *va = v0.p, *vb = v1.p;
+    if (H) {
+      k_he_keys<<<grid_for(H), B, 0, s>>>(m->faces.p, H, nvu, ka, va);
+      GH_LAUNCH_CHECK();
+      radix_sort_pairs(ka, kb, va, vb, H, end_bit, s);
+    }
+    Scratch<int32_t> flag(H + 1, s), eid(H + 1, s);
+    if (H) {
+      k_heads<<<grid_for(H), B, 0, s>>>(ka, H, flag.p);
+      GH_LAUNCH_CHECK();
+      exclusive_scan(flag.p, eid.p, H, s);
+      int32_t last_id = read_scalar(eid.p + H - 1, s), last_flag = read_scalar(flag.p + H - 1, s);
+      E = (int64_t)last_id + last_flag;
+    }
+    m->ne = (int32_t)E;
+    m->edge_v.alloc(2 * E, s);
+    m->edge_he.alloc(2 * E, s);
+    if (E) {
+      Scratch<int32_t> start(E, s);
+      k_edge_starts<<<grid_for(H), B, 0, s>>>(flag.p, eid.p, H, start.p);
+      Scratch<unsigned long long> err_edge(1, s);
+      const unsigned long long none = ~0ull;
+      GH_CUDA(cudaMemcpyAsync(err_edge.p, &none, sizeof(none), cudaMemcpyHostToDevice, s));
+      k_edges<<<grid_for(E), B, 0, s>>>(ka, va, start.p, E, H, nvu, m->faces.p, m->edge_v.p, m->edge_he.p,
+                                        m->he_edge.p, m->he_twin.p, err_edge.p);
+      GH_LAUNCH_CHECK();
+      const unsigned long long ee = read_scalar(err_edge.p, s);
+      if (ee != none) {
+        const int64_t e = (int64_t)(ee >> 32);
+        const int code = (int)((ee >> 24) & 0xff);
+        const long long inc = (long long)(ee & 0xffffff);
+        int32_t ev[2];
+        GH_CUDA(cudaMemcpyAsync(ev, m->edge_v.p + 2 * e, sizeof(ev), cudaMemcpyDeviceToHost, s));
+        GH_CUDA(cudaStreamSynchronize(s));
+        const std::string pair = "(" + std::to_string(ev[0]) + "," + std::to_string(ev[1]) + ")";
+        if (code == 1) fail(GH_ERR_MESH, "non-manifold edge " + pair + ": " + std::to_string(inc) + " incident faces");
+        fail(GH_ERR_MESH, "inconsistent winding across edge " + pair);
+      }
+      m->launches += 4;
+    }
+  }
+
+  // interior edges (mesh.hpp:194-201)
+  {
+    Scratch<int32_t> flag(E + 1, s), idx(E + 1, s);
+    int32_t ni = 0;
+    m->interior_edge_index.alloc(E, s);
+    if (E) {
+      k_interior_flag<<<grid_for(E), B, 0, s>>>(m->edge_he.p, E, flag.p);
+      exclusive_scan(flag.p, idx.p, E, s);
+      ni = read_scalar(idx.p + E - 1, s) + read_scalar(flag.p + E - 1, s);
+    }
+    m->ni = ni;
+    m->interior_edges.alloc(ni, s);
+    if (E) {
+      k_interior_fill<<<grid_for(E), B, 0, s>>>(flag.p, idx.p, E, m->interior_edges.p, m->interior_edge_index.p);
+      GH_LAUNCH_CHECK();
+      m->launches += 3;
+    }
+  }
+
+  // cotangents, weights, boundary flags
+  m->he_cot.alloc(H, s);
+  m->edge_weight.alloc(E, s);
+  m->on_boundary.alloc(V, s);
+  if (V) GH_CUDA(cudaMemsetAsync(m->on_boundary.p, 0, V, s));
+  if (F) k_cot<<<grid_for(F), B, 0, s>>>(m->pos.p, m->faces.p, F, m->he_cot.p);
+  if (E) k_edge_weight<<<grid_for(E), B, 0, s>>>(m->edge_he.p, m->edge_v.p, m->he_cot.p, E, m->edge_weight.p,
+                                                  m->on_boundary.p);
+  GH_LAUNCH_CHECK();
+  m->launches += 2;
+
+  // vertex -> corner CSR (mesh.hpp:272-283) and vertex areas (222-224)
+  m->vc_offset.alloc(V + 1, s);
+  m->vc_corner.alloc(H, s);
+  m->vertex_area.alloc(V, s);
+  {
+    Scratch<int32_t> cnt(V + 1, s);
+    GH_CUDA(cudaMemsetAsync(cnt.p, 0, sizeof(int32_t) * (V + 1), s));
+    if (H) k_count_i32<<<grid_for(H), B, 0, s>>>(m->faces.p, H, cnt.p);
+    exclusive_scan(cnt.p, m->vc_offset.p, V + 1, s);
+    Scratch<uint32_t> k0(H, s), k1(H, s);
+    Scratch<int32_t> v1(H, s);
+    uint32_t *ka = k0.p, *kb = k1.p;
+    int32_t *va = m->vc_corner.p, *vb = v1.p;
+    if (H) {
+      k_iota_u32<<<grid_for(H), B, 0, s>>>(ka, m->faces.p, va, H);
+      GH_LAUNCH_CHECK();
+      radix_sort_pairs(ka, kb, va, vb, H, bits_for(nvu), s);
+      if (va != m->vc_corner.p) GH_CUDA(cudaMemcpyAsync(m->vc_corner.p, va, sizeof(int32_t) * H, cudaMemcpyDeviceToDevice, s));
+    }
+    if (V) k_vertex_area<<<grid_for(V), B, 0, s>>>(m->vc_offset.p, m->vc_corner.p, m->face_area.p, V, m->vertex_area.p);
+    GH_LAUNCH_CHECK();
+    m->launches += 3;
+  }
+
+  // vertex adjacency CSR, rows sorted by neighbour (mesh.hpp:234-266) + row sums (267-270)
+  m->vv_offset.alloc(V + 1, s);
+  m->vv_index.alloc(2 * E, s);
+  m->vv_edge.alloc(2 * E, s);
+  m->vv_weight.alloc(2 * E, s);
+  m->vertex_weight_sum.alloc(V, s);
+  {
+    Scratch<int32_t> degree(V + 1, s);
+    GH_CUDA(cudaMemsetAsync(degree.p, 0, sizeof(int32_t) * (V + 1), s));
+    Scratch<uint64_t> k0(2 * E, s), k1(2 * E, s);
+    Scratch<int32_t> v0(2 * E, s), v1(2 * E, s);
+    uint64_t *ka = k0.p, *kb = k1.p;
+    int32_t *va = v0.p, *vb = v1.p;
+    if (E) {
+      k_vv_keys<<<grid_for(E), B, 0, s>>>(m->edge_v.p, E, nvu, ka, va, degree.p);
+      GH_LAUNCH_CHECK();
+      radix_sort_pairs(ka, kb, va, vb, 2 * E, end_bit, s);
+    }
+    exclusive_scan(degree.p, m->vv_offset.p, V + 1, s);
+    if (E) {
+      k_vv_fill<<<grid_for(2 * E), B, 0, s>>>(ka, va, 2 * E, nvu, m->edge_weight.p, m->vv_index.p, m->vv_edge.p,
+                                               m->vv_weight.p);
+      GH_LAUNCH_CHECK();
+    }
+    if (V) k_row_sum<<<grid_for(V), B, 0, s>>>(m->vv_offset.p, m->vv_weight.p, V, m->vertex_weight_sum.p);
+    GH_LAUNCH_CHECK();
+    m->launches += 3;
+  }
+
+  // boundary vertex count (for gh_mesh_info)
+  if (V) {
+    k_boundary_count<<<kReduceGrid, B, 0, s>>>(m->on_boundary.p, V, m->partials.p);
+    reduce_partials(m, m->scalars.p + 1);
+    m->boundary_vertices = (int32_t)read_scalar(m->scalars.p + 1, s);
+  }
+  GH_CUDA(cudaStreamSynchronize(s));
+}
+
+double mesh_average_edge_length(gh_mesh* m) {
+  if (m->ne == 0) return NAN;
+  k_edge_len_partial<<<kReduceGrid, B, 0, m->stream>>>(m->pos.p, m->edge_v.p, m->ne, m->partials.p);
+  GH_LAUNCH_CHECK();
+  m->launches++;
+  reduce_partials(m, m->scalars.p + 2);
+  return read_scalar(m->scalars.p + 2, m->stream) / (double)m->ne;
+}
+
+void face_gradient_dev(gh_mesh* m, const double* d_u, double* d_grad) {
+  if (!m->nf) return;
+  k_face_gradient<<<grid_for(m->nf), B, 0, m->stream>>>(m->pos.p, m->faces.p, m->face_normal.p, m->face_area.p, d_u,
+                                                        m->nf, d_grad);
+  GH_LAUNCH_CHECK();
+  m->launches++;
+}
+
+}  // namespace gh
