@@ -1,0 +1,213 @@
+"""Parity of the B200 path with the reference (GPU, through the C ABI).
+
+Bar: bit-identical per-element results (TriMesh arrays, BFS levels/parents/
+rings, u, H, zero_count, G, X, distances) against the golden fixtures made by
+the unmodified reference and against the C oracle on the same seeded inputs;
+ADMM iteration counts and stop decisions identical, residual histories within
+1e-12 relative (the device sums in a fixed tree order, the reference left to
+right). Full-size configs are covered by reduced-sweep bitwise runs and by
+size-independent properties (determinism, maximum principle, BFS invariants).
+"""
+import glob
+import json
+import os
+import subprocess
+
+import numpy as np
+import pytest
+
+from conftest import GOLDEN, ROOT
+from oracle.oracle import ARRAYS
+
+pytestmark = pytest.mark.gpu
+
+CASES = sorted(os.path.basename(p)[:-4] for p in glob.glob(os.path.join(GOLDEN, "*.npz")))
+INDEX = json.load(open(os.path.join(GOLDEN, "index.json")))
+RESIDUAL_RTOL = 1e-12
+
+
+def bits(a):
+    a = np.ascontiguousarray(a)
+    return a.view(np.uint64) if a.dtype == np.float64 else a
+
+
+def assert_same(a, b, what=""):
+    a, b = np.asarray(a), np.asarray(b)
+    assert a.shape == b.shape, (what, a.shape, b.shape)
+    if not np.array_equal(bits(a.ravel()), bits(b.ravel())):
+        diff = np.flatnonzero(bits(a.ravel()) != bits(b.ravel()))
+        raise AssertionError(f"{what}: {diff.size} elements differ, first at {diff[:5]}")
+
+
+def check_history(got, want, what):
+    assert len(got) == len(want), what
+    for g, w in zip(got, want):
+        assert g == pytest.approx(w, rel=RESIDUAL_RTOL, abs=1e-300), what
+
+
+@pytest.mark.parametrize("case", CASES)
+def test_golden_case_bitwise(gpu, case):
+    gh = gpu
+    g = np.load(os.path.join(GOLDEN, case + ".npz"))
+    mesh = gh.build_mesh(g["positions"], g["faces"])
+    for name, _ in ARRAYS:
+        assert_same(mesh.download(name).ravel(), g["mesh_" + name].ravel(), name)
+    lv = gh.bfs_levels(mesh, g["sources"])
+    assert_same(lv.level_of_vertex, g["level_of_vertex"], "level")
+    assert_same(lv.parent_of_vertex, g["parent_of_vertex"], "parent")
+    assert_same(lv.order, g["order"], "rings")
+    assert_same(lv.offsets, g["offsets"], "ring offsets")
+    assert lv.unreachable_count == int(g["unreachable"])
+    t, sweeps, iters = float(g["t"]), int(g["sweeps"]), int(g["admm_iters"])
+    assert gh.average_edge_length(mesh) == pytest.approx(float(g["avg_edge_length"]), rel=1e-13)
+    u = gh.gs_diffuse(mesh, lv, t, gh.DiffusionConfig(sweeps=sweeps))
+    assert_same(u, g["u"], "u")
+    nh = gh.normalized_target_gradients(mesh, u)
+    assert_same(nh.field, g["H"], "H")
+    assert nh.zero_count == int(g["zero_count"])
+    cfg = gh.AdmmConfig(max_iterations=iters)
+    fr = gh.admm_face_optimize(mesh, g["H"], cfg)
+    er = gh.admm_edge_optimize(mesh, g["H"], cfg)
+    for tag, r, field, key in (("face", fr, fr.gradients, "G"), ("edge", er, er.differences, "X")):
+        assert r.report.iterations == int(g[f"{tag}_iterations"]), tag
+        assert r.report.converged == bool(g[f"{tag}_converged"]), tag
+        check_history(r.report.primal_history, g[f"{tag}_primal"], tag + " primal")
+        check_history(r.report.dual_history, g[f"{tag}_dual"], tag + " dual")
+        assert r.report.state_bytes_formula == int(g[f"{tag}_state_bytes_formula"])
+        assert_same(field, g[key], key)
+    d_face = gh.integrate_face_gradients(mesh, lv, g["G"])
+    d_edge = gh.integrate_edge_differences(mesh, lv, g["X"])
+    assert_same(d_face, g["d_face"], "d_face")
+    assert_same(d_edge, g["d_edge"], "d_edge")
+    assert gh.field_hash(d_face) == int(g["hash_d_face"])
+    if "u_warm3" in g:
+        u2 = gh.gs_diffuse(mesh, lv, t, gh.DiffusionConfig(sweeps=3), initial=u)
+        assert_same(u2, g["u_warm3"], "warm start")
+    e1 = gh.diffusion_residual(mesh, u, t, g["sources"], levels=lv)
+    assert e1 == pytest.approx(float(g["e1"]), rel=1e-12, abs=1e-300)
+    # the fused device-resident chain equals the stage-by-stage results
+    for method, key in (("face", "d_face"), ("edge", "d_edge")):
+        d, rep = gh.distance(lv, method, sweeps, t, admm=cfg)
+        assert_same(d, g[key], "fused " + method)
+        assert rep.zero_count == int(g["zero_count"])
+
+
+@pytest.mark.parametrize("name", sorted(INDEX["errors"]))
+def test_mesh_errors_match_reference(gpu, name):
+    e = INDEX["errors"][name]
+    with pytest.raises(gpu.MeshError) as info:
+        gpu.build_mesh(np.asarray(e["positions"], float), np.asarray(e["faces"], np.int32))
+    assert str(info.value) == e["message"]
+
+
+def test_invalid_arguments(gpu):
+    gh = gpu
+    g = np.load(os.path.join(GOLDEN, "unit_square.npz"))
+    mesh = gh.build_mesh(g["positions"], g["faces"])
+    with pytest.raises(ValueError, match="empty source set"):
+        gh.bfs_levels(mesh, [])
+    with pytest.raises(ValueError, match="out of range"):
+        gh.bfs_levels(mesh, [9])
+    lv = gh.bfs_levels(mesh, [0])
+    with pytest.raises(ValueError, match="t must be positive"):
+        gh.gs_diffuse(mesh, lv, 0.0, gh.DiffusionConfig(sweeps=1))
+    with pytest.raises(ValueError, match="mu must be positive"):
+        gh.admm_face_optimize(mesh, g["H"], gh.AdmmConfig(mu=0.0))
+    with pytest.raises(ValueError, match="m must be positive"):
+        gh.diffusion_time(mesh, -1.0)
+
+
+def _oracle_chain(o, w, sweeps, t):
+    mesh = o.build_mesh(w.positions, w.faces)
+    lv = mesh.bfs(w.sources)
+    if t is None:
+        t = mesh.diffusion_time(w.m)
+    u, _ = mesh.gs_diffuse(lv, t, sweeps)
+    H, zc = mesh.normalized_target_gradients(u)
+    G, fr = mesh.admm_face(H)
+    X, er = mesh.admm_edge(H)
+    return dict(t=t, level=lv.level_of_vertex, parent=lv.parent_of_vertex, u=u, H=H, zc=zc, G=G, X=X, fr=fr, er=er,
+                d_face=mesh.integrate_face(lv, G), d_edge=mesh.integrate_edge(lv, X))
+
+
+@pytest.mark.parametrize("config,scale,sweeps", [(2, 8, 400), (3, 16, 300), (4, 64, 200), (5, 128, 200)])
+def test_configs_reduced_size_vs_oracle(gpu, port_oracle, config, scale, sweeps):
+    """BASELINE configs 2-5 at reduced linear size, every stage bitwise vs the C oracle."""
+    from paper_1812_06060_b200 import meshgen
+    gh = gpu
+    w = meshgen.config(config, scale=scale)
+    ref = _oracle_chain(port_oracle, w, sweeps, w.t)
+    mesh = gh.build_mesh(w.positions, w.faces)
+    lv = gh.bfs_levels(mesh, w.sources)
+    assert_same(lv.level_of_vertex, ref["level"], "level")
+    assert_same(lv.parent_of_vertex, ref["parent"], "parent")
+    u = gh.gs_diffuse(mesh, lv, ref["t"], gh.DiffusionConfig(sweeps=sweeps))
+    assert_same(u, ref["u"], "u")
+    for method, key in (("face", "d_face"), ("edge", "d_edge")):
+        d, rep = gh.distance(lv, method, sweeps, ref["t"])
+        assert_same(d, ref[key], f"C{config} {method} distances")
+        r = ref["fr"] if method == "face" else ref["er"]
+        assert rep.admm_iterations == r.iterations and rep.converged == r.converged
+        assert rep.zero_count == ref["zc"]
+
+
+def test_config1_full_with_device_t(gpu, port_oracle):
+    """Config 1 end to end with t from the device mean edge length: distances agree
+    with the reference within 1e-9 relative (t differs from the reference's
+    sequential sum by a few ulps) and the error vs the great-circle geodesic
+    equals the reference's."""
+    from paper_1812_06060_b200 import meshgen
+    gh = gpu
+    w = meshgen.config(1)
+    g = np.load(os.path.join(GOLDEN, "icosphere5_config1.npz"))
+    d, rep = gh.distance_host(w.positions, w.faces, w.sources, "face", 1000, None, 1.0)
+    assert rep.t == pytest.approx(float(g["t"]), rel=1e-13)
+    np.testing.assert_allclose(d, g["d_face"], rtol=1e-9, atol=0)
+    P = w.positions
+    exact = np.arccos(np.clip(P @ P[0] / (np.linalg.norm(P, axis=1) * np.linalg.norm(P[0])), -1, 1))
+    mask = np.arange(len(d)) != 0
+    eps_gpu = np.sum(np.abs(d[mask] - exact[mask]) / exact[mask]) / len(d)
+    eps_ref = np.sum(np.abs(g["d_face"][mask] - exact[mask]) / exact[mask]) / len(d)
+    assert eps_gpu == pytest.approx(eps_ref, rel=1e-9)
+    assert eps_ref == pytest.approx(0.047449, rel=1e-4)  # eps_face = 4.7449 %
+
+
+@pytest.mark.slow
+def test_config3_full_size_properties(gpu, port_oracle):
+    """Config 3 at full size (8.4M vertices): mesh + BFS bitwise vs the oracle,
+    3 sweeps bitwise, and the full 1000-sweep solve deterministic and inside
+    the maximum-principle bound 0 <= u <= 1/min A_s (test_diffusion.cpp:92-109)."""
+    from paper_1812_06060_b200 import meshgen
+    gh = gpu
+    w = meshgen.config(3)
+    om = port_oracle.build_mesh(w.positions, w.faces)
+    ol = om.bfs(w.sources)
+    mesh = gh.build_mesh(w.positions, w.faces)
+    lv = gh.bfs_levels(mesh, w.sources)
+    for name in ("edge_vertices", "vv_index", "vv_weight", "vertex_area", "vertex_weight_sum"):
+        assert_same(mesh.download(name).ravel(), om.array(name), name)
+    assert_same(lv.level_of_vertex, ol.level_of_vertex, "level")
+    assert_same(lv.parent_of_vertex, ol.parent_of_vertex, "parent")
+    t = om.diffusion_time(1.0)
+    u3, _ = om.gs_diffuse(ol, t, 3)
+    assert_same(gh.gs_diffuse(mesh, lv, t, gh.DiffusionConfig(sweeps=3)), u3, "u after 3 sweeps")
+    a = gh.gs_diffuse(mesh, lv, t, gh.DiffusionConfig(sweeps=1000))
+    b = gh.gs_diffuse(mesh, lv, t, gh.DiffusionConfig(sweeps=1000))
+    assert_same(a, b, "determinism")
+    va = om.array("vertex_area")
+    assert a.min() >= 0.0 and a.max() <= 1.0 / va[w.sources].min() * (1 + 1e-12)
+
+
+def test_cpp_wrapper_runs_reference_chain(gpu):
+    """The C++ drop-in (include/geoheat_b200.hpp) reproduces the reference's config-1 hashes."""
+    from paper_1812_06060_b200 import _build
+    exe = os.path.join(_build.LIBDIR, "wrapper_parity")
+    if not os.path.exists(exe):
+        src = os.path.join(ROOT, "tests", "cpp", "wrapper_parity.cpp")
+        _build.build_meshgen()
+        subprocess.run(["g++", "-std=c++20", "-O2", "-I", os.path.join(ROOT, "include"), src, "-o", exe, "-L",
+                        _build.LIBDIR, "-lgeoheat_b200", "-lgh_meshgen", f"-Wl,-rpath,{_build.LIBDIR}"], check=True)
+    t = float(np.load(os.path.join(GOLDEN, "icosphere5_config1.npz"))["t"])
+    r = subprocess.run([exe, t.hex()], capture_output=True, text=True, timeout=300)
+    assert r.returncode == 0, r.stdout + r.stderr
+    assert "PASS" in r.stdout
