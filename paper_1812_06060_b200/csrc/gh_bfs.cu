@@ -260,17 +260,15 @@ void bfs_build(gh_levels* L, const int32_t* h_sources, int32_t ns) {
   // ---- diffusion layout: (parity, level, index) row order, SELL-32
   L->h_pstart.assign(nlev, 0);
   L->h_pend.assign(nlev, 0);
+  // every level starts on a 32-row chunk boundary, even levels first
   int64_t cursor = 0;
-  for (int32_t l = 0; l < nlev; l += 2) {
-    L->h_pstart[l] = (int32_t)cursor;
-    cursor += sizes[l];
-    L->h_pend[l] = (int32_t)cursor;
-  }
-  cursor = (cursor + 31) & ~int64_t(31);
-  for (int32_t l = 1; l < nlev; l += 2) {
-    L->h_pstart[l] = (int32_t)cursor;
-    cursor += sizes[l];
-    L->h_pend[l] = (int32_t)cursor;
+  for (int p = 0; p < 2; ++p) {
+    for (int32_t l = p; l < nlev; l += 2) {
+      cursor = (cursor + 31) & ~int64_t(31);
+      L->h_pstart[l] = (int32_t)cursor;
+      cursor += sizes[l];
+      L->h_pend[l] = (int32_t)cursor;
+    }
   }
   cursor = (cursor + 31) & ~int64_t(31);
   if (cursor > 0x7fffffffLL) fail(GH_ERR_INVALID, "mesh too large for the diffusion layout");
@@ -307,6 +305,14 @@ void bfs_build(gh_levels* L, const int32_t* h_sources, int32_t ns) {
     GH_CUDA(cub::DeviceScan::ExclusiveSum(t.p, tmp, width.p, L->chunk_ptr.p, L->nchunks + 1, s));
   }
   const int64_t nnz_padded = read_scalar(L->chunk_ptr.p + L->nchunks, s);
+  {
+    std::vector<int64_t> cp(L->nchunks + 1);
+    GH_CUDA(cudaMemcpyAsync(cp.data(), L->chunk_ptr.p, sizeof(int64_t) * cp.size(), cudaMemcpyDeviceToHost, s));
+    GH_CUDA(cudaStreamSynchronize(s));
+    int64_t wmax = 0;
+    for (int32_t c = 0; c < L->nchunks; ++c) wmax = std::max(wmax, (cp[c + 1] - cp[c]) / 32);
+    L->max_chunk_width = (int32_t)wmax;
+  }
   L->col.alloc(nnz_padded, s);
   L->wt.alloc(nnz_padded, s);
   if (nnz_padded) {
@@ -320,6 +326,7 @@ void bfs_build(gh_levels* L, const int32_t* h_sources, int32_t ns) {
                                                L->chunk_ptr.p, L->nrows, L->col.p, L->wt.p, L->area_r.p, L->wsum_r.p);
   GH_LAUNCH_CHECK();
   L->den.alloc(L->nrows, s);
+  L->counter.alloc(1, s);
   L->ubuf.alloc(2 * (size_t)L->nrows, s);
   L->u_orig.alloc(V, s);
   L->den_t = 0.0;

@@ -19,6 +19,8 @@
 #include <cooperative_groups.h>
 
 #include <algorithm>
+#include <cstdlib>
+#include <string>
 
 #include "gh_internal.cuh"
 
@@ -28,6 +30,7 @@ namespace {
 
 constexpr int B = gh::kBlock;
 constexpr int kMaxSmemLevels = 12 * 1024;  // pend table in shared memory (48 KB)
+constexpr int kUnroll = 8;                  // rows up to this valence take the unrolled path
 
 __global__ void k_den(const double* __restrict__ area, const double* __restrict__ wsum, double t, int64_t n,
                       double* __restrict__ den) {
@@ -112,18 +115,295 @@ __global__ void __launch_bounds__(B) k_diffuse_pipelined(DiffuseArgs a) {
         const double* prev = a.ubuf + ((sweep & 1) ^ 1) * a.nrows;
         const int32_t d = __ldg(a.deg + r);
         const int64_t base = __ldg(a.chunk_ptr + c) + lane;
+        const double den = __ldg(a.den + r);
         double num = 0.0;
-        for (int32_t k = 0; k < d; ++k) {
-          const int32_t cc = __ldg(a.col + base + 32 * (int64_t)k);
-          const double w = __ldg(a.wt + base + 32 * (int64_t)k);
-          const double* src = cc < 0 ? cur : prev;
-          num += w * __ldcg(src + (cc & 0x7fffffff));  // diffusion.hpp:79
+        if (d <= kUnroll) {
+          // all column/weight loads, then all gathers, then the row sum in the
+          // reference's order: two dependent memory round trips per row
+          int32_t cc[kUnroll];
+          double w[kUnroll], v[kUnroll];
+#pragma unroll
+          for (int k = 0; k < kUnroll; ++k)
+            if (k < d) {
+              cc[k] = __ldg(a.col + base + 32 * k);
+              w[k] = __ldg(a.wt + base + 32 * k);
+            }
+#pragma unroll
+          for (int k = 0; k < kUnroll; ++k)
+            if (k < d) v[k] = __ldcg((cc[k] < 0 ? cur : prev) + (cc[k] & 0x7fffffff));
+#pragma unroll
+          for (int k = 0; k < kUnroll; ++k)
+            if (k < d) num += w[k] * v[k];  // diffusion.hpp:79
+        } else {
+          for (int32_t k = 0; k < d; ++k) {
+            const int32_t cc = __ldg(a.col + base + 32 * (int64_t)k);
+            const double w = __ldg(a.wt + base + 32 * (int64_t)k);
+            const double* src = cc < 0 ? cur : prev;
+            num += w * __ldcg(src + (cc & 0x7fffffff));  // diffusion.hpp:79
+          }
         }
         const double u0 = L == 0 ? 1.0 : 0.0;
-        __stcg(cur + r, (u0 + t * num) / __ldg(a.den + r));  // diffusion.hpp:82
+        __stcg(cur + r, (u0 + t * num) / den);  // diffusion.hpp:82
       }
     }
     grid.sync();
+  }
+}
+
+
+// ---------------------------------------------------------------- bulk-staged schedule
+// Same step/barrier schedule, but the streamed operands of each 32-row chunk
+// (SELL columns + weights, den, deg: ~86 B of the ~100 B per update) are moved
+// HBM -> shared memory by the bulk-copy engine (cp.async.bulk + mbarrier
+// complete_tx), issued by one producer warp into a ring of chunk slots, while
+// kConsumerWarps warps consume chunks: read the row from shared memory, gather
+// the 6-ish neighbour u values (L2), and store u. The DRAM stream no longer
+// waits behind the gather latency of the warps, so many more bytes are in
+// flight per SM. Rows are still summed in the reference's order (bitwise).
+constexpr int kConsumerWarps = 8;
+constexpr int kTileChunks = kConsumerWarps;  // chunks per ring slot, one per consumer warp
+constexpr int kTmaThreads = 32 * (kConsumerWarps + 1);
+
+struct TmaArgs {
+  const int32_t* pstart;
+  const int32_t* pend;
+  const int32_t* chunk_level;
+  const int64_t* chunk_ptr;
+  const uint16_t* deg;
+  const int32_t* col;
+  const double* wt;
+  const double* den;
+  double* ubuf;
+  int64_t nrows;
+  int32_t nlev, sweeps;
+  int32_t wcap;      // widest chunk (neighbours per row) a slot holds
+  int32_t nslots;    // ring slots per block
+  int32_t slot_bytes;
+  int32_t table_in_smem;
+  int32_t* barrier;  // consumer grid-barrier counter (zeroed per launch)
+  double t;
+};
+
+__device__ __forceinline__ uint32_t smem_u32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
+
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+  asm volatile(
+      "{\n.reg .pred p;\nWAIT_%=:\n"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+      "@!p bra WAIT_%=;\n}" ::"r"(smem_u32(bar)),
+      "r"(parity)
+      : "memory");
+}
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
+  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                   smem_u32(dst)),
+               "l"(src), "r"(bytes), "r"(smem_u32(bar))
+               : "memory");
+}
+
+// contiguous share of the step's chunk range [c0, c1) for block b
+__device__ __forceinline__ void block_share(int64_t c0, int64_t c1, int64_t b, int64_t nb, int64_t& cb,
+                                            int64_t& ce) {
+  const int64_t n = c1 - c0, q = n / nb, rem = n % nb;
+  cb = c0 + b * q + (b < rem ? b : rem);
+  ce = cb + q + (b < rem ? 1 : 0);
+}
+
+__device__ __forceinline__ bool step_range(const TmaArgs& a, const int32_t* pend, int64_t tau, int64_t& rb,
+                                           int64_t& re) {
+  int64_t lhi = tau < a.nlev - 1 ? tau : a.nlev - 1;
+  if ((lhi ^ tau) & 1) --lhi;
+  int64_t llo = tau - 2 * (int64_t)(a.sweeps - 1);
+  if (llo < 0) llo = tau & 1;
+  if (llo > lhi) return false;
+  rb = __ldg(a.pstart + llo);
+  re = pend[lhi];
+  return true;
+}
+
+__device__ __forceinline__ int32_t ld_acquire_gpu(const int32_t* p) {
+  int32_t v;
+  asm volatile("ld.acquire.gpu.global.s32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+
+// Grid barrier among the consumer warps only (the producer warp never waits on
+// it, so it streams the next step's tiles while the grid drains the current
+// one). Monotonic arrival counter: step k completes at (k + 1) * gridDim.x.
+__device__ __forceinline__ void consumer_grid_barrier(int32_t* counter, int64_t k) {
+  asm volatile("bar.sync 1, %0;" ::"r"(32 * kConsumerWarps) : "memory");
+  if (threadIdx.x == 0) {
+    __threadfence();
+    atomicAdd(counter, 1);
+    const int32_t target = (int32_t)((k + 1) * gridDim.x);
+    unsigned ns = 16;
+    while (ld_acquire_gpu(counter) < target) {
+      __nanosleep(ns);
+      if (ns < 128) ns <<= 1;
+    }
+    __threadfence();
+  }
+  asm volatile("bar.sync 1, %0;" ::"r"(32 * kConsumerWarps) : "memory");
+}
+
+// slot layout: header 128 B (int32: chunk offsets [0..8], fits [15], chunk levels [16..23])
+//              | den 8 x 256 B | deg 8 x 64 B | columns | weights
+constexpr int kHdr = 128;
+constexpr int kDenOff = kHdr;
+constexpr int kDegOff = kDenOff + kTileChunks * 256;
+constexpr int kColOff = kDegOff + kTileChunks * 64;
+
+__global__ void __launch_bounds__(kTmaThreads, 3) k_diffuse_tma(TmaArgs a) {
+  extern __shared__ __align__(128) unsigned char smem[];
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem);
+  uint64_t* empty = full + a.nslots;
+  int32_t* sh_pend = reinterpret_cast<int32_t*>(empty + a.nslots);
+  const size_t table_bytes = a.table_in_smem ? ((sizeof(int32_t) * a.nlev + 127) & ~size_t(127)) : 0;
+  unsigned char* slots = reinterpret_cast<unsigned char*>(empty + a.nslots) + table_bytes;
+  slots = reinterpret_cast<unsigned char*>((reinterpret_cast<uintptr_t>(slots) + 127) & ~uintptr_t(127));
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  if (threadIdx.x == 0) {
+    for (int i = 0; i < a.nslots; ++i) {
+      mbar_init(full + i, 1);
+      mbar_init(empty + i, kConsumerWarps);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  const int32_t* pend = a.pend;
+  if (a.table_in_smem) {
+    for (int i = threadIdx.x; i < a.nlev; i += blockDim.x) sh_pend[i] = a.pend[i];
+    pend = sh_pend;
+  }
+  __syncthreads();
+
+  const int64_t nb = gridDim.x, b = blockIdx.x;
+  const int64_t nsteps = (int64_t)(a.nlev - 1) + 2 * (int64_t)(a.sweeps - 1) + 1;
+  const uint32_t col_cap = (uint32_t)kTileChunks * 32u * a.wcap;  // entries
+  // ring position: slot index and its use parity advance tile by tile (no 64-bit modulo)
+  int slot = 0;
+  uint32_t use = 0;
+  int64_t issued = 0;
+
+  if (warp == kConsumerWarps) {
+    // ---- producer warp: runs ahead across steps, bounded by the ring
+    for (int64_t tau = 0; tau < nsteps; ++tau) {
+      int64_t rb, re;
+      if (!step_range(a, pend, tau, rb, re)) continue;
+      int64_t cb, ce;
+      block_share(rb >> 5, (re + 31) >> 5, b, nb, cb, ce);
+      const int64_t ntile = (ce - cb + kTileChunks - 1) / kTileChunks;
+      for (int64_t t0 = 0; t0 < ntile; t0 += 32 / kTileChunks) {
+        // chunk pointers / levels for 32 chunks (4 tiles)
+        const int64_t cbase = cb + t0 * kTileChunks;
+        const int64_t cl = cbase + lane < ce ? cbase + lane : ce;
+        const int64_t p0 = __ldg(a.chunk_ptr + cl);
+        const int32_t lv0 = cbase + lane < ce ? __ldg(a.chunk_level + cl) : 0;
+        const int64_t p_last = __ldg(a.chunk_ptr + (cbase + 32 < ce ? cbase + 32 : ce));
+        for (int j = 0; j < 32 / kTileChunks && t0 + j < ntile; ++j) {
+          if (issued >= a.nslots) mbar_wait(empty + slot, use ^ 1u);
+          const int64_t c0 = cbase + j * kTileChunks;
+          const int nch = (int)(ce - c0 < kTileChunks ? ce - c0 : kTileChunks);
+          const int64_t base = __shfl_sync(0xffffffffu, p0, j * kTileChunks);
+          const int src = j * kTileChunks + (lane <= kTileChunks ? lane : 0);
+          int64_t pi = __shfl_sync(0xffffffffu, p0, src < 32 ? src : 31);
+          const int32_t li = __shfl_sync(0xffffffffu, lv0, (j * kTileChunks + (lane & (kTileChunks - 1))) & 31);
+          if (j * kTileChunks + lane == 32) pi = p_last;
+          int32_t* hdr = reinterpret_cast<int32_t*>(slots + (size_t)slot * a.slot_bytes);
+          if (lane <= nch) hdr[lane] = (int32_t)(pi - base);
+          if (lane < kTileChunks) hdr[16 + lane] = li;
+          const int64_t pend_tile = __shfl_sync(0xffffffffu, pi, nch);
+          const uint32_t ncol = (uint32_t)(pend_tile - base);
+          const bool fits = ncol <= col_cap;
+          if (lane == 0) hdr[15] = fits ? 1 : 0;
+          __syncwarp();
+          if (lane == 0) {
+            unsigned char* sb = reinterpret_cast<unsigned char*>(hdr);
+            const uint32_t bytes = (uint32_t)nch * (256u + 64u) + (fits ? ncol * 12u : 0u);
+            mbar_expect_tx(full + slot, bytes);
+            bulk_g2s(sb + kDenOff, a.den + c0 * 32, (uint32_t)nch * 256u, full + slot);
+            bulk_g2s(sb + kDegOff, a.deg + c0 * 32, (uint32_t)nch * 64u, full + slot);
+            if (fits && ncol) {
+              bulk_g2s(sb + kColOff, a.col + base, ncol * 4u, full + slot);
+              bulk_g2s(sb + kColOff + col_cap * 4u, a.wt + base, ncol * 8u, full + slot);
+            }
+          }
+          __syncwarp();
+          ++issued;
+          if (++slot == a.nslots) {
+            slot = 0;
+            use ^= 1u;
+          }
+        }
+      }
+    }
+    return;
+  }
+
+  // ---- consumer warps: warp w takes chunk w of every tile
+  int64_t nbar = 0;
+  for (int64_t tau = 0; tau < nsteps; ++tau) {
+    int64_t rb, re;
+    if (!step_range(a, pend, tau, rb, re)) continue;
+    int64_t cb, ce;
+    block_share(rb >> 5, (re + 31) >> 5, b, nb, cb, ce);
+    const int64_t ntile = (ce - cb + kTileChunks - 1) / kTileChunks;
+    for (int64_t j = 0; j < ntile; ++j) {
+      mbar_wait(full + slot, use);
+      const unsigned char* sb = slots + (size_t)slot * a.slot_bytes;
+      const int32_t* hdr = reinterpret_cast<const int32_t*>(sb);
+      const int64_t c = cb + j * kTileChunks + warp;
+      const int64_t r = c * 32 + lane;
+      if (c < ce && r >= rb && r < re) {
+        int32_t L = hdr[16 + warp];
+        while (r >= pend[L]) L += 2;
+        const int32_t sweep = (int32_t)((tau - L) >> 1);
+        double* cur = a.ubuf + (sweep & 1) * a.nrows;
+        const double* prev = a.ubuf + ((sweep & 1) ^ 1) * a.nrows;
+        const int32_t off = hdr[warp];
+        const double den = reinterpret_cast<const double*>(sb + kDenOff)[warp * 32 + lane];
+        const int32_t d = reinterpret_cast<const uint16_t*>(sb + kDegOff)[warp * 32 + lane];
+        double num = 0.0;
+        if (hdr[15] && d <= kUnroll) {
+          const int32_t* scol = reinterpret_cast<const int32_t*>(sb + kColOff) + off + lane;
+          const double* swt = reinterpret_cast<const double*>(sb + kColOff + (size_t)col_cap * 4u) + off + lane;
+          double v[kUnroll];
+#pragma unroll
+          for (int k = 0; k < kUnroll; ++k)
+            if (k < d) {
+              const int32_t cc = scol[32 * k];
+              v[k] = __ldcg((cc < 0 ? cur : prev) + (cc & 0x7fffffff));
+            }
+#pragma unroll
+          for (int k = 0; k < kUnroll; ++k)
+            if (k < d) num += swt[32 * k] * v[k];  // diffusion.hpp:79
+        } else {
+          const int64_t q0 = __ldg(a.chunk_ptr + c) + lane;
+          for (int32_t k = 0; k < d; ++k) {
+            const int32_t cc = __ldg(a.col + q0 + 32 * (int64_t)k);
+            const double w = __ldg(a.wt + q0 + 32 * (int64_t)k);
+            num += w * __ldcg((cc < 0 ? cur : prev) + (cc & 0x7fffffff));
+          }
+        }
+        const double u0 = L == 0 ? 1.0 : 0.0;
+        __stcg(cur + r, (u0 + a.t * num) / den);  // diffusion.hpp:82
+      }
+      __syncwarp();
+      if (lane == 0) mbar_arrive(empty + slot);
+      if (++slot == a.nslots) {
+        slot = 0;
+        use ^= 1u;
+      }
+    }
+    consumer_grid_barrier(a.barrier, nbar++);
   }
 }
 
@@ -176,22 +456,49 @@ double diffuse_dev(gh_levels* L, double t, int32_t sweeps, const double* d_initi
     k_init_buffers<<<grid_for(L->nrows), B, 0, s>>>(L->perm.p, L->level.p, d_initial, L->nrows, L->ubuf.p);
     GH_LAUNCH_CHECK();
     m->launches++;
-    DiffuseArgs a{L->pstart.p, L->pend.p, L->chunk_level.p, L->chunk_ptr.p, L->deg.p, L->col.p, L->wt.p, L->den.p,
-                  L->ubuf.p, L->nrows, L->nlev, sweeps, t};
-    const bool smem = L->nlev <= kMaxSmemLevels;
-    void* fn = smem ? (void*)k_diffuse_pipelined<true> : (void*)k_diffuse_pipelined<false>;
-    const size_t shmem = smem ? sizeof(int32_t) * (size_t)L->nlev : 0;
     int nsm = 0, per_sm = 0;
     GH_CUDA(cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, m->device));
-    GH_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, B, shmem));
-    if (per_sm < 1) fail(GH_ERR_CUDA, "diffusion kernel cannot be resident");
-    const int grid = nsm * per_sm;
-    void* args[] = {&a};
     EventTimer timer(s);
-    timer.start();
-    GH_CUDA(cudaLaunchCooperativeKernel(fn, grid, B, args, shmem, s));
-    GH_LAUNCH_CHECK();
-    timer.stop();
+    const char* sched = std::getenv("GH_DIFFUSE_SCHEDULE");
+    if (sched && std::string(sched) == "barrier") {
+      DiffuseArgs a{L->pstart.p, L->pend.p, L->chunk_level.p, L->chunk_ptr.p, L->deg.p, L->col.p, L->wt.p,
+                    L->den.p, L->ubuf.p, L->nrows, L->nlev, sweeps, t};
+      const bool smem = L->nlev <= kMaxSmemLevels;
+      void* fn = smem ? (void*)k_diffuse_pipelined<true> : (void*)k_diffuse_pipelined<false>;
+      const size_t shmem = smem ? sizeof(int32_t) * (size_t)L->nlev : 0;
+      GH_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, B, shmem));
+      if (per_sm < 1) fail(GH_ERR_CUDA, "diffusion kernel cannot be resident");
+      void* args[] = {&a};
+      timer.start();
+      GH_CUDA(cudaLaunchCooperativeKernel(fn, nsm * per_sm, B, args, shmem, s));
+      GH_LAUNCH_CHECK();
+      timer.stop();
+    } else {
+      // slot = 64 B header + per chunk (den 256 B + deg 64 B + wcap x 32 x 12 B of columns/weights)
+      const int32_t wcap = std::min<int32_t>(std::max<int32_t>(L->max_chunk_width, 1), 16);
+      const int32_t slot_bytes = ((kColOff + kTileChunks * 32 * wcap * 12) + 127) & ~127;
+      const bool table = L->nlev <= kMaxSmemLevels;
+      const size_t table_bytes = table ? ((sizeof(int32_t) * L->nlev + 127) & ~size_t(127)) : 0;
+      // three blocks per SM when three rings of >= 3 slots fit (228 KB per SM, 1 KB reserved per block)
+      int32_t nslots = 0;
+      for (int per = 3; per >= 1 && nslots < 3; --per) {
+        const int64_t budget = 228 * 1024 / per - 1024;
+        nslots = (int32_t)std::min<int64_t>(8, (budget - (int64_t)table_bytes - 256) / (slot_bytes + 16));
+      }
+      if (nslots < 2) nslots = 2;
+      const size_t shmem = 16 * (size_t)nslots + table_bytes + 128 + (size_t)nslots * slot_bytes;
+      GH_CUDA(cudaFuncSetAttribute((void*)k_diffuse_tma, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)shmem));
+      TmaArgs a{L->pstart.p, L->pend.p, L->chunk_level.p, L->chunk_ptr.p, L->deg.p, L->col.p, L->wt.p, L->den.p,
+                L->ubuf.p, L->nrows, L->nlev, sweeps, wcap, nslots, slot_bytes, table ? 1 : 0, L->counter.p, t};
+      GH_CUDA(cudaMemsetAsync(L->counter.p, 0, sizeof(int32_t), s));
+      GH_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_diffuse_tma, kTmaThreads, shmem));
+      if (per_sm < 1) fail(GH_ERR_CUDA, "diffusion kernel cannot be resident");
+      void* args[] = {&a};
+      timer.start();
+      GH_CUDA(cudaLaunchCooperativeKernel((void*)k_diffuse_tma, nsm * per_sm, kTmaThreads, args, shmem, s));
+      GH_LAUNCH_CHECK();
+      timer.stop();
+    }
     m->launches++;
     ms = timer.ms();
     const double* result = L->ubuf.p + ((sweeps - 1) & 1) * (int64_t)L->nrows;
