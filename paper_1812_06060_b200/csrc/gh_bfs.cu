@@ -326,7 +326,7 @@ void bfs_build(gh_levels* L, const int32_t* h_sources, int32_t ns) {
                                                L->chunk_ptr.p, L->nrows, L->col.p, L->wt.p, L->area_r.p, L->wsum_r.p);
   GH_LAUNCH_CHECK();
   L->den.alloc(L->nrows, s);
-  L->counter.alloc(1, s);
+  L->rows_done.alloc(nlev, s);
   L->ubuf.alloc(2 * (size_t)L->nrows, s);
   L->u_orig.alloc(V, s);
   L->den_t = 0.0;

@@ -154,7 +154,7 @@ struct gh_levels {
   int32_t u_sweeps = 0;
   gh::DevBuf<double> u_orig;                       // last diffusion result, original order [V]
   int32_t max_chunk_width = 0;                     // widest SELL chunk (neighbours per row)
-  gh::DevBuf<int32_t> counter;                     // grid-barrier counter of the diffusion kernel
+  gh::DevBuf<unsigned long long> rows_done;        // per-level progress counters of the diffusion kernel
   uint64_t device_bytes() const;
 };
 
