@@ -312,7 +312,7 @@ def main():
         "config": dict(base_cfg, t=t, levels=lv.level_count(), max_level_width=lv.max_level_width,
                        parallelism="single-gpu" if world == 1 else f"replicas x{world}"),
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
-                     "traffic": traffic, "peak_source": peak_src, "kernel": "k_diffuse_pipelined",
+                     "traffic": traffic, "peak_source": peak_src, "kernel": "k_diffuse_tma",
                      "algorithmic_bytes_per_launch": bytes_per_sweep * w.sweeps,
                      "bytes_per_vertex_update": bytes_per_sweep / reach, "traffic_source": traffic_src},
         "e2e": {"value": e2e_value, "unit": "vertex-updates/s", "seconds": e2e_sec,

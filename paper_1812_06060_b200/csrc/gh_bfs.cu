@@ -17,15 +17,12 @@
 // and each column carries a flag bit saying "this neighbour sits one level
 // closer to the sources", which selects the sweep buffer to read.
 
-#include <cooperative_groups.h>
 #include <cub/device/device_radix_sort.cuh>
 #include <cub/device/device_scan.cuh>
 
 #include <algorithm>
 
 #include "gh_internal.cuh"
-
-namespace cg = cooperative_groups;
 
 namespace {
 
@@ -41,33 +38,45 @@ __global__ void k_bfs_seed(int32_t* __restrict__ level, const int32_t* __restric
 }
 
 // One ring per iteration; level_size[d] counts ring d. Returns nlev in *out.
-__global__ void __launch_bounds__(B) k_bfs(const int32_t* __restrict__ vv_off, const int32_t* __restrict__ vv_idx,
-                                           int32_t* __restrict__ level, int32_t* __restrict__ fa,
-                                           int32_t* __restrict__ fb, int32_t* __restrict__ level_size,
-                                           int32_t* __restrict__ out) {
-  cg::grid_group grid = cg::this_grid();
+constexpr int kBfsBlock = 512;
+__global__ void __launch_bounds__(kBfsBlock) k_bfs(const int32_t* __restrict__ vv_off, const int32_t* __restrict__ vv_idx,
+                                                   int32_t* __restrict__ level, int32_t* __restrict__ fa,
+                                                   int32_t* __restrict__ fb, int32_t* __restrict__ level_size,
+                                                   int32_t* __restrict__ out, unsigned* __restrict__ bar) {
+  // 8 lanes per frontier vertex, one neighbour each, so a ring costs a few
+  // dependent memory round trips instead of one per neighbour
   const int64_t tid = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  const int64_t groups = ((int64_t)gridDim.x * blockDim.x) >> 3;
+  const int sub = threadIdx.x & 7, lane = threadIdx.x & 31;
   int32_t* cur = fa;
   int32_t* nxt = fb;
   int32_t ncur = __ldcg(level_size);
   int32_t depth = 1;
   for (;;) {
-    for (int64_t i = tid; i < ncur; i += stride) {
-      const int32_t v = __ldcg(cur + i);
-      const int32_t a1 = vv_off[v + 1];
-      for (int32_t a = vv_off[v]; a < a1; ++a) {
-        const int32_t w = vv_idx[a];
-        if (__ldcg(level + w) == -1 && atomicCAS(level + w, -1, depth) == -1) {
-          cg::coalesced_group g = cg::coalesced_threads();
-          int32_t base = 0;
-          if (g.thread_rank() == 0) base = atomicAdd(level_size + depth, (int32_t)g.size());
-          base = g.shfl(base, 0);
-          nxt[base + g.thread_rank()] = w;
+    const int64_t rounds = (ncur + groups - 1) / groups;
+    for (int64_t k = 0; k < rounds; ++k) {
+      const int64_t i = (tid >> 3) + k * groups;
+      int32_t a = 0, a1 = 0;
+      if (i < ncur) {
+        const int32_t v = __ldcg(cur + i);
+        a = vv_off[v] + sub;
+        a1 = vv_off[v + 1];
+      }
+      for (; __any_sync(0xffffffffu, a < a1); a += 8) {
+        bool claimed = false;
+        int32_t w = 0;
+        if (a < a1) {
+          w = vv_idx[a];
+          claimed = atomicCAS(level + w, -1, depth) == -1;
         }
+        const unsigned mask = __ballot_sync(0xffffffffu, claimed);
+        int32_t base = 0;
+        if (lane == 0 && mask) base = atomicAdd(level_size + depth, __popc(mask));
+        base = __shfl_sync(0xffffffffu, base, 0);
+        if (claimed) nxt[base + __popc(mask & ((1u << lane) - 1u))] = w;
       }
     }
-    grid.sync();
+    ghd::grid_barrier(bar, (unsigned)(depth - 1));
     const int32_t nn = __ldcg(level_size + depth);
     if (nn == 0) break;
     int32_t* t = cur;
@@ -195,7 +204,7 @@ void bfs_build(gh_levels* L, const int32_t* h_sources, int32_t ns) {
 
   L->level.alloc(V, s);
   L->parent.alloc(V, s);
-  Scratch<int32_t> fa(V + 1, s), fb(V + 1, s), level_size(V + 2, s), dsrc(n0, s), nlev_d(1, s);
+  Scratch<int32_t> fa(V + 1, s), fb(V + 1, s), level_size(V + 2, s), dsrc(n0, s), nlev_d(2, s);
   GH_CUDA(cudaMemsetAsync(level_size.p, 0, sizeof(int32_t) * (V + 2), s));
   GH_CUDA(cudaMemcpyAsync(level_size.p, &n0, sizeof(int32_t), cudaMemcpyHostToDevice, s));
   GH_CUDA(cudaMemcpyAsync(dsrc.p, src.data(), sizeof(int32_t) * n0, cudaMemcpyHostToDevice, s));
@@ -208,8 +217,9 @@ void bfs_build(gh_levels* L, const int32_t* h_sources, int32_t ns) {
   {
     int dev = m->device, nsm = 0, per_sm = 0;
     GH_CUDA(cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev));
-    GH_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_bfs, B, 0));
-    int grid = nsm * std::max(1, std::min(per_sm, 4));
+    GH_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_bfs, kBfsBlock, 0));
+    if (per_sm < 1) fail(GH_ERR_CUDA, "BFS kernel cannot be resident");
+    int grid = nsm;  // one block per SM: the barrier cost grows with the block count
     const int32_t* vo = m->vv_offset.p;
     const int32_t* vi = m->vv_index.p;
     int32_t* lv = L->level.p;
@@ -217,8 +227,10 @@ void bfs_build(gh_levels* L, const int32_t* h_sources, int32_t ns) {
     int32_t* pb = fb.p;
     int32_t* ls = level_size.p;
     int32_t* out = nlev_d.p;
-    void* args[] = {&vo, &vi, &lv, &pa, &pb, &ls, &out};
-    GH_CUDA(cudaLaunchCooperativeKernel((void*)k_bfs, grid, B, args, 0, s));
+    unsigned* bar = reinterpret_cast<unsigned*>(nlev_d.p + 1);
+    GH_CUDA(cudaMemsetAsync(bar, 0, sizeof(unsigned), s));
+    void* args[] = {&vo, &vi, &lv, &pa, &pb, &ls, &out, &bar};
+    GH_CUDA(cudaLaunchCooperativeKernel((void*)k_bfs, grid, kBfsBlock, args, 0, s));
     GH_LAUNCH_CHECK();
   }
   const int32_t nlev = read_scalar(nlev_d.p, s);

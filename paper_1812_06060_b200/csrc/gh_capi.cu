@@ -88,6 +88,25 @@ void keep_pool_memory(int device) {
   done[device] = true;
 }
 
+// One non-blocking stream and a small pinned scratch per (host thread, device),
+// created on first use and kept for the life of the thread: creating and
+// destroying them per mesh cost up to hundreds of ms per end-to-end solve.
+void thread_context(int device, cudaStream_t* stream, double** pinned) {
+  struct Ctx {
+    cudaStream_t stream = nullptr;
+    double* pinned = nullptr;
+  };
+  thread_local Ctx ctx[64];
+  if (device < 0 || device >= 64) gh::fail(GH_ERR_CUDA, "device ordinal out of range");
+  Ctx& c = ctx[device];
+  if (!c.stream) {
+    GH_CUDA(cudaStreamCreateWithFlags(&c.stream, cudaStreamNonBlocking));
+    GH_CUDA(cudaMallocHost(&c.pinned, 8 * sizeof(double)));
+  }
+  *stream = c.stream;
+  *pinned = c.pinned;
+}
+
 int take_launches(gh_mesh* m) {
   int n = m->launches;
   m->launches = 0;
@@ -145,8 +164,7 @@ gh_status gh_mesh_create(const double* positions, int32_t nv, const int32_t* fac
     if (g_device >= 0) GH_CUDA(cudaSetDevice(g_device));
     GH_CUDA(cudaGetDevice(&m->device));
     keep_pool_memory(m->device);
-    GH_CUDA(cudaStreamCreateWithFlags(&m->stream, cudaStreamNonBlocking));
-    GH_CUDA(cudaMallocHost(&m->pinned_scalars, 8 * sizeof(double)));
+    thread_context(m->device, &m->stream, &m->pinned_scalars);
     m->nv = nv;
     m->nf = nf;
     gh::mesh_build(m.get(), positions, faces);
@@ -157,11 +175,7 @@ gh_status gh_mesh_create(const double* positions, int32_t nv, const int32_t* fac
 static void free_mesh(gh_mesh* mesh) {
   cudaSetDevice(mesh->device);
   cudaStreamSynchronize(mesh->stream);
-  cudaStream_t s = mesh->stream;
-  double* p = mesh->pinned_scalars;
-  delete mesh;
-  if (p) cudaFreeHost(p);
-  if (s) cudaStreamDestroy(s);
+  delete mesh;  // buffers return to the stream-ordered pool; stream and pinned scratch are per thread
 }
 
 gh_status gh_mesh_destroy(gh_mesh* mesh) {

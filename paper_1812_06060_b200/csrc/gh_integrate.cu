@@ -4,18 +4,15 @@
 // before the addition (integrate.hpp:56, 72). inc depends only on the
 // optimised field and the geometry, so it is computed for every vertex in one
 // fully parallel gather kernel. The chain d(v) = d(parent) + inc(v) is then
-// evaluated level by level in a cooperative persistent kernel (one grid
-// barrier per BFS level, as the reference's run_levels has one omp barrier per
-// level), which reproduces the reference's additions exactly.
-
-#include <cooperative_groups.h>
+// evaluated in BFS order by a co-resident kernel whose threads wait on their
+// parent's published value (no per-level barrier), which reproduces the
+// reference's additions exactly.
 
 #include <algorithm>
 #include <cmath>
 
 #include "gh_internal.cuh"
 
-namespace cg = cooperative_groups;
 using namespace ghd;
 
 namespace {
@@ -69,26 +66,39 @@ __global__ void k_inc_edge(const int32_t* __restrict__ order, const int32_t* __r
   }
 }
 
-// d = +inf everywhere, 0 on D_0 (integrate.hpp:20, 52)
+// d = 0 on D_0, +inf on unreachable vertices (integrate.hpp:20, 52), and a
+// "pending" NaN payload no arithmetic produces on every vertex still to come.
+constexpr unsigned long long kPending = 0x7FF4DEADBEEF0001ull;
+
 __global__ void k_dist_init(const int32_t* __restrict__ level, int64_t nv, double* __restrict__ d) {
   for (int64_t v = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; v < nv; v += (int64_t)gridDim.x * blockDim.x)
-    d[v] = level[v] == 0 ? 0.0 : INFINITY;
+    d[v] = level[v] == 0 ? 0.0 : (level[v] < 0 ? INFINITY : __longlong_as_double((long long)kPending));
 }
 
-// level-synchronous chain (run_levels, integrate.hpp:19-36)
+// d(v) = d(parent) + inc(v) in BFS order (run_levels, integrate.hpp:19-36):
+// each thread walks its positions in increasing BFS order and waits until its
+// parent's distance is published. Parents precede children in BFS order and
+// every thread handles its positions in increasing order, so with all blocks
+// co-resident the smallest pending position can always proceed. The additions
+// are the reference's, hence bitwise; no per-level grid barrier.
 __global__ void __launch_bounds__(B) k_chain(const int32_t* __restrict__ order, const int32_t* __restrict__ parent,
-                                             const int32_t* __restrict__ offsets, int32_t nlev,
-                                             const double* __restrict__ inc, double* __restrict__ d) {
-  cg::grid_group grid = cg::this_grid();
-  const int64_t tid = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+                                             int64_t b, int64_t e, const double* __restrict__ inc,
+                                             double* __restrict__ d) {
   const int64_t stride = (int64_t)gridDim.x * blockDim.x;
-  for (int32_t L = 1; L < nlev; ++L) {
-    const int64_t b = offsets[L], e = offsets[L + 1];
-    for (int64_t i = b + tid; i < e; i += stride) {
-      const int32_t v = order[i];
-      __stcg(d + v, __ldcg(d + parent[v]) + inc[i]);
+  for (int64_t i = b + blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < e; i += stride) {
+    const int32_t v = order[i];
+    const int32_t p = parent[v];
+    const double step = inc[i];
+    unsigned long long x;
+    unsigned ns = 0;
+    for (;;) {
+      asm volatile("ld.volatile.global.u64 %0, [%1];" : "=l"(x) : "l"(d + p) : "memory");
+      if (x != kPending) break;
+      __nanosleep(ns);
+      ns = ns < 256 ? ns + 32 : 256;
     }
-    grid.sync();
+    const double dv = __longlong_as_double((long long)x) + step;
+    asm volatile("st.volatile.global.f64 [%0], %1;" ::"l"(d + v), "d"(dv) : "memory");
   }
 }
 
@@ -98,18 +108,16 @@ void run_chain(gh_levels* L, const double* inc, double* d) {
   k_dist_init<<<gh::grid_for(m->nv), B, 0, s>>>(L->level.p, m->nv, d);
   GH_LAUNCH_CHECK();
   m->launches++;
-  if (L->nlev <= 1) return;
+  const int64_t b = L->h_offsets.size() > 1 ? L->h_offsets[1] : 0, e = L->nreach;
+  if (e <= b) return;
   int nsm = 0, per_sm = 0;
   GH_CUDA(cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, m->device));
   GH_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_chain, B, 0));
-  // a level holds at most max_width vertices; no need for more threads
-  const int64_t want = (L->max_width + B - 1) / B;
+  const int64_t want = (e - b + B - 1) / B;
   const int grid = (int)std::max<int64_t>(1, std::min<int64_t>((int64_t)nsm * std::max(1, per_sm), want));
   const int32_t* order = L->order.p;
   const int32_t* parent = L->parent.p;
-  const int32_t* offsets = L->offsets.p;
-  int32_t nlev = L->nlev;
-  void* args[] = {&order, &parent, &offsets, &nlev, &inc, &d};
+  void* args[] = {&order, &parent, (void*)&b, (void*)&e, &inc, &d};
   GH_CUDA(cudaLaunchCooperativeKernel((void*)k_chain, grid, B, args, 0, s));
   GH_LAUNCH_CHECK();
   m->launches++;

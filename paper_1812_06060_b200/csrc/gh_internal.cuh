@@ -224,6 +224,27 @@ __device__ __forceinline__ v3 normalized(v3 a) {
   return n2 > 0.0 ? divs(a, sqrt(n2)) : a;
 }
 
+__device__ __forceinline__ unsigned ld_acquire_u32(const unsigned* p) {
+  unsigned v;
+  asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+
+// Grid-wide barrier for cooperative (co-resident) launches: one monotonic
+// arrival counter, zeroed before the launch; the k-th barrier (k = 0, 1, ...)
+// completes at (k + 1) * gridDim.x arrivals. Cheaper than cg::grid_group::sync
+// for the many short levels of BFS.
+__device__ __forceinline__ void grid_barrier(unsigned* counter, unsigned k) {
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    __threadfence();
+    atomicAdd(counter, 1u);
+    const unsigned target = (k + 1) * gridDim.x;
+    while (ld_acquire_u32(counter) < target) __nanosleep(32);
+  }
+  __syncthreads();
+}
+
 // Block-wide sum in a fixed tree order (deterministic for a fixed blockDim).
 template <int BLOCK>
 __device__ __forceinline__ double block_sum(double v) {
