@@ -102,7 +102,7 @@ typedef struct {
   double final_dual;
   double* primal_history;
   double* dual_history;
-  double* residual_history; /* reserved for E1 early stop, may be NULL */
+  double* residual_history; /* E1 per sweep (gh_gs_diffuse_tol), may be NULL */
   int32_t history_capacity;
   uint64_t state_bytes_formula;   /* solver_state_bytes (grad_face.hpp:217-223) */
   uint64_t state_bytes_allocated; /* device bytes the solver state occupies     */
@@ -181,6 +181,11 @@ gh_status gh_bfs_download(const gh_levels* levels, int32_t* level_of_vertex, int
  * keep the result on the device only (benchmarking; see gh_levels_u_device). */
 gh_status gh_gs_diffuse(gh_levels* levels, double t, int32_t sweeps, const double* initial, double* u_out,
                         gh_solver_report* report);
+/* gs_diffuse with DiffusionConfig::residual_tolerance (diffusion.hpp:19,
+ * 110-117): after every sweep E1 is computed and the iteration stops once
+ * E1 <= tolerance; report->residual_history receives E1 per sweep. */
+gh_status gh_gs_diffuse_tol(gh_levels* levels, double t, int32_t sweeps, double tolerance, const double* initial,
+                            double* u_out, gh_solver_report* report);
 /* diffusion_residual (diffusion.hpp:35-49), E1 of a host u. */
 gh_status gh_diffusion_residual(gh_levels* levels, const double* u, double t, double* e1_out);
 

@@ -256,13 +256,21 @@ inline VertexScalarField gs_diffuse(const TriMesh& mesh, const BfsLevels& levels
                                     const DiffusionConfig& config, SolverReport* report = nullptr,
                                     const VertexScalarField* initial = nullptr) {
   config.validate();
-  if (config.residual_tolerance)
-    throw std::invalid_argument("gs_diffuse: residual_tolerance is not supported on the device path yet");
   VertexScalarField u(static_cast<std::size_t>(mesh.vertex_count()));
   gh_solver_report r{};
-  detail::check(gh_gs_diffuse(levels.handle(), t, config.sweeps, initial ? initial->data() : nullptr, u.data(), &r));
+  std::vector<double> hist(static_cast<std::size_t>(config.sweeps > 0 ? config.sweeps : 1));
+  if (config.residual_tolerance) {
+    r.residual_history = hist.data();
+    r.history_capacity = static_cast<std::int32_t>(hist.size());
+    detail::check(gh_gs_diffuse_tol(levels.handle(), t, config.sweeps, *config.residual_tolerance,
+                                    initial ? initial->data() : nullptr, u.data(), &r));
+  } else {
+    detail::check(gh_gs_diffuse(levels.handle(), t, config.sweeps, initial ? initial->data() : nullptr, u.data(), &r));
+  }
   if (report) {
     report->iterations = r.iterations;
+    report->converged = r.converged != 0;
+    if (config.residual_tolerance) report->residual_history.assign(hist.begin(), hist.begin() + r.iterations);
     report->wall_seconds = r.wall_seconds;
   }
   return u;

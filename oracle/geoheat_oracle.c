@@ -528,11 +528,36 @@ int gho_bfs(const gho_mesh* m, const int32_t* sources, int32_t ns, gho_levels** 
 
 /* ---------------------------------------------------------------- diffusion */
 
+static void gs_sweep(const gho_mesh* m, const gho_levels* l, double t, const double* u0, double* u,
+                     double* level_prev, int threads) {
+  const int32_t* lov = l->level_of_vertex;
+#pragma omp parallel num_threads(threads) if (threads > 1)
+  for (int32_t li = 0; li < l->nlev; ++li) {
+    const int32_t b = l->offsets[li], e = l->offsets[li + 1];
+#pragma omp for schedule(static)
+    for (int32_t i = b; i < e; ++i) level_prev[l->order[i]] = u[l->order[i]];
+#pragma omp for schedule(static)
+    for (int32_t i = b; i < e; ++i) {
+      const int32_t j = l->order[i];
+      double num = 0.0;
+      for (int32_t a = m->vv_offset[j]; a < m->vv_offset[j + 1]; ++a) {
+        const int32_t k = m->vv_index[a];
+        const double value = lov[k] == li ? level_prev[k] : u[k];
+        num += m->vv_weight[a] * value;
+      }
+      const double den = m->vertex_area[j] + t * m->vertex_weight_sum[j];
+      u[j] = (u0[j] + t * num) / den;
+    }
+  }
+}
+
 /* gs_diffuse (diffusion.hpp:57-124): BFS-ordered Gauss-Seidel, Jacobi within
  * a level. With threads > 1 each level is split statically, as the reference
- * does under OpenMP; the result does not depend on the split. */
-int gho_gs_diffuse(const gho_mesh* m, const gho_levels* l, double t, int32_t sweeps, const double* initial,
-                   double* u, gho_report* report) {
+ * does under OpenMP; the result does not depend on the split. With tolerance
+ * >= 0, E1 is evaluated after every sweep and the loop stops once E1 <= tol
+ * (diffusion.hpp:110-117). */
+static int diffuse(const gho_mesh* m, const gho_levels* l, double t, int32_t sweeps, double tolerance,
+                   const double* initial, double* u, gho_report* report) {
   if (sweeps < 0 || !(t > 0.0)) return 2;
   double t0 = now_seconds();
   const int64_t V = m->nv;
@@ -544,37 +569,38 @@ int gho_gs_diffuse(const gho_mesh* m, const gho_levels* l, double t, int32_t swe
   }
   if (initial) memcpy(u, initial, sizeof(double) * V);
   double* level_prev = (double*)calloc((size_t)V + 1, sizeof(double));
-  const int32_t* lov = l->level_of_vertex;
   const int threads = thread_count();
-
+  int32_t done = 0, converged = 0;
   for (int32_t sweep = 0; sweep < sweeps; ++sweep) {
-#pragma omp parallel num_threads(threads) if (threads > 1)
-    for (int32_t li = 0; li < l->nlev; ++li) {
-      const int32_t b = l->offsets[li], e = l->offsets[li + 1];
-#pragma omp for schedule(static)
-      for (int32_t i = b; i < e; ++i) level_prev[l->order[i]] = u[l->order[i]];
-#pragma omp for schedule(static)
-      for (int32_t i = b; i < e; ++i) {
-        const int32_t j = l->order[i];
-        double num = 0.0;
-        for (int32_t a = m->vv_offset[j]; a < m->vv_offset[j + 1]; ++a) {
-          const int32_t k = m->vv_index[a];
-          const double value = lov[k] == li ? level_prev[k] : u[k];
-          num += m->vv_weight[a] * value;
-        }
-        const double den = m->vertex_area[j] + t * m->vertex_weight_sum[j];
-        u[j] = (u0[j] + t * num) / den;
+    gs_sweep(m, l, t, u0, u, level_prev, threads);
+    ++done;
+    if (tolerance >= 0.0) {
+      const double e1 = gho_diffusion_residual(m, u, t, l->order, l->offsets[1]);
+      if (report && report->primal_history && sweep < report->history_capacity) report->primal_history[sweep] = e1;
+      if (e1 <= tolerance) {
+        converged = 1;
+        break;
       }
     }
   }
   free(level_prev);
   free(u0);
   if (report) {
-    report->iterations = sweeps;
-    report->converged = 0;
+    report->iterations = done;
+    report->converged = converged;
     report->wall_seconds = now_seconds() - t0;
   }
   return 0;
+}
+
+int gho_gs_diffuse(const gho_mesh* m, const gho_levels* l, double t, int32_t sweeps, const double* initial,
+                   double* u, gho_report* report) {
+  return diffuse(m, l, t, sweeps, -1.0, initial, u, report);
+}
+
+int gho_gs_diffuse_tol(const gho_mesh* m, const gho_levels* l, double t, int32_t sweeps, double tolerance,
+                       const double* initial, double* u, gho_report* report) {
+  return diffuse(m, l, t, sweeps, tolerance, initial, u, report);
 }
 
 /* diffusion_residual (diffusion.hpp:35-49) */

@@ -88,6 +88,10 @@ void gho_levels_get(const gho_levels* levels, int32_t* level_of_vertex, int32_t*
 void gho_set_threads(int32_t threads);
 int gho_gs_diffuse(const gho_mesh* mesh, const gho_levels* levels, double t, int32_t sweeps,
                    const double* initial, double* u_out, gho_report* report);
+/* gs_diffuse with DiffusionConfig::residual_tolerance (diffusion.hpp:110-117);
+ * report->primal_history receives E1 per sweep (capacity entries). */
+int gho_gs_diffuse_tol(const gho_mesh* mesh, const gho_levels* levels, double t, int32_t sweeps, double tolerance,
+                       const double* initial, double* u_out, gho_report* report);
 double gho_diffusion_residual(const gho_mesh* mesh, const double* u, double t, const int32_t* sources,
                               int32_t ns);
 void gho_face_gradient(const gho_mesh* mesh, const double* u, double* grad_out);

@@ -103,6 +103,7 @@ class Oracle:
         L.gho_levels_get.argtypes = [vp, vp, vp, vp, vp]
         L.gho_set_threads.argtypes = [i32]
         L.gho_gs_diffuse.argtypes = [vp, vp, f64, i32, vp, vp, C.POINTER(_Report)]
+        L.gho_gs_diffuse_tol.argtypes = [vp, vp, f64, i32, f64, vp, vp, C.POINTER(_Report)]
         L.gho_diffusion_residual.argtypes = [vp, vp, f64, vp, i32]
         L.gho_diffusion_residual.restype = f64
         L.gho_face_gradient.argtypes = [vp, vp, vp]
@@ -209,6 +210,21 @@ class OMesh:
         if rc != 0:
             raise ValueError("gs_diffuse: invalid argument")
         return u, OracleReport(iterations=rep.iterations, wall_seconds=rep.wall_seconds)
+
+    def gs_diffuse_tol(self, levels: "OLevels", t: float, sweeps: int, tolerance: float, initial=None):
+        """gs_diffuse with DiffusionConfig::residual_tolerance; returns (u, report with E1 history)."""
+        u = np.zeros(self.nv, np.float64)
+        init = None if initial is None else np.ascontiguousarray(initial, dtype=np.float64)
+        hist = np.zeros(max(int(sweeps), 1))
+        rep = _Report()
+        rep.primal_history = hist.ctypes.data_as(C.POINTER(C.c_double))
+        rep.history_capacity = hist.size
+        rc = self.L.gho_gs_diffuse_tol(self.h, levels.h, float(t), int(sweeps), float(tolerance), _p(init), _p(u),
+                                       C.byref(rep))
+        if rc != 0:
+            raise ValueError("gs_diffuse: invalid argument")
+        return u, OracleReport(iterations=rep.iterations, converged=bool(rep.converged),
+                               primal_history=hist[:rep.iterations].tolist(), wall_seconds=rep.wall_seconds)
 
     def diffusion_residual(self, u, t, sources) -> float:
         u = np.ascontiguousarray(u, dtype=np.float64)

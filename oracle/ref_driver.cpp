@@ -189,6 +189,30 @@ int gho_gs_diffuse(const gho_mesh* mesh, const gho_levels* levels, double t, int
   return 0;
 }
 
+// gs_diffuse with residual_tolerance (diffusion.hpp:110-117)
+int gho_gs_diffuse_tol(const gho_mesh* mesh, const gho_levels* levels, double t, int32_t sweeps, double tolerance,
+                       const double* initial, double* u_out, gho_report* report) {
+  DiffusionConfig cfg;
+  cfg.sweeps = sweeps;
+  cfg.residual_tolerance = tolerance;
+  SolverReport rep;
+  try {
+    VertexScalarField u;
+    if (initial) {
+      VertexScalarField init(initial, initial + mesh->m.vertex_count());
+      u = gs_diffuse(mesh->m, levels->l, t, cfg, &rep, &init);
+    } else {
+      u = gs_diffuse(mesh->m, levels->l, t, cfg, &rep);
+    }
+    std::memcpy(u_out, u.data(), u.size() * sizeof(double));
+  } catch (const std::invalid_argument&) {
+    return 2;
+  }
+  rep.primal_history = rep.residual_history;
+  fill_report(rep, report);
+  return 0;
+}
+
 // diffusion_residual (diffusion.hpp:35-49)
 double gho_diffusion_residual(const gho_mesh* mesh, const double* u, double t, const int32_t* sources,
                               int32_t ns) {

@@ -73,6 +73,7 @@ SIGNATURES = [
     ("gh_bfs_get_info", st, [vp, C.POINTER(gh_levels_info)]),
     ("gh_bfs_download", st, [vp, vp, vp, vp, vp]),
     ("gh_gs_diffuse", st, [vp, f64, i32, vp, vp, C.POINTER(gh_solver_report)]),
+    ("gh_gs_diffuse_tol", st, [vp, f64, i32, f64, vp, vp, C.POINTER(gh_solver_report)]),
     ("gh_diffusion_residual", st, [vp, vp, f64, C.POINTER(f64)]),
     ("gh_normalized_target_gradients", st, [vp, vp, vp, C.POINTER(i32)]),
     ("gh_admm_face_optimize", st, [vp, vp, C.POINTER(gh_admm_config), vp, C.POINTER(gh_solver_report)]),

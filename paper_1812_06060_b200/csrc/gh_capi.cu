@@ -350,6 +350,48 @@ gh_status gh_gs_diffuse(gh_levels* levels, double t, int32_t sweeps, const doubl
   });
 }
 
+gh_status gh_gs_diffuse_tol(gh_levels* levels, double t, int32_t sweeps, double tolerance, const double* initial,
+                            double* u_out, gh_solver_report* report) {
+  return guarded([&] {
+    require(levels != nullptr, "gh_gs_diffuse_tol: null levels");
+    gh_mesh* m = levels->mesh;
+    use_device_of(m);
+    cudaStream_t s = m->stream;
+    const double w0 = now_s();
+    take_launches(m);
+    // E1 is checked after every sweep (diffusion.hpp:110-117), so sweeps run one
+    // launch at a time, each warm-started from the previous u (a sweep depends
+    // on u only, so this is bit-identical to running them back to back).
+    gh::Scratch<double> cur(m->nv, s);
+    if (initial) GH_CUDA(cudaMemcpyAsync(cur.p, initial, sizeof(double) * m->nv, cudaMemcpyHostToDevice, s));
+    double ms = 0.0;
+    int done = 0;
+    bool converged = false;
+    if (sweeps == 0) ms += gh::diffuse_dev(levels, t, 0, initial ? cur.p : nullptr);
+    for (int k = 0; k < sweeps; ++k) {
+      ms += gh::diffuse_dev(levels, t, 1, (k > 0 || initial) ? cur.p : nullptr);
+      ++done;
+      const double e1 = gh::diffusion_residual_dev(levels, levels->u_orig.p, t);
+      if (report && report->residual_history && k < report->history_capacity) report->residual_history[k] = e1;
+      if (e1 <= tolerance) {
+        converged = true;
+        break;
+      }
+      GH_CUDA(cudaMemcpyAsync(cur.p, levels->u_orig.p, sizeof(double) * m->nv, cudaMemcpyDeviceToDevice, s));
+    }
+    if (u_out) to_host(u_out, levels->u_orig.p, m->nv, s);
+    else GH_CUDA(cudaStreamSynchronize(s));
+    if (report) {
+      report->iterations = done;
+      report->converged = converged ? 1 : 0;
+      report->wall_seconds = now_s() - w0;
+      report->device_ms = ms;
+      report->kernel_launches = take_launches(m);
+      report->state_bytes_allocated = levels->device_bytes();
+    }
+  });
+}
+
 gh_status gh_diffusion_residual(gh_levels* levels, const double* u, double t, double* e1_out) {
   return guarded([&] {
     require(levels && u && e1_out, "gh_diffusion_residual: null argument");

@@ -297,17 +297,25 @@ def gs_diffuse(mesh: TriMesh, levels: BfsLevels, t: float, config: DiffusionConf
     if levels.mesh is not mesh:
         raise ValueError("gs_diffuse: levels were built on a different mesh")
     config.validate()
-    if config.residual_tolerance is not None:
-        raise NotImplementedError("residual_tolerance early stop is not on the device path yet (SURVEY §8(f) row 1)")
     init = None if initial is None else _f64(initial)
     if init is not None and init.size != mesh.vertex_count():
         raise ValueError("gs_diffuse: initial has the wrong length")
     u = None if keep_on_device else np.empty(mesh.vertex_count(), np.float64)
     rep = gh_solver_report()
-    _check(mesh._lib.gh_gs_diffuse(levels._h, float(t), int(config.sweeps), _ptr(init), _ptr(u), C.byref(rep)))
+    if config.residual_tolerance is None:
+        _check(mesh._lib.gh_gs_diffuse(levels._h, float(t), int(config.sweeps), _ptr(init), _ptr(u), C.byref(rep)))
+        hist = []
+    else:
+        rh = np.zeros(max(int(config.sweeps), 1))
+        rep.residual_history = rh.ctypes.data_as(C.POINTER(C.c_double))
+        rep.history_capacity = rh.size
+        _check(mesh._lib.gh_gs_diffuse_tol(levels._h, float(t), int(config.sweeps), float(config.residual_tolerance),
+                                           _ptr(init), _ptr(u), C.byref(rep)))
+        hist = rh[:rep.iterations].tolist()
     if report is not None:
         report.iterations = rep.iterations
         report.converged = bool(rep.converged)
+        report.residual_history = hist
         report.wall_seconds = rep.wall_seconds
         report.device_ms = rep.device_ms
         report.kernel_launches = rep.kernel_launches

@@ -38,6 +38,14 @@ CASES = [
     ("hex_disk5_converges", "hex_disk", (5,), [0], dict(m=1.0), 300, 400),
 ]
 
+# DiffusionConfig::residual_tolerance early stop (diffusion.hpp:110-117); the first
+# mirrors test_diffusion.cpp:140-154 (hex_disk_mesh(6), 10000 sweeps, 1e-8)
+TOL_CASES = [
+    ("tol_hex_disk6", "hex_disk", (6,), [0], 1.0, 10000, 1e-8),
+    ("tol_icosphere3", "icosphere", (3,), [0, 100], 1.0, 3000, 1e-6),
+    ("tol_torus24x12_never", "torus", (24, 12), [5], 1.0, 40, 1e-30),
+]
+
 # build_mesh rejection cases (mesh.hpp:133-183), from test_mesh.cpp:48-75
 ERROR_CASES = [
     ("repeated_vertex", [[0, 0, 0], [1, 0, 0], [0, 1, 0]], [[0, 1, 1]]),
@@ -96,6 +104,20 @@ def main():
                            edge_iterations=int(out["edge_iterations"]), face_converged=int(out["face_converged"]),
                            edge_converged=int(out["edge_converged"]))
         print(name, index[name])
+    tol_index = {}
+    for name, gen, params, sources, m, sweeps, tol in TOL_CASES:
+        P, F = o.test_mesh(gen, *params)
+        mesh = o.build_mesh(P, F)
+        lv = mesh.bfs(sources)
+        t = mesh.diffusion_time(m)
+        u, rep = mesh.gs_diffuse_tol(lv, t, sweeps, tol)
+        np.savez_compressed(os.path.join(HERE, "tol", f"{name}.npz"), positions=P, faces=F,
+                            sources=np.asarray(sources, np.int32), t=np.float64(t), sweeps=np.int32(sweeps),
+                            tolerance=np.float64(tol), u=u, iterations=np.int32(rep.iterations),
+                            converged=np.int32(rep.converged), residual_history=np.asarray(rep.primal_history))
+        tol_index[name] = dict(iterations=rep.iterations, converged=rep.converged,
+                               last_e1=rep.primal_history[-1] if rep.primal_history else None)
+        print(name, tol_index[name])
     errors = {}
     for name, P, F in ERROR_CASES:
         try:
@@ -106,7 +128,7 @@ def main():
         except ValueError as e:
             errors[name] = "invalid: " + str(e)
     with open(os.path.join(HERE, "index.json"), "w") as f:
-        json.dump({"cases": index, "errors": {n: dict(positions=P, faces=F, message=errors[n])
+        json.dump({"cases": index, "tolerance_cases": tol_index, "errors": {n: dict(positions=P, faces=F, message=errors[n])
                                               for n, P, F in ERROR_CASES},
                    "generated_by": "tests/golden/make_golden.py with oracle/_ref/libgeoheat_ref.so"}, f, indent=1)
     print(json.dumps(errors, indent=1))

@@ -211,3 +211,26 @@ def test_cpp_wrapper_runs_reference_chain(gpu):
     r = subprocess.run([exe, t.hex()], capture_output=True, text=True, timeout=300)
     assert r.returncode == 0, r.stdout + r.stderr
     assert "PASS" in r.stdout
+
+
+TOL_CASES = sorted(os.path.basename(p)[:-4] for p in glob.glob(os.path.join(GOLDEN, "tol", "*.npz")))
+
+
+@pytest.mark.parametrize("case", TOL_CASES)
+def test_residual_tolerance_early_stop(gpu, case):
+    """gs_diffuse with residual_tolerance (diffusion.hpp:110-117): same stop sweep, bitwise u,
+    E1 history within 1e-12 (device tree sum vs the reference's left-to-right sum), and the
+    stop decision is not within 1e-9 of the threshold on either side."""
+    gh = gpu
+    g = np.load(os.path.join(GOLDEN, "tol", case + ".npz"))
+    mesh = gh.build_mesh(g["positions"], g["faces"])
+    lv = gh.bfs_levels(mesh, g["sources"])
+    rep = gh.SolverReport()
+    cfg = gh.DiffusionConfig(sweeps=int(g["sweeps"]), residual_tolerance=float(g["tolerance"]))
+    u = gh.gs_diffuse(mesh, lv, float(g["t"]), cfg, rep)
+    assert rep.iterations == int(g["iterations"]) and rep.converged == bool(g["converged"])
+    assert_same(u, g["u"], "u")
+    check_history(rep.residual_history, g["residual_history"], "E1")
+    tol = float(g["tolerance"])
+    for e1 in rep.residual_history:
+        assert abs(e1 / tol - 1.0) > 1e-9

@@ -215,3 +215,18 @@ def test_threads_do_not_change_bits(port_oracle):
         o.set_threads(0)
     for u in outs:
         assert_same(u, g["u"])
+
+
+TOL_CASES = sorted(os.path.basename(p)[:-4] for p in glob.glob(os.path.join(GOLDEN, "tol", "*.npz")))
+
+
+@pytest.mark.parametrize("case", TOL_CASES)
+def test_port_residual_tolerance_matches_reference(port_oracle, case):
+    """DiffusionConfig::residual_tolerance early stop (diffusion.hpp:110-117)."""
+    g = np.load(os.path.join(GOLDEN, "tol", case + ".npz"))
+    mesh = port_oracle.build_mesh(g["positions"], g["faces"])
+    lv = mesh.bfs(g["sources"])
+    u, rep = mesh.gs_diffuse_tol(lv, float(g["t"]), int(g["sweeps"]), float(g["tolerance"]))
+    assert rep.iterations == int(g["iterations"]) and rep.converged == bool(g["converged"])
+    assert_same(u, g["u"], "u")
+    assert_same(rep.primal_history, g["residual_history"], "E1 history")
