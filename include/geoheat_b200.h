@@ -217,6 +217,32 @@ gh_status gh_distance_host(const double* positions, int32_t nv, const int32_t* f
                            const int32_t* sources, int32_t ns, const gh_pipeline_config* config, double* d_out,
                            gh_run_report* report);
 
+/* ---- BFS-band sharding of the diffusion
+ * Levels are cut into nbands contiguous bands of about equal rows; band r
+ * computes its own levels and keeps ghost copies of levels lb-1 and le, which
+ * the neighbours write directly (peer stores + per-level counters) while
+ * the single dataflow kernel runs. Results are bit-identical to gh_gs_diffuse. */
+typedef struct gh_band gh_band;
+/* The band plan: cut_out[nbands + 1] level boundaries for ring offsets[nlev + 1]
+ * (host only; the same plan every rank computes). */
+gh_status gh_plan_bands(const int32_t* offsets, int32_t nlev, int32_t nbands, int32_t* cut_out);
+/* All bands in one process on the current device (one launch): the
+ * single-GPU emulation of the multi-GPU schedule. nbands <= 8. */
+gh_status gh_gs_diffuse_bands(gh_levels* levels, int32_t nbands, double t, int32_t sweeps, const double* initial,
+                              double* u_out, gh_solver_report* report);
+/* One band per process/GPU: create, export its IPC blob, connect to the
+ * neighbours' blobs, prepare (all ranks) -> barrier -> launch (all ranks). */
+gh_status gh_band_create(gh_levels* levels, int32_t rank, int32_t nranks, gh_band** out);
+gh_status gh_band_destroy(gh_band* band);
+gh_status gh_band_info(const gh_band* band, int32_t* lb, int32_t* le, int32_t* own_rows);
+/* blob NULL: *size receives the blob size. */
+gh_status gh_band_export(const gh_band* band, void* blob, int32_t capacity, int32_t* size);
+/* lower_blob / upper_blob NULL for the first / last band. */
+gh_status gh_band_connect(gh_band* band, const void* lower_blob, const void* upper_blob);
+gh_status gh_band_prepare(gh_band* band, double t, const double* initial);
+/* u_out (host [V], may be NULL): this band's vertices hold the result. */
+gh_status gh_band_launch(gh_band* band, double t, int32_t sweeps, double* u_out, gh_solver_report* report);
+
 /* field_hash (report.hpp:145-153): FNV-1a over the bytes of n doubles. */
 uint64_t gh_field_hash(const double* values, int64_t n);
 

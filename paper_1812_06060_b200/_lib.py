@@ -83,6 +83,15 @@ SIGNATURES = [
     ("gh_integrate_edge_differences", st, [vp, vp, vp]),
     ("gh_distance", st, [vp, C.POINTER(gh_pipeline_config), vp, C.POINTER(gh_run_report)]),
     ("gh_distance_host", st, [vp, i32, vp, i32, vp, i32, C.POINTER(gh_pipeline_config), vp, C.POINTER(gh_run_report)]),
+    ("gh_plan_bands", st, [vp, i32, i32, vp]),
+    ("gh_gs_diffuse_bands", st, [vp, i32, f64, i32, vp, vp, C.POINTER(gh_solver_report)]),
+    ("gh_band_create", st, [vp, i32, i32, C.POINTER(vp)]),
+    ("gh_band_destroy", st, [vp]),
+    ("gh_band_info", st, [vp, C.POINTER(i32), C.POINTER(i32), C.POINTER(i32)]),
+    ("gh_band_export", st, [vp, vp, i32, C.POINTER(i32)]),
+    ("gh_band_connect", st, [vp, vp, vp]),
+    ("gh_band_prepare", st, [vp, f64, vp]),
+    ("gh_band_launch", st, [vp, f64, i32, vp, C.POINTER(gh_solver_report)]),
     ("gh_field_hash", C.c_uint64, [vp, i64]),
 ]
 

@@ -1,0 +1,244 @@
+// Diffusion layout of a BFS band.
+//
+// Rows of the band's own levels [lb, le) are renumbered by (level parity,
+// level, original index), every level starting on a 32-row chunk boundary, so
+// the rows a pipeline step touches are one contiguous range and a chunk holds
+// one level. The ghost levels lb-1 and le (copies of the neighbours' boundary
+// levels) follow. The CSR of the own rows is laid out SELL-32 (entry k of lane
+// j at chunk_ptr + 32k + j); each row keeps the reference's neighbour order
+// (ascending original index, mesh.hpp:255-266) and each column carries a flag
+// bit "one level closer to the sources", which selects the sweep buffer.
+//
+// Band plan: levels are cut into contiguous bands of about equal row counts.
+// By the BFS property (|level difference| <= 1 across an edge) a band only
+// touches its two neighbours, through one ring each.
+
+#include <cub/device/device_scan.cuh>
+
+#include <algorithm>
+
+#include "gh_internal.cuh"
+
+namespace {
+
+constexpr int B = gh::kBlock;
+
+// local row of every vertex of levels [glo, ghi] (own and ghost)
+__global__ void k_band_renumber(const int32_t* __restrict__ order, const int32_t* __restrict__ level, int64_t b,
+                                int64_t e, const int32_t* __restrict__ boff, const int32_t* __restrict__ pstart,
+                                int32_t* __restrict__ perm, int32_t* __restrict__ local) {
+  for (int64_t i = b + blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < e; i += (int64_t)gridDim.x * blockDim.x) {
+    const int32_t v = order[i];
+    const int32_t L = level[v];
+    const int32_t r = pstart[L] + (int32_t)(i - boff[L]);
+    perm[r] = v;
+    local[v] = r;
+  }
+}
+
+// per own chunk: its level, width = longest row, and the row lengths
+__global__ void k_chunk_meta(const int32_t* __restrict__ perm, const int32_t* __restrict__ level,
+                             const int32_t* __restrict__ vv_off, int64_t nchunks, int32_t* __restrict__ chunk_level,
+                             int64_t* __restrict__ width, uint16_t* __restrict__ deg, int32_t* __restrict__ maxdeg) {
+  const int lane = threadIdx.x & 31;
+  const int64_t warp = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+  const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  for (int64_t c = warp; c < nchunks; c += nwarps) {
+    const int64_t r = c * 32 + lane;
+    const int32_t v = perm[r];
+    const int32_t d = v >= 0 ? vv_off[v + 1] - vv_off[v] : 0;
+    int32_t m = d;
+    for (int o = 16; o > 0; o >>= 1) m = max(m, __shfl_xor_sync(0xffffffffu, m, o));
+    deg[r] = (uint16_t)(d > 65535 ? 65535 : d);
+    if (lane == 0) {
+      width[c] = 32 * (int64_t)m;
+      chunk_level[c] = level[perm[c * 32]];  // levels are chunk aligned: row 0 of a chunk is real
+      if (m > 65535) atomicMax(maxdeg, m);
+    }
+  }
+}
+
+__global__ void k_sell_fill(const int32_t* __restrict__ perm, const int32_t* __restrict__ level,
+                            const int32_t* __restrict__ local, const int32_t* __restrict__ vv_off,
+                            const int32_t* __restrict__ vv_idx, const double* __restrict__ vv_w,
+                            const double* __restrict__ va, const double* __restrict__ wsum,
+                            const int64_t* __restrict__ chunk_ptr, int64_t own_rows, int32_t* __restrict__ col,
+                            double* __restrict__ wt, double* __restrict__ area_r, double* __restrict__ wsum_r) {
+  for (int64_t r = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; r < own_rows;
+       r += (int64_t)gridDim.x * blockDim.x) {
+    const int32_t v = perm[r];
+    if (v < 0) continue;
+    const int32_t L = level[v];
+    const int64_t base = chunk_ptr[r >> 5] + (r & 31);
+    const int32_t a0 = vv_off[v], a1 = vv_off[v + 1];
+    for (int32_t a = a0; a < a1; ++a) {
+      const int32_t nb = vv_idx[a];
+      const uint32_t flag = level[nb] == L - 1 ? 0x80000000u : 0u;
+      col[base + 32 * (int64_t)(a - a0)] = (int32_t)((uint32_t)local[nb] | flag);
+      wt[base + 32 * (int64_t)(a - a0)] = vv_w[a];
+    }
+    area_r[r] = va[v];
+    wsum_r[r] = wsum[v];
+  }
+}
+
+template <class T>
+T read_scalar(const T* d, cudaStream_t s) {
+  T v;
+  GH_CUDA(cudaMemcpyAsync(&v, d, sizeof(T), cudaMemcpyDeviceToHost, s));
+  GH_CUDA(cudaStreamSynchronize(s));
+  return v;
+}
+
+}  // namespace
+
+namespace gh {
+
+Band::~Band() {
+  if (ubuf || rows_done) cudaSetDevice(device);
+  if (ubuf) cudaFree(ubuf);
+  if (rows_done) cudaFree(rows_done);
+}
+
+uint64_t Band::device_bytes() const {
+  return pstart.bytes() + pend.bytes() + perm.bytes() + chunk_level.bytes() + chunk_ptr.bytes() + deg.bytes() +
+         col.bytes() + wt.bytes() + area_r.bytes() + wsum_r.bytes() + den.bytes() + 2 * sizeof(double) * nrows +
+         sizeof(unsigned long long) * nlev;
+}
+
+// Cut levels into nbands contiguous bands of about equal row counts; band r
+// owns levels [cut[r], cut[r+1]). Mirrored in paper_1812_06060_b200/bands.py.
+std::vector<int32_t> plan_bands(const std::vector<int32_t>& offsets, int32_t nbands) {
+  const int32_t nlev = (int32_t)offsets.size() - 1;
+  if (nbands < 1) fail(GH_ERR_INVALID, "plan_bands: need at least one band");
+  if (nbands > nlev) fail(GH_ERR_INVALID, "plan_bands: more bands than BFS levels");
+  const int64_t total = offsets[nlev];
+  std::vector<int32_t> cut(nbands + 1, 0);
+  cut[nbands] = nlev;
+  int32_t L = 0;
+  for (int32_t r = 1; r < nbands; ++r) {
+    const int64_t target = total * r / nbands;
+    while (L < nlev && offsets[L] < target) ++L;  // first level starting at or after the target row
+    if (L > 0 && target - offsets[L - 1] < offsets[L] - target) --L;  // or the closer boundary before it
+    L = std::max(L, cut[r - 1] + 1);              // every band owns at least one level
+    L = std::min(L, nlev - (nbands - r));         // and leaves one for each later band
+    cut[r] = L;
+  }
+  return cut;
+}
+
+void band_build(gh_levels* L, Band* b, int32_t lb, int32_t le) {
+  gh_mesh* m = L->mesh;
+  cudaStream_t s = m->stream;
+  const int32_t nlev = L->nlev;
+  const int64_t V = m->nv;
+  const std::vector<int32_t>& off = L->h_offsets;
+  b->lb = lb;
+  b->le = le;
+  b->nlev = nlev;
+  b->device = m->device;
+  b->h_pstart.assign(nlev, 0);
+  b->h_pend.assign(nlev, 0);
+  int64_t cursor = 0;
+  for (int p = 0; p < 2; ++p) {
+    for (int32_t l = lb + ((lb & 1) != p); l < le; l += 2) {
+      cursor = (cursor + 31) & ~int64_t(31);
+      b->h_pstart[l] = (int32_t)cursor;
+      cursor += off[l + 1] - off[l];
+      b->h_pend[l] = (int32_t)cursor;
+    }
+  }
+  cursor = (cursor + 31) & ~int64_t(31);
+  b->own_rows = (int32_t)cursor;
+  for (int32_t g : {lb - 1, le}) {
+    if (g < 0 || g >= nlev) continue;
+    b->h_pstart[g] = (int32_t)cursor;
+    cursor += off[g + 1] - off[g];
+    b->h_pend[g] = (int32_t)cursor;
+    cursor = (cursor + 31) & ~int64_t(31);
+  }
+  if (cursor > 0x7fffffffLL) fail(GH_ERR_INVALID, "mesh too large for the diffusion layout");
+  b->nrows = (int32_t)cursor;
+  b->own_chunks = b->own_rows / 32;
+  b->pstart.alloc(nlev, s);
+  b->pend.alloc(nlev, s);
+  GH_CUDA(cudaMemcpyAsync(b->pstart.p, b->h_pstart.data(), sizeof(int32_t) * nlev, cudaMemcpyHostToDevice, s));
+  GH_CUDA(cudaMemcpyAsync(b->pend.p, b->h_pend.data(), sizeof(int32_t) * nlev, cudaMemcpyHostToDevice, s));
+  b->perm.alloc(b->nrows, s);
+  GH_CUDA(cudaMemsetAsync(b->perm.p, 0xff, sizeof(int32_t) * b->nrows, s));
+  Scratch<int32_t> local(V, s);
+  GH_CUDA(cudaMemsetAsync(local.p, 0xff, sizeof(int32_t) * V, s));
+  const int32_t glo = std::max(lb - 1, 0), ghi = std::min(le, nlev - 1);
+  const int64_t pb = off[glo], pe = off[ghi + 1];
+  if (pe > pb) {
+    k_band_renumber<<<grid_for(pe - pb), B, 0, s>>>(L->order.p, L->level.p, pb, pe, L->offsets.p, b->pstart.p,
+                                                    b->perm.p, local.p);
+    GH_LAUNCH_CHECK();
+  }
+  b->chunk_level.alloc(b->own_chunks, s);
+  b->deg.alloc(b->nrows, s);
+  GH_CUDA(cudaMemsetAsync(b->deg.p, 0, sizeof(uint16_t) * b->nrows, s));
+  b->chunk_ptr.alloc(b->own_chunks + 1, s);
+  {
+    Scratch<int64_t> width(b->own_chunks + 1, s);
+    Scratch<int32_t> maxdeg(1, s);
+    GH_CUDA(cudaMemsetAsync(maxdeg.p, 0, sizeof(int32_t), s));
+    GH_CUDA(cudaMemsetAsync(width.p + b->own_chunks, 0, sizeof(int64_t), s));
+    if (b->own_chunks)
+      k_chunk_meta<<<grid_for((int64_t)b->own_chunks * 32), B, 0, s>>>(b->perm.p, L->level.p, m->vv_offset.p,
+                                                                       b->own_chunks, b->chunk_level.p, width.p,
+                                                                       b->deg.p, maxdeg.p);
+    GH_LAUNCH_CHECK();
+    if (read_scalar(maxdeg.p, s) > 65535) fail(GH_ERR_INVALID, "vertex valence above 65535 is not supported");
+    size_t tmp = 0;
+    GH_CUDA(cub::DeviceScan::ExclusiveSum(nullptr, tmp, width.p, b->chunk_ptr.p, b->own_chunks + 1, s));
+    Scratch<char> t(tmp, s);
+    GH_CUDA(cub::DeviceScan::ExclusiveSum(t.p, tmp, width.p, b->chunk_ptr.p, b->own_chunks + 1, s));
+  }
+  std::vector<int64_t> cp(b->own_chunks + 1);
+  GH_CUDA(cudaMemcpyAsync(cp.data(), b->chunk_ptr.p, sizeof(int64_t) * cp.size(), cudaMemcpyDeviceToHost, s));
+  GH_CUDA(cudaStreamSynchronize(s));
+  int64_t wmax = 0;
+  for (int32_t c = 0; c < b->own_chunks; ++c) wmax = std::max(wmax, (cp[c + 1] - cp[c]) / 32);
+  b->max_chunk_width = (int32_t)wmax;
+  const int64_t nnz = cp[b->own_chunks];
+  b->col.alloc(nnz, s);
+  b->wt.alloc(nnz, s);
+  if (nnz) {
+    GH_CUDA(cudaMemsetAsync(b->col.p, 0, sizeof(int32_t) * nnz, s));
+    GH_CUDA(cudaMemsetAsync(b->wt.p, 0, sizeof(double) * nnz, s));
+  }
+  b->area_r.alloc(b->nrows, s);
+  b->wsum_r.alloc(b->nrows, s);
+  GH_CUDA(cudaMemsetAsync(b->area_r.p, 0, sizeof(double) * b->nrows, s));
+  GH_CUDA(cudaMemsetAsync(b->wsum_r.p, 0, sizeof(double) * b->nrows, s));
+  if (b->own_rows)
+    k_sell_fill<<<grid_for(b->own_rows), B, 0, s>>>(b->perm.p, L->level.p, local.p, m->vv_offset.p, m->vv_index.p,
+                                                    m->vv_weight.p, m->vertex_area.p, m->vertex_weight_sum.p,
+                                                    b->chunk_ptr.p, b->own_rows, b->col.p, b->wt.p, b->area_r.p,
+                                                    b->wsum_r.p);
+  GH_LAUNCH_CHECK();
+  b->den.alloc(b->nrows, s);
+  b->den_t = 0.0;
+  if (!b->ubuf) {
+    GH_CUDA(cudaMalloc(&b->ubuf, sizeof(double) * 2 * (size_t)b->nrows));
+    GH_CUDA(cudaMalloc(&b->rows_done, sizeof(unsigned long long) * nlev));
+  }
+  m->launches += 4;
+  GH_CUDA(cudaStreamSynchronize(s));
+}
+
+void band_link(Band* lower, Band* upper) {
+  // upper.lb == lower.le: the lower band's last level is upper's lower ghost,
+  // the upper band's first level is lower's upper ghost
+  lower->hi_ubuf = upper->ubuf;
+  lower->hi_done = upper->rows_done;
+  lower->hi_nrows = upper->nrows;
+  lower->hi_ghost = upper->ghost_row(lower->le - 1);
+  upper->lo_ubuf = lower->ubuf;
+  upper->lo_done = lower->rows_done;
+  upper->lo_nrows = lower->nrows;
+  upper->lo_ghost = lower->ghost_row(upper->lb);
+}
+
+}  // namespace gh

@@ -601,3 +601,198 @@ uint64_t gh_field_hash(const double* values, int64_t n) {
 }
 
 }  // extern "C"
+
+// ---------------------------------------------------------------- BFS bands (multi-GPU)
+
+struct gh_band {
+  gh_levels* levels = nullptr;
+  gh::Band band;
+  int32_t rank = 0, nranks = 1;
+  std::vector<void*> opened;  // peer allocations mapped with cudaIpcOpenMemHandle
+};
+
+namespace {
+
+struct BandBlob {
+  cudaIpcMemHandle_t ubuf;
+  cudaIpcMemHandle_t done;
+  int64_t nrows;
+  int32_t lb, le;
+  int32_t ghost_lo_row;  // row of level lb-1 inside this band, -1 without one
+  int32_t ghost_hi_row;  // row of level le inside this band, -1 without one
+  int32_t device, magic;
+};
+constexpr int32_t kBlobMagic = 0x67686264;  // "ghbd"
+
+}  // namespace
+
+extern "C" {
+
+gh_status gh_plan_bands(const int32_t* offsets, int32_t nlev, int32_t nbands, int32_t* cut_out) {
+  return guarded([&] {
+    require(offsets && cut_out && nlev >= 1, "gh_plan_bands: bad arguments");
+    const std::vector<int32_t> off(offsets, offsets + nlev + 1);
+    const std::vector<int32_t> cut = gh::plan_bands(off, nbands);
+    std::memcpy(cut_out, cut.data(), sizeof(int32_t) * cut.size());
+  });
+}
+
+gh_status gh_gs_diffuse_bands(gh_levels* levels, int32_t nbands, double t, int32_t sweeps, const double* initial,
+                              double* u_out, gh_solver_report* report) {
+  return guarded([&] {
+    require(levels != nullptr, "gh_gs_diffuse_bands: null levels");
+    gh_mesh* m = levels->mesh;
+    use_device_of(m);
+    cudaStream_t s = m->stream;
+    const double w0 = now_s();
+    take_launches(m);
+    const std::vector<int32_t> cut = gh::plan_bands(levels->h_offsets, nbands);
+    std::vector<std::unique_ptr<gh::Band>> own;
+    std::vector<gh::Band*> bands;
+    for (int32_t r = 0; r < nbands; ++r) {
+      own.emplace_back(new gh::Band());
+      gh::band_build(levels, own.back().get(), cut[r], cut[r + 1]);
+      bands.push_back(own.back().get());
+    }
+    for (int32_t r = 0; r + 1 < nbands; ++r) gh::band_link(bands[r], bands[r + 1]);
+    gh::Scratch<double> dinit(initial ? m->nv : 0, s);
+    if (initial) GH_CUDA(cudaMemcpyAsync(dinit.p, initial, sizeof(double) * m->nv, cudaMemcpyHostToDevice, s));
+    const double ms = gh::diffuse_bands_dev(levels, bands, t, sweeps, initial ? dinit.p : nullptr);
+    if (u_out) to_host(u_out, levels->u_orig.p, m->nv, s);
+    else GH_CUDA(cudaStreamSynchronize(s));
+    if (report) {
+      report->iterations = sweeps;
+      report->converged = 0;
+      report->wall_seconds = now_s() - w0;
+      report->device_ms = ms;
+      report->kernel_launches = take_launches(m);
+    }
+  });
+}
+
+gh_status gh_band_create(gh_levels* levels, int32_t rank, int32_t nranks, gh_band** out) {
+  return guarded([&] {
+    require(levels && out, "gh_band_create: null argument");
+    require(nranks >= 1 && rank >= 0 && rank < nranks, "gh_band_create: bad rank");
+    use_device_of(levels->mesh);
+    const std::vector<int32_t> cut = gh::plan_bands(levels->h_offsets, nranks);
+    std::unique_ptr<gh_band> b(new gh_band());
+    b->levels = levels;
+    b->rank = rank;
+    b->nranks = nranks;
+    gh::band_build(levels, &b->band, cut[rank], cut[rank + 1]);
+    *out = b.release();
+  });
+}
+
+gh_status gh_band_destroy(gh_band* band) {
+  return guarded([&] {
+    if (!band) return;
+    cudaSetDevice(band->levels->mesh->device);
+    cudaStreamSynchronize(band->levels->mesh->stream);
+    for (void* p : band->opened) cudaIpcCloseMemHandle(p);
+    delete band;
+  });
+}
+
+gh_status gh_band_info(const gh_band* band, int32_t* lb, int32_t* le, int32_t* own_rows) {
+  return guarded([&] {
+    require(band != nullptr, "gh_band_info: null band");
+    if (lb) *lb = band->band.lb;
+    if (le) *le = band->band.le;
+    if (own_rows) *own_rows = band->band.own_rows;
+  });
+}
+
+gh_status gh_band_export(const gh_band* band, void* blob, int32_t capacity, int32_t* size) {
+  return guarded([&] {
+    require(band && size, "gh_band_export: null argument");
+    *size = (int32_t)sizeof(BandBlob);
+    if (!blob) return;
+    require(capacity >= (int32_t)sizeof(BandBlob), "gh_band_export: blob buffer too small");
+    const gh::Band& b = band->band;
+    BandBlob x{};
+    GH_CUDA(cudaSetDevice(b.device));
+    GH_CUDA(cudaIpcGetMemHandle(&x.ubuf, b.ubuf));
+    GH_CUDA(cudaIpcGetMemHandle(&x.done, b.rows_done));
+    x.nrows = b.nrows;
+    x.lb = b.lb;
+    x.le = b.le;
+    x.ghost_lo_row = b.lb > 0 ? b.ghost_row(b.lb - 1) : -1;
+    x.ghost_hi_row = b.le < b.nlev ? b.ghost_row(b.le) : -1;
+    x.device = b.device;
+    x.magic = kBlobMagic;
+    std::memcpy(blob, &x, sizeof(x));
+  });
+}
+
+gh_status gh_band_connect(gh_band* band, const void* lower_blob, const void* upper_blob) {
+  return guarded([&] {
+    require(band != nullptr, "gh_band_connect: null band");
+    gh::Band& b = band->band;
+    GH_CUDA(cudaSetDevice(b.device));
+    auto open = [&](const cudaIpcMemHandle_t& h) {
+      void* p = nullptr;
+      GH_CUDA(cudaIpcOpenMemHandle(&p, h, cudaIpcMemLazyEnablePeerAccess));
+      band->opened.push_back(p);
+      return p;
+    };
+    if (lower_blob) {
+      BandBlob x;
+      std::memcpy(&x, lower_blob, sizeof(x));
+      require(x.magic == kBlobMagic && x.le == b.lb, "gh_band_connect: lower blob is not the lower neighbour");
+      b.lo_ubuf = static_cast<double*>(open(x.ubuf));
+      b.lo_done = static_cast<unsigned long long*>(open(x.done));
+      b.lo_nrows = x.nrows;
+      b.lo_ghost = x.ghost_hi_row;  // our first level is its upper ghost
+    }
+    if (upper_blob) {
+      BandBlob x;
+      std::memcpy(&x, upper_blob, sizeof(x));
+      require(x.magic == kBlobMagic && x.lb == b.le, "gh_band_connect: upper blob is not the upper neighbour");
+      b.hi_ubuf = static_cast<double*>(open(x.ubuf));
+      b.hi_done = static_cast<unsigned long long*>(open(x.done));
+      b.hi_nrows = x.nrows;
+      b.hi_ghost = x.ghost_lo_row;  // our last level is its lower ghost
+    }
+  });
+}
+
+gh_status gh_band_prepare(gh_band* band, double t, const double* initial) {
+  return guarded([&] {
+    require(band != nullptr, "gh_band_prepare: null band");
+    if (!(t > 0.0)) gh::fail(GH_ERR_INVALID, "gs_diffuse: t must be positive");
+    gh_mesh* m = band->levels->mesh;
+    use_device_of(m);
+    cudaStream_t s = m->stream;
+    gh::Scratch<double> dinit(initial ? m->nv : 0, s);
+    if (initial) GH_CUDA(cudaMemcpyAsync(dinit.p, initial, sizeof(double) * m->nv, cudaMemcpyHostToDevice, s));
+    std::vector<gh::Band*> one{&band->band};
+    gh::bands_prepare(band->levels, one, t, initial ? dinit.p : nullptr);
+    GH_CUDA(cudaStreamSynchronize(s));
+  });
+}
+
+gh_status gh_band_launch(gh_band* band, double t, int32_t sweeps, double* u_out, gh_solver_report* report) {
+  return guarded([&] {
+    require(band != nullptr, "gh_band_launch: null band");
+    require(sweeps >= 1, "gh_band_launch: sweeps must be >= 1");
+    gh_mesh* m = band->levels->mesh;
+    use_device_of(m);
+    cudaStream_t s = m->stream;
+    const double w0 = now_s();
+    take_launches(m);
+    std::vector<gh::Band*> one{&band->band};
+    const double ms = gh::bands_launch(band->levels, one, t, sweeps);
+    if (u_out) to_host(u_out, band->levels->u_orig.p, m->nv, s);
+    else GH_CUDA(cudaStreamSynchronize(s));
+    if (report) {
+      report->iterations = sweeps;
+      report->wall_seconds = now_s() - w0;
+      report->device_ms = ms;
+      report->kernel_launches = take_launches(m);
+    }
+  });
+}
+
+}  // extern "C"

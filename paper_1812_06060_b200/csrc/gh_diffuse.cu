@@ -62,6 +62,7 @@ __global__ void k_init_orig(const int32_t* __restrict__ level, const double* __r
     u[v] = initial ? initial[v] : (level[v] == 0 ? 1.0 : 0.0);
 }
 
+// own rows of a band -> original vertex order
 __global__ void k_scatter(const int32_t* __restrict__ perm, const double* __restrict__ src, int64_t nrows,
                           double* __restrict__ u) {
   for (int64_t r = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; r < nrows; r += (int64_t)gridDim.x * blockDim.x) {
@@ -70,21 +71,14 @@ __global__ void k_scatter(const int32_t* __restrict__ perm, const double* __rest
   }
 }
 
-// ---------------------------------------------------------------- bulk-staged schedule
-// Same step/barrier schedule, but the streamed operands of each 32-row chunk
-// (SELL columns + weights, den, deg: ~86 B of the ~100 B per update) are moved
-// HBM -> shared memory by the bulk-copy engine (cp.async.bulk + mbarrier
-// complete_tx), issued by one producer warp into a ring of chunk slots, while
-// kConsumerWarps warps consume chunks: read the row from shared memory, gather
-// the 6-ish neighbour u values (L2), and store u. The DRAM stream no longer
-// waits behind the gather latency of the warps, so many more bytes are in
-// flight per SM. Rows are still summed in the reference's order (bitwise).
+// ---------------------------------------------------------------- the kernel
 constexpr int kConsumerWarps = 8;
 constexpr int kChunksPerWarp = 2;                            // chunks a consumer warp has in flight
 constexpr int kTileChunks = kConsumerWarps * kChunksPerWarp;  // chunks per ring slot
 constexpr int kTmaThreads = 32 * (kConsumerWarps + 1);
 
-struct TmaArgs {
+// one BFS band (gh::Band) as the kernel sees it
+struct BandArgs {
   const int32_t* pstart;
   const int32_t* pend;
   const int32_t* chunk_level;
@@ -93,14 +87,28 @@ struct TmaArgs {
   const int32_t* col;
   const double* wt;
   const double* den;
-  double* ubuf;
-  int64_t nrows;
+  double* ubuf;                   // [2][nrows]
+  unsigned long long* rows_done;  // [nlev]
+  double* lo_ubuf;                // lower neighbour (holds our level lb as a ghost), or null
+  unsigned long long* lo_done;
+  double* hi_ubuf;                // upper neighbour (holds our level le-1 as a ghost), or null
+  unsigned long long* hi_done;
+  int64_t nrows, lo_nrows, hi_nrows;
+  int32_t lo_ghost, hi_ghost;     // first row of the ghost copy inside the neighbour
+  int32_t lb, le;                 // own levels
+};
+
+constexpr int kMaxBands = 8;  // bands per launch (one per GPU in production; more when emulated)
+
+struct TmaArgs {
+  BandArgs bands[kMaxBands];
+  int32_t block_start[kMaxBands + 1];  // blocks of band i are [block_start[i], block_start[i+1])
+  int32_t nbands;
   int32_t nlev, sweeps;
-  int32_t wcap;      // widest chunk (neighbours per row) a slot holds
-  int32_t nslots;    // ring slots per block
+  int32_t wcap;        // widest chunk (neighbours per row) a slot holds
+  int32_t nslots;      // ring slots per block
   int32_t slot_bytes;
   int32_t table_in_smem;
-  unsigned long long* rows_done;  // per level: rows finished over all sweeps (zeroed per launch)
   double t;
 };
 
@@ -131,35 +139,31 @@ __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t by
 }
 
 // contiguous share of the step's chunk range [c0, c1) for block b
-__device__ __forceinline__ void block_share(int64_t c0, int64_t c1, int64_t b, int64_t nb, int64_t& cb,
-                                            int64_t& ce) {
-  const int64_t n = c1 - c0, q = n / nb, rem = n % nb;
+__device__ __forceinline__ void block_share(int32_t c0, int32_t c1, int32_t b, int32_t nb, int32_t& cb,
+                                            int32_t& ce) {
+  const int32_t n = c1 - c0, q = n / nb, rem = n % nb;
   cb = c0 + b * q + (b < rem ? b : rem);
   ce = cb + q + (b < rem ? 1 : 0);
 }
 
-__device__ __forceinline__ bool step_range(const TmaArgs& a, const int32_t* pstart, const int32_t* pend, int64_t tau,
-                                           int64_t& rb, int64_t& re) {
-  int64_t lhi = tau < a.nlev - 1 ? tau : a.nlev - 1;
+__device__ __forceinline__ unsigned long long ld_acquire_sys_u64(const unsigned long long* p) {
+  unsigned long long v;
+  asm volatile("ld.acquire.sys.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+  return v;
+}
+
+// rows [rb, re) of the band's own levels active at step tau (L = tau - 2s, 0 <= s < S)
+__device__ __forceinline__ bool step_range(int32_t sweeps, int32_t lb, int32_t le, const int32_t* pstart,
+                                           const int32_t* pend, int32_t tau, int32_t& rb, int32_t& re) {
+  int32_t lhi = tau < le - 1 ? tau : le - 1;
   if ((lhi ^ tau) & 1) --lhi;
-  int64_t llo = tau - 2 * (int64_t)(a.sweeps - 1);
-  if (llo < 0) llo = tau & 1;
+  int32_t llo = tau - 2 * (sweeps - 1);
+  if (llo < lb) llo = lb;
+  if ((llo ^ tau) & 1) ++llo;
   if (llo > lhi) return false;
   rb = pstart[llo];
   re = pend[lhi];
   return true;
-}
-
-__device__ __forceinline__ unsigned long long ld_acquire_u64(const unsigned long long* p) {
-  unsigned long long v;
-  asm volatile("ld.acquire.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
-  return v;
-}
-
-__device__ __forceinline__ int32_t ld_acquire_gpu(const int32_t* p) {
-  int32_t v;
-  asm volatile("ld.acquire.gpu.global.s32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
-  return v;
 }
 
 // slot layout: header 256 B (int32: chunk offsets [0..kTileChunks], fits [31], chunk levels [32..])
@@ -169,8 +173,22 @@ constexpr int kDenOff = kHdr;
 constexpr int kDegOff = kDenOff + kTileChunks * 256;
 constexpr int kColOff = kDegOff + kTileChunks * 64;
 
-__global__ void __launch_bounds__(kTmaThreads, 2) k_diffuse_tma(TmaArgs a) {
+// kLinked: the band has neighbour bands (multi-GPU or emulated); the
+// single-band (whole mesh, one GPU) instance compiles without the ghost traffic.
+template <bool kLinked>
+__global__ void __launch_bounds__(kTmaThreads, 2) k_diffuse_tma(const __grid_constant__ TmaArgs a) {
   extern __shared__ __align__(128) unsigned char smem[];
+  // this block's band and its rank inside the band
+  int bi = 0;
+  while (bi + 1 < a.nbands && (int32_t)blockIdx.x >= a.block_start[bi + 1]) ++bi;
+  // the band descriptor stays in the kernel's parameter (constant) bank: fields
+  // are cheap to re-load there, which keeps them out of the register budget
+  const BandArgs* vba = &a.bands[bi];
+  const BandArgs& sba = a.bands[bi];
+  const int32_t band_lb = sba.lb, band_le = sba.le;
+  const int32_t b = (int32_t)blockIdx.x - a.block_start[bi];
+  const int32_t nb = a.block_start[bi + 1] - a.block_start[bi];
+
   uint64_t* full = reinterpret_cast<uint64_t*>(smem);
   uint64_t* empty = full + a.nslots;
   int32_t* sh_pend = reinterpret_cast<int32_t*>(empty + a.nslots);
@@ -186,66 +204,66 @@ __global__ void __launch_bounds__(kTmaThreads, 2) k_diffuse_tma(TmaArgs a) {
     }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
-  const int32_t* pend = a.pend;
-  const int32_t* pstart = a.pstart;
+  const int32_t* pend = sba.pend;
+  const int32_t* pstart = sba.pstart;
   if (a.table_in_smem) {
     for (int i = threadIdx.x; i < a.nlev; i += blockDim.x) {
-      sh_pend[i] = a.pend[i];
-      sh_pstart[i] = a.pstart[i];
+      sh_pend[i] = sba.pend[i];
+      sh_pstart[i] = sba.pstart[i];
     }
     pend = sh_pend;
     pstart = sh_pstart;
   }
   __syncthreads();
 
-  const int64_t nb = gridDim.x, b = blockIdx.x;
-  const int64_t nsteps = (int64_t)(a.nlev - 1) + 2 * (int64_t)(a.sweeps - 1) + 1;
+  const int32_t nsteps = (band_le - 1) + 2 * (a.sweeps - 1) + 1;
   const uint32_t col_cap = (uint32_t)kTileChunks * 32u * a.wcap;  // entries
-  // ring position: slot index and its use parity advance tile by tile (no 64-bit modulo)
+  // ring position: slot index and its use parity advance tile by tile
   int slot = 0;
   uint32_t use = 0;
-  int64_t issued = 0;
+  int32_t issued = 0;
 
   if (warp == kConsumerWarps) {
-    // ---- producer warp: runs ahead across steps, bounded by the ring. Work is a
-    // stream of batches of 32 chunks (4 tiles); the chunk pointers and levels
-    // of the next batch are loaded while the current batch is issued.
+    // ---- producer warp: streams the band's share of every step into the ring,
+    // running ahead across steps (the CSR is read-only). Work is a stream of
+    // batches of 32 chunks; the chunk pointers and levels of the next batch are
+    // loaded while the current batch is issued.
     constexpr int kTilesPerBatch = 32 / kTileChunks;
-    int64_t tau = -1, cb = 0, ce = 0, ntile = 0, t0 = -kTilesPerBatch;
-    auto advance = [&](int64_t& xtau, int64_t& xcb, int64_t& xce, int64_t& xnt, int64_t& xt0) -> bool {
+    int32_t tau = -1, cb = 0, ce = 0, ntile = 0, t0 = -kTilesPerBatch;
+    auto advance = [&](int32_t& xtau, int32_t& xcb, int32_t& xce, int32_t& xnt, int32_t& xt0) -> bool {
       xt0 += kTilesPerBatch;
       while (xt0 >= xnt) {
         if (++xtau >= nsteps) return false;
-        int64_t rb, re;
+        int32_t rb, re;
         xt0 = 0;
         xnt = 0;
-        if (!step_range(a, pstart, pend, xtau, rb, re)) continue;
+        if (!step_range(a.sweeps, band_lb, band_le, pstart, pend, xtau, rb, re)) continue;
         block_share(rb >> 5, (re + 31) >> 5, b, nb, xcb, xce);
         xnt = (xce - xcb + kTileChunks - 1) / kTileChunks;
       }
       return true;
     };
-    auto load = [&](int64_t xcb, int64_t xce, int64_t xt0, int64_t& p0, int32_t& lv0, int64_t& plast) {
-      const int64_t cbase = xcb + xt0 * kTileChunks;
-      const int64_t cl = cbase + lane < xce ? cbase + lane : xce;
-      p0 = __ldg(a.chunk_ptr + cl);
-      lv0 = cbase + lane < xce ? __ldg(a.chunk_level + cl) : 0;
-      plast = __ldg(a.chunk_ptr + (cbase + 32 < xce ? cbase + 32 : xce));
+    auto load = [&](int32_t xcb, int32_t xce, int32_t xt0, int64_t& p0, int32_t& lv0, int64_t& plast) {
+      const int32_t cbase = xcb + xt0 * kTileChunks;
+      const int32_t cl = cbase + lane < xce ? cbase + lane : xce;
+      p0 = __ldg(vba->chunk_ptr + cl);
+      lv0 = cbase + lane < xce ? __ldg(vba->chunk_level + cl) : 0;
+      plast = __ldg(vba->chunk_ptr + (cbase + 32 < xce ? cbase + 32 : xce));
     };
     int64_t p0 = 0, p_last = 0;
     int32_t lv0 = 0;
     bool have = advance(tau, cb, ce, ntile, t0);
     if (have) load(cb, ce, t0, p0, lv0, p_last);
     while (have) {
-      int64_t ntau = tau, ncb = cb, nce = ce, nnt = ntile, nt0 = t0;
+      int32_t ntau = tau, ncb = cb, nce = ce, nnt = ntile, nt0 = t0;
       int64_t np0 = 0, np_last = 0;
       int32_t nlv0 = 0;
       const bool have_next = advance(ntau, ncb, nce, nnt, nt0);
       if (have_next) load(ncb, nce, nt0, np0, nlv0, np_last);
-      const int64_t cbase = cb + t0 * kTileChunks;
+      const int32_t cbase = cb + t0 * kTileChunks;
       for (int j = 0; j < kTilesPerBatch && t0 + j < ntile; ++j) {
         if (issued >= a.nslots) mbar_wait(empty + slot, use ^ 1u);
-        const int64_t c0 = cbase + j * kTileChunks;
+        const int32_t c0 = cbase + j * kTileChunks;
         const int nch = (int)(ce - c0 < kTileChunks ? ce - c0 : kTileChunks);
         const int64_t base = __shfl_sync(0xffffffffu, p0, j * kTileChunks);
         const int src = j * kTileChunks + (lane <= kTileChunks ? lane : 0);
@@ -264,15 +282,15 @@ __global__ void __launch_bounds__(kTmaThreads, 2) k_diffuse_tma(TmaArgs a) {
           unsigned char* sb = reinterpret_cast<unsigned char*>(hdr);
           const uint32_t bytes = (uint32_t)nch * (256u + 64u) + (fits ? ncol * 12u : 0u);
           mbar_expect_tx(full + slot, bytes);
-          bulk_g2s(sb + kDenOff, a.den + c0 * 32, (uint32_t)nch * 256u, full + slot);
-          bulk_g2s(sb + kDegOff, a.deg + c0 * 32, (uint32_t)nch * 64u, full + slot);
+          bulk_g2s(sb + kDenOff, vba->den + (int64_t)c0 * 32, (uint32_t)nch * 256u, full + slot);
+          bulk_g2s(sb + kDegOff, vba->deg + (int64_t)c0 * 32, (uint32_t)nch * 64u, full + slot);
           if (fits && ncol) {
-            bulk_g2s(sb + kColOff, a.col + base, ncol * 4u, full + slot);
-            bulk_g2s(sb + kColOff + col_cap * 4u, a.wt + base, ncol * 8u, full + slot);
+            bulk_g2s(sb + kColOff, vba->col + base, ncol * 4u, full + slot);
+            bulk_g2s(sb + kColOff + col_cap * 4u, vba->wt + base, ncol * 8u, full + slot);
           }
         }
         __syncwarp();
-        ++issued;
+        if (issued < a.nslots) ++issued;
         if (++slot == a.nslots) {
           slot = 0;
           use ^= 1u;
@@ -285,32 +303,31 @@ __global__ void __launch_bounds__(kTmaThreads, 2) k_diffuse_tma(TmaArgs a) {
     return;
   }
 
-  // ---- consumer warps: warp w takes chunk w of every tile. No grid barrier:
-  // before a chunk of level L at step tau, the warp waits (acquire) until
-  // levels L-1, L, L+1 have completed the sweeps its operands come from
-  // (rows_done[X] >= ((tau - X + 1) / 2) * |D_X|); after the step the block
-  // publishes its rows per level (release). Every level starts on a chunk
-  // boundary, so a chunk holds rows of exactly one level.
+  // ---- consumer warps: warp w takes chunks w and w + 8 of every tile. No grid
+  // barrier: before a chunk of level L at step tau the warp waits (acquire)
+  // until levels L-1, L, L+1 have finished the sweeps its operands come from
+  // (rows_done[X] >= ((tau - X + 1) / 2) * |D_X|; ghost levels are counted by
+  // the neighbour band); after the step the block publishes its rows per
+  // level (release), to the neighbour as well for a boundary level.
   int32_t seen_L = -1, seen_L2 = -1;
-  int64_t seen_tau = -1;
-  for (int64_t tau = 0; tau < nsteps; ++tau) {
-    int64_t rb, re;
-    if (!step_range(a, pstart, pend, tau, rb, re)) continue;
-    int64_t cb, ce;
+  int32_t seen_tau = -1;
+  for (int32_t tau = 0; tau < nsteps; ++tau) {
+    int32_t rb, re;
+    if (!step_range(a.sweeps, band_lb, band_le, pstart, pend, tau, rb, re)) continue;
+    int32_t cb, ce;
     block_share(rb >> 5, (re + 31) >> 5, b, nb, cb, ce);
-    const int64_t ntile = (ce - cb + kTileChunks - 1) / kTileChunks;
+    const int32_t ntile = (ce - cb + kTileChunks - 1) / kTileChunks;
     if (ntile == 0) continue;
     int32_t lv_first = 0, lv_last = 0;
     if (warp == 0 && lane == 0) {
-      lv_first = __ldg(a.chunk_level + cb);
-      lv_last = __ldg(a.chunk_level + ce - 1);
+      lv_first = __ldg(vba->chunk_level + cb);
+      lv_last = __ldg(vba->chunk_level + ce - 1);
     }
-    for (int64_t j = 0; j < ntile; ++j) {
+    for (int32_t j = 0; j < ntile; ++j) {
       mbar_wait(full + slot, use);
       const unsigned char* sb = slots + (size_t)slot * a.slot_bytes;
       const int32_t* hdr = reinterpret_cast<const int32_t*>(sb);
       const bool fits = hdr[31] != 0;
-      // this warp's chunks in the tile: q = warp + kConsumerWarps * i
       int32_t Lq[kChunksPerWarp];
       bool live[kChunksPerWarp];
 #pragma unroll
@@ -322,13 +339,14 @@ __global__ void __launch_bounds__(kTmaThreads, 2) k_diffuse_tma(TmaArgs a) {
       if (Lq[0] != seen_L || Lq[kChunksPerWarp - 1] != seen_L2 || tau != seen_tau) {
         // operands: wait for levels L-1, L, L+1 of each chunk (lanes 3i..3i+2)
         const int i = lane / 3;
-        if (i < kChunksPerWarp && Lq[i] >= 0) {
-          const int32_t X = Lq[i] - 1 + lane % 3;
+        const int32_t Li = i == 0 ? Lq[0] : Lq[kChunksPerWarp - 1];  // no dynamic register-array index
+        if (i < kChunksPerWarp && Li >= 0) {
+          const int32_t X = Li - 1 + lane % 3;
           if (X >= 0 && X < a.nlev) {
             const unsigned long long need =
                 (unsigned long long)((tau - X + 1) >> 1) * (unsigned long long)(pend[X] - pstart[X]);
             unsigned ns = 32;
-            while (ld_acquire_u64(a.rows_done + X) < need) {
+            while (ld_acquire_sys_u64(vba->rows_done + X) < need) {
               __nanosleep(ns);
               if (ns < 256) ns <<= 1;
             }
@@ -347,12 +365,12 @@ __global__ void __launch_bounds__(kTmaThreads, 2) k_diffuse_tma(TmaArgs a) {
 #pragma unroll
       for (int i = 0; i < kChunksPerWarp; ++i) {
         const int q = warp + kConsumerWarps * i;
-        const int64_t c = cb + j * kTileChunks + q;
-        const int64_t r = c * 32 + lane;
+        const int32_t c = cb + j * kTileChunks + q;
+        const int32_t r = c * 32 + lane;
         on[i] = live[i] && r < pend[Lq[i]];
         const int32_t sweep = (int32_t)((tau - Lq[i]) >> 1);
-        cur[i] = a.ubuf + (sweep & 1) * a.nrows;
-        prev[i] = a.ubuf + ((sweep & 1) ^ 1) * a.nrows;
+        cur[i] = vba->ubuf + (sweep & 1) * vba->nrows;
+        prev[i] = vba->ubuf + ((sweep & 1) ^ 1) * vba->nrows;
         den[i] = reinterpret_cast<const double*>(sb + kDenOff)[q * 32 + lane];
         d[i] = on[i] ? reinterpret_cast<const uint16_t*>(sb + kDegOff)[q * 32 + lane] : 0;
         fast[i] = fits && d[i] <= kUnroll;
@@ -372,7 +390,7 @@ __global__ void __launch_bounds__(kTmaThreads, 2) k_diffuse_tma(TmaArgs a) {
 #pragma unroll
       for (int i = 0; i < kChunksPerWarp; ++i) {
         const int q = warp + kConsumerWarps * i;
-        const int64_t c = cb + j * kTileChunks + q;
+        const int32_t c = cb + j * kTileChunks + q;
         if (fast[i]) {
           const double* swt =
               reinterpret_cast<const double*>(sb + kColOff + (size_t)col_cap * 4u) + hdr[q] + lane;
@@ -380,16 +398,24 @@ __global__ void __launch_bounds__(kTmaThreads, 2) k_diffuse_tma(TmaArgs a) {
           for (int k = 0; k < kUnroll; ++k)
             if (k < d[i]) num[i] += swt[32 * k] * v[i][k];  // diffusion.hpp:79
         } else if (on[i]) {
-          const int64_t q0 = __ldg(a.chunk_ptr + c) + lane;
+          const int64_t q0 = __ldg(vba->chunk_ptr + c) + lane;
           for (int32_t k = 0; k < d[i]; ++k) {
-            const int32_t cc = __ldg(a.col + q0 + 32 * (int64_t)k);
-            const double w = __ldg(a.wt + q0 + 32 * (int64_t)k);
+            const int32_t cc = __ldg(vba->col + q0 + 32 * (int64_t)k);
+            const double w = __ldg(vba->wt + q0 + 32 * (int64_t)k);
             num[i] += w * __ldcg((cc < 0 ? cur[i] : prev[i]) + (cc & 0x7fffffff));
           }
         }
         if (on[i]) {
+          const int32_t r = c * 32 + lane;
           const double u0 = Lq[i] == 0 ? 1.0 : 0.0;
-          __stcg(cur[i] + c * 32 + lane, (u0 + a.t * num[i]) / den[i]);  // diffusion.hpp:82
+          const double un = (u0 + a.t * num[i]) / den[i];  // diffusion.hpp:82
+          __stcg(cur[i] + r, un);
+          // boundary levels also land in the neighbour band's ghost copy
+          const int64_t par = ((tau - Lq[i]) >> 1) & 1;
+          if (kLinked && Lq[i] == band_lb && vba->lo_ubuf)
+            __stcg(vba->lo_ubuf + par * vba->lo_nrows + vba->lo_ghost + (r - pstart[Lq[i]]), un);
+          if (kLinked && Lq[i] == band_le - 1 && vba->hi_ubuf)
+            __stcg(vba->hi_ubuf + par * vba->hi_nrows + vba->hi_ghost + (r - pstart[Lq[i]]), un);
         }
       }
       __syncwarp();
@@ -405,11 +431,18 @@ __global__ void __launch_bounds__(kTmaThreads, 2) k_diffuse_tma(TmaArgs a) {
       lv_first = __shfl_sync(0xffffffffu, lv_first, 0);
       lv_last = __shfl_sync(0xffffffffu, lv_last, 0);
       for (int32_t X = lv_first + 2 * lane; X <= lv_last; X += 64) {
-        const int64_t lo = cb * 32 > pstart[X] ? cb * 32 : pstart[X];
-        const int64_t hi = ce * 32 < pend[X] ? ce * 32 : pend[X];
+        const int32_t lo = cb * 32 > pstart[X] ? cb * 32 : pstart[X];
+        const int32_t hi = ce * 32 < pend[X] ? ce * 32 : pend[X];
         if (hi > lo) {
-          __threadfence();
-          atomicAdd(a.rows_done + X, (unsigned long long)(hi - lo));
+          const unsigned long long n = (unsigned long long)(hi - lo);
+          unsigned long long* lo_done = kLinked ? vba->lo_done : nullptr;
+          unsigned long long* hi_done = kLinked ? vba->hi_done : nullptr;
+          const bool to_lo = X == band_lb && lo_done, to_hi = X == band_le - 1 && hi_done;
+          if (to_lo || to_hi) __threadfence_system();
+          else __threadfence();
+          atomicAdd(vba->rows_done + X, n);
+          if (to_lo) atomicAdd_system(lo_done + X, n);
+          if (to_hi) atomicAdd_system(hi_done + X, n);
         }
       }
     }
@@ -445,61 +478,147 @@ __global__ void k_residual(const int32_t* __restrict__ vv_off, const int32_t* __
 
 namespace gh {
 
-double diffuse_dev(gh_levels* L, double t, int32_t sweeps, const double* d_initial) {
+namespace {
+
+BandArgs band_args(const Band& b) {
+  BandArgs x{};
+  x.pstart = b.pstart.p;
+  x.pend = b.pend.p;
+  x.chunk_level = b.chunk_level.p;
+  x.chunk_ptr = b.chunk_ptr.p;
+  x.deg = b.deg.p;
+  x.col = b.col.p;
+  x.wt = b.wt.p;
+  x.den = b.den.p;
+  x.ubuf = b.ubuf;
+  x.rows_done = b.rows_done;
+  x.lo_ubuf = b.lo_ubuf;
+  x.lo_done = b.lo_done;
+  x.hi_ubuf = b.hi_ubuf;
+  x.hi_done = b.hi_done;
+  x.nrows = b.nrows;
+  x.lo_nrows = b.lo_nrows;
+  x.hi_nrows = b.hi_nrows;
+  x.lo_ghost = b.lo_ghost;
+  x.hi_ghost = b.hi_ghost;
+  x.lb = b.lb;
+  x.le = b.le;
+  return x;
+}
+
+}  // namespace
+
+// Prepare bands for a solve: den for this t, both sweep buffers = the start
+// state (own and ghost rows), progress counters zeroed. Across processes,
+// every band must be prepared before any band is launched.
+void bands_prepare(gh_levels* L, std::vector<Band*>& bands, double t, const double* d_initial) {
   gh_mesh* m = L->mesh;
   cudaStream_t s = m->stream;
-  const int64_t V = m->nv;
-  if (sweeps < 0) fail(GH_ERR_INVALID, "DiffusionConfig: sweeps must be >= 0");
-  if (!(t > 0.0)) fail(GH_ERR_INVALID, "gs_diffuse: t must be positive");
-  if (L->den_t != t) {
-    k_den<<<grid_for(L->nrows), B, 0, s>>>(L->area_r.p, L->wsum_r.p, t, L->nrows, L->den.p);
+  for (Band* b : bands) {
+    if (b->den_t != t) {
+      k_den<<<grid_for(b->nrows), B, 0, s>>>(b->area_r.p, b->wsum_r.p, t, b->nrows, b->den.p);
+      GH_LAUNCH_CHECK();
+      m->launches++;
+      b->den_t = t;
+    }
+    k_init_buffers<<<grid_for(b->nrows), B, 0, s>>>(b->perm.p, L->level.p, d_initial, b->nrows, b->ubuf);
     GH_LAUNCH_CHECK();
     m->launches++;
-    L->den_t = t;
+    GH_CUDA(cudaMemsetAsync(b->rows_done, 0, sizeof(unsigned long long) * b->nlev, s));
   }
-  k_init_orig<<<grid_for(V), B, 0, s>>>(L->level.p, d_initial, V, L->u_orig.p);
+}
+
+// Run the bands in one cooperative launch on the current device, blocks split
+// in proportion to their rows, then scatter their own rows to u_orig.
+double bands_launch(gh_levels* L, std::vector<Band*>& bands, double t, int32_t sweeps) {
+  gh_mesh* m = L->mesh;
+  cudaStream_t s = m->stream;
+  int32_t wmax = 1;
+  int64_t rows = 0;
+  for (Band* b : bands) {
+    wmax = std::max(wmax, b->max_chunk_width);
+    rows += b->own_rows;
+  }
+  // slot = 256 B header + per chunk (den 256 B + deg 64 B + wcap x 32 x 12 B of columns/weights)
+  const int32_t wcap = std::min<int32_t>(wmax, 16);
+  const int32_t slot_bytes = ((kColOff + kTileChunks * 32 * wcap * 12) + 127) & ~127;
+  const bool table = L->nlev <= kMaxSmemLevels;
+  const size_t table_bytes = table ? ((2 * sizeof(int32_t) * L->nlev + 127) & ~size_t(127)) : 0;
+  // two blocks per SM with a ring of >= 2 slots each (228 KB per SM, 1 KB reserved per block)
+  int32_t nslots = 0;
+  for (int per = 2; per >= 1 && nslots < 2; --per) {
+    const int64_t budget = 228 * 1024 / per - 1024;
+    nslots = (int32_t)std::min<int64_t>(8, (budget - (int64_t)table_bytes - 256) / (slot_bytes + 16));
+  }
+  if (nslots < 2) nslots = 2;
+  const size_t shmem = 16 * (size_t)nslots + table_bytes + 128 + (size_t)nslots * slot_bytes;
+  bool linked = false;
+  for (Band* b : bands) linked |= b->lo_ubuf != nullptr || b->hi_ubuf != nullptr;
+  void* fn = linked ? (void*)k_diffuse_tma<true> : (void*)k_diffuse_tma<false>;
+  GH_CUDA(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)shmem));
+  int nsm = 0, per_sm = 0;
+  GH_CUDA(cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, m->device));
+  GH_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, kTmaThreads, shmem));
+  if (per_sm < 1) fail(GH_ERR_CUDA, "diffusion kernel cannot be resident");
+  const int32_t nbands = (int32_t)bands.size();
+  const int32_t grid = std::max<int32_t>(nsm * per_sm, nbands);
+  // blocks per band in proportion to own rows, at least one each
+  std::vector<int32_t> start(nbands + 1, 0);
+  for (int32_t i = 0; i < nbands; ++i) {
+    const int64_t share = rows ? (int64_t)(grid - nbands) * bands[i]->own_rows / rows : 0;
+    start[i + 1] = start[i] + 1 + (int32_t)share;
+  }
+  start[nbands] = std::min(start[nbands], grid);
+  if (nbands > kMaxBands) fail(GH_ERR_INVALID, "too many bands for one launch");
+  TmaArgs a{};
+  for (int32_t i = 0; i < nbands; ++i) a.bands[i] = band_args(*bands[i]);
+  for (int32_t i = 0; i <= nbands; ++i) a.block_start[i] = start[i];
+  a.nbands = nbands;
+  a.nlev = L->nlev;
+  a.sweeps = sweeps;
+  a.wcap = wcap;
+  a.nslots = nslots;
+  a.slot_bytes = slot_bytes;
+  a.table_in_smem = table ? 1 : 0;
+  a.t = t;
+  void* kargs[] = {&a};
+  EventTimer timer(s);
+  timer.start();
+  GH_CUDA(cudaLaunchCooperativeKernel(fn, start[nbands], kTmaThreads, kargs, shmem, s));
+  GH_LAUNCH_CHECK();
+  timer.stop();
+  m->launches++;
+  const double ms = timer.ms();
+  for (Band* b : bands) {
+    const double* result = b->ubuf + ((sweeps - 1) & 1) * (int64_t)b->nrows;
+    k_scatter<<<grid_for(b->own_rows), B, 0, s>>>(b->perm.p, result, b->own_rows, L->u_orig.p);
+    GH_LAUNCH_CHECK();
+    m->launches++;
+  }
+  return ms;
+}
+
+
+namespace {
+}  // namespace
+
+double diffuse_dev(gh_levels* L, double t, int32_t sweeps, const double* d_initial) {
+  std::vector<Band*> one{&L->main};
+  return diffuse_bands_dev(L, one, t, sweeps, d_initial);
+}
+
+double diffuse_bands_dev(gh_levels* L, std::vector<Band*>& bands, double t, int32_t sweeps, const double* d_initial) {
+  gh_mesh* m = L->mesh;
+  cudaStream_t s = m->stream;
+  if (sweeps < 0) fail(GH_ERR_INVALID, "DiffusionConfig: sweeps must be >= 0");
+  if (!(t > 0.0)) fail(GH_ERR_INVALID, "gs_diffuse: t must be positive");
+  k_init_orig<<<grid_for(m->nv), B, 0, s>>>(L->level.p, d_initial, m->nv, L->u_orig.p);
   GH_LAUNCH_CHECK();
   m->launches++;
   double ms = 0.0;
   if (sweeps > 0 && L->nreach > 0) {
-    k_init_buffers<<<grid_for(L->nrows), B, 0, s>>>(L->perm.p, L->level.p, d_initial, L->nrows, L->ubuf.p);
-    GH_LAUNCH_CHECK();
-    m->launches++;
-    int nsm = 0, per_sm = 0;
-    GH_CUDA(cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, m->device));
-    EventTimer timer(s);
-    {
-      // slot = 64 B header + per chunk (den 256 B + deg 64 B + wcap x 32 x 12 B of columns/weights)
-      const int32_t wcap = std::min<int32_t>(std::max<int32_t>(L->max_chunk_width, 1), 16);
-      const int32_t slot_bytes = ((kColOff + kTileChunks * 32 * wcap * 12) + 127) & ~127;
-      const bool table = L->nlev <= kMaxSmemLevels;
-      const size_t table_bytes = table ? ((2 * sizeof(int32_t) * L->nlev + 127) & ~size_t(127)) : 0;
-      // two blocks per SM with a ring of >= 2 slots each (228 KB per SM, 1 KB reserved per block)
-      int32_t nslots = 0;
-      for (int per = 2; per >= 1 && nslots < 2; --per) {
-        const int64_t budget = 228 * 1024 / per - 1024;
-        nslots = (int32_t)std::min<int64_t>(8, (budget - (int64_t)table_bytes - 256) / (slot_bytes + 16));
-      }
-      if (nslots < 2) nslots = 2;
-      const size_t shmem = 16 * (size_t)nslots + table_bytes + 128 + (size_t)nslots * slot_bytes;
-      GH_CUDA(cudaFuncSetAttribute((void*)k_diffuse_tma, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)shmem));
-      TmaArgs a{L->pstart.p, L->pend.p, L->chunk_level.p, L->chunk_ptr.p, L->deg.p, L->col.p, L->wt.p, L->den.p,
-                L->ubuf.p, L->nrows, L->nlev, sweeps, wcap, nslots, slot_bytes, table ? 1 : 0, L->rows_done.p, t};
-      GH_CUDA(cudaMemsetAsync(L->rows_done.p, 0, sizeof(unsigned long long) * L->nlev, s));
-      GH_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_diffuse_tma, kTmaThreads, shmem));
-      if (per_sm < 1) fail(GH_ERR_CUDA, "diffusion kernel cannot be resident");
-      void* args[] = {&a};
-      timer.start();
-      GH_CUDA(cudaLaunchCooperativeKernel((void*)k_diffuse_tma, nsm * per_sm, kTmaThreads, args, shmem, s));
-      GH_LAUNCH_CHECK();
-      timer.stop();
-    }
-    m->launches++;
-    ms = timer.ms();
-    const double* result = L->ubuf.p + ((sweeps - 1) & 1) * (int64_t)L->nrows;
-    k_scatter<<<grid_for(L->nrows), B, 0, s>>>(L->perm.p, result, L->nrows, L->u_orig.p);
-    GH_LAUNCH_CHECK();
-    m->launches++;
+    bands_prepare(L, bands, t, d_initial);
+    ms = bands_launch(L, bands, t, sweeps);
   }
   L->u_valid = 1;
   L->u_sweeps = sweeps;

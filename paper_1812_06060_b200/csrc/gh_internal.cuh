@@ -130,31 +130,62 @@ struct gh_mesh {
   uint64_t device_bytes() const;
 };
 
+namespace gh {
+
+// Diffusion layout of one BFS band: own levels [lb, le) plus ghost copies of
+// the neighbouring levels lb-1 and le. The single-GPU
+// path is one band [0, nlev) without ghosts; multi-GPU runs one band per GPU,
+// and the single-GPU emulation runs several bands in one launch.
+//   rows: own levels in (parity, level, original index) order, each level
+//   32-row aligned; then the ghost levels, each 32-row aligned.
+struct Band {
+  int32_t lb = 0, le = 0, nlev = 0;
+  int32_t nrows = 0;      // own + ghost rows (32-aligned)
+  int32_t own_rows = 0;   // rows [0, own_rows) are own levels
+  int32_t own_chunks = 0;
+  int32_t max_chunk_width = 0;
+  int32_t device = 0;
+  std::vector<int32_t> h_pstart, h_pend;  // by level; valid on own and ghost levels
+  DevBuf<int32_t> pstart, pend;
+  DevBuf<int32_t> perm;         // row -> original vertex (-1 for padding)
+  DevBuf<int32_t> chunk_level;  // level of each own chunk (a chunk holds one level)
+  DevBuf<int64_t> chunk_ptr;    // SELL-32 chunk offsets (own chunks)
+  DevBuf<uint16_t> deg;         // row lengths
+  DevBuf<int32_t> col;          // local row of the neighbour | 0x80000000 if one level closer to the sources
+  DevBuf<double> wt;            // cotan weights in the reference's row order
+  DevBuf<double> area_r, wsum_r, den;
+  double den_t = 0.0;
+  // state shared with neighbour bands: plain cudaMalloc so it can be IPC-exported
+  double* ubuf = nullptr;                   // [2][nrows] sweep-parity buffers
+  unsigned long long* rows_done = nullptr;  // [nlev] rows finished per level over all sweeps
+  // links to the neighbours' copies of this band's boundary levels
+  double* lo_ubuf = nullptr;
+  unsigned long long* lo_done = nullptr;
+  int64_t lo_nrows = 0;
+  int32_t lo_ghost = 0;  // row of level lb inside the lower neighbour
+  double* hi_ubuf = nullptr;
+  unsigned long long* hi_done = nullptr;
+  int64_t hi_nrows = 0;
+  int32_t hi_ghost = 0;  // row of level le-1 inside the upper neighbour
+  Band() = default;
+  Band(const Band&) = delete;
+  Band& operator=(const Band&) = delete;
+  ~Band();
+  uint64_t device_bytes() const;
+  int32_t ghost_row(int32_t level) const { return h_pstart[level]; }
+};
+
+}  // namespace gh
+
 struct gh_levels {
   gh_mesh* mesh = nullptr;
   int32_t nlev = 0, unreachable = 0, nreach = 0, max_width = 0;
   std::vector<int32_t> h_offsets;  // BFS order ring boundaries (nlev + 1)
   gh::DevBuf<int32_t> level, parent, order, offsets;  // level/parent [V], order [nreach], offsets [nlev+1]
-  // diffusion layout: rows renumbered by (level parity, level, original index)
-  int32_t nrows = 0;      // size of the new index space (odd class starts 32-aligned)
-  int32_t nchunks = 0;    // nrows / 32
-  std::vector<int32_t> h_pstart, h_pend;           // per level: new-index range
-  gh::DevBuf<int32_t> pstart, pend;                // same, on device
-  gh::DevBuf<int32_t> perm;                        // new row -> original vertex (-1 for padding rows)
-  gh::DevBuf<int32_t> chunk_level;                 // level of each chunk's first row
-  gh::DevBuf<int64_t> chunk_ptr;                   // SELL-32 chunk offsets
-  gh::DevBuf<uint16_t> deg;                        // row lengths
-  gh::DevBuf<int32_t> col;                         // new-index neighbour | 0x80000000 if at level L-1
-  gh::DevBuf<double> wt;                           // cotan weights, reference row order
-  gh::DevBuf<double> area_r, wsum_r;               // vertex_area / vertex_weight_sum in row order
-  gh::DevBuf<double> den;                          // A_j + t * sum theta_j for the current t
-  gh::DevBuf<double> ubuf;                         // 2 * nrows: sweep-parity double buffer
-  double den_t = 0.0;                              // t that `den` holds
-  int32_t u_valid = 0;                             // ubuf holds a finished solve
+  gh::Band main;                                       // the whole level range
+  int32_t u_valid = 0;
   int32_t u_sweeps = 0;
-  gh::DevBuf<double> u_orig;                       // last diffusion result, original order [V]
-  int32_t max_chunk_width = 0;                     // widest SELL chunk (neighbours per row)
-  gh::DevBuf<unsigned long long> rows_done;        // per-level progress counters of the diffusion kernel
+  gh::DevBuf<double> u_orig;  // last diffusion result, original order [V]
   uint64_t device_bytes() const;
 };
 
@@ -165,11 +196,22 @@ void mesh_build(gh_mesh* m, const double* h_pos, const int32_t* h_faces);
 double mesh_average_edge_length(gh_mesh* m);
 void face_gradient_dev(gh_mesh* m, const double* d_u, double* d_grad);
 
-// BFS + diffusion layout (gh_bfs.cu)
+// BFS (gh_bfs.cu)
 void bfs_build(gh_levels* L, const int32_t* h_sources, int32_t ns);
+
+// band layouts (gh_band.cu)
+std::vector<int32_t> plan_bands(const std::vector<int32_t>& offsets, int32_t nbands);
+void band_build(gh_levels* L, Band* b, int32_t lb, int32_t le);
+void band_link(Band* lower, Band* upper);  // same-process neighbours (emulation)
 
 // diffusion (gh_diffuse.cu): result stays in L->u_orig (original order)
 double diffuse_dev(gh_levels* L, double t, int32_t sweeps, const double* d_initial);
+// the same solve split into bands that each compute their own levels and
+// exchange boundary levels; all bands on the current device in one launch
+double diffuse_bands_dev(gh_levels* L, std::vector<Band*>& bands, double t, int32_t sweeps, const double* d_initial);
+// the two halves of diffuse_bands_dev, for bands that live in other processes
+void bands_prepare(gh_levels* L, std::vector<Band*>& bands, double t, const double* d_initial);
+double bands_launch(gh_levels* L, std::vector<Band*>& bands, double t, int32_t sweeps);
 double diffusion_residual_dev(gh_levels* L, const double* d_u, double t);
 
 // normalisation + optimisation (gh_grad.cu)

@@ -234,3 +234,27 @@ def test_residual_tolerance_early_stop(gpu, case):
     tol = float(g["tolerance"])
     for e1 in rep.residual_history:
         assert abs(e1 / tol - 1.0) > 1e-9
+
+
+@pytest.mark.parametrize("nbands", [2, 3, 4, 8])
+def test_band_sharded_diffusion_bitwise(gpu, nbands):
+    """The multi-GPU band schedule (ghost levels written by the neighbour band
+    through its peer pointers + per-level counters), emulated with all bands in
+    one launch on this GPU: bit-identical to gs_diffuse on every fixture with
+    enough levels and on config 3 at reduced size."""
+    from paper_1812_06060_b200 import bands, meshgen
+    gh = gpu
+    for case in CASES:
+        g = np.load(os.path.join(GOLDEN, case + ".npz"))
+        if len(g["offsets"]) - 1 < nbands or int(g["sweeps"]) == 0:
+            continue
+        mesh = gh.build_mesh(g["positions"], g["faces"])
+        lv = gh.bfs_levels(mesh, g["sources"])
+        u = bands.gs_diffuse_bands(mesh, lv, nbands, float(g["t"]), int(g["sweeps"]))
+        assert_same(u, g["u"], f"{case} with {nbands} bands")
+    w = meshgen.config(3, scale=8)
+    mesh = gh.build_mesh(w.positions, w.faces)
+    lv = gh.bfs_levels(mesh, w.sources)
+    t = gh.diffusion_time(mesh, 1.0)
+    one = gh.gs_diffuse(mesh, lv, t, gh.DiffusionConfig(sweeps=200))
+    assert_same(bands.gs_diffuse_bands(mesh, lv, nbands, t, 200), one, f"config 3/8 with {nbands} bands")
