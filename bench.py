@@ -18,9 +18,11 @@ config that fits one GPU with the CPU reference timed beside it: torus
   --impl reference  the reference's own CPU gs_diffuse (oracle/_ref, the
          unmodified reference headers, all host threads) on a bounded sample.
 
-Multi-GPU (torchrun, N > 1): every rank runs the same workload on its own GPU
-(replicas; the band-sharded path of SURVEY §8(e) is not built yet), value is
-the total over ranks / the max time over ranks.
+Multi-GPU (torchrun, N > 1): the diffusion is sharded into BFS bands, one per
+rank; ranks exchange their boundary levels through CUDA IPC
+peer memory inside the one diffusion kernel. value = the whole solve's
+vertex-updates / the slowest rank's kernel time (strong scaling: the mesh is
+fixed); the roofline is rank 0's own band.
 """
 from __future__ import annotations
 
@@ -116,7 +118,7 @@ def load_peaks():
 
 def algorithmic_bytes_per_sweep(vv_offset: np.ndarray, reach_mask: np.ndarray) -> int:
     """28 + 12*deg bytes per vertex-update (row ptr 4, deg x (col 4 + weight 8),
-    den 8, u read 8, u write 8), summed over reachable vertices."""
+    den 8, u read 8, u write 8), summed over the vertices in the mask."""
     deg = np.diff(vv_offset.astype(np.int64))[reach_mask]
     return int(28 * deg.size + 12 * deg.sum())
 
@@ -228,69 +230,95 @@ def main():
         print(json.dumps(line), flush=True)
         return
 
+    import ctypes as C
+
     import paper_1812_06060_b200 as gh
+    from paper_1812_06060_b200 import bands as GB
     from paper_1812_06060_b200 import geoheat as G
+    L = gh.geoheat._lib.load()
     if world > 1:
-        gh.geoheat._lib.load().gh_set_device(local)
+        G._check(L.gh_set_device(local))
     mesh = gh.build_mesh(w.positions, w.faces)
     lv = gh.bfs_levels(mesh, w.sources)
     t = w.t if w.t is not None else gh.diffusion_time(mesh, w.m)
     reach = mesh.vertex_count() - lv.unreachable_count
     vv_off = mesh.download("vv_offset")
-    reach_mask = lv.level_of_vertex >= 0
-    bytes_per_sweep = algorithmic_bytes_per_sweep(vv_off, reach_mask)
+    level = lv.level_of_vertex
     cfg = G.DiffusionConfig(m=w.m, sweeps=w.sweeps)
 
-    # ---- value: device-resident diffusion solves
+    # ---- value: device-resident diffusion solves (one launch per step)
+    band = None
+    if world > 1:
+        # BFS-band sharding: this rank computes its band of levels;
+        # neighbours exchange boundary levels through peer memory inside the kernel
+        band = GB.Band(lv, rank, world)
+        band.connect_via(dist)
+        mine = band.own_mask()
+    else:
+        mine = level >= 0
+    bytes_per_sweep = algorithmic_bytes_per_sweep(vv_off, mine)
+    rows_mine = int(mine.sum())
+
+    def one_solve(rep):
+        if band is None:
+            G.gs_diffuse(mesh, lv, t, cfg, rep, keep_on_device=True)
+        else:
+            band.prepare(t)
+            barrier(dist)  # every rank's counters are zeroed before any kernel runs
+            band.launch(t, w.sweeps, rep, copy_out=False)
+
     launches = 0
     for _ in range(a.warmup):
-        G.gs_diffuse(mesh, lv, t, cfg, keep_on_device=True)
+        one_solve(G.SolverReport())
     barrier(dist)
     cuda_sync()
     kernel_ms = []
     with ClockSampler(local) as clk:
         for _ in range(a.steps):
             rep = G.SolverReport()
-            G.gs_diffuse(mesh, lv, t, cfg, rep, keep_on_device=True)
+            one_solve(rep)
             kernel_ms.append(rep.device_ms)
             launches += rep.kernel_launches
     cuda_sync()
     barrier(dist)
     step_ms = float(np.mean(kernel_ms))
     step_ms_max = max_over_ranks(dist, step_ms, local)
-    value = world * reach * w.sweeps / (step_ms_max * 1e-3)
+    value = reach * w.sweeps / (step_ms_max * 1e-3)  # total work over all ranks / slowest rank
 
     peak, peak_src = load_peaks()
     achieved = bytes_per_sweep * w.sweeps / (step_ms * 1e-3) / 1e9
-    traffic, traffic_src = recorded_traffic(workload, w.sweeps)
+    traffic, traffic_src = recorded_traffic(workload, w.sweeps) if world == 1 else (None, None)
 
     # ---- e2e: host arrays in -> distances out through the C ABI, pinned buffers
-    L = gh.geoheat._lib.load()
-    import ctypes as C
     P = np.ascontiguousarray(w.positions, dtype=np.float64)
     Fc = np.ascontiguousarray(w.faces, dtype=np.int32)
+    S = np.ascontiguousarray(w.sources, dtype=np.int32)
     nbytes_p, nbytes_f, nbytes_d = P.nbytes, Fc.nbytes, 8 * P.shape[0]
     pp, pf, pd = C.c_void_p(), C.c_void_p(), C.c_void_p()
     for ptr, nb in ((pp, nbytes_p), (pf, nbytes_f), (pd, nbytes_d)):
         G._check(L.gh_host_alloc(nb, C.byref(ptr)))
-    np.ctypeslib.as_array((C.c_double * P.size).from_address(pp.value))[:] = P.ravel()
-    np.ctypeslib.as_array((C.c_int32 * Fc.size).from_address(pf.value))[:] = Fc.ravel()
-    S = np.ascontiguousarray(w.sources, dtype=np.int32)
+    C.memmove(pp, P.ctypes.data, P.nbytes)
+    C.memmove(pf, Fc.ctypes.data, Fc.nbytes)
     pcfg = G._pipeline_config(w.method, w.sweeps, w.t, w.m, G.AdmmConfig(max_iterations=w.admm_iters))
-    e2e_s, e2e_rep = [], None
+    e2e_s, stages, e2e_extra = [], {}, {}
     for i in range(1 + a.e2e_steps):
-        rr = G.gh_run_report()
         barrier(dist)
         t0 = time.perf_counter()
-        G._check(L.gh_distance_host(pp, P.shape[0], pf, Fc.shape[0], S.ctypes.data_as(C.c_void_p), S.size,
-                                    C.byref(pcfg), pd, C.byref(rr)))
-        dt = time.perf_counter() - t0
-        if i > 0:  # first call is a warm-up (module load, pool growth)
+        if world == 1:
+            rr = G.gh_run_report()
+            G._check(L.gh_distance_host(pp, P.shape[0], pf, Fc.shape[0], S.ctypes.data_as(C.c_void_p), S.size,
+                                        C.byref(pcfg), pd, C.byref(rr)))
+            dt = time.perf_counter() - t0
+            stages = {"build": rr.build_ms, "bfs_layout": rr.bfs_ms, "diffusion": rr.diffusion_ms,
+                      "normalize": rr.normalize_ms, "admm": rr.optimization_ms, "integrate": rr.integration_ms,
+                      "d2h": rr.d2h_ms}
+            e2e_extra = {"admm_iterations": rr.admm_iterations, "zero_count": rr.zero_count}
+        else:
+            dt, stages, e2e_extra = sharded_e2e(G, GB, L, w, P, Fc, S, pp, pf, pd, rank, world, local, dist)
+        if i > 0:  # the first call is a warm-up (module load, pool growth)
             e2e_s.append(dt)
-            e2e_rep = rr
-            launches_e2e = rr.kernel_launches
     e2e_sec = max_over_ranks(dist, float(np.mean(e2e_s)), local)
-    e2e_value = world * reach * w.sweeps / e2e_sec
+    e2e_value = reach * w.sweeps / e2e_sec
     for ptr in (pp, pf, pd):
         L.gh_host_free(ptr)
 
@@ -307,27 +335,68 @@ def main():
                    "sample": f"unavailable: {e}"}
     line = {
         "metric": METRIC, "value": value, "unit": "vertex-updates/s", "n_gpus": world, "steps": a.steps,
-        "warmup": a.warmup, "ms_per_step": step_ms_max, "higher_is_better": True, "scaling": "weak",
-        "vs_baseline": None, "dtype": "f64", "data": "synthetic (seeded BASELINE config mesh, DESIGN.md §5)",
+        "warmup": a.warmup, "ms_per_step": step_ms_max, "higher_is_better": True,
+        "scaling": "weak" if world == 1 else "strong", "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic (seeded BASELINE config mesh, DESIGN.md §5)",
         "config": dict(base_cfg, t=t, levels=lv.level_count(), max_level_width=lv.max_level_width,
-                       parallelism="single-gpu" if world == 1 else f"replicas x{world}"),
+                       parallelism="single-gpu" if world == 1 else f"bfs-bands x{world}",
+                       **({} if band is None else {"band_levels_rank0": [band.lb, band.le],
+                                                   "band_rows_rank0": rows_mine})),
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
                      "traffic": traffic, "peak_source": peak_src, "kernel": "k_diffuse_tma",
                      "algorithmic_bytes_per_launch": bytes_per_sweep * w.sweeps,
-                     "bytes_per_vertex_update": bytes_per_sweep / reach, "traffic_source": traffic_src},
+                     "bytes_per_vertex_update": bytes_per_sweep / max(rows_mine, 1), "traffic_source": traffic_src,
+                     "scope": "per GPU (rank 0)" if world > 1 else "whole launch"},
         "e2e": {"value": e2e_value, "unit": "vertex-updates/s", "seconds": e2e_sec,
                 "h2d_bytes_per_step": nbytes_p + nbytes_f + S.nbytes, "d2h_bytes_per_step": nbytes_d,
-                "stages_ms": {"build": e2e_rep.build_ms, "bfs_layout": e2e_rep.bfs_ms,
-                              "diffusion": e2e_rep.diffusion_ms, "normalize": e2e_rep.normalize_ms,
-                              "admm": e2e_rep.optimization_ms, "integrate": e2e_rep.integration_ms,
-                              "d2h": e2e_rep.d2h_ms},
-                "admm_iterations": e2e_rep.admm_iterations, "zero_count": e2e_rep.zero_count},
+                "stages_ms": stages, **e2e_extra},
         "gpu_launches": launches,
         "clocks": clk.summary(),
         "cpu_baseline": cpu,
     }
     print(json.dumps(line), flush=True)
 
+
+def sharded_e2e(G, GB, L, w, P, Fc, S, pp, pf, pd, rank, world, local, dist):
+    """One end-to-end solve with the diffusion sharded over the ranks: every rank
+    builds the mesh and BFS from the pinned host arrays, runs its band, the
+    band results are merged (NCCL all-reduce of the per-rank vertices), and
+    normalisation, ADMM and integration run through the C ABI on every rank."""
+    import ctypes as C
+
+    import torch
+    t0 = time.perf_counter()
+    mesh_h = C.c_void_p()
+    G._check(L.gh_mesh_create(pp, P.shape[0], pf, Fc.shape[0], C.byref(mesh_h)))
+    mesh = G.TriMesh(mesh_h)
+    t1 = time.perf_counter()
+    lv = G.bfs_levels(mesh, S)
+    t_ = w.t if w.t is not None else G.diffusion_time(mesh, w.m)
+    band = GB.Band(lv, rank, world)
+    band.connect_via(dist)
+    band.prepare(t_)
+    t2 = time.perf_counter()
+    barrier(dist)
+    rep = G.SolverReport()
+    u = band.launch(t_, w.sweeps, rep)
+    t3 = time.perf_counter()
+    mine = torch.from_numpy(np.where(band.own_mask(), u, 0.0)).cuda(local)
+    dist.all_reduce(mine)
+    u = mine.cpu().numpy()
+    u[lv.level_of_vertex < 0] = 0.0
+    t4 = time.perf_counter()
+    H = G.normalized_target_gradients(mesh, u)
+    if w.method == "face":
+        r = G.admm_face_optimize(mesh, H.field, G.AdmmConfig(max_iterations=w.admm_iters))
+        d = G.integrate_face_gradients(mesh, lv, r.gradients)
+    else:
+        r = G.admm_edge_optimize(mesh, H.field, G.AdmmConfig(max_iterations=w.admm_iters))
+        d = G.integrate_edge_differences(mesh, lv, r.differences)
+    C.memmove(pd, d.ctypes.data, d.nbytes)
+    t5 = time.perf_counter()
+    stages = {"build": 1e3 * (t1 - t0), "bfs_band_setup": 1e3 * (t2 - t1), "diffusion": rep.device_ms,
+              "diffusion_wall": 1e3 * (t3 - t2), "merge_u": 1e3 * (t4 - t3), "normalize_admm_integrate": 1e3 * (t5 - t4)}
+    return t5 - t0, stages, {"admm_iterations": r.report.iterations, "zero_count": H.zero_count}
 
 if __name__ == "__main__":
     main()

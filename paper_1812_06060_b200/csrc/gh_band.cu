@@ -98,6 +98,7 @@ Band::~Band() {
   if (ubuf || rows_done) cudaSetDevice(device);
   if (ubuf) cudaFree(ubuf);
   if (rows_done) cudaFree(rows_done);
+  if (stalled) cudaFree(stalled);
 }
 
 uint64_t Band::device_bytes() const {
@@ -223,6 +224,7 @@ void band_build(gh_levels* L, Band* b, int32_t lb, int32_t le) {
   if (!b->ubuf) {
     GH_CUDA(cudaMalloc(&b->ubuf, sizeof(double) * 2 * (size_t)b->nrows));
     GH_CUDA(cudaMalloc(&b->rows_done, sizeof(unsigned long long) * nlev));
+    GH_CUDA(cudaMalloc(&b->stalled, sizeof(int32_t)));
   }
   m->launches += 4;
   GH_CUDA(cudaStreamSynchronize(s));

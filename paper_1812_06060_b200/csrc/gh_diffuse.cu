@@ -36,7 +36,6 @@ namespace {
 
 constexpr int B = gh::kBlock;
 constexpr int kMaxSmemLevels = 6 * 1024;  // pstart/pend tables in shared memory (48 KB)
-constexpr int kUnroll = 8;                  // rows up to this valence take the unrolled path
 
 __global__ void k_den(const double* __restrict__ area, const double* __restrict__ wsum, double t, int64_t n,
                       double* __restrict__ den) {
@@ -93,6 +92,7 @@ struct BandArgs {
   unsigned long long* lo_done;
   double* hi_ubuf;                // upper neighbour (holds our level le-1 as a ghost), or null
   unsigned long long* hi_done;
+  int32_t* stalled;               // set when a dependency never arrives (a dead peer): the kernel bails out
   int64_t nrows, lo_nrows, hi_nrows;
   int32_t lo_ghost, hi_ghost;     // first row of the ghost copy inside the neighbour
   int32_t lb, le;                 // own levels
@@ -173,9 +173,9 @@ constexpr int kDenOff = kHdr;
 constexpr int kDegOff = kDenOff + kTileChunks * 256;
 constexpr int kColOff = kDegOff + kTileChunks * 64;
 
-// kLinked: the band has neighbour bands (multi-GPU or emulated); the
-// single-band (whole mesh, one GPU) instance compiles without the ghost traffic.
-template <bool kLinked>
+// kUnroll: rows up to this valence are gathered fully unrolled (6 covers
+// icosphere and torus meshes and saves the registers of two more gathers).
+template <int kUnroll>
 __global__ void __launch_bounds__(kTmaThreads, 2) k_diffuse_tma(const __grid_constant__ TmaArgs a) {
   extern __shared__ __align__(128) unsigned char smem[];
   // this block's band and its rank inside the band
@@ -346,9 +346,14 @@ __global__ void __launch_bounds__(kTmaThreads, 2) k_diffuse_tma(const __grid_con
             const unsigned long long need =
                 (unsigned long long)((tau - X + 1) >> 1) * (unsigned long long)(pend[X] - pstart[X]);
             unsigned ns = 32;
+            const long long t0 = clock64();
             while (ld_acquire_sys_u64(vba->rows_done + X) < need) {
               __nanosleep(ns);
               if (ns < 256) ns <<= 1;
+              if (clock64() - t0 > (1ll << 35)) {  // ~17 s at 1.9 GHz: a neighbour is gone
+                atomicExch(vba->stalled, 1);
+                break;
+              }
             }
           }
         }
@@ -412,9 +417,9 @@ __global__ void __launch_bounds__(kTmaThreads, 2) k_diffuse_tma(const __grid_con
           __stcg(cur[i] + r, un);
           // boundary levels also land in the neighbour band's ghost copy
           const int64_t par = ((tau - Lq[i]) >> 1) & 1;
-          if (kLinked && Lq[i] == band_lb && vba->lo_ubuf)
+          if (Lq[i] == band_lb && vba->lo_ubuf)
             __stcg(vba->lo_ubuf + par * vba->lo_nrows + vba->lo_ghost + (r - pstart[Lq[i]]), un);
-          if (kLinked && Lq[i] == band_le - 1 && vba->hi_ubuf)
+          if (Lq[i] == band_le - 1 && vba->hi_ubuf)
             __stcg(vba->hi_ubuf + par * vba->hi_nrows + vba->hi_ghost + (r - pstart[Lq[i]]), un);
         }
       }
@@ -435,8 +440,8 @@ __global__ void __launch_bounds__(kTmaThreads, 2) k_diffuse_tma(const __grid_con
         const int32_t hi = ce * 32 < pend[X] ? ce * 32 : pend[X];
         if (hi > lo) {
           const unsigned long long n = (unsigned long long)(hi - lo);
-          unsigned long long* lo_done = kLinked ? vba->lo_done : nullptr;
-          unsigned long long* hi_done = kLinked ? vba->hi_done : nullptr;
+          unsigned long long* lo_done = vba->lo_done;
+          unsigned long long* hi_done = vba->hi_done;
           const bool to_lo = X == band_lb && lo_done, to_hi = X == band_le - 1 && hi_done;
           if (to_lo || to_hi) __threadfence_system();
           else __threadfence();
@@ -492,6 +497,7 @@ BandArgs band_args(const Band& b) {
   x.den = b.den.p;
   x.ubuf = b.ubuf;
   x.rows_done = b.rows_done;
+  x.stalled = b.stalled;
   x.lo_ubuf = b.lo_ubuf;
   x.lo_done = b.lo_done;
   x.hi_ubuf = b.hi_ubuf;
@@ -525,6 +531,7 @@ void bands_prepare(gh_levels* L, std::vector<Band*>& bands, double t, const doub
     GH_LAUNCH_CHECK();
     m->launches++;
     GH_CUDA(cudaMemsetAsync(b->rows_done, 0, sizeof(unsigned long long) * b->nlev, s));
+    GH_CUDA(cudaMemsetAsync(b->stalled, 0, sizeof(int32_t), s));
   }
 }
 
@@ -552,9 +559,7 @@ double bands_launch(gh_levels* L, std::vector<Band*>& bands, double t, int32_t s
   }
   if (nslots < 2) nslots = 2;
   const size_t shmem = 16 * (size_t)nslots + table_bytes + 128 + (size_t)nslots * slot_bytes;
-  bool linked = false;
-  for (Band* b : bands) linked |= b->lo_ubuf != nullptr || b->hi_ubuf != nullptr;
-  void* fn = linked ? (void*)k_diffuse_tma<true> : (void*)k_diffuse_tma<false>;
+  void* fn = wmax <= 6 ? (void*)k_diffuse_tma<6> : (void*)k_diffuse_tma<8>;
   GH_CUDA(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)shmem));
   int nsm = 0, per_sm = 0;
   GH_CUDA(cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, m->device));
@@ -590,6 +595,10 @@ double bands_launch(gh_levels* L, std::vector<Band*>& bands, double t, int32_t s
   m->launches++;
   const double ms = timer.ms();
   for (Band* b : bands) {
+    int32_t stalled = 0;
+    GH_CUDA(cudaMemcpyAsync(&stalled, b->stalled, sizeof(int32_t), cudaMemcpyDeviceToHost, s));
+    GH_CUDA(cudaStreamSynchronize(s));
+    if (stalled) fail(GH_ERR_INTERNAL, "diffusion: a band dependency never arrived (neighbour band not running?)");
     const double* result = b->ubuf + ((sweeps - 1) & 1) * (int64_t)b->nrows;
     k_scatter<<<grid_for(b->own_rows), B, 0, s>>>(b->perm.p, result, b->own_rows, L->u_orig.p);
     GH_LAUNCH_CHECK();

@@ -158,6 +158,7 @@ struct Band {
   // state shared with neighbour bands: plain cudaMalloc so it can be IPC-exported
   double* ubuf = nullptr;                   // [2][nrows] sweep-parity buffers
   unsigned long long* rows_done = nullptr;  // [nlev] rows finished per level over all sweeps
+  int32_t* stalled = nullptr;               // dependency-timeout flag of the last launch
   // links to the neighbours' copies of this band's boundary levels
   double* lo_ubuf = nullptr;
   unsigned long long* lo_done = nullptr;

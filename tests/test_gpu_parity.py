@@ -258,3 +258,22 @@ def test_band_sharded_diffusion_bitwise(gpu, nbands):
     t = gh.diffusion_time(mesh, 1.0)
     one = gh.gs_diffuse(mesh, lv, t, gh.DiffusionConfig(sweeps=200))
     assert_same(bands.gs_diffuse_bands(mesh, lv, nbands, t, 200), one, f"config 3/8 with {nbands} bands")
+
+
+def test_band_export_and_neighbour_checks(gpu):
+    """Multi-process band handles: the IPC blob round-trips and connect() refuses
+    a blob that is not the adjacent band (before any peer mapping)."""
+    from paper_1812_06060_b200 import bands
+    gh = gpu
+    g = np.load(os.path.join(GOLDEN, "icosphere3.npz"))
+    mesh = gh.build_mesh(g["positions"], g["faces"])
+    lv = gh.bfs_levels(mesh, g["sources"])
+    b0, b1, b2 = (bands.Band(lv, r, 3) for r in range(3))
+    plan = bands.plan_bands(lv.offsets, 3)
+    assert [b0.lb, b0.le, b1.lb, b1.le, b2.lb, b2.le] == [plan[0], plan[1], plan[1], plan[2], plan[2], plan[3]]
+    blobs = [b.export() for b in (b0, b1, b2)]
+    assert len(set(map(len, blobs))) == 1
+    with pytest.raises(ValueError, match="lower neighbour"):
+        b2.connect(blobs[0], None)  # band 0 is not band 2's lower neighbour
+    with pytest.raises(ValueError, match="upper neighbour"):
+        b0.connect(None, blobs[2])
