@@ -345,14 +345,17 @@ __global__ void __launch_bounds__(kTmaThreads, 2) k_diffuse_tma(const __grid_con
           if (X >= 0 && X < a.nlev) {
             const unsigned long long need =
                 (unsigned long long)((tau - X + 1) >> 1) * (unsigned long long)(pend[X] - pstart[X]);
-            unsigned ns = 32;
-            const long long t0 = clock64();
-            while (ld_acquire_sys_u64(vba->rows_done + X) < need) {
-              __nanosleep(ns);
-              if (ns < 256) ns <<= 1;
-              if (clock64() - t0 > (1ll << 35)) {  // ~17 s at 1.9 GHz: a neighbour is gone
-                atomicExch(vba->stalled, 1);
-                break;
+            if (ld_acquire_sys_u64(vba->rows_done + X) < need) {
+              const long long t0 = clock64();
+              unsigned ns = 64;
+              for (unsigned it = 1;; ++it) {
+                __nanosleep(ns);
+                if (ld_acquire_sys_u64(vba->rows_done + X) >= need) break;
+                if (ns < 512) ns <<= 1;
+                if ((it & 255) == 0 && clock64() - t0 > (1ll << 35)) {  // ~17 s: a neighbour is gone
+                  atomicExch(vba->stalled, 1);
+                  break;
+                }
               }
             }
           }
