@@ -73,3 +73,19 @@ def test_cpp_wrapper_compiles():
            "-L", _build.LIBDIR, "-lgeoheat_b200", "-lgh_meshgen", f"-Wl,-rpath,{_build.LIBDIR}"]
     r = subprocess.run(cmd, capture_output=True, text=True)
     assert r.returncode == 0, r.stderr
+
+
+REF = "/root/reference/proj"
+
+
+@pytest.mark.skipif(not os.path.isdir(REF + "/include/geoheat"), reason="needs the reference headers (build container)")
+def test_dropin_compiles_against_reference_types():
+    """run_pipeline's chain instantiated with the reference's namespace and with
+    geoheat::b200 using the reference's own types (GEOHEAT_B200_REFERENCE_TYPES)."""
+    src = os.path.join(ROOT, "tests", "cpp", "dropin_run_pipeline.cpp")
+    exe = os.path.join(_build.LIBDIR, "dropin_run_pipeline")
+    cmd = ["g++", "-std=gnu++20", "-O2", "-fopenmp", "-ffp-contract=off", "-I", os.path.join(ROOT, "oracle", "eigen_shim"),
+           "-I", REF + "/include", "-I", REF + "/tests", "-I", os.path.join(ROOT, "include"), src, "-o", exe,
+           "-L", _build.LIBDIR, "-lgeoheat_b200", f"-Wl,-rpath,{_build.LIBDIR}"]
+    r = subprocess.run(cmd, capture_output=True, text=True)
+    assert r.returncode == 0, r.stderr[-3000:]

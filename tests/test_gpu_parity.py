@@ -277,3 +277,16 @@ def test_band_export_and_neighbour_checks(gpu):
         b2.connect(blobs[0], None)  # band 0 is not band 2's lower neighbour
     with pytest.raises(ValueError, match="upper neighbour"):
         b0.connect(None, blobs[2])
+
+
+def test_dropin_reference_program_bitwise(gpu):
+    """tests/cpp/dropin_run_pipeline.cpp: the same run_pipeline chain compiled with
+    the reference's functions and with geoheat::b200 on the reference's own types;
+    built in the build container (needs /root/reference), run here."""
+    from paper_1812_06060_b200 import _build
+    exe = os.path.join(_build.LIBDIR, "dropin_run_pipeline")
+    if not os.path.exists(exe):
+        pytest.skip("drop-in program not prebuilt (built by tests/test_abi.py in the build container)")
+    r = subprocess.run([exe], capture_output=True, text=True, timeout=600)
+    assert r.returncode == 0, r.stdout + r.stderr
+    assert r.stdout.count("identical") == 2
