@@ -37,7 +37,7 @@ struct Error {
 #define GH_LAUNCH_CHECK() GH_CUDA(cudaGetLastError())
 
 constexpr int kBlock = 256;
-constexpr int kReduceGrid = 1024;  // fixed partial count => reproducible reductions
+constexpr int kReduceGrid = 4096;  // fixed partial count => reproducible reductions
 
 inline unsigned grid_for(int64_t n, int block = kBlock, int64_t cap = 148 * 32) {
   int64_t g = (n + block - 1) / block;
