@@ -167,6 +167,51 @@ gh_status gh_diffusion_time(gh_mesh* mesh, double m, double* t_out);
 /* face_gradient (mesh.hpp:314-327): u [V] -> grad [3F]. */
 gh_status gh_face_gradient(gh_mesh* mesh, const double* u, double* grad_out);
 
+/* ---- mesh I/O: load_mesh / save_mesh / distance writers (mesh_io.hpp)
+ * Same accepted inputs, values and error messages (status GH_ERR_MESH) as
+ * the reference loader. Binary little-endian PLY records are decoded on the
+ * device straight into the mesh arrays; OBJ and ASCII PLY are tokenised by
+ * host threads with std::istream >> double semantics. */
+typedef enum { GH_FORMAT_OBJ = 0, GH_FORMAT_PLY = 1 } gh_mesh_format;   /* MeshFormat (mesh_io.hpp:18) */
+typedef enum { GH_DISTANCES_TXT = 0, GH_DISTANCES_CSV = 1 } gh_distance_format;
+
+typedef struct {
+  int32_t format;          /* gh_mesh_format */
+  int32_t binary;          /* PLY body is binary_little_endian */
+  int32_t device_decoded;  /* binary records were decoded on the device */
+  int32_t host_threads;    /* threads that read / tokenised the input */
+  uint64_t bytes;          /* input size */
+  double read_ms;          /* map the file, stream binary records to the device */
+  double parse_ms;         /* header, tokenising or device record decode */
+  double build_ms;         /* build_mesh on the device (text formats) */
+  double total_ms;
+  int32_t kernel_launches;
+  int32_t reserved;
+} gh_load_report;
+
+/* format_from_path (mesh_io.hpp:271-278): ".obj" / ".ply", case-insensitive. */
+gh_status gh_mesh_format_from_path(const char* path, int32_t* format_out);
+/* load_mesh(path) (mesh_io.hpp:280-285) -> device mesh. report may be NULL. */
+gh_status gh_mesh_load(const char* path, gh_mesh** out, gh_load_report* report);
+/* load_mesh(istream, format) (mesh_io.hpp:267-269) over a host buffer. */
+gh_status gh_mesh_load_memory(const void* data, uint64_t bytes, int32_t format, gh_mesh** out,
+                              gh_load_report* report);
+/* The host tokeniser alone for the text formats (OBJ, ASCII PLY): positions
+ * [3V] and faces [3F] as load_obj / load_ply hand them to build_mesh. Arrays
+ * are malloc'd, released with gh_free. Binary PLY is rejected (its records
+ * are decoded on the device by gh_mesh_load*). threads <= 0: automatic. */
+gh_status gh_mesh_parse_text(const void* data, uint64_t bytes, int32_t format, int32_t threads, double** positions,
+                             int64_t* nv, int32_t** faces, int64_t* nf);
+/* save_obj / save_ply (mesh_io.hpp:287-319) into a malloc'd buffer (gh_free).
+ * quality (host [V]) adds the per-vertex "quality" property; PLY only. */
+gh_status gh_mesh_serialize(gh_mesh* mesh, int32_t format, const double* quality, void** data, uint64_t* bytes);
+/* save_mesh (mesh_io.hpp:321-326) with save_ply's optional quality. */
+gh_status gh_mesh_save(gh_mesh* mesh, const char* path, const double* quality);
+/* write_distances_txt / write_distances_csv (mesh_io.hpp:329-344). */
+gh_status gh_format_distances(const double* d, int64_t n, int32_t format, void** data, uint64_t* bytes);
+gh_status gh_write_distances(const char* path, const double* d, int64_t n, int32_t format);
+void gh_free(void* p);
+
 /* ---- BFS: bfs_levels (bfs.hpp:26-72) */
 gh_status gh_bfs_create(gh_mesh* mesh, const int32_t* sources, int32_t ns, gh_levels** out);
 gh_status gh_bfs_destroy(gh_levels* levels);

@@ -122,6 +122,11 @@ class Oracle:
             L.gho_ref_analytic.argtypes = [vp, i32, vp, i32, vp]
             L.gho_ref_mean_relative_error.argtypes = [vp, vp, C.c_int64, vp, i32]
             L.gho_ref_mean_relative_error.restype = f64
+            L.gho_ref_load_mesh.argtypes = [C.c_char_p, C.c_int64, i32, C.POINTER(vp), C.c_char_p, i32]
+            L.gho_ref_save_mesh.argtypes = [vp, i32, vp, C.POINTER(C.c_int64)]
+            L.gho_ref_save_mesh.restype = C.POINTER(C.c_char)
+            L.gho_ref_write_distances.argtypes = [vp, C.c_int64, i32, C.POINTER(C.c_int64)]
+            L.gho_ref_write_distances.restype = C.POINTER(C.c_char)
 
     # ---- mesh
     def build_mesh(self, positions, faces) -> "OMesh":
@@ -159,6 +164,37 @@ class Oracle:
         self.lib.gho_ref_free(pos)
         self.lib.gho_ref_free(fcs)
         return P, Fa
+
+
+    def load_mesh(self, data: bytes, fmt: int) -> "OMesh":
+        """load_mesh(istream, format) of the reference (0 OBJ, 1 PLY); raises
+        OracleMeshError with the reference's exception text."""
+        assert self.kind == "reference"
+        h = C.c_void_p()
+        err = C.create_string_buffer(1024)
+        rc = self.lib.gho_ref_load_mesh(data, len(data), int(fmt), C.byref(h), err, 1024)
+        if rc != 0:
+            raise OracleMeshError(err.value.decode(errors="replace"))
+        return OMesh(self, h)
+
+    def _take(self, ptr, n) -> bytes:
+        out = C.string_at(ptr, n.value)
+        self.lib.gho_ref_free(ptr)
+        return out
+
+    def save_mesh(self, mesh: "OMesh", fmt: int, quality=None) -> bytes:
+        assert self.kind == "reference"
+        q = None if quality is None else np.ascontiguousarray(quality, dtype=np.float64)
+        n = C.c_int64()
+        ptr = self.lib.gho_ref_save_mesh(mesh.h, int(fmt), _p(q) if q is not None else None, C.byref(n))
+        return self._take(ptr, n)
+
+    def write_distances(self, d, csv: bool) -> bytes:
+        assert self.kind == "reference"
+        v = np.ascontiguousarray(d, dtype=np.float64)
+        n = C.c_int64()
+        ptr = self.lib.gho_ref_write_distances(_p(v), v.size, 1 if csv else 0, C.byref(n))
+        return self._take(ptr, n)
 
 
 class OMesh:

@@ -13,6 +13,7 @@
 #include "geoheat/grad_face.hpp"
 #include "geoheat/integrate.hpp"
 #include "geoheat/mesh.hpp"
+#include "geoheat/mesh_io.hpp"
 #include "geoheat/parallel.hpp"
 #include "geoheat/reference.hpp"
 #include "geoheat/report.hpp"
@@ -22,6 +23,7 @@
 
 #include <cstdlib>
 #include <cstring>
+#include <sstream>
 #include <string>
 
 using namespace geoheat;
@@ -348,6 +350,50 @@ double gho_ref_mean_relative_error(const double* d, const double* d_ref, int64_t
                                    int32_t ns) {
   VertexScalarField a(d, d + n), b(d_ref, d_ref + n);
   return mean_relative_error(a, b, std::span<const Index>(sources, ns));
+}
+
+// ---- reference mesh I/O (mesh_io.hpp), the checker for gh_mesh_load* and
+// the writers. load: rc 0 ok, 1 with the exception text in err.
+int gho_ref_load_mesh(const char* data, int64_t n, int32_t format, gho_mesh** out, char* err, int32_t errlen) {
+  try {
+    std::istringstream in(std::string(data, static_cast<size_t>(n)), std::ios::in | std::ios::binary);
+    TriMesh m = load_mesh(in, format == 0 ? MeshFormat::OBJ : MeshFormat::PLY);
+    *out = new gho_mesh{std::move(m)};
+    return 0;
+  } catch (const std::exception& e) {
+    put_err(err, errlen, e.what());
+    return 1;
+  }
+}
+
+// save_obj / save_ply (quality may be NULL) and the distance writers; the
+// bytes are malloc'd (gho_ref_free).
+static char* dup_bytes(const std::string& s, int64_t* n) {
+  char* p = static_cast<char*>(std::malloc(s.size() ? s.size() : 1));
+  std::memcpy(p, s.data(), s.size());
+  *n = static_cast<int64_t>(s.size());
+  return p;
+}
+
+char* gho_ref_save_mesh(const gho_mesh* mesh, int32_t format, const double* quality, int64_t* n) {
+  std::ostringstream os(std::ios::out | std::ios::binary);
+  if (format == 0) {
+    save_obj(os, mesh->m);
+  } else if (quality) {
+    VertexScalarField q(quality, quality + mesh->m.vertex_count());
+    save_ply(os, mesh->m, &q);
+  } else {
+    save_ply(os, mesh->m);
+  }
+  return dup_bytes(os.str(), n);
+}
+
+char* gho_ref_write_distances(const double* d, int64_t count, int32_t csv, int64_t* n) {
+  VertexScalarField v(d, d + count);
+  std::ostringstream os(std::ios::out | std::ios::binary);
+  if (csv) write_distances_csv(os, v);
+  else write_distances_txt(os, v);
+  return dup_bytes(os.str(), n);
 }
 
 }  // extern "C"

@@ -27,6 +27,8 @@ ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 NVCC_FLAGS = ARCH + ["-O3", "-lineinfo", "-std=c++17", "-fmad=false", "-Xcompiler", "-fPIC,-O2,-ffp-contract=off",
                      "-Xptxas", "-v", "-I", os.path.join(ROOT, "include")]
 
+HOST_FLAGS = ["-std=c++17", "-O3", "-fPIC", "-g1", "-Wall", "-pthread", "-ffp-contract=off"]
+
 
 def _nvcc() -> str:
     for cand in (shutil.which("nvcc"), "/usr/local/cuda/bin/nvcc"):
@@ -56,8 +58,11 @@ def build_meshgen(force: bool = False) -> str:
 def build_cuda(force: bool = False, verbose: bool = False) -> str:
     os.makedirs(LIBDIR, exist_ok=True)
     sources = sorted(glob.glob(os.path.join(CSRC, "*.cu")))
-    headers = sorted(glob.glob(os.path.join(CSRC, "*.cuh"))) + [os.path.join(ROOT, "include", "geoheat_b200.h")]
-    if not force and _newer(CUDA_LIB, sources + headers):
+    host_sources = sorted(glob.glob(os.path.join(CSRC, "*.cpp")))
+    headers = (sorted(glob.glob(os.path.join(CSRC, "*.cuh"))) + sorted(glob.glob(os.path.join(CSRC, "*.hpp"))) +
+               [os.path.join(ROOT, "include", "geoheat_b200.h")])
+    sources_all = sources + host_sources
+    if not force and _newer(CUDA_LIB, sources_all + headers):
         return CUDA_LIB
     nvcc = _nvcc()
     objdir = os.path.join(LIBDIR, "obj")
@@ -65,7 +70,11 @@ def build_cuda(force: bool = False, verbose: bool = False) -> str:
 
     def compile_one(src):
         obj = os.path.join(objdir, os.path.basename(src) + ".o")
-        r = subprocess.run([nvcc, *NVCC_FLAGS, "-c", src, "-o", obj], capture_output=True, text=True)
+        if src.endswith(".cpp"):  # host-only code (mesh I/O): the host compiler directly
+            cmd = ["g++", *HOST_FLAGS, "-c", src, "-o", obj]
+        else:
+            cmd = [nvcc, *NVCC_FLAGS, "-c", src, "-o", obj]
+        r = subprocess.run(cmd, capture_output=True, text=True)
         if r.returncode != 0:
             raise RuntimeError(f"nvcc failed on {src}:\n{r.stderr}")
         with open(obj + ".ptxas.txt", "w") as f:
@@ -73,9 +82,9 @@ def build_cuda(force: bool = False, verbose: bool = False) -> str:
         return obj
 
     with cf.ThreadPoolExecutor(max_workers=min(8, len(sources))) as ex:
-        objs = list(ex.map(compile_one, sources))
+        objs = list(ex.map(compile_one, sources_all))
     tmp = CUDA_LIB + ".tmp"
-    r = subprocess.run([nvcc, *ARCH, "-shared", "-o", tmp, *objs], capture_output=True, text=True)
+    r = subprocess.run([nvcc, *ARCH, "-shared", "-o", tmp, *objs, "-lpthread"], capture_output=True, text=True)
     if r.returncode != 0:
         raise RuntimeError(f"link failed:\n{r.stderr}")
     os.replace(tmp, CUDA_LIB)

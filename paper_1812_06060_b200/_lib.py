@@ -52,6 +52,13 @@ class gh_run_report(C.Structure):
                 ("solver_state_bytes", C.c_uint64), ("kernel_launches", C.c_int32), ("reserved", C.c_int32)]
 
 
+class gh_load_report(C.Structure):
+    _fields_ = [("format", C.c_int32), ("binary", C.c_int32), ("device_decoded", C.c_int32),
+                ("host_threads", C.c_int32), ("bytes", C.c_uint64), ("read_ms", C.c_double),
+                ("parse_ms", C.c_double), ("build_ms", C.c_double), ("total_ms", C.c_double),
+                ("kernel_launches", C.c_int32), ("reserved", C.c_int32)]
+
+
 # (name, restype, argtypes) for every exported symbol of include/geoheat_b200.h
 vp, i32, i64, f64, st = C.c_void_p, C.c_int32, C.c_int64, C.c_double, C.c_int
 SIGNATURES = [
@@ -68,6 +75,16 @@ SIGNATURES = [
     ("gh_average_edge_length", st, [vp, C.POINTER(f64)]),
     ("gh_diffusion_time", st, [vp, f64, C.POINTER(f64)]),
     ("gh_face_gradient", st, [vp, vp, vp]),
+    ("gh_mesh_format_from_path", st, [C.c_char_p, C.POINTER(i32)]),
+    ("gh_mesh_load", st, [C.c_char_p, C.POINTER(vp), C.POINTER(gh_load_report)]),
+    ("gh_mesh_load_memory", st, [C.c_char_p, C.c_uint64, i32, C.POINTER(vp), C.POINTER(gh_load_report)]),
+    ("gh_mesh_parse_text", st, [C.c_char_p, C.c_uint64, i32, i32, C.POINTER(C.POINTER(f64)), C.POINTER(i64),
+                                C.POINTER(C.POINTER(C.c_int32)), C.POINTER(i64)]),
+    ("gh_mesh_serialize", st, [vp, i32, vp, C.POINTER(vp), C.POINTER(C.c_uint64)]),
+    ("gh_mesh_save", st, [vp, C.c_char_p, vp]),
+    ("gh_format_distances", st, [vp, i64, i32, C.POINTER(vp), C.POINTER(C.c_uint64)]),
+    ("gh_write_distances", st, [C.c_char_p, vp, i64, i32]),
+    ("gh_free", None, [vp]),
     ("gh_bfs_create", st, [vp, vp, i32, C.POINTER(vp)]),
     ("gh_bfs_destroy", st, [vp]),
     ("gh_bfs_get_info", st, [vp, C.POINTER(gh_levels_info)]),

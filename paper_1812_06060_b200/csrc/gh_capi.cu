@@ -5,11 +5,15 @@
 // types map to codes as in tools/geoheat.cpp:337-349).
 
 #include <chrono>
+#include <algorithm>
+#include <cstdlib>
 #include <cstring>
+#include <functional>
 #include <memory>
 #include <new>
 
 #include "gh_internal.cuh"
+#include "gh_meshio.hpp"
 
 namespace {
 
@@ -149,28 +153,177 @@ gh_status gh_host_free(void* p) {
   });
 }
 
+// A fresh handle on the selected device with the thread's stream.
+static std::unique_ptr<gh_mesh> new_mesh() {
+  int ndev = 0;
+  if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev == 0) {
+    (void)cudaGetLastError();
+    gh::fail(GH_ERR_CUDA, "no CUDA device available (the geoheat_b200 path has no CPU fallback)");
+  }
+  std::unique_ptr<gh_mesh> m(new gh_mesh());
+  if (g_device >= 0) GH_CUDA(cudaSetDevice(g_device));
+  GH_CUDA(cudaGetDevice(&m->device));
+  keep_pool_memory(m->device);
+  thread_context(m->device, &m->stream, &m->pinned_scalars);
+  return m;
+}
+
 gh_status gh_mesh_create(const double* positions, int32_t nv, const int32_t* faces, int32_t nf, gh_mesh** out) {
   return guarded([&] {
     require(out != nullptr, "gh_mesh_create: null output");
     require(nv >= 0 && nf >= 0, "gh_mesh_create: negative size");
     require((nv == 0 || positions) && (nf == 0 || faces), "gh_mesh_create: null input array");
     require((int64_t)nf * 3 <= 0x7fffffffLL, "gh_mesh_create: more than 2^31 halfedges");
-    int ndev = 0;
-    if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev == 0) {
-      (void)cudaGetLastError();
-      gh::fail(GH_ERR_CUDA, "no CUDA device available (the geoheat_b200 path has no CPU fallback)");
-    }
-    std::unique_ptr<gh_mesh> m(new gh_mesh());
-    if (g_device >= 0) GH_CUDA(cudaSetDevice(g_device));
-    GH_CUDA(cudaGetDevice(&m->device));
-    keep_pool_memory(m->device);
-    thread_context(m->device, &m->stream, &m->pinned_scalars);
+    std::unique_ptr<gh_mesh> m = new_mesh();
     m->nv = nv;
     m->nf = nf;
     gh::mesh_build(m.get(), positions, faces);
     *out = m.release();
   });
 }
+
+// ---- mesh I/O (gh_load.cu, gh_meshio.cpp)
+static gh_status load_common(gh_mesh** out, gh_load_report* report, const std::function<void(gh_mesh*)>& body) {
+  return guarded([&] {
+    require(out != nullptr, "gh_mesh_load: null output");
+    const double t0 = now_s();
+    if (report) *report = gh_load_report{};
+    std::unique_ptr<gh_mesh> m = new_mesh();
+    body(m.get());
+    GH_CUDA(cudaStreamSynchronize(m->stream));
+    if (report) {
+      report->total_ms = (now_s() - t0) * 1e3;
+      report->kernel_launches = take_launches(m.get());
+    }
+    *out = m.release();
+  });
+}
+
+gh_status gh_mesh_format_from_path(const char* path, int32_t* format_out) {
+  return guarded([&] {
+    require(path && format_out, "gh_mesh_format_from_path: null argument");
+    try {
+      *format_out = (int32_t)ghio::format_from_path(path);
+    } catch (const ghio::LoadError& e) {
+      gh::fail(GH_ERR_MESH, e.msg);
+    }
+  });
+}
+
+gh_status gh_mesh_load(const char* path, gh_mesh** out, gh_load_report* report) {
+  if (!path) return set_err(GH_ERR_INVALID, "gh_mesh_load: null path");
+  return load_common(out, report, [&](gh_mesh* m) { gh::load_mesh_file(m, path, 0, report); });
+}
+
+gh_status gh_mesh_load_memory(const void* data, uint64_t bytes, int32_t format, gh_mesh** out,
+                              gh_load_report* report) {
+  if (!data && bytes) return set_err(GH_ERR_INVALID, "gh_mesh_load_memory: null data");
+  if (format != GH_FORMAT_OBJ && format != GH_FORMAT_PLY)
+    return set_err(GH_ERR_INVALID, "gh_mesh_load_memory: unknown format");
+  return load_common(out, report, [&](gh_mesh* m) {
+    gh::load_mesh_bytes(m, (const unsigned char*)data, bytes, format, 0, report);
+  });
+}
+
+gh_status gh_mesh_parse_text(const void* data, uint64_t bytes, int32_t format, int32_t threads, double** positions,
+                             int64_t* nv, int32_t** faces, int64_t* nf) {
+  return guarded([&] {
+    require((data || !bytes) && positions && nv && faces && nf, "gh_mesh_parse_text: null argument");
+    require(format == GH_FORMAT_OBJ || format == GH_FORMAT_PLY, "gh_mesh_parse_text: unknown format");
+    ghio::HostMesh hm;
+    try {
+      if (format == GH_FORMAT_OBJ) {
+        ghio::parse_obj((const char*)data, bytes, threads, hm);
+      } else {
+        const ghio::PlyHeader h = ghio::parse_ply_header((const char*)data, bytes);
+        require(!h.binary, "gh_mesh_parse_text: binary PLY records are decoded on the device (gh_mesh_load_memory)");
+        ghio::parse_ply_ascii(h, (const char*)data, bytes, threads, hm);
+      }
+    } catch (const ghio::LoadError& e) {
+      gh::fail(GH_ERR_MESH, e.msg);
+    }
+    double* p = (double*)std::malloc(sizeof(double) * std::max<size_t>(1, hm.pos.size()));
+    int32_t* f = (int32_t*)std::malloc(sizeof(int32_t) * std::max<size_t>(1, hm.faces.size()));
+    if (!p || !f) {
+      std::free(p);
+      std::free(f);
+      throw std::bad_alloc();
+    }
+    std::memcpy(p, hm.pos.data(), sizeof(double) * hm.pos.size());
+    std::memcpy(f, hm.faces.data(), sizeof(int32_t) * hm.faces.size());
+    *positions = p;
+    *faces = f;
+    *nv = (int64_t)hm.pos.size() / 3;
+    *nf = (int64_t)hm.faces.size() / 3;
+  });
+}
+
+static void* to_malloc(const std::string& s, uint64_t* bytes) {
+  void* p = std::malloc(std::max<size_t>(1, s.size()));
+  if (!p) throw std::bad_alloc();
+  std::memcpy(p, s.data(), s.size());
+  *bytes = s.size();
+  return p;
+}
+
+static void write_file(const char* path, const std::string& s) {
+  FILE* f = std::fopen(path, "wb");
+  if (!f) gh::fail(GH_ERR_MESH, std::string("cannot open output file '") + path + "'");
+  const size_t w = s.empty() ? 0 : std::fwrite(s.data(), 1, s.size(), f);
+  const int c = std::fclose(f);
+  if (w != s.size() || c != 0) gh::fail(GH_ERR_MESH, std::string("write failed for '") + path + "'");
+}
+
+gh_status gh_mesh_serialize(gh_mesh* mesh, int32_t format, const double* quality, void** data, uint64_t* bytes) {
+  return guarded([&] {
+    require(mesh && data && bytes, "gh_mesh_serialize: null argument");
+    require(format == GH_FORMAT_OBJ || format == GH_FORMAT_PLY, "gh_mesh_serialize: unknown format");
+    require(!quality || format == GH_FORMAT_PLY, "gh_mesh_serialize: quality is written by PLY only");
+    use_device_of(mesh);
+    *data = to_malloc(gh::serialize_mesh(mesh, format, quality), bytes);
+  });
+}
+
+gh_status gh_mesh_save(gh_mesh* mesh, const char* path, const double* quality) {
+  return guarded([&] {
+    require(mesh && path, "gh_mesh_save: null argument");
+    use_device_of(mesh);
+    // save_mesh opens the file before it infers the format (mesh_io.hpp:321-326)
+    FILE* probe = std::fopen(path, "wb");
+    if (!probe) gh::fail(GH_ERR_MESH, std::string("cannot open output file '") + path + "'");
+    std::fclose(probe);
+    int format = 0;
+    try {
+      format = (int)ghio::format_from_path(path);
+    } catch (const ghio::LoadError& e) {
+      gh::fail(GH_ERR_MESH, e.msg);
+    }
+    require(!quality || format == GH_FORMAT_PLY, "gh_mesh_save: quality is written by PLY only");
+    write_file(path, gh::serialize_mesh(mesh, format, quality));
+  });
+}
+
+gh_status gh_format_distances(const double* d, int64_t n, int32_t format, void** data, uint64_t* bytes) {
+  return guarded([&] {
+    require((d || n == 0) && n >= 0 && data && bytes, "gh_format_distances: bad argument");
+    require(format == GH_DISTANCES_TXT || format == GH_DISTANCES_CSV, "gh_format_distances: unknown format");
+    std::string s;
+    ghio::format_distances(d, n, format == GH_DISTANCES_CSV, 0, s);
+    *data = to_malloc(s, bytes);
+  });
+}
+
+gh_status gh_write_distances(const char* path, const double* d, int64_t n, int32_t format) {
+  return guarded([&] {
+    require(path && (d || n == 0) && n >= 0, "gh_write_distances: bad argument");
+    require(format == GH_DISTANCES_TXT || format == GH_DISTANCES_CSV, "gh_write_distances: unknown format");
+    std::string s;
+    ghio::format_distances(d, n, format == GH_DISTANCES_CSV, 0, s);
+    write_file(path, s);
+  });
+}
+
+void gh_free(void* p) { std::free(p); }
 
 static void free_mesh(gh_mesh* mesh) {
   cudaSetDevice(mesh->device);

@@ -194,6 +194,10 @@ namespace gh {
 
 // mesh build / queries (gh_mesh.cu)
 void mesh_build(gh_mesh* m, const double* h_pos, const int32_t* h_faces);
+// gh_load.cu: load_mesh into an initialised handle (device, stream set).
+void load_mesh_bytes(gh_mesh* m, const unsigned char* bytes, uint64_t n, int format, int threads, gh_load_report* rep);
+void load_mesh_file(gh_mesh* m, const char* path, int threads, gh_load_report* rep);
+std::string serialize_mesh(gh_mesh* m, int format, const double* quality);
 double mesh_average_edge_length(gh_mesh* m);
 void face_gradient_dev(gh_mesh* m, const double* d_u, double* d_grad);
 

@@ -345,19 +345,38 @@ T read_scalar(const T* d, cudaStream_t s) {
 
 // Host restatement of one face's checks, only to word the error message of the
 // first failing face exactly like mesh.hpp:133-142 (std::to_string = "%f").
-std::string face_error(const double* P, const int32_t* Fc, int64_t f, int32_t nv, double degenerate) {
-  const int32_t* t = Fc + 3 * f;
+// Inputs are the face's three indices and, once they are in range, the
+// three corner positions (fetched from wherever the mesh arrays live).
+std::string face_error(const int32_t t[3], int64_t f, int32_t nv, const double* (*corner)(const void*, int32_t),
+                       const void* ctx) {
   for (int k = 0; k < 3; ++k)
     if (t[k] < 0 || t[k] >= nv) return "face " + std::to_string(f) + ": vertex index out of range";
   if (t[0] == t[1] || t[1] == t[2] || t[0] == t[2])
     return "face " + std::to_string(f) + ": repeated vertex (degenerate face)";
-  auto L = [&](int32_t i, int k) { return P[3 * (int64_t)i + k]; };
-  double ux = L(t[1], 0) - L(t[0], 0), uy = L(t[1], 1) - L(t[0], 1), uz = L(t[1], 2) - L(t[0], 2);
-  double vx = L(t[2], 0) - L(t[0], 0), vy = L(t[2], 1) - L(t[0], 1), vz = L(t[2], 2) - L(t[0], 2);
+  double P[3][3];
+  for (int k = 0; k < 3; ++k) {
+    const double* c = corner(ctx, t[k]);
+    P[k][0] = c[0];
+    P[k][1] = c[1];
+    P[k][2] = c[2];
+  }
+  double ux = P[1][0] - P[0][0], uy = P[1][1] - P[0][1], uz = P[1][2] - P[0][2];
+  double vx = P[2][0] - P[0][0], vy = P[2][1] - P[0][1], vz = P[2][2] - P[0][2];
   double nx = uy * vz - uz * vy, ny = uz * vx - ux * vz, nz = ux * vy - uy * vx;
   double area = 0.5 * std::sqrt((nx * nx + ny * ny) + nz * nz);
-  (void)degenerate;
   return "face " + std::to_string(f) + ": degenerate (area " + std::to_string(area) + ")";
+}
+
+struct DeviceCorners {
+  const double* pos;
+  cudaStream_t s;
+  double buf[3];
+};
+const double* device_corner(const void* ctx, int32_t v) {
+  DeviceCorners* c = (DeviceCorners*)const_cast<void*>(ctx);
+  GH_CUDA(cudaMemcpyAsync(c->buf, c->pos + 3 * (int64_t)v, 3 * sizeof(double), cudaMemcpyDeviceToHost, c->s));
+  GH_CUDA(cudaStreamSynchronize(c->s));
+  return c->buf;
 }
 
 }  // namespace
@@ -384,10 +403,14 @@ void mesh_build(gh_mesh* m, const double* h_pos, const int32_t* h_faces) {
   const uint64_t nvu = (uint64_t)(V > 0 ? V : 1);
   m->partials.alloc(kReduceGrid * 6, s);
   m->scalars.alloc(16, s);
-  m->pos.alloc(3 * V, s);
-  m->faces.alloc(3 * F, s);
-  if (V) GH_CUDA(cudaMemcpyAsync(m->pos.p, h_pos, sizeof(double) * 3 * V, cudaMemcpyHostToDevice, s));
-  if (F) GH_CUDA(cudaMemcpyAsync(m->faces.p, h_faces, sizeof(int32_t) * 3 * F, cudaMemcpyHostToDevice, s));
+  // h_pos == h_faces == nullptr: the loader already decoded the arrays into
+  // m->pos / m->faces on the device.
+  if (h_pos || h_faces || m->pos.n != (size_t)(3 * V) || m->faces.n != (size_t)(3 * F)) {
+    m->pos.alloc(3 * V, s);
+    m->faces.alloc(3 * F, s);
+    if (V) GH_CUDA(cudaMemcpyAsync(m->pos.p, h_pos, sizeof(double) * 3 * V, cudaMemcpyHostToDevice, s));
+    if (F) GH_CUDA(cudaMemcpyAsync(m->faces.p, h_faces, sizeof(int32_t) * 3 * F, cudaMemcpyHostToDevice, s));
+  }
 
   // bbox -> degenerate threshold
   const unsigned gb = grid_for(V, B, 512);
@@ -407,7 +430,13 @@ void mesh_build(gh_mesh* m, const double* h_pos, const int32_t* h_faces) {
     GH_LAUNCH_CHECK();
   }
   const int32_t bad_face = read_scalar(err_face.p, s);
-  if (bad_face != big) fail(GH_ERR_MESH, face_error(h_pos, h_faces, bad_face, m->nv, 0.0));
+  if (bad_face != big) {
+    int32_t t[3];
+    GH_CUDA(cudaMemcpyAsync(t, m->faces.p + 3 * (int64_t)bad_face, sizeof(t), cudaMemcpyDeviceToHost, s));
+    GH_CUDA(cudaStreamSynchronize(s));
+    DeviceCorners ctx{m->pos.p, s, {0, 0, 0}};
+    fail(GH_ERR_MESH, face_error(t, bad_face, m->nv, device_corner, &ctx));
+  }
   m->launches += 3;
 
   // edges: stable radix sort of halfedge keys

@@ -15,6 +15,7 @@ from __future__ import annotations
 import atexit
 import ctypes as C
 import enum
+import os
 from dataclasses import dataclass, field
 from typing import Optional, Sequence
 
@@ -198,6 +199,105 @@ def build_mesh(positions, faces) -> TriMesh:
     h = C.c_void_p()
     _check(_lib.load().gh_mesh_create(_ptr(P), P.shape[0], _ptr(Fc), Fc.shape[0], C.byref(h)))
     return TriMesh(h)
+
+
+# ---- mesh I/O (mesh_io.hpp)
+class MeshFormat(enum.IntEnum):
+    OBJ = 0
+    PLY = 1
+
+
+@dataclass
+class LoadReport:
+    format: int
+    binary: bool
+    device_decoded: bool
+    host_threads: int
+    bytes: int
+    read_ms: float
+    parse_ms: float
+    build_ms: float
+    total_ms: float
+    kernel_launches: int
+
+
+def _load_report(r) -> LoadReport:
+    return LoadReport(r.format, bool(r.binary), bool(r.device_decoded), r.host_threads, r.bytes, r.read_ms,
+                      r.parse_ms, r.build_ms, r.total_ms, r.kernel_launches)
+
+
+def format_from_path(path: str) -> MeshFormat:
+    """format_from_path (mesh_io.hpp:271-278)."""
+    f = C.c_int32()
+    _check(_lib.load().gh_mesh_format_from_path(os.fsencode(path), C.byref(f)))
+    return MeshFormat(f.value)
+
+
+def load_mesh(source, format: Optional[MeshFormat] = None, with_report: bool = False):
+    """load_mesh (mesh_io.hpp:267-285): a path (format from its extension) or
+    bytes plus a MeshFormat; returns the device TriMesh (and a LoadReport)."""
+    h = C.c_void_p()
+    rep = _lib.gh_load_report()
+    if isinstance(source, (bytes, bytearray, memoryview)):
+        if format is None:
+            raise ValueError("load_mesh(bytes) needs a format")
+        data = bytes(source)
+        _check(_lib.load().gh_mesh_load_memory(data, len(data), int(format), C.byref(h), C.byref(rep)))
+    else:
+        _check(_lib.load().gh_mesh_load(os.fsencode(os.fspath(source)), C.byref(h), C.byref(rep)))
+    mesh = TriMesh(h)
+    return (mesh, _load_report(rep)) if with_report else mesh
+
+
+def parse_mesh_text(data: bytes, format: MeshFormat, threads: int = 0):
+    """Host tokeniser of the text formats: (positions [V,3], faces [F,3]) as the
+    reference hands them to build_mesh."""
+    L = _lib.load()
+    pp, fp = C.POINTER(C.c_double)(), C.POINTER(C.c_int32)()
+    nv, nf = C.c_int64(), C.c_int64()
+    _check(L.gh_mesh_parse_text(bytes(data), len(data), int(format), int(threads), C.byref(pp), C.byref(nv),
+                                C.byref(fp), C.byref(nf)))
+    try:
+        P = np.ctypeslib.as_array(pp, shape=(max(nv.value, 1) * 3,))[:3 * nv.value].copy().reshape(-1, 3)
+        Fc = np.ctypeslib.as_array(fp, shape=(max(nf.value, 1) * 3,))[:3 * nf.value].copy().reshape(-1, 3)
+    finally:
+        L.gh_free(C.cast(pp, C.c_void_p))
+        L.gh_free(C.cast(fp, C.c_void_p))
+    return P, Fc
+
+
+def _take_bytes(ptr: C.c_void_p, n: C.c_uint64) -> bytes:
+    try:
+        return C.string_at(ptr, n.value)
+    finally:
+        _lib.load().gh_free(ptr)
+
+
+def serialize_mesh(mesh: TriMesh, format: MeshFormat, quality=None) -> bytes:
+    """save_obj / save_ply (mesh_io.hpp:287-319) to bytes."""
+    q = None if quality is None else _f64(quality)
+    ptr, n = C.c_void_p(), C.c_uint64()
+    _check(_lib.load().gh_mesh_serialize(mesh._h, int(format), _ptr(q), C.byref(ptr), C.byref(n)))
+    return _take_bytes(ptr, n)
+
+
+def save_mesh(path: str, mesh: TriMesh, quality=None) -> None:
+    """save_mesh (mesh_io.hpp:321-326); quality adds save_ply's per-vertex property."""
+    q = None if quality is None else _f64(quality)
+    _check(_lib.load().gh_mesh_save(mesh._h, os.fsencode(os.fspath(path)), _ptr(q)))
+
+
+def format_distances(d, csv: bool = False) -> bytes:
+    """write_distances_txt / write_distances_csv (mesh_io.hpp:329-344) to bytes."""
+    v = _f64(d)
+    ptr, n = C.c_void_p(), C.c_uint64()
+    _check(_lib.load().gh_format_distances(_ptr(v), v.size, 1 if csv else 0, C.byref(ptr), C.byref(n)))
+    return _take_bytes(ptr, n)
+
+
+def write_distances(path: str, d, csv: bool = False) -> None:
+    v = _f64(d)
+    _check(_lib.load().gh_write_distances(os.fsencode(os.fspath(path)), _ptr(v), v.size, 1 if csv else 0))
 
 
 def average_edge_length(mesh: TriMesh) -> float:
