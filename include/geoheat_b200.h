@@ -112,7 +112,9 @@ typedef struct {
 } gh_solver_report;
 
 /* Pipeline selection (PipelineOptions, tools/geoheat.cpp:27-38). */
-typedef enum { GH_METHOD_FACE = 0, GH_METHOD_EDGE = 1 } gh_method;
+typedef enum { GH_METHOD_FACE = 0, GH_METHOD_EDGE = 1, GH_METHOD_POISSON = 2 } gh_method;
+/* gh_pipeline_config.flags */
+enum { GH_PIPE_DIFFUSION_E1 = 1 /* also compute diffusion_residual of u (geoheat.cpp:117) */ };
 
 typedef struct {
   int32_t method;   /* gh_method */
@@ -120,6 +122,9 @@ typedef struct {
   double t;         /* diffusion time; <= 0 means m * h^2 from the mesh */
   double m;         /* smoothing factor used when t <= 0 */
   gh_admm_config admm;
+  double cg_tol;    /* GH_METHOD_POISSON: CG tolerance (the CLI's --eps) */
+  int32_t flags;    /* GH_PIPE_* */
+  int32_t reserved;
 } gh_pipeline_config;
 
 /* Per-stage record of gh_distance (RunReport, report.hpp:50-90). */
@@ -142,7 +147,9 @@ typedef struct {
   uint64_t h2d_bytes, d2h_bytes;
   uint64_t solver_state_bytes;
   int32_t kernel_launches;
-  int32_t reserved;
+  int32_t cg_iterations;  /* GH_METHOD_POISSON: heat + Poisson CG iterations */
+  double diffusion_e1;    /* GH_PIPE_DIFFUSION_E1, else -1 */
+  double poisson_residual;/* GH_METHOD_POISSON: final relative residual (reported as final_primal) */
 } gh_run_report;
 
 /* ---- runtime */
@@ -261,6 +268,34 @@ gh_status gh_distance(gh_levels* levels, const gh_pipeline_config* config, doubl
 gh_status gh_distance_host(const double* positions, int32_t nv, const int32_t* faces, int32_t nf,
                            const int32_t* sources, int32_t ns, const gh_pipeline_config* config, double* d_out,
                            gh_run_report* report);
+
+/* ---- classic heat method on CG: poisson_heat_method (reference.hpp:176-216)
+ * Jacobi-preconditioned CG (cg_solve, reference.hpp:35-109) on the heat
+ * operator, normalised gradients, integrated divergence, CG on the reduced
+ * Poisson operator; sources are the levels' ring 0. GH_ERR_SOLVER on a CG
+ * breakdown. d_out: host [V] (inf for unreachable vertices). */
+typedef struct {
+  int32_t heat_iterations, poisson_iterations;
+  double heat_residual, poisson_residual; /* relative residuals */
+  double heat_seconds, poisson_seconds;
+  int32_t kernel_launches, reserved;
+} gh_poisson_report;
+gh_status gh_poisson_heat_method(gh_levels* levels, double t, double cg_tol, double* d_out, gh_poisson_report* report);
+
+/* ---- evaluation layer of the CLI */
+/* triangulation_quality (mesh.hpp:297-310), tree-summed. */
+gh_status gh_triangulation_quality(gh_mesh* mesh, double* tau_out);
+/* midpoint_subdivide (subdivide.hpp:13-45) -> a new device mesh. */
+gh_status gh_mesh_subdivide(gh_mesh* mesh, int32_t levels, gh_mesh** out);
+typedef enum { GH_SURFACE_PLANE = 0, GH_SURFACE_SPHERE = 1 } gh_analytic_surface; /* AnalyticSurface */
+/* analytic_oracle (reference.hpp:283-321); GH_ERR_INVALID off the surface. */
+gh_status gh_analytic_distance(gh_mesh* mesh, int32_t kind, const int32_t* sources, int32_t ns, double* d_out);
+/* dijkstra_edge_distance (reference.hpp:219-244). */
+gh_status gh_dijkstra_distance(gh_mesh* mesh, const int32_t* sources, int32_t ns, double* d_out);
+/* mean_relative_error (reference.hpp:247-266) and recovery_error (268-276)
+ * of two host fields, on the current device. */
+gh_status gh_error_metrics(const double* d, const double* d_ref, int64_t n, const int32_t* sources, int32_t ns,
+                           double* mean_rel_error, int32_t* excluded, double* e2);
 
 /* ---- BFS-band sharding of the diffusion
  * Levels are cut into nbands contiguous bands of about equal rows; band r

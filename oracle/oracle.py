@@ -127,6 +127,14 @@ class Oracle:
             L.gho_ref_save_mesh.restype = C.POINTER(C.c_char)
             L.gho_ref_write_distances.argtypes = [vp, C.c_int64, i32, C.POINTER(C.c_int64)]
             L.gho_ref_write_distances.restype = C.POINTER(C.c_char)
+            L.gho_ref_poisson.argtypes = [vp, vp, i32, f64, f64, vp, vp, vp, C.c_char_p, i32]
+            L.gho_ref_dijkstra.argtypes = [vp, vp, i32, vp]
+            L.gho_ref_subdivide.argtypes = [vp, i32]
+            L.gho_ref_subdivide.restype = vp
+            L.gho_ref_recovery_error.argtypes = [vp, vp, C.c_int64]
+            L.gho_ref_recovery_error.restype = f64
+            L.gho_ref_mre_excluded.argtypes = [vp, vp, C.c_int64, vp, i32]
+            L.gho_ref_mre_excluded.restype = i32
 
     # ---- mesh
     def build_mesh(self, positions, faces) -> "OMesh":
@@ -188,6 +196,38 @@ class Oracle:
         n = C.c_int64()
         ptr = self.lib.gho_ref_save_mesh(mesh.h, int(fmt), _p(q) if q is not None else None, C.byref(n))
         return self._take(ptr, n)
+
+    def poisson(self, mesh: "OMesh", sources, t: float, tol: float):
+        """poisson_heat_method -> (d, (heat_it, poisson_it), (heat_res, poisson_res))."""
+        assert self.kind == "reference"
+        S = np.ascontiguousarray(sources, dtype=np.int32)
+        d = np.empty(mesh.nv, np.float64)
+        it = np.zeros(2, np.int32)
+        res = np.zeros(2, np.float64)
+        err = C.create_string_buffer(512)
+        if self.lib.gho_ref_poisson(mesh.h, _p(S), S.size, float(t), float(tol), _p(d), _p(it), _p(res), err, 512):
+            raise OracleMeshError(err.value.decode())
+        return d, (int(it[0]), int(it[1])), (float(res[0]), float(res[1]))
+
+    def dijkstra(self, mesh: "OMesh", sources) -> np.ndarray:
+        assert self.kind == "reference"
+        S = np.ascontiguousarray(sources, dtype=np.int32)
+        d = np.empty(mesh.nv, np.float64)
+        self.lib.gho_ref_dijkstra(mesh.h, _p(S), S.size, _p(d))
+        return d
+
+    def subdivide(self, mesh: "OMesh", levels: int) -> "OMesh":
+        assert self.kind == "reference"
+        return OMesh(self, C.c_void_p(self.lib.gho_ref_subdivide(mesh.h, int(levels))))
+
+    def recovery_error(self, d, d_ref) -> float:
+        a, b = np.ascontiguousarray(d, np.float64), np.ascontiguousarray(d_ref, np.float64)
+        return float(self.lib.gho_ref_recovery_error(_p(a), _p(b), a.size))
+
+    def mre_excluded(self, d, d_ref, sources) -> int:
+        a, b = np.ascontiguousarray(d, np.float64), np.ascontiguousarray(d_ref, np.float64)
+        S = np.ascontiguousarray(sources, dtype=np.int32)
+        return int(self.lib.gho_ref_mre_excluded(_p(a), _p(b), a.size, _p(S), S.size))
 
     def write_distances(self, d, csv: bool) -> bytes:
         assert self.kind == "reference"

@@ -17,6 +17,7 @@
 #include "geoheat/parallel.hpp"
 #include "geoheat/reference.hpp"
 #include "geoheat/report.hpp"
+#include "geoheat/subdivide.hpp"
 #include "test_meshes.hpp"  // reference tests/test_meshes.hpp (generators only)
 
 #include "geoheat_oracle.h"
@@ -394,6 +395,47 @@ char* gho_ref_write_distances(const double* d, int64_t count, int32_t csv, int64
   if (csv) write_distances_csv(os, v);
   else write_distances_txt(os, v);
   return dup_bytes(os.str(), n);
+}
+
+// ---- the evaluation layer and the CG heat method (reference.hpp,
+// subdivide.hpp), checkers for gh_poisson_heat_method, gh_dijkstra_distance,
+// gh_mesh_subdivide and gh_error_metrics.
+int gho_ref_poisson(const gho_mesh* mesh, const int32_t* sources, int32_t ns, double t, double tol, double* d_out,
+                    int32_t* iters, double* residuals, char* err, int32_t errlen) {
+  try {
+    PoissonReport rep;
+    VertexScalarField d = poisson_heat_method(mesh->m, std::span<const Index>(sources, ns), t, tol, &rep);
+    std::memcpy(d_out, d.data(), d.size() * sizeof(double));
+    iters[0] = rep.heat_iterations;
+    iters[1] = rep.poisson_iterations;
+    residuals[0] = rep.heat_residual;
+    residuals[1] = rep.poisson_residual;
+    return 0;
+  } catch (const std::exception& e) {
+    put_err(err, errlen, e.what());
+    return 1;
+  }
+}
+
+void gho_ref_dijkstra(const gho_mesh* mesh, const int32_t* sources, int32_t ns, double* d_out) {
+  VertexScalarField d = dijkstra_edge_distance(mesh->m, std::span<const Index>(sources, ns));
+  std::memcpy(d_out, d.data(), d.size() * sizeof(double));
+}
+
+gho_mesh* gho_ref_subdivide(const gho_mesh* mesh, int32_t levels) {
+  return new gho_mesh{midpoint_subdivide(mesh->m, levels)};
+}
+
+double gho_ref_recovery_error(const double* d, const double* d_ref, int64_t n) {
+  VertexScalarField a(d, d + n), b(d_ref, d_ref + n);
+  return recovery_error(a, b);
+}
+
+int32_t gho_ref_mre_excluded(const double* d, const double* d_ref, int64_t n, const int32_t* sources, int32_t ns) {
+  VertexScalarField a(d, d + n), b(d_ref, d_ref + n);
+  Index excluded = 0;
+  mean_relative_error(a, b, std::span<const Index>(sources, ns), &excluded);
+  return excluded;
 }
 
 }  // extern "C"

@@ -39,7 +39,7 @@ class gh_solver_report(C.Structure):
 
 class gh_pipeline_config(C.Structure):
     _fields_ = [("method", C.c_int32), ("sweeps", C.c_int32), ("t", C.c_double), ("m", C.c_double),
-                ("admm", gh_admm_config)]
+                ("admm", gh_admm_config), ("cg_tol", C.c_double), ("flags", C.c_int32), ("reserved", C.c_int32)]
 
 
 class gh_run_report(C.Structure):
@@ -49,7 +49,14 @@ class gh_run_report(C.Structure):
                 ("diffusion_ms", C.c_double), ("normalize_ms", C.c_double), ("optimization_ms", C.c_double),
                 ("integration_ms", C.c_double), ("h2d_ms", C.c_double), ("d2h_ms", C.c_double),
                 ("total_ms", C.c_double), ("h2d_bytes", C.c_uint64), ("d2h_bytes", C.c_uint64),
-                ("solver_state_bytes", C.c_uint64), ("kernel_launches", C.c_int32), ("reserved", C.c_int32)]
+                ("solver_state_bytes", C.c_uint64), ("kernel_launches", C.c_int32), ("cg_iterations", C.c_int32),
+                ("diffusion_e1", C.c_double), ("poisson_residual", C.c_double)]
+
+
+class gh_poisson_report(C.Structure):
+    _fields_ = [("heat_iterations", C.c_int32), ("poisson_iterations", C.c_int32), ("heat_residual", C.c_double),
+                ("poisson_residual", C.c_double), ("heat_seconds", C.c_double), ("poisson_seconds", C.c_double),
+                ("kernel_launches", C.c_int32), ("reserved", C.c_int32)]
 
 
 class gh_load_report(C.Structure):
@@ -109,6 +116,12 @@ SIGNATURES = [
     ("gh_band_connect", st, [vp, vp, vp]),
     ("gh_band_prepare", st, [vp, f64, vp]),
     ("gh_band_launch", st, [vp, f64, i32, vp, C.POINTER(gh_solver_report)]),
+    ("gh_poisson_heat_method", st, [vp, f64, f64, vp, C.POINTER(gh_poisson_report)]),
+    ("gh_triangulation_quality", st, [vp, C.POINTER(f64)]),
+    ("gh_mesh_subdivide", st, [vp, i32, C.POINTER(vp)]),
+    ("gh_analytic_distance", st, [vp, i32, vp, i32, vp]),
+    ("gh_dijkstra_distance", st, [vp, vp, i32, vp]),
+    ("gh_error_metrics", st, [vp, vp, i64, vp, i32, C.POINTER(f64), C.POINTER(i32), C.POINTER(f64)]),
     ("gh_field_hash", C.c_uint64, [vp, i64]),
 ]
 

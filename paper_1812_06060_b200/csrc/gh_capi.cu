@@ -642,15 +642,32 @@ namespace {
 void distance_on_device(gh_levels* L, const gh_pipeline_config& c, double* d_dist, gh_run_report* rep) {
   gh_mesh* m = L->mesh;
   cudaStream_t s = m->stream;
-  require(c.method == GH_METHOD_FACE || c.method == GH_METHOD_EDGE, "gh_distance: unknown method");
+  require(c.method == GH_METHOD_FACE || c.method == GH_METHOD_EDGE || c.method == GH_METHOD_POISSON,
+          "gh_distance: unknown method");
   double t = c.t;
   if (!(t > 0.0)) {
     if (!(c.m > 0.0)) gh::fail(GH_ERR_INVALID, "diffusion_time: m must be positive");
     const double h = gh::mesh_average_edge_length(m);
     t = c.m * h * h;
   }
+  if (rep) rep->diffusion_e1 = -1.0;
+  if (c.method == GH_METHOD_POISSON) {  // geoheat.cpp:96-103
+    require(c.cg_tol > 0.0, "gh_distance: cg_tol must be positive");
+    const gh::PoissonOut po = gh::poisson_heat_dev(L, t, c.cg_tol, d_dist);
+    if (rep) {
+      rep->t = t;
+      rep->cg_iterations = po.heat_iterations + po.poisson_iterations;
+      rep->final_primal = po.poisson_residual;
+      rep->poisson_residual = po.poisson_residual;
+      rep->diffusion_ms = po.heat_seconds * 1e3;
+      rep->optimization_ms = po.poisson_seconds * 1e3;
+      rep->solver_state_bytes = state_formula(m, GH_METHOD_FACE);  // geoheat.cpp:145-147
+    }
+    return;
+  }
   gh::EventTimer tn(s), ti(s);
   const double diff_ms = gh::diffuse_dev(L, t, c.sweeps, nullptr);
+  if (rep && (c.flags & GH_PIPE_DIFFUSION_E1)) rep->diffusion_e1 = gh::diffusion_residual_dev(L, L->u_orig.p, t);
   gh::Scratch<double> H(3 * (size_t)m->nf, s);
   tn.start();
   const int32_t zc = gh::normalize_dev(m, L->u_orig.p, H.p);
@@ -741,6 +758,113 @@ gh_status gh_distance_host(const double* positions, int32_t nv, const int32_t* f
   gh_status s3 = gh_mesh_destroy(mesh);
   if (st == GH_OK) st = s2 != GH_OK ? s2 : s3;
   return st;
+}
+
+gh_status gh_poisson_heat_method(gh_levels* levels, double t, double cg_tol, double* d_out, gh_poisson_report* report) {
+  return guarded([&] {
+    require(levels && d_out, "gh_poisson_heat_method: null argument");
+    require(t > 0.0 && cg_tol > 0.0, "gh_poisson_heat_method: t and cg_tol must be positive");
+    gh_mesh* m = levels->mesh;
+    use_device_of(m);
+    take_launches(m);
+    gh::Scratch<double> dd(m->nv, m->stream);
+    const gh::PoissonOut po = gh::poisson_heat_dev(levels, t, cg_tol, dd.p);
+    to_host(d_out, dd.p, m->nv, m->stream);
+    if (report) {
+      report->heat_iterations = po.heat_iterations;
+      report->poisson_iterations = po.poisson_iterations;
+      report->heat_residual = po.heat_residual;
+      report->poisson_residual = po.poisson_residual;
+      report->heat_seconds = po.heat_seconds;
+      report->poisson_seconds = po.poisson_seconds;
+      report->kernel_launches = take_launches(m);
+      report->reserved = 0;
+    }
+  });
+}
+
+gh_status gh_triangulation_quality(gh_mesh* mesh, double* tau_out) {
+  return guarded([&] {
+    require(mesh && tau_out, "gh_triangulation_quality: null argument");
+    use_device_of(mesh);
+    *tau_out = gh::triangulation_quality_dev(mesh);
+  });
+}
+
+gh_status gh_mesh_subdivide(gh_mesh* mesh, int32_t levels, gh_mesh** out) {
+  return guarded([&] {
+    require(mesh && out, "gh_mesh_subdivide: null argument");
+    use_device_of(mesh);
+    std::unique_ptr<gh_mesh> cur = new_mesh();
+    if (levels <= 0) {
+      gh::copy_mesh_arrays(mesh, cur.get());  // midpoint_subdivide(mesh, 0) returns the mesh
+    } else {
+      gh::subdivide_once(mesh, cur.get());
+      for (int32_t i = 1; i < levels; ++i) {
+        std::unique_ptr<gh_mesh> next = new_mesh();
+        gh::subdivide_once(cur.get(), next.get());
+        cur = std::move(next);
+      }
+    }
+    GH_CUDA(cudaStreamSynchronize(cur->stream));
+    *out = cur.release();
+  });
+}
+
+static void check_sources(const gh_mesh* m, const int32_t* sources, int32_t ns) {
+  require(ns >= 0 && (ns == 0 || sources), "null sources");
+  for (int32_t i = 0; i < ns; ++i)
+    if (sources[i] < 0 || sources[i] >= m->nv)
+      gh::fail(GH_ERR_INVALID, "source index " + std::to_string(sources[i]) + " out of range");
+}
+
+gh_status gh_analytic_distance(gh_mesh* mesh, int32_t kind, const int32_t* sources, int32_t ns, double* d_out) {
+  return guarded([&] {
+    require(mesh && d_out, "gh_analytic_distance: null argument");
+    require(kind == GH_SURFACE_PLANE || kind == GH_SURFACE_SPHERE, "gh_analytic_distance: unknown surface");
+    check_sources(mesh, sources, ns);
+    use_device_of(mesh);
+    cudaStream_t s = mesh->stream;
+    gh::Scratch<int32_t> src(ns, s);
+    gh::Scratch<double> d(mesh->nv, s);
+    if (ns) GH_CUDA(cudaMemcpyAsync(src.p, sources, sizeof(int32_t) * ns, cudaMemcpyHostToDevice, s));
+    gh::analytic_dev(mesh, kind, src.p, ns, d.p);
+    to_host(d_out, d.p, mesh->nv, s);
+  });
+}
+
+gh_status gh_dijkstra_distance(gh_mesh* mesh, const int32_t* sources, int32_t ns, double* d_out) {
+  return guarded([&] {
+    require(mesh && d_out, "gh_dijkstra_distance: null argument");
+    check_sources(mesh, sources, ns);
+    use_device_of(mesh);
+    cudaStream_t s = mesh->stream;
+    gh::Scratch<int32_t> src(ns, s);
+    gh::Scratch<double> d(mesh->nv, s);
+    if (ns) GH_CUDA(cudaMemcpyAsync(src.p, sources, sizeof(int32_t) * ns, cudaMemcpyHostToDevice, s));
+    gh::dijkstra_dev(mesh, src.p, ns, d.p);
+    to_host(d_out, d.p, mesh->nv, s);
+  });
+}
+
+gh_status gh_error_metrics(const double* d, const double* d_ref, int64_t n, const int32_t* sources, int32_t ns,
+                           double* mean_rel_error, int32_t* excluded, double* e2) {
+  return guarded([&] {
+    require(n > 0 && d && d_ref && mean_rel_error && excluded && e2, "gh_error_metrics: bad argument");
+    require(ns >= 0 && (ns == 0 || sources), "gh_error_metrics: null sources");
+    int ndev = 0;
+    if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev == 0) {
+      (void)cudaGetLastError();
+      gh::fail(GH_ERR_CUDA, "no CUDA device available (the geoheat_b200 path has no CPU fallback)");
+    }
+    if (g_device >= 0) GH_CUDA(cudaSetDevice(g_device));
+    int dev = 0;
+    GH_CUDA(cudaGetDevice(&dev));
+    cudaStream_t s;
+    double* pinned;
+    thread_context(dev, &s, &pinned);
+    gh::errors_dev(s, d, d_ref, n, sources, ns, mean_rel_error, excluded, e2);
+  });
 }
 
 uint64_t gh_field_hash(const double* values, int64_t n) {

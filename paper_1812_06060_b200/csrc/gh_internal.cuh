@@ -239,6 +239,22 @@ void integrate_edge_dev(gh_levels* L, const double* d_x, double* d_d);
 // deterministic reductions (gh_mesh.cu): sum of partials[0..kReduceGrid)
 void reduce_partials(gh_mesh* m, double* d_result_slot);
 
+// classic heat method on CG (gh_poisson.cu)
+struct PoissonOut {
+  int heat_iterations = 0, poisson_iterations = 0;
+  double heat_residual = 0, poisson_residual = 0, heat_seconds = 0, poisson_seconds = 0;
+};
+PoissonOut poisson_heat_dev(gh_levels* L, double t, double tol, double* d_d);
+
+// evaluation layer (gh_metrics.cu)
+double triangulation_quality_dev(gh_mesh* m);
+void subdivide_once(gh_mesh* src, gh_mesh* dst);
+void copy_mesh_arrays(gh_mesh* src, gh_mesh* dst);
+void analytic_dev(gh_mesh* m, int kind, const int32_t* d_src, int32_t ns, double* d_out);
+void dijkstra_dev(gh_mesh* m, const int32_t* d_src, int32_t ns, double* d_out);
+void errors_dev(cudaStream_t s, const double* d, const double* r, int64_t n, const int32_t* src, int32_t ns,
+                double* mre, int32_t* excluded, double* e2);
+
 }  // namespace gh
 
 // ---------------------------------------------------------------- device helpers

@@ -225,7 +225,12 @@ void load_binary_ply(gh_mesh* m, const ghio::PlyHeader& h, const unsigned char* 
     ghio::HostMesh hm;
     ghio::walk_binary(h, src, 0, 0, 0, 0, &hm);
     if (rep) rep->parse_ms = ms_since(t0);
+    auto tb = std::chrono::steady_clock::now();
     from_host(m, hm);
+    if (rep) {
+      GH_CUDA(cudaStreamSynchronize(m->stream));
+      rep->build_ms = ms_since(tb);
+    }
     return;
   }
   const uint64_t vs = (uint64_t)L.vstride, fs = (uint64_t)L.fstride;
@@ -279,7 +284,12 @@ void load_binary_ply(gh_mesh* m, const ghio::PlyHeader& h, const unsigned char* 
   }
   if (h.elements.size() > 2) ghio::walk_binary(h, src, 2, 0, vbytes + (uint64_t)L.nf * fs, L.nv, nullptr);
   if (rep) rep->parse_ms = ms_since(td);
+  auto tb = std::chrono::steady_clock::now();
   gh::mesh_build(m, nullptr, nullptr);
+  if (rep) {
+    GH_CUDA(cudaStreamSynchronize(s));
+    rep->build_ms = ms_since(tb);
+  }
 }
 
 }  // namespace
@@ -305,7 +315,10 @@ void load_mesh_bytes(gh_mesh* m, const unsigned char* bytes, uint64_t n, int for
       }
       auto tb = std::chrono::steady_clock::now();
       from_host(m, hm);
-      if (rep) rep->build_ms = ms_since(tb);
+      if (rep) {
+        GH_CUDA(cudaStreamSynchronize(m->stream));
+        rep->build_ms = ms_since(tb);
+      }
       return;
     }
     const ghio::PlyHeader h = ghio::parse_ply_header((const char*)bytes, n);
@@ -319,7 +332,10 @@ void load_mesh_bytes(gh_mesh* m, const unsigned char* bytes, uint64_t n, int for
       }
       auto tb = std::chrono::steady_clock::now();
       from_host(m, hm);
-      if (rep) rep->build_ms = ms_since(tb);
+      if (rep) {
+        GH_CUDA(cudaStreamSynchronize(m->stream));
+        rep->build_ms = ms_since(tb);
+      }
       return;
     }
     double parse0 = ms_since(t0);

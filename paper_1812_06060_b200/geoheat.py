@@ -546,11 +546,19 @@ class RunReport:
     d2h_bytes: int = 0
     solver_state_bytes: int = 0
     kernel_launches: int = 0
+    cg_iterations: int = 0
+    diffusion_e1: float = -1.0
+    poisson_residual: float = 0.0
 
 
-def _pipeline_config(method, sweeps, t, m, admm: AdmmConfig) -> gh_pipeline_config:
-    meth = 0 if method in ("face", OptimizerKind.Face, 0) else 1
-    return gh_pipeline_config(meth, int(sweeps), float(t if t is not None else 0.0), float(m), admm._c())
+_METHODS = {"face": 0, "edge": 1, "poisson": 2}
+
+
+def _pipeline_config(method, sweeps, t, m, admm: AdmmConfig, cg_tol: float = 1e-5,
+                     diffusion_e1: bool = False) -> gh_pipeline_config:
+    meth = _METHODS[method] if isinstance(method, str) else int(method)
+    return gh_pipeline_config(meth, int(sweeps), float(t if t is not None else 0.0), float(m), admm._c(),
+                              float(cg_tol), 1 if diffusion_e1 else 0, 0)
 
 
 def _run_report(r: gh_run_report) -> RunReport:
@@ -559,10 +567,11 @@ def _run_report(r: gh_run_report) -> RunReport:
 
 
 def distance(levels: BfsLevels, method: str = "face", sweeps: int = 1000, t: Optional[float] = None, m: float = 1.0,
-             admm: AdmmConfig = AdmmConfig()):
-    """The solver chain of run_pipeline (tools/geoheat.cpp:108-143), device-resident between stages."""
+             admm: AdmmConfig = AdmmConfig(), cg_tol: float = 1e-5, diffusion_e1: bool = False):
+    """The solver chain of run_pipeline (tools/geoheat.cpp:96-143), device-resident between stages;
+    method "face" | "edge" | "poisson" (the CG heat method, cg_tol = the CLI's --eps)."""
     d = np.empty(levels.mesh.vertex_count(), np.float64)
-    cfg = _pipeline_config(method, sweeps, t, m, admm)
+    cfg = _pipeline_config(method, sweeps, t, m, admm, cg_tol, diffusion_e1)
     rep = gh_run_report()
     _check(levels._lib.gh_distance(levels._h, C.byref(cfg), _ptr(d), C.byref(rep)))
     return d, _run_report(rep)
@@ -580,6 +589,74 @@ def distance_host(positions, faces, sources, method: str = "face", sweeps: int =
     _check(_lib.load().gh_distance_host(_ptr(P), P.shape[0], _ptr(Fc), Fc.shape[0], _ptr(S), S.size, C.byref(cfg),
                                         _ptr(d), C.byref(rep)))
     return d, _run_report(rep)
+
+
+@dataclass
+class PoissonReport:
+    """PoissonReport (reference.hpp:167-174)."""
+    heat_iterations: int
+    poisson_iterations: int
+    heat_residual: float
+    poisson_residual: float
+    heat_seconds: float
+    poisson_seconds: float
+    kernel_launches: int
+
+
+def poisson_heat_method(mesh: TriMesh, sources: Sequence[int], t: float, cg_tol: float,
+                        levels: Optional[BfsLevels] = None):
+    """poisson_heat_method (reference.hpp:176-216) on the device -> (d, PoissonReport)."""
+    lv = levels if levels is not None else bfs_levels(mesh, sources)
+    d = np.empty(mesh.vertex_count(), np.float64)
+    rep = _lib.gh_poisson_report()
+    _check(lv._lib.gh_poisson_heat_method(lv._h, float(t), float(cg_tol), _ptr(d), C.byref(rep)))
+    return d, PoissonReport(rep.heat_iterations, rep.poisson_iterations, rep.heat_residual, rep.poisson_residual,
+                            rep.heat_seconds, rep.poisson_seconds, rep.kernel_launches)
+
+
+def triangulation_quality(mesh: TriMesh) -> float:
+    """triangulation_quality (mesh.hpp:297-310)."""
+    v = C.c_double()
+    _check(mesh._lib.gh_triangulation_quality(mesh._h, C.byref(v)))
+    return v.value
+
+
+def midpoint_subdivide(mesh: TriMesh, levels: int) -> TriMesh:
+    """midpoint_subdivide (subdivide.hpp:13-45) on the device."""
+    h = C.c_void_p()
+    _check(mesh._lib.gh_mesh_subdivide(mesh._h, int(levels), C.byref(h)))
+    return TriMesh(h)
+
+
+class AnalyticSurface(enum.IntEnum):
+    PlaneEuclidean = 0
+    SphereGreatCircle = 1
+
+
+def analytic_oracle(kind: AnalyticSurface, mesh: TriMesh, sources: Sequence[int]) -> np.ndarray:
+    """analytic_oracle (reference.hpp:283-321); ValueError off the surface."""
+    S = np.ascontiguousarray(sources, dtype=np.int32)
+    d = np.empty(mesh.vertex_count(), np.float64)
+    _check(mesh._lib.gh_analytic_distance(mesh._h, int(kind), _ptr(S), S.size, _ptr(d)))
+    return d
+
+
+def dijkstra_edge_distance(mesh: TriMesh, sources: Sequence[int]) -> np.ndarray:
+    """dijkstra_edge_distance (reference.hpp:219-244)."""
+    S = np.ascontiguousarray(sources, dtype=np.int32)
+    d = np.empty(mesh.vertex_count(), np.float64)
+    _check(mesh._lib.gh_dijkstra_distance(mesh._h, _ptr(S), S.size, _ptr(d)))
+    return d
+
+
+def error_metrics(d, d_ref, sources: Sequence[int]):
+    """(mean_relative_error, excluded, recovery_error) (reference.hpp:247-276)."""
+    a, b = _f64(d), _f64(d_ref)
+    S = np.ascontiguousarray(sources, dtype=np.int32)
+    mre, e2, exc = C.c_double(), C.c_double(), C.c_int32()
+    _check(_lib.load().gh_error_metrics(_ptr(a), _ptr(b), a.size, _ptr(S), S.size, C.byref(mre), C.byref(exc),
+                                        C.byref(e2)))
+    return mre.value, exc.value, e2.value
 
 
 def field_hash(values) -> int:
