@@ -150,6 +150,7 @@ typedef struct {
   int32_t cg_iterations;  /* GH_METHOD_POISSON: heat + Poisson CG iterations */
   double diffusion_e1;    /* GH_PIPE_DIFFUSION_E1, else -1 */
   double poisson_residual;/* GH_METHOD_POISSON: final relative residual (reported as final_primal) */
+  uint64_t state_bytes_allocated; /* device bytes of the optimiser state (SolverReport field) */
 } gh_run_report;
 
 /* ---- runtime */

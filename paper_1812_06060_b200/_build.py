@@ -22,6 +22,8 @@ CSRC = os.path.join(PKG, "csrc")
 LIBDIR = os.path.join(PKG, "lib")
 CUDA_LIB = os.path.join(LIBDIR, "libgeoheat_b200.so")
 MESHGEN_LIB = os.path.join(LIBDIR, "libgh_meshgen.so")
+CLI_BIN = os.path.join(LIBDIR, "geoheat_b200")
+CLI_SRC = os.path.join(PKG, "cli", "geoheat_cli.cpp")
 
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 NVCC_FLAGS = ARCH + ["-O3", "-lineinfo", "-std=c++17", "-fmad=false", "-Xcompiler", "-fPIC,-O2,-ffp-contract=off",
@@ -94,9 +96,25 @@ def build_cuda(force: bool = False, verbose: bool = False) -> str:
     return CUDA_LIB
 
 
+def build_cli(force: bool = False) -> str:
+    """The reference CLI (tools/geoheat.cpp) on the C ABI: lib/geoheat_b200."""
+    lib = build_cuda()
+    header = os.path.join(ROOT, "include", "geoheat_b200.h")
+    if force or not _newer(CLI_BIN, [CLI_SRC, header, lib]):
+        tmp = CLI_BIN + ".tmp"
+        r = subprocess.run(["g++", "-std=c++17", "-O2", "-Wall", "-I", os.path.join(ROOT, "include"), "-o", tmp, CLI_SRC,
+                            "-L", LIBDIR, "-lgeoheat_b200", "-Wl,-rpath,$ORIGIN", "-pthread"],
+                           capture_output=True, text=True)
+        if r.returncode != 0:
+            raise RuntimeError(f"CLI build failed:\n{r.stderr}")
+        os.replace(tmp, CLI_BIN)
+    return CLI_BIN
+
+
 def build_all(force: bool = False) -> None:
     build_meshgen(force)
     build_cuda(force)
+    build_cli(force)
 
 
 if __name__ == "__main__":

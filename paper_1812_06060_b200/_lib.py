@@ -50,7 +50,8 @@ class gh_run_report(C.Structure):
                 ("integration_ms", C.c_double), ("h2d_ms", C.c_double), ("d2h_ms", C.c_double),
                 ("total_ms", C.c_double), ("h2d_bytes", C.c_uint64), ("d2h_bytes", C.c_uint64),
                 ("solver_state_bytes", C.c_uint64), ("kernel_launches", C.c_int32), ("cg_iterations", C.c_int32),
-                ("diffusion_e1", C.c_double), ("poisson_residual", C.c_double)]
+                ("diffusion_e1", C.c_double), ("poisson_residual", C.c_double),
+                ("state_bytes_allocated", C.c_uint64)]
 
 
 class gh_poisson_report(C.Structure):

@@ -699,6 +699,7 @@ void distance_on_device(gh_levels* L, const gh_pipeline_config& c, double* d_dis
     rep->optimization_ms = r.device_ms;
     rep->integration_ms = ti.ms();
     rep->solver_state_bytes = state_formula(m, c.method);
+    rep->state_bytes_allocated = r.state_bytes;
   }
 }
 

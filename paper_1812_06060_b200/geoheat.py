@@ -549,6 +549,7 @@ class RunReport:
     cg_iterations: int = 0
     diffusion_e1: float = -1.0
     poisson_residual: float = 0.0
+    state_bytes_allocated: int = 0
 
 
 _METHODS = {"face": 0, "edge": 1, "poisson": 2}
