@@ -146,10 +146,20 @@ __device__ __forceinline__ void block_share(int32_t c0, int32_t c1, int32_t b, i
   ce = cb + q + (b < rem ? 1 : 0);
 }
 
+__device__ __forceinline__ unsigned long long ld_acquire_gpu_u64(const unsigned long long* p) {
+  unsigned long long v;
+  asm volatile("ld.acquire.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+  return v;
+}
 __device__ __forceinline__ unsigned long long ld_acquire_sys_u64(const unsigned long long* p) {
   unsigned long long v;
   asm volatile("ld.acquire.sys.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
   return v;
+}
+// own levels are counted by this GPU's blocks; the two ghost levels by the
+// neighbour band's GPU (system scope)
+__device__ __forceinline__ unsigned long long ld_done(const unsigned long long* p, bool ghost) {
+  return ghost ? ld_acquire_sys_u64(p) : ld_acquire_gpu_u64(p);
 }
 
 // rows [rb, re) of the band's own levels active at step tau (L = tau - 2s, 0 <= s < S)
@@ -345,12 +355,13 @@ __global__ void __launch_bounds__(kTmaThreads, 2) k_diffuse_tma(const __grid_con
           if (X >= 0 && X < a.nlev) {
             const unsigned long long need =
                 (unsigned long long)((tau - X + 1) >> 1) * (unsigned long long)(pend[X] - pstart[X]);
-            if (ld_acquire_sys_u64(vba->rows_done + X) < need) {
+            const bool ghost = X < band_lb || X >= band_le;
+            if (ld_done(vba->rows_done + X, ghost) < need) {
               const long long t0 = clock64();
               unsigned ns = 64;
               for (unsigned it = 1;; ++it) {
                 __nanosleep(ns);
-                if (ld_acquire_sys_u64(vba->rows_done + X) >= need) break;
+                if (ld_done(vba->rows_done + X, ghost) >= need) break;
                 if (ns < 512) ns <<= 1;
                 if ((it & 255) == 0 && clock64() - t0 > (1ll << 35)) {  // ~17 s: a neighbour is gone
                   atomicExch(vba->stalled, 1);
