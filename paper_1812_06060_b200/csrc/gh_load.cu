@@ -122,6 +122,8 @@ void stage_to_device(const unsigned char* src, uint64_t n, unsigned char* dst, i
       GH_CUDA(cudaStreamSynchronize(s));
     } catch (const gh::Error& e) {
       errors[j] = e.msg;
+    } catch (...) {  // nothing may escape a std::thread
+      errors[j] = "host->device staging failed";
     }
     if (s) {
       cudaStreamSynchronize(s);

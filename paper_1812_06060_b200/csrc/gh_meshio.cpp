@@ -17,6 +17,7 @@
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
+#include <exception>
 #include <functional>
 #include <memory>
 #include <thread>
@@ -45,6 +46,12 @@ void parallel_for(int n, const std::function<void(int)>& body) {
     } catch (const std::bad_alloc&) {
       errors[i] = "std::bad_alloc";
       bad[i] = 2;
+    } catch (const std::exception& e) {  // nothing may escape a std::thread
+      errors[i] = e.what();
+      bad[i] = 1;
+    } catch (...) {
+      errors[i] = "unknown error in a mesh I/O worker";
+      bad[i] = 1;
     }
   };
   for (int i = 1; i < n; ++i) pool.emplace_back(run, i);
