@@ -270,8 +270,8 @@ gh_status gh_distance_host(const double* positions, int32_t nv, const int32_t* f
                            const int32_t* sources, int32_t ns, const gh_pipeline_config* config, double* d_out,
                            gh_run_report* report);
 
-/* ---- classic heat method on CG: poisson_heat_method (reference.hpp:176-216)
- * Jacobi-preconditioned CG (cg_solve, reference.hpp:35-109) on the heat
+/* ---- classic heat method on CG: poisson_heat_method (reference.hpp:175-216)
+ * Jacobi-preconditioned CG (cg_solve, reference.hpp:35-84) on the heat
  * operator, normalised gradients, integrated divergence, CG on the reduced
  * Poisson operator; sources are the levels' ring 0. GH_ERR_SOLVER on a CG
  * breakdown. d_out: host [V] (inf for unreachable vertices). */
@@ -286,14 +286,14 @@ gh_status gh_poisson_heat_method(gh_levels* levels, double t, double cg_tol, dou
 /* ---- evaluation layer of the CLI */
 /* triangulation_quality (mesh.hpp:297-310), tree-summed. */
 gh_status gh_triangulation_quality(gh_mesh* mesh, double* tau_out);
-/* midpoint_subdivide (subdivide.hpp:13-45) -> a new device mesh. */
+/* midpoint_subdivide (subdivide.hpp:14-44) -> a new device mesh. */
 gh_status gh_mesh_subdivide(gh_mesh* mesh, int32_t levels, gh_mesh** out);
 typedef enum { GH_SURFACE_PLANE = 0, GH_SURFACE_SPHERE = 1 } gh_analytic_surface; /* AnalyticSurface */
 /* analytic_oracle (reference.hpp:283-321); GH_ERR_INVALID off the surface. */
 gh_status gh_analytic_distance(gh_mesh* mesh, int32_t kind, const int32_t* sources, int32_t ns, double* d_out);
-/* dijkstra_edge_distance (reference.hpp:219-244). */
+/* dijkstra_edge_distance (reference.hpp:220-245). */
 gh_status gh_dijkstra_distance(gh_mesh* mesh, const int32_t* sources, int32_t ns, double* d_out);
-/* mean_relative_error (reference.hpp:247-266) and recovery_error (268-276)
+/* mean_relative_error (reference.hpp:250-266) and recovery_error (268-276)
  * of two host fields, on the current device. */
 gh_status gh_error_metrics(const double* d, const double* d_ref, int64_t n, const int32_t* sources, int32_t ns,
                            double* mean_rel_error, int32_t* excluded, double* e2);

@@ -15,8 +15,12 @@
 
 #include <array>
 #include <cstdint>
+#include <cstdlib>
 #include <cstring>
+#include <iterator>
+#include <istream>
 #include <optional>
+#include <ostream>
 #include <span>
 #include <stdexcept>
 #include <string>
@@ -28,7 +32,10 @@
 #ifdef GEOHEAT_B200_REFERENCE_TYPES
 namespace geoheat::b200 {
 using ::geoheat::AdmmConfig;
+using ::geoheat::AnalyticSurface;
 using ::geoheat::DiffusionConfig;
+using ::geoheat::MeshFormat;
+using ::geoheat::PoissonReport;
 using ::geoheat::Index;
 using ::geoheat::MeshError;
 using ::geoheat::SolverError;
@@ -71,6 +78,16 @@ struct DiffusionConfig {  // diffusion.hpp:16-25
     if (!(m > 0.0)) throw std::invalid_argument("DiffusionConfig: m must be positive");
     if (sweeps < 0) throw std::invalid_argument("DiffusionConfig: sweeps must be >= 0");
   }
+};
+enum class MeshFormat { OBJ, PLY };                            // mesh_io.hpp:18
+enum class AnalyticSurface { PlaneEuclidean, SphereGreatCircle };  // reference.hpp:278
+struct PoissonReport {                                             // reference.hpp:163-170
+  int heat_iterations = 0;
+  int poisson_iterations = 0;
+  double heat_residual = 0.0;
+  double poisson_residual = 0.0;
+  double heat_seconds = 0.0;
+  double poisson_seconds = 0.0;
 };
 struct AdmmConfig {  // grad_face.hpp:15-26
   int max_iterations = 10;
@@ -363,6 +380,142 @@ inline VertexScalarField integrate_edge_differences(const TriMesh& mesh, const B
 /// field_hash (report.hpp:145-153).
 inline std::uint64_t field_hash(const VertexScalarField& values) {
   return gh_field_hash(values.data(), static_cast<std::int64_t>(values.size()));
+}
+
+// ---- mesh I/O (mesh_io.hpp): binary PLY decoded on the device, text
+// formats tokenised by host threads; same messages as the reference.
+
+/// format_from_path (mesh_io.hpp:271-278).
+inline MeshFormat format_from_path(const std::string& path) {
+  std::int32_t f = 0;
+  detail::check(gh_mesh_format_from_path(path.c_str(), &f));
+  return f == GH_FORMAT_OBJ ? MeshFormat::OBJ : MeshFormat::PLY;
+}
+
+/// load_mesh(path) (mesh_io.hpp:280-285).
+inline TriMesh load_mesh(const std::string& path) {
+  gh_mesh* h = nullptr;
+  detail::check(gh_mesh_load(path.c_str(), &h, nullptr));
+  return TriMesh(h);
+}
+
+/// load_mesh(istream, format) (mesh_io.hpp:267-269).
+inline TriMesh load_mesh(std::istream& in, MeshFormat format) {
+  const std::string data((std::istreambuf_iterator<char>(in)), std::istreambuf_iterator<char>());
+  gh_mesh* h = nullptr;
+  detail::check(gh_mesh_load_memory(data.data(), data.size(), format == MeshFormat::OBJ ? GH_FORMAT_OBJ : GH_FORMAT_PLY,
+                                    &h, nullptr));
+  return TriMesh(h);
+}
+
+namespace detail {
+struct Bytes {  // a gh_free'd buffer
+  void* p = nullptr;
+  std::uint64_t n = 0;
+  ~Bytes() { gh_free(p); }
+};
+}  // namespace detail
+
+/// save_obj (mesh_io.hpp:287-295).
+inline void save_obj(std::ostream& os, const TriMesh& mesh) {
+  detail::Bytes b;
+  detail::check(gh_mesh_serialize(mesh.handle(), GH_FORMAT_OBJ, nullptr, &b.p, &b.n));
+  os.write(static_cast<const char*>(b.p), static_cast<std::streamsize>(b.n));
+}
+
+/// save_ply (mesh_io.hpp:297-319): binary little-endian, optional per-vertex quality.
+inline void save_ply(std::ostream& os, const TriMesh& mesh, const VertexScalarField* quality = nullptr) {
+  detail::Bytes b;
+  detail::check(gh_mesh_serialize(mesh.handle(), GH_FORMAT_PLY, quality ? quality->data() : nullptr, &b.p, &b.n));
+  os.write(static_cast<const char*>(b.p), static_cast<std::streamsize>(b.n));
+}
+
+/// save_mesh (mesh_io.hpp:321-326).
+inline void save_mesh(const std::string& path, const TriMesh& mesh) {
+  detail::check(gh_mesh_save(mesh.handle(), path.c_str(), nullptr));
+}
+
+/// write_distances_txt / write_distances_csv (mesh_io.hpp:329-344).
+inline void write_distances_txt(std::ostream& os, const VertexScalarField& d) {
+  detail::Bytes b;
+  detail::check(gh_format_distances(d.data(), static_cast<std::int64_t>(d.size()), GH_DISTANCES_TXT, &b.p, &b.n));
+  os.write(static_cast<const char*>(b.p), static_cast<std::streamsize>(b.n));
+}
+inline void write_distances_csv(std::ostream& os, const VertexScalarField& d) {
+  detail::Bytes b;
+  detail::check(gh_format_distances(d.data(), static_cast<std::int64_t>(d.size()), GH_DISTANCES_CSV, &b.p, &b.n));
+  os.write(static_cast<const char*>(b.p), static_cast<std::streamsize>(b.n));
+}
+
+// ---- the classic heat method and the evaluation layer (reference.hpp,
+// subdivide.hpp, mesh.hpp:297-310)
+
+/// poisson_heat_method (reference.hpp:175-216) on device CG.
+inline VertexScalarField poisson_heat_method(const TriMesh& mesh, std::span<const Index> sources, double t,
+                                             double cg_tol, PoissonReport* report = nullptr) {
+  BfsLevels levels = bfs_levels(mesh, sources);
+  VertexScalarField d(static_cast<std::size_t>(mesh.vertex_count()));
+  gh_poisson_report r{};
+  detail::check(gh_poisson_heat_method(levels.handle(), t, cg_tol, d.data(), &r));
+  if (report) {
+    report->heat_iterations = r.heat_iterations;
+    report->poisson_iterations = r.poisson_iterations;
+    report->heat_residual = r.heat_residual;
+    report->poisson_residual = r.poisson_residual;
+    report->heat_seconds = r.heat_seconds;
+    report->poisson_seconds = r.poisson_seconds;
+  }
+  return d;
+}
+
+/// dijkstra_edge_distance (reference.hpp:220-245).
+inline VertexScalarField dijkstra_edge_distance(const TriMesh& mesh, std::span<const Index> sources) {
+  VertexScalarField d(static_cast<std::size_t>(mesh.vertex_count()));
+  detail::check(gh_dijkstra_distance(mesh.handle(), sources.data(), static_cast<std::int32_t>(sources.size()), d.data()));
+  return d;
+}
+
+/// analytic_oracle (reference.hpp:283-321).
+inline VertexScalarField analytic_oracle(AnalyticSurface kind, const TriMesh& mesh, std::span<const Index> sources) {
+  VertexScalarField d(static_cast<std::size_t>(mesh.vertex_count()));
+  detail::check(gh_analytic_distance(mesh.handle(),
+                                     kind == AnalyticSurface::PlaneEuclidean ? GH_SURFACE_PLANE : GH_SURFACE_SPHERE,
+                                     sources.data(), static_cast<std::int32_t>(sources.size()), d.data()));
+  return d;
+}
+
+/// mean_relative_error (reference.hpp:250-266).
+inline double mean_relative_error(const VertexScalarField& d, const VertexScalarField& d_ref,
+                                  std::span<const Index> sources, Index* excluded = nullptr) {
+  double mre = 0.0, e2 = 0.0;
+  std::int32_t exc = 0;
+  detail::check(gh_error_metrics(d.data(), d_ref.data(), static_cast<std::int64_t>(d.size()), sources.data(),
+                                 static_cast<std::int32_t>(sources.size()), &mre, &exc, &e2));
+  if (excluded) *excluded = exc;
+  return mre;
+}
+
+/// recovery_error (reference.hpp:269-276).
+inline double recovery_error(const VertexScalarField& d, const VertexScalarField& d_ref) {
+  double mre = 0.0, e2 = 0.0;
+  std::int32_t exc = 0;
+  detail::check(gh_error_metrics(d.data(), d_ref.data(), static_cast<std::int64_t>(d.size()), nullptr, 0, &mre, &exc,
+                                 &e2));
+  return e2;
+}
+
+/// midpoint_subdivide (subdivide.hpp:14-44).
+inline TriMesh midpoint_subdivide(const TriMesh& mesh, int levels) {
+  gh_mesh* h = nullptr;
+  detail::check(gh_mesh_subdivide(mesh.handle(), levels, &h));
+  return TriMesh(h);
+}
+
+/// triangulation_quality (mesh.hpp:297-310).
+inline double triangulation_quality(const TriMesh& mesh) {
+  double tau = 0.0;
+  detail::check(gh_triangulation_quality(mesh.handle(), &tau));
+  return tau;
 }
 
 }  // namespace geoheat::b200

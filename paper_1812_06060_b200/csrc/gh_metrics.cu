@@ -1,11 +1,11 @@
 // The reference's evaluation layer on the device, for the CLI drop-in
 // (tools/geoheat.cpp:71-100, 164-181, 265-275):
 //   triangulation_quality   mesh.hpp:297-310
-//   midpoint_subdivide      subdivide.hpp:13-45
+//   midpoint_subdivide      subdivide.hpp:14-44
 //   analytic_oracle         reference.hpp:283-321
-//   dijkstra_edge_distance  reference.hpp:219-244
-//   mean_relative_error     reference.hpp:247-266
-//   recovery_error          reference.hpp:268-276
+//   dijkstra_edge_distance  reference.hpp:220-245
+//   mean_relative_error     reference.hpp:250-266
+//   recovery_error          reference.hpp:269-276
 // Per-element values follow the reference formulas (-fmad=false). Sums over
 // all faces / vertices use the library's fixed-shape tree (as average edge
 // length does), so tau, the sphere's centre and radius and the two error
@@ -50,7 +50,7 @@ __global__ void k_quality_partial(const double* __restrict__ pos, const int32_t*
   if (threadIdx.x == 0) part[blockIdx.x] = sum;
 }
 
-// subdivide.hpp:17-40: originals, then one midpoint per edge in edge order;
+// subdivide.hpp:14-36: originals, then one midpoint per edge in edge order;
 // four faces per face.
 __global__ void k_subdivide(const double* __restrict__ pos, const int32_t* __restrict__ faces,
                             const int32_t* __restrict__ he_edge, const int32_t* __restrict__ edge_v, int64_t nv,

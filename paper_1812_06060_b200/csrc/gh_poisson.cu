@@ -1,11 +1,11 @@
 // The classic heat method on a CG backend:
-// poisson_heat_method (reference.hpp:176-216) = Jacobi-preconditioned CG on
-// the heat operator A - t*Lc (HeatOperator, reference.hpp:111-128), gradient
-// normalisation, integrated divergence (reference.hpp:160-175), and CG on the
+// poisson_heat_method (reference.hpp:175-216) = Jacobi-preconditioned CG on
+// the heat operator A - t*Lc (HeatOperator, reference.hpp:86-104), gradient
+// normalisation, integrated divergence (reference.hpp:142-160), and CG on the
 // reduced Poisson operator -Lc over the reachable non-source vertices
-// (ReducedPoissonOperator, reference.hpp:130-158).
+// (ReducedPoissonOperator, reference.hpp:107-139).
 //
-// The CG iteration (cg_solve, reference.hpp:35-109) runs device-driven: the
+// The CG iteration (cg_solve, reference.hpp:35-84) runs device-driven: the
 // scalars (alpha, beta, r.z, |r|) live in device memory, small single-block
 // kernels compute them, every kernel of an iteration returns at once when the
 // solve has finished, and a chunk of iterations is captured once as a CUDA
@@ -207,7 +207,7 @@ struct CgOut {
   bool converged = false, breakdown = false;
 };
 
-// cg_solve (reference.hpp:35-109) on the device; x receives the solution.
+// cg_solve (reference.hpp:35-84) on the device; x receives the solution.
 template <class Op>
 CgOut cg_solve_dev(gh_mesh* m, const Op& op, const double* d_rhs, double tol, int64_t max_iters, double* d_x) {
   cudaStream_t s = m->stream;
@@ -271,7 +271,7 @@ CgOut cg_solve_dev(gh_mesh* m, const Op& op, const double* d_rhs, double tol, in
   return out;
 }
 
-// integrated_divergence (reference.hpp:160-175)
+// integrated_divergence (reference.hpp:142-160)
 __global__ void k_divergence(const double* __restrict__ pos, const int32_t* __restrict__ faces,
                              const double* __restrict__ cot, const int32_t* __restrict__ vc_off,
                              const int32_t* __restrict__ vc_corner, const double* __restrict__ X, int64_t nv,

@@ -594,7 +594,7 @@ def distance_host(positions, faces, sources, method: str = "face", sweeps: int =
 
 @dataclass
 class PoissonReport:
-    """PoissonReport (reference.hpp:167-174)."""
+    """PoissonReport (reference.hpp:163-170)."""
     heat_iterations: int
     poisson_iterations: int
     heat_residual: float
@@ -606,7 +606,7 @@ class PoissonReport:
 
 def poisson_heat_method(mesh: TriMesh, sources: Sequence[int], t: float, cg_tol: float,
                         levels: Optional[BfsLevels] = None):
-    """poisson_heat_method (reference.hpp:176-216) on the device -> (d, PoissonReport)."""
+    """poisson_heat_method (reference.hpp:175-216) on the device -> (d, PoissonReport)."""
     lv = levels if levels is not None else bfs_levels(mesh, sources)
     d = np.empty(mesh.vertex_count(), np.float64)
     rep = _lib.gh_poisson_report()
@@ -623,7 +623,7 @@ def triangulation_quality(mesh: TriMesh) -> float:
 
 
 def midpoint_subdivide(mesh: TriMesh, levels: int) -> TriMesh:
-    """midpoint_subdivide (subdivide.hpp:13-45) on the device."""
+    """midpoint_subdivide (subdivide.hpp:14-44) on the device."""
     h = C.c_void_p()
     _check(mesh._lib.gh_mesh_subdivide(mesh._h, int(levels), C.byref(h)))
     return TriMesh(h)
@@ -643,7 +643,7 @@ def analytic_oracle(kind: AnalyticSurface, mesh: TriMesh, sources: Sequence[int]
 
 
 def dijkstra_edge_distance(mesh: TriMesh, sources: Sequence[int]) -> np.ndarray:
-    """dijkstra_edge_distance (reference.hpp:219-244)."""
+    """dijkstra_edge_distance (reference.hpp:220-245)."""
     S = np.ascontiguousarray(sources, dtype=np.int32)
     d = np.empty(mesh.vertex_count(), np.float64)
     _check(mesh._lib.gh_dijkstra_distance(mesh._h, _ptr(S), S.size, _ptr(d)))
@@ -651,7 +651,7 @@ def dijkstra_edge_distance(mesh: TriMesh, sources: Sequence[int]) -> np.ndarray:
 
 
 def error_metrics(d, d_ref, sources: Sequence[int]):
-    """(mean_relative_error, excluded, recovery_error) (reference.hpp:247-276)."""
+    """(mean_relative_error, excluded, recovery_error) (reference.hpp:250-276)."""
     a, b = _f64(d), _f64(d_ref)
     S = np.ascontiguousarray(sources, dtype=np.int32)
     mre, e2, exc = C.c_double(), C.c_double(), C.c_int32()

@@ -2,11 +2,11 @@
 rows 3-4) against the compiled reference (oracle/_ref, built from
 /root/reference; it ships with the repo snapshot).
 
-  poisson_heat_method   reference.hpp:176-216 — distances to 1e-9 relative,
+  poisson_heat_method   reference.hpp:175-216 — distances to 1e-9 relative,
                         same CG iteration counts (dot products are tree sums
                         here, left-to-right there)
-  dijkstra_edge_distance reference.hpp:219-244 — bit-identical
-  midpoint_subdivide    subdivide.hpp:13-45 — bit-identical meshes
+  dijkstra_edge_distance reference.hpp:220-245 — bit-identical
+  midpoint_subdivide    subdivide.hpp:14-44 — bit-identical meshes
   analytic_oracle       reference.hpp:283-321 — plane bit-identical, sphere
                         to 1e-12 (centre/radius are tree sums, acos differs)
   triangulation_quality, mean_relative_error, recovery_error — to 1e-12
