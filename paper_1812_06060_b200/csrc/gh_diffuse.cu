@@ -131,11 +131,19 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
       "r"(parity)
       : "memory");
 }
-__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
-  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
-                   smem_u32(dst)),
-               "l"(src), "r"(bytes), "r"(smem_u32(bar))
-               : "memory");
+// The CSR stream is read once per sweep: copy it with an L2 evict-first
+// policy so it does not push the reused u values out of L2.
+__device__ __forceinline__ uint64_t l2_evict_first_policy() {
+  uint64_t p;
+  asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(p));
+  return p;
+}
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar, uint64_t policy) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint [%0], [%1], %2, [%3], %4;" ::"r"(
+          smem_u32(dst)),
+      "l"(src), "r"(bytes), "r"(smem_u32(bar)), "l"(policy)
+      : "memory");
 }
 
 // contiguous share of the step's chunk range [c0, c1) for block b
@@ -292,11 +300,12 @@ __global__ void __launch_bounds__(kTmaThreads, 2) k_diffuse_tma(const __grid_con
           unsigned char* sb = reinterpret_cast<unsigned char*>(hdr);
           const uint32_t bytes = (uint32_t)nch * (256u + 64u) + (fits ? ncol * 12u : 0u);
           mbar_expect_tx(full + slot, bytes);
-          bulk_g2s(sb + kDenOff, vba->den + (int64_t)c0 * 32, (uint32_t)nch * 256u, full + slot);
-          bulk_g2s(sb + kDegOff, vba->deg + (int64_t)c0 * 32, (uint32_t)nch * 64u, full + slot);
+          const uint64_t pol = l2_evict_first_policy();
+          bulk_g2s(sb + kDenOff, vba->den + (int64_t)c0 * 32, (uint32_t)nch * 256u, full + slot, pol);
+          bulk_g2s(sb + kDegOff, vba->deg + (int64_t)c0 * 32, (uint32_t)nch * 64u, full + slot, pol);
           if (fits && ncol) {
-            bulk_g2s(sb + kColOff, vba->col + base, ncol * 4u, full + slot);
-            bulk_g2s(sb + kColOff + col_cap * 4u, vba->wt + base, ncol * 8u, full + slot);
+            bulk_g2s(sb + kColOff, vba->col + base, ncol * 4u, full + slot, pol);
+            bulk_g2s(sb + kColOff + col_cap * 4u, vba->wt + base, ncol * 8u, full + slot, pol);
           }
         }
         __syncwarp();
