@@ -324,6 +324,12 @@ gh_status gh_band_prepare(gh_band* band, double t, const double* initial);
 /* u_out (host [V], may be NULL): this band's vertices hold the result. */
 gh_status gh_band_launch(gh_band* band, double t, int32_t sweeps, double* u_out, gh_solver_report* report);
 
+/* deterministic_sum (parallel.hpp:50-54): the left-to-right sum of n host
+ * doubles, bit-identical. Non-negative terms take the parallel exact path
+ * (the library uses it for average_edge_length); any negative term falls
+ * back to one device thread adding in order. */
+gh_status gh_deterministic_sum(const double* terms, int64_t n, double* sum_out);
+
 /* field_hash (report.hpp:145-153): FNV-1a over the bytes of n doubles. */
 uint64_t gh_field_hash(const double* values, int64_t n);
 

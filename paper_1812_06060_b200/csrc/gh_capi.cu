@@ -868,6 +868,27 @@ gh_status gh_error_metrics(const double* d, const double* d_ref, int64_t n, cons
   });
 }
 
+gh_status gh_deterministic_sum(const double* terms, int64_t n, double* sum_out) {
+  return guarded([&] {
+    require(sum_out && n >= 0 && (n == 0 || terms), "gh_deterministic_sum: bad argument");
+    int ndev = 0;
+    if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev == 0) {
+      (void)cudaGetLastError();
+      gh::fail(GH_ERR_CUDA, "no CUDA device available (the geoheat_b200 path has no CPU fallback)");
+    }
+    if (g_device >= 0) GH_CUDA(cudaSetDevice(g_device));
+    int dev = 0;
+    GH_CUDA(cudaGetDevice(&dev));
+    keep_pool_memory(dev);
+    cudaStream_t s;
+    double* pinned;
+    thread_context(dev, &s, &pinned);
+    gh::Scratch<double> x(n, s);
+    if (n) GH_CUDA(cudaMemcpyAsync(x.p, terms, sizeof(double) * n, cudaMemcpyHostToDevice, s));
+    *sum_out = gh::deterministic_sum_dev(x.p, n, s);
+  });
+}
+
 uint64_t gh_field_hash(const double* values, int64_t n) {
   uint64_t h = 1469598103934665603ull;  // report.hpp:145-153
   const unsigned char* b = reinterpret_cast<const unsigned char*>(values);

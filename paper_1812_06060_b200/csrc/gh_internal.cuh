@@ -238,6 +238,10 @@ void integrate_edge_dev(gh_levels* L, const double* d_x, double* d_d);
 
 // deterministic reductions (gh_mesh.cu): sum of partials[0..kReduceGrid)
 void reduce_partials(gh_mesh* m, double* d_result_slot);
+// the reference's left-to-right sum of n non-negative doubles, bit for bit (gh_seqsum.cu)
+double sequential_sum_nonneg(const double* d_x, int64_t n, cudaStream_t s, int* launches);
+// any signs: the exact path when every term is >= 0, else one thread in order
+double deterministic_sum_dev(const double* d_x, int64_t n, cudaStream_t s);
 
 // classic heat method on CG (gh_poisson.cu)
 struct PoissonOut {

@@ -269,14 +269,11 @@ __global__ void k_boundary_count(const uint8_t* __restrict__ f, int64_t n, doubl
   if (threadIdx.x == 0) part[blockIdx.x] = s;
 }
 
-// per-edge length partials for average_edge_length (mesh.hpp:289-293)
-__global__ void k_edge_len_partial(const double* __restrict__ pos, const int32_t* __restrict__ edge_v, int64_t ne,
-                                   double* __restrict__ part) {
-  double s = 0.0;
+// per-edge lengths for average_edge_length (mesh.hpp:289-293)
+__global__ void k_edge_len(const double* __restrict__ pos, const int32_t* __restrict__ edge_v, int64_t ne,
+                           double* __restrict__ len) {
   for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < ne; e += (int64_t)gridDim.x * blockDim.x)
-    s += norm(sub(ld3(pos, edge_v[2 * e + 1]), ld3(pos, edge_v[2 * e])));
-  s = block_sum<B>(s);
-  if (threadIdx.x == 0) part[blockIdx.x] = s;
+    len[e] = norm(sub(ld3(pos, edge_v[2 * e + 1]), ld3(pos, edge_v[2 * e])));
 }
 
 __global__ void k_reduce_final(const double* __restrict__ part, int n, double* __restrict__ out) {
@@ -584,13 +581,14 @@ void mesh_build(gh_mesh* m, const double* h_pos, const int32_t* h_faces) {
   GH_CUDA(cudaStreamSynchronize(s));
 }
 
+// the reference's edge-order sum, bit for bit, so t = m h^2 matches too
 double mesh_average_edge_length(gh_mesh* m) {
   if (m->ne == 0) return NAN;
-  k_edge_len_partial<<<kReduceGrid, B, 0, m->stream>>>(m->pos.p, m->edge_v.p, m->ne, m->partials.p);
+  Scratch<double> len(m->ne, m->stream);
+  k_edge_len<<<grid_for(m->ne), B, 0, m->stream>>>(m->pos.p, m->edge_v.p, m->ne, len.p);
   GH_LAUNCH_CHECK();
   m->launches++;
-  reduce_partials(m, m->scalars.p + 2);
-  return read_scalar(m->scalars.p + 2, m->stream) / (double)m->ne;
+  return sequential_sum_nonneg(len.p, m->ne, m->stream, &m->launches) / (double)m->ne;
 }
 
 void face_gradient_dev(gh_mesh* m, const double* d_u, double* d_grad) {

@@ -660,6 +660,14 @@ def error_metrics(d, d_ref, sources: Sequence[int]):
     return mre.value, exc.value, e2.value
 
 
+def deterministic_sum(terms) -> float:
+    """deterministic_sum (parallel.hpp:50-54): the left-to-right sum, bit for bit, on the device."""
+    v = _f64(terms)
+    out = C.c_double()
+    _check(_lib.load().gh_deterministic_sum(_ptr(v), v.size, C.byref(out)))
+    return out.value
+
+
 def field_hash(values) -> int:
     """field_hash (report.hpp:145-153)."""
     v = _f64(values)

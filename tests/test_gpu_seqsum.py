@@ -1,0 +1,56 @@
+"""deterministic_sum (parallel.hpp:50-54) on the device, bit for bit: the
+reference's left-to-right sum (numpy's cumsum accumulates in the same order),
+including ties to even at binade steps, terms that jump binades, zeros,
+denormals, huge dynamic range and (ordered fallback) negative terms — and
+average_edge_length / t = m h^2 now equal the reference's bits."""
+import numpy as np
+import pytest
+
+pytestmark = pytest.mark.gpu
+
+
+def seq(x):
+    return float(np.cumsum(np.asarray(x, np.float64))[-1]) if len(x) else 0.0
+
+
+@pytest.mark.parametrize("n", [1, 7, 4096, 4097, 5000, 100_003, 3_000_000])
+def test_uniform_and_lognormal(gpu, n):
+    g = gpu.geoheat
+    rng = np.random.RandomState(n)
+    for x in (rng.uniform(0, 1, n), np.exp(rng.normal(0, 6, n)), rng.uniform(0, 1e-3, n) * (rng.uniform(size=n) > 0.3)):
+        assert g.deterministic_sum(x) == seq(x)
+
+
+def test_ties_and_binade_jumps(gpu):
+    g = gpu.geoheat
+    rng = np.random.RandomState(7)
+    n = 200_000
+    # halves and quarters on a large running sum: exact ties at u = 1, 2, 4, ...
+    x = rng.choice([0.5, 1.5, 0.25, 2.5, 1.0, 3.0], size=n)
+    x[5000] = 2.0 ** 53  # a term far above the running sum (binade jump)
+    x[100_000] = 2.0 ** 60
+    assert g.deterministic_sum(x) == seq(x)
+    y = np.concatenate([[2.0 ** 52], rng.choice([0.5, 1.0, 1.5], size=n)])
+    assert g.deterministic_sum(y) == seq(y)
+    # denormals and zeros
+    z = np.concatenate([np.zeros(5000), rng.uniform(0, 1, 5000) * 5e-324 * 1e3, rng.uniform(0, 1e-300, 10_000)])
+    assert g.deterministic_sum(z) == seq(z)
+
+
+def test_negative_terms_take_the_ordered_path(gpu):
+    g = gpu.geoheat
+    rng = np.random.RandomState(3)
+    x = rng.normal(0, 1, 50_000)
+    assert g.deterministic_sum(x) == seq(x)
+    assert g.deterministic_sum(np.array([])) == 0.0
+
+
+@pytest.mark.parametrize("config,scale", [(1, 1), (2, 1), (3, 2), (4, 16)])
+def test_average_edge_length_bitwise(gpu, port_oracle, config, scale):
+    from paper_1812_06060_b200 import meshgen
+    g = gpu.geoheat
+    w = meshgen.config(config, scale=scale)
+    mesh = g.build_mesh(w.positions, w.faces)
+    om = port_oracle.build_mesh(w.positions, w.faces)
+    assert g.average_edge_length(mesh) == om.average_edge_length()
+    assert g.diffusion_time(mesh, 1.0) == om.diffusion_time(1.0)
