@@ -6,11 +6,12 @@
 //   dijkstra_edge_distance  reference.hpp:220-245
 //   mean_relative_error     reference.hpp:250-266
 //   recovery_error          reference.hpp:269-276
-// Per-element values follow the reference formulas (-fmad=false). Sums over
-// all faces / vertices use the library's fixed-shape tree (as average edge
-// length does), so tau, the sphere's centre and radius and the two error
-// metrics agree with the reference to rounding, not bit for bit; plane and
-// Dijkstra distances and subdivided meshes are bit-identical.
+// Per-element values follow the reference formulas (-fmad=false), and the
+// sums of non-negative terms (tau, the sphere's radius, both error metrics)
+// are the reference's left-to-right sums bit for bit (gh_seqsum.cu); only
+// the sphere's centre (a signed sum of positions) is a fixed-shape tree, so
+// the sphere oracle agrees to rounding. Plane and Dijkstra distances and
+// subdivided meshes are bit-identical.
 
 #include <cmath>
 
@@ -34,20 +35,17 @@ T read_scalar(const T* d, cudaStream_t s) {
   return v;
 }
 
-__global__ void k_quality_partial(const double* __restrict__ pos, const int32_t* __restrict__ faces,
-                                  const double* __restrict__ area, int64_t nf, double* __restrict__ part) {
-  double sum = 0.0;
+__global__ void k_quality_terms(const double* __restrict__ pos, const int32_t* __restrict__ faces,
+                                const double* __restrict__ area, int64_t nf, double* __restrict__ term) {
   const double k = 2.0 * sqrt(3.0);
   GRID_STRIDE(f, nf) {
     const v3 p0 = ld3(pos, faces[3 * f]), p1 = ld3(pos, faces[3 * f + 1]), p2 = ld3(pos, faces[3 * f + 2]);
     const double a = ghd::norm(sub(p1, p2)), b = ghd::norm(sub(p2, p0)), c = ghd::norm(sub(p0, p1));
     const double s = 0.5 * ((a + b) + c);
     const double inradius = area[f] / s;
-    const double longest = fmax(fmax(a, b), c);
-    sum += k * inradius / longest;
+    const double longest = fmax(fmax(a, b), c);  // std::max({a, b, c}) on finite lengths
+    term[f] = k * inradius / longest;
   }
-  sum = block_sum<B>(sum);
-  if (threadIdx.x == 0) part[blockIdx.x] = sum;
 }
 
 // subdivide.hpp:14-36: originals, then one midpoint per edge in edge order;
@@ -131,11 +129,8 @@ __global__ void k_sum3(const double* __restrict__ pos, int64_t nv, double* __res
   }
 }
 
-__global__ void k_radius(const double* __restrict__ pos, int64_t nv, v3 c, double* __restrict__ part) {
-  double s = 0.0;
-  GRID_STRIDE(v, nv) s += ghd::norm(sub(ld3(pos, v), c));
-  s = block_sum<B>(s);
-  if (threadIdx.x == 0) part[blockIdx.x] = s;
+__global__ void k_radius_terms(const double* __restrict__ pos, int64_t nv, v3 c, double* __restrict__ term) {
+  GRID_STRIDE(v, nv) term[v] = ghd::norm(sub(ld3(pos, v), c));
 }
 
 __global__ void k_sphere(const double* __restrict__ pos, int64_t nv, const int32_t* __restrict__ src, int32_t ns,
@@ -195,45 +190,23 @@ __global__ void k_clear(int64_t n, int32_t* __restrict__ a) {
   GRID_STRIDE(i, n) a[i] = 0;
 }
 
-// mean_relative_error / recovery_error terms
-__global__ void k_errors(const double* __restrict__ d, const double* __restrict__ r, const uint8_t* __restrict__ is_src,
-                         int64_t n, double* __restrict__ part) {
-  double mre = 0.0, skipped = 0.0, e2 = 0.0;
+// mean_relative_error / recovery_error terms (zeros where the reference skips
+// a vertex: adding +0 to a non-negative running sum changes nothing)
+__global__ void k_error_terms(const double* __restrict__ d, const double* __restrict__ r,
+                              const uint8_t* __restrict__ is_src, int64_t n, double* __restrict__ mre_t,
+                              double* __restrict__ e2_t, int32_t* __restrict__ skipped) {
+  int32_t sk = 0;
   GRID_STRIDE(v, n) {
     const double diff = d[v] - r[v];
-    e2 += diff * diff;
-    if (is_src[v]) continue;
-    if (r[v] == 0.0 || !isfinite(r[v]) || !isfinite(d[v])) {
-      skipped += 1.0;
-      continue;
+    e2_t[v] = diff * diff;
+    double m = 0.0;
+    if (!is_src[v]) {
+      if (r[v] == 0.0 || !isfinite(r[v]) || !isfinite(d[v])) ++sk;
+      else m = fabs(d[v] - r[v]) / fabs(r[v]);
     }
-    mre += fabs(d[v] - r[v]) / fabs(r[v]);
+    mre_t[v] = m;
   }
-  mre = block_sum<B>(mre);
-  skipped = block_sum<B>(skipped);
-  e2 = block_sum<B>(e2);
-  if (threadIdx.x == 0) {
-    part[blockIdx.x] = mre;
-    part[G + blockIdx.x] = skipped;
-    part[2 * G + blockIdx.x] = e2;
-  }
-}
-
-// the fixed tree of gh::reduce_partials, for three partial arrays
-__global__ void k_final3(const double* __restrict__ part, double* __restrict__ out) {
-  __shared__ double sh[1024];
-  for (int k = 0; k < 3; ++k) {
-    double acc = 0.0;
-    for (unsigned i = threadIdx.x; i < G; i += 1024) acc += part[k * G + i];
-    sh[threadIdx.x] = acc;
-    __syncthreads();
-    for (int w = 512; w > 0; w >>= 1) {
-      if (threadIdx.x < w) sh[threadIdx.x] += sh[threadIdx.x + w];
-      __syncthreads();
-    }
-    if (threadIdx.x == 0) out[k] = sh[0];
-    __syncthreads();
-  }
+  if (sk) atomicAdd(skipped, sk);
 }
 
 __global__ void k_mark_sources(const int32_t* __restrict__ src, int32_t ns, int64_t n, uint8_t* __restrict__ f) {
@@ -246,11 +219,11 @@ __global__ void k_mark_sources(const int32_t* __restrict__ src, int32_t ns, int6
 namespace gh {
 
 double triangulation_quality_dev(gh_mesh* m) {
-  k_quality_partial<<<G, B, 0, m->stream>>>(m->pos.p, m->faces.p, m->face_area.p, m->nf, m->partials.p);
+  Scratch<double> term(m->nf, m->stream);
+  k_quality_terms<<<grid_for(m->nf), B, 0, m->stream>>>(m->pos.p, m->faces.p, m->face_area.p, m->nf, term.p);
   GH_LAUNCH_CHECK();
   m->launches++;
-  reduce_partials(m, m->scalars.p + 12);
-  return read_scalar(m->scalars.p + 12, m->stream) / (double)m->nf;
+  return sequential_sum_nonneg(term.p, m->nf, m->stream, &m->launches) / (double)m->nf;
 }
 
 void subdivide_once(gh_mesh* src, gh_mesh* dst) {
@@ -316,10 +289,10 @@ void analytic_dev(gh_mesh* m, int kind, const int32_t* d_src, int32_t ns, double
     c3[k] = read_scalar(slot, s) / (double)nv;
   }
   const v3 c{c3[0], c3[1], c3[2]};
-  k_radius<<<G, B, 0, s>>>(m->pos.p, nv, c, m->partials.p);
+  Scratch<double> term(nv, s);
+  k_radius_terms<<<grid_for(nv), B, 0, s>>>(m->pos.p, nv, c, term.p);
   m->launches++;
-  reduce_partials(m, slot);
-  const double radius = read_scalar(slot, s) / (double)nv;
+  const double radius = sequential_sum_nonneg(term.p, nv, s, &m->launches) / (double)nv;
   k_sphere<<<grid_for(nv), B, 0, s>>>(m->pos.p, nv, d_src, ns, c, radius, d_out, bad.p);
   m->launches++;
   if (read_scalar(bad.p, s)) fail(GH_ERR_INVALID, "analytic_oracle: mesh vertices are not on a common sphere");
@@ -350,25 +323,24 @@ void dijkstra_dev(gh_mesh* m, const int32_t* d_src, int32_t ns, double* d_out) {
 
 void errors_dev(cudaStream_t s, const double* d, const double* r, int64_t n, const int32_t* src, int32_t ns,
                 double* mre, int32_t* excluded, double* e2) {
-  Scratch<double> dd(n, s), rr(n, s), part(3 * (size_t)G, s), out(3, s);
+  Scratch<double> dd(n, s), rr(n, s), mt(n, s), et(n, s);
   Scratch<uint8_t> is_src(n, s);
-  Scratch<int32_t> ds(ns, s);
+  Scratch<int32_t> ds(ns, s), sk(1, s);
   GH_CUDA(cudaMemcpyAsync(dd.p, d, sizeof(double) * n, cudaMemcpyHostToDevice, s));
   GH_CUDA(cudaMemcpyAsync(rr.p, r, sizeof(double) * n, cudaMemcpyHostToDevice, s));
   GH_CUDA(cudaMemsetAsync(is_src.p, 0, n, s));
+  GH_CUDA(cudaMemsetAsync(sk.p, 0, sizeof(int32_t), s));
   if (ns) {
     GH_CUDA(cudaMemcpyAsync(ds.p, src, sizeof(int32_t) * ns, cudaMemcpyHostToDevice, s));
     k_mark_sources<<<1, 256, 0, s>>>(ds.p, ns, n, is_src.p);
   }
-  k_errors<<<G, B, 0, s>>>(dd.p, rr.p, is_src.p, n, part.p);
-  k_final3<<<1, 1024, 0, s>>>(part.p, out.p);
+  k_error_terms<<<grid_for(n), B, 0, s>>>(dd.p, rr.p, is_src.p, n, mt.p, et.p, sk.p);
   GH_LAUNCH_CHECK();
-  double h[3];
-  GH_CUDA(cudaMemcpyAsync(h, out.p, sizeof(h), cudaMemcpyDeviceToHost, s));
-  GH_CUDA(cudaStreamSynchronize(s));
-  *mre = h[0] / (double)n;
-  *excluded = (int32_t)h[1];
-  *e2 = std::sqrt(h[2]) / (double)n;
+  // left-to-right sums as the reference (reference.hpp:250-276); the e2 terms
+  // may be inf/nan when a field is infinite, which takes the ordered path
+  *mre = deterministic_sum_dev(mt.p, n, s) / (double)n;
+  *e2 = std::sqrt(deterministic_sum_dev(et.p, n, s)) / (double)n;
+  *excluded = read_scalar(sk.p, s);
 }
 
 }  // namespace gh
