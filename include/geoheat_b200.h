@@ -168,7 +168,7 @@ gh_status gh_mesh_destroy(gh_mesh* mesh);
 gh_status gh_mesh_get_info(const gh_mesh* mesh, gh_mesh_info* info);
 /* Copy one TriMesh array to host (`count` elements of the array's type). */
 gh_status gh_mesh_download(const gh_mesh* mesh, int32_t which, void* host_out, int64_t count);
-/* average_edge_length (mesh.hpp:289-293); deterministic pairwise sum. */
+/* average_edge_length (mesh.hpp:289-293): the edge-order sum, bit-identical. */
 gh_status gh_average_edge_length(gh_mesh* mesh, double* h_out);
 /* diffusion_time (diffusion.hpp:28-32): t = m * h * h. */
 gh_status gh_diffusion_time(gh_mesh* mesh, double m, double* t_out);
@@ -284,7 +284,7 @@ typedef struct {
 gh_status gh_poisson_heat_method(gh_levels* levels, double t, double cg_tol, double* d_out, gh_poisson_report* report);
 
 /* ---- evaluation layer of the CLI */
-/* triangulation_quality (mesh.hpp:297-310), tree-summed. */
+/* triangulation_quality (mesh.hpp:297-310): the face-order sum, bit-identical. */
 gh_status gh_triangulation_quality(gh_mesh* mesh, double* tau_out);
 /* midpoint_subdivide (subdivide.hpp:14-44) -> a new device mesh. */
 gh_status gh_mesh_subdivide(gh_mesh* mesh, int32_t levels, gh_mesh** out);
