@@ -26,15 +26,29 @@
 
 namespace {
 
-constexpr int kSeg = 1024;       // terms per segment
-constexpr int kSeqPrefix = 4096; // leading terms summed sequentially
+constexpr int kSeg = 1024;        // terms per segment
+constexpr int kSeqPrefix = 4096;  // leading terms summed sequentially
 constexpr int kMaxBinades = 48;
+constexpr int kWalkThreads = 1024;
 
-__global__ void k_seq(const double* __restrict__ x, int64_t b, int64_t e, double* __restrict__ out) {
-  if (threadIdx.x != 0 || blockIdx.x != 0) return;
-  double s = out[0];
-  for (int64_t k = b; k < e; ++k) s += x[k];
-  out[0] = s;
+// s += x[b..e) in order: the block stages 1024 terms at a time in shared
+// memory (coalesced) and thread 0 adds them one by one.
+__device__ double block_ordered_add(double s, const double* __restrict__ x, int64_t b, int64_t e, double* sh) {
+  for (int64_t c = b; c < e; c += kWalkThreads) {
+    const int64_t m = e - c < kWalkThreads ? e - c : kWalkThreads;
+    __syncthreads();
+    if (threadIdx.x < m) sh[threadIdx.x] = x[c + threadIdx.x];
+    __syncthreads();
+    if (threadIdx.x == 0)
+      for (int k = 0; k < m; ++k) s += sh[k];
+  }
+  return s;  // valid in thread 0
+}
+
+__global__ void k_seq_block(const double* __restrict__ x, int64_t b, int64_t e, double* __restrict__ acc) {
+  __shared__ double sh[kWalkThreads];
+  const double s = block_ordered_add(acc[0], x, b, e, sh);
+  if (threadIdx.x == 0) acc[0] = s;
 }
 
 __global__ void k_tree_partial(const double* __restrict__ x, int64_t b, int64_t n, double* __restrict__ part) {
@@ -45,49 +59,97 @@ __global__ void k_tree_partial(const double* __restrict__ x, int64_t b, int64_t 
   if (threadIdx.x == 0) part[blockIdx.x] = s;
 }
 
+// the binades [e0, e0 + nb) the running sum can visit, from the sequential
+// prefix acc[0] and an upper bound of the rest (nb = 0: no fast path)
+__global__ void k_binades(const double* __restrict__ part, int nparts, const double* __restrict__ acc,
+                          int32_t* __restrict__ prm) {
+  double r = 0.0;
+  for (int i = threadIdx.x; i < nparts; i += blockDim.x) r += part[i];
+  const double rest = ghd::block_sum<1024>(r);  // any order: only a bound
+  if (threadIdx.x != 0) return;
+  const double s0 = acc[0];
+  int nb = 0, e0 = 0;
+  if (s0 > 0.0 && isfinite(rest)) {
+    e0 = ilogb(s0);
+    const int e1 = ilogb((s0 + rest) * (1.0 + 1.0 / (1 << 20)));
+    nb = e1 - e0 + 1;
+    if (nb < 1 || nb > kMaxBinades || e0 - 52 < -1000 || e0 + nb > 1000) nb = 0;  // keep 2^(52-e) finite
+  }
+  prm[0] = e0;
+  prm[1] = nb;
+}
+
 // per segment g and binade j: Q[j][g] = sum rint(x * 2^(52 - e0 - j)), F[j][g] = tie or big term present
-__global__ void k_segments(const double* __restrict__ x, int64_t b, int64_t n, int64_t nseg, int e0, int nb,
-                           long long* __restrict__ Q, int32_t* __restrict__ F) {
-  __shared__ long long sq[kMaxBinades];
-  __shared__ int32_t sf[kMaxBinades];
-  for (int64_t g = blockIdx.x; g < nseg; g += gridDim.x) {
-    if (threadIdx.x < nb) {
-      sq[threadIdx.x] = 0;
-      sf[threadIdx.x] = 0;
+constexpr int kSegThreads = 256;
+constexpr int kPerThread = kSeg / kSegThreads;
+__global__ void __launch_bounds__(kSegThreads) k_segments(const double* __restrict__ x, int64_t b, int64_t n,
+                                                          int64_t nseg, const int32_t* __restrict__ prm,
+                                                          long long* __restrict__ Q, int32_t* __restrict__ F) {
+  const int e0 = prm[0], nb = prm[1];
+  __shared__ long long sq[kSegThreads / 32][kMaxBinades];
+  __shared__ int32_t sf[kSegThreads / 32][kMaxBinades];
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  for (int64_t g = blockIdx.x; g < nseg && nb > 0; g += gridDim.x) {
+    double xv[kPerThread];
+    bool in[kPerThread];
+#pragma unroll
+    for (int i = 0; i < kPerThread; ++i) {
+      const int64_t k = b + g * kSeg + i * kSegThreads + threadIdx.x;
+      in[i] = k < n;
+      xv[i] = in[i] ? x[k] : 0.0;
     }
-    __syncthreads();
-    const int64_t k = b + g * kSeg + threadIdx.x;
-    const bool in = k < n;
-    const double xv = in ? x[k] : 0.0;
+    double scale = ldexp(1.0, 52 - e0), lim = ldexp(1.0, e0);  // exact powers of two
     for (int j = 0; j < nb; ++j) {
-      const int e = e0 + j;
-      const double y = ldexp(xv, 52 - e);  // exact scaling
-      const double r = rint(y);
-      const bool flag = in && (xv >= ldexp(1.0, e) || y - floor(y) == 0.5);
-      long long q = flag ? 0 : (long long)r;
+      long long q = 0;
+      bool flag = false;
+#pragma unroll
+      for (int i = 0; i < kPerThread; ++i) {
+        const double y = xv[i] * scale;  // exact scaling
+        const bool f = in[i] && (xv[i] >= lim || y - floor(y) == 0.5);
+        flag |= f;
+        q += f ? 0 : (long long)rint(y);
+      }
       for (int o = 16; o > 0; o >>= 1) q += __shfl_down_sync(0xffffffffu, q, o);
       const unsigned any = __ballot_sync(0xffffffffu, flag);
-      if ((threadIdx.x & 31) == 0) {
-        if (q) atomicAdd(reinterpret_cast<unsigned long long*>(&sq[j]), (unsigned long long)q);
-        if (any) sf[j] = 1;
+      if (lane == 0) {
+        sq[w][j] = q;
+        sf[w][j] = any ? 1 : 0;
       }
+      scale *= 0.5;
+      lim *= 2.0;
     }
     __syncthreads();
     if (threadIdx.x < nb) {
-      Q[(int64_t)threadIdx.x * nseg + g] = sq[threadIdx.x];
-      F[(int64_t)threadIdx.x * nseg + g] = sf[threadIdx.x];
+      long long tq = 0;
+      int32_t tf = 0;
+      for (int v = 0; v < kSegThreads / 32; ++v) {
+        tq += sq[v][threadIdx.x];
+        tf |= sf[v][threadIdx.x];
+      }
+      Q[(int64_t)threadIdx.x * nseg + g] = tq;
+      F[(int64_t)threadIdx.x * nseg + g] = tf;
     }
     __syncthreads();
   }
 }
 
-// inclusive -> stored as exclusive prefix with a leading 0: P[j][0..nseg]
+// per binade: exclusive prefix with a leading 0, P[j][0..nseg]. The sums
+// saturate at 2^62: only comparisons against < 2^53 matter, and the prefix of
+// the binade the walk is in stays below 2^53 up to its position (those terms
+// summed to less than 2^(e+1)), while lower binades' prefixes may grow past
+// the int64 range.
+constexpr unsigned long long kCap = 1ull << 62;
+__device__ __forceinline__ unsigned long long sat_add(unsigned long long a, unsigned long long b) {
+  const unsigned long long c = a + b;  // both <= 2^62: no wrap
+  return c < kCap ? c : kCap;
+}
 __global__ void k_prefix(const long long* __restrict__ Q, const int32_t* __restrict__ F, int64_t nseg,
-                         long long* __restrict__ PQ, int32_t* __restrict__ PF) {
+                         const int32_t* __restrict__ prm, long long* __restrict__ PQ, int32_t* __restrict__ PF) {
   const int j = blockIdx.x;
-  __shared__ long long carry_q;
+  if (j >= prm[1]) return;
+  __shared__ unsigned long long carry_q;
   __shared__ int32_t carry_f;
-  __shared__ long long wq[32];
+  __shared__ unsigned long long wq[32];
   __shared__ int32_t wf[32];
   if (threadIdx.x == 0) {
     carry_q = 0;
@@ -99,13 +161,13 @@ __global__ void k_prefix(const long long* __restrict__ Q, const int32_t* __restr
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
   for (int64_t base = 0; base < nseg; base += blockDim.x) {
     const int64_t g = base + threadIdx.x;
-    long long q = g < nseg ? Q[(int64_t)j * nseg + g] : 0;
+    unsigned long long q = g < nseg ? (unsigned long long)Q[(int64_t)j * nseg + g] : 0;
     int32_t f = g < nseg ? F[(int64_t)j * nseg + g] : 0;
     for (int o = 1; o < 32; o <<= 1) {  // warp inclusive scan
-      const long long tq = __shfl_up_sync(0xffffffffu, q, o);
+      const unsigned long long tq = __shfl_up_sync(0xffffffffu, q, o);
       const int32_t tf = __shfl_up_sync(0xffffffffu, f, o);
       if (lane >= o) {
-        q += tq;
+        q = sat_add(q, tq);
         f += tf;
       }
     }
@@ -115,13 +177,13 @@ __global__ void k_prefix(const long long* __restrict__ Q, const int32_t* __restr
     }
     __syncthreads();
     if (w == 0) {
-      long long a = lane < (int)(blockDim.x >> 5) ? wq[lane] : 0;
+      unsigned long long a = lane < (int)(blockDim.x >> 5) ? wq[lane] : 0;
       int32_t c = lane < (int)(blockDim.x >> 5) ? wf[lane] : 0;
       for (int o = 1; o < 32; o <<= 1) {
-        const long long ta = __shfl_up_sync(0xffffffffu, a, o);
+        const unsigned long long ta = __shfl_up_sync(0xffffffffu, a, o);
         const int32_t tc = __shfl_up_sync(0xffffffffu, c, o);
         if (lane >= o) {
-          a += ta;
+          a = sat_add(a, ta);
           c += tc;
         }
       }
@@ -129,56 +191,107 @@ __global__ void k_prefix(const long long* __restrict__ Q, const int32_t* __restr
       wf[lane] = c;
     }
     __syncthreads();
-    const long long off_q = carry_q + (w ? wq[w - 1] : 0);
+    const unsigned long long off_q = sat_add(carry_q, w ? wq[w - 1] : 0);
     const int32_t off_f = carry_f + (w ? wf[w - 1] : 0);
     if (g < nseg) {
-      PQ[(int64_t)j * (nseg + 1) + g + 1] = off_q + q;
+      PQ[(int64_t)j * (nseg + 1) + g + 1] = (long long)sat_add(off_q, q);
       PF[(int64_t)j * (nseg + 1) + g + 1] = off_f + f;
     }
     __syncthreads();
     if (threadIdx.x == blockDim.x - 1) {
-      carry_q = off_q + q;
+      carry_q = sat_add(off_q, q);
       carry_f = off_f + f;
     }
     __syncthreads();
   }
 }
 
-// the walk of step 4; out[0] holds s on entry (the sequential prefix) and on exit
-__global__ void k_walk(const double* __restrict__ x, int64_t b, int64_t n, int64_t nseg, int e0, int nb,
-                       const long long* __restrict__ PQ, const int32_t* __restrict__ PF, double* __restrict__ out,
-                       int32_t* __restrict__ fail) {
-  if (threadIdx.x != 0 || blockIdx.x != 0) return;
-  double s = out[0];
+// Step 4, one block: thread 0 keeps the running sum and searches; the block
+// stages each segment that has to be added term by term. acc[0]: the
+// sequential prefix on entry, the sum on exit.
+__global__ void k_walk(const double* __restrict__ x, int64_t b, int64_t n, int64_t nseg,
+                       const int32_t* __restrict__ prm, const long long* __restrict__ PQ,
+                       const int32_t* __restrict__ PF, double* __restrict__ acc) {
+  __shared__ double sh[kWalkThreads];
+  __shared__ int64_t seg;   // next segment to add term by term, -1: done, -2: rest term by term
+  __shared__ int64_t from;  // segment the walk continues at
+  __shared__ int64_t first; // search: first stopping candidate
+  __shared__ int walk_j;
+  __shared__ long long walk_A;
+  __shared__ double walk_u;
+  const int e0 = prm[0], nb = prm[1];
+  double s = acc[0];
   int64_t g = 0;
   const long long top = 1ll << 53;
-  while (g < nseg) {
-    const int e = ilogb(s);
-    const int j = e - e0;
-    if (s <= 0.0 || j < 0 || j >= nb) {  // outside the precomputed binades: finish term by term
-      for (int64_t k = b + g * kSeg; k < n; ++k) s += x[k];
-      *fail = 1;
+  while (true) {
+    if (threadIdx.x == 0) {
+      if (g >= nseg) {
+        seg = -1;
+      } else {
+        const int e = ilogb(s);
+        const int j = e - e0;
+        if (nb == 0 || !(s > 0.0) || j < 0 || j >= nb) {
+          seg = -2;  // outside the precomputed binades
+          from = g;
+        } else {
+          const double u = ldexp(1.0, e - 52);
+          const long long A = (long long)(s / u);
+          walk_j = j;
+          walk_A = A;
+          walk_u = u;
+          seg = -3;  // search below
+        }
+      }
+    }
+    __syncthreads();
+    if (seg == -3) {
+      // first segment >= g that is flagged or would leave the binade: the block
+      // tests 1024 evenly spaced candidates, then the 1024 segments of the hit
+      const long long* pq = PQ + (int64_t)walk_j * (nseg + 1);
+      const int32_t* pf = PF + (int64_t)walk_j * (nseg + 1);
+      const long long A = walk_A, q0 = pq[g];
+      const int32_t f0 = pf[g];
+      auto stop = [&](int64_t m) { return pf[m + 1] > f0 || A + (pq[m + 1] - q0) >= top; };
+      int64_t lo = g, hi = nseg;  // the answer lies in [lo, hi]; hi = nseg: none
+      while (hi - lo > 1) {
+        const int64_t step = (hi - lo + kWalkThreads - 1) / kWalkThreads;
+        const int64_t m = lo + threadIdx.x * step;
+        if (threadIdx.x == 0) first = hi;
+        __syncthreads();
+        if (m < hi && stop(m)) atomicMin(reinterpret_cast<unsigned long long*>(&first), (unsigned long long)m);
+        __syncthreads();
+        const int64_t f = first;
+        __syncthreads();
+        // the first stop lies in (f - step, f]; when f = hi none of the candidates stopped
+        const int64_t nlo = f - step + 1 > lo ? f - step + 1 : lo;
+        if (f == hi) {
+          lo = hi - step + 1 > lo ? hi - step + 1 : lo;
+        } else {
+          hi = f;
+          lo = nlo;
+        }
+        if (step == 1) break;
+      }
+      if (threadIdx.x == 0) {
+        int64_t r = lo;
+        while (r < hi && !stop(r)) ++r;  // at most one candidate left
+        s = (double)(A + (pq[r] - q0)) * walk_u;  // exact: a multiple of u below 2^(e+1)
+        seg = r < nseg ? r : -1;
+      }
+      __syncthreads();
+    }
+    const int64_t sg = seg;
+    if (sg == -1) break;
+    if (sg == -2) {
+      s = block_ordered_add(s, x, b + from * kSeg, n, sh);
       break;
     }
-    const double u = ldexp(1.0, e - 52);
-    const long long A = (long long)(s / u);
-    const long long* pq = PQ + (int64_t)j * (nseg + 1);
-    const int32_t* pf = PF + (int64_t)j * (nseg + 1);
-    // first segment g' >= g that is flagged or would leave the binade
-    int64_t lo = g, hi = nseg;
-    while (lo < hi) {
-      const int64_t mid = (lo + hi) >> 1;
-      const bool stop = pf[mid + 1] > pf[g] || A + (pq[mid + 1] - pq[g]) >= top;
-      if (stop) hi = mid;
-      else lo = mid + 1;
-    }
-    s = (double)(A + (pq[lo] - pq[g])) * u;  // exact: a multiple of u below 2^(e+1)
-    if (lo == nseg) break;
-    const int64_t kb = b + lo * kSeg, ke = kb + kSeg < n ? kb + kSeg : n;
-    for (int64_t k = kb; k < ke; ++k) s += x[k];  // the reference's own additions
-    g = lo + 1;
+    const int64_t kb = b + sg * kSeg;
+    s = block_ordered_add(s, x, kb, kb + kSeg < n ? kb + kSeg : n, sh);  // the reference's own additions
+    g = sg + 1;
+    __syncthreads();
   }
-  out[0] = s;
+  if (threadIdx.x == 0) acc[0] = s;
 }
 
 __global__ void k_any_negative(const double* __restrict__ x, int64_t n, int32_t* __restrict__ flag) {
@@ -190,49 +303,33 @@ __global__ void k_any_negative(const double* __restrict__ x, int64_t n, int32_t*
 
 namespace gh {
 
+// Device-resident: one host synchronisation (the result) per sum.
 double sequential_sum_nonneg(const double* d_x, int64_t n, cudaStream_t s, int* launches) {
-  Scratch<double> acc(2, s);
-  GH_CUDA(cudaMemsetAsync(acc.p, 0, 2 * sizeof(double), s));
+  if (n == 0) return 0.0;
+  Scratch<double> acc(1, s);
+  GH_CUDA(cudaMemsetAsync(acc.p, 0, sizeof(double), s));
   const int64_t K = n < kSeqPrefix ? n : kSeqPrefix;
-  k_seq<<<1, 32, 0, s>>>(d_x, 0, K, acc.p);
-  GH_LAUNCH_CHECK();
+  k_seq_block<<<1, kWalkThreads, 0, s>>>(d_x, 0, K, acc.p);
   int nl = 1;
-  double h[2] = {0.0, 0.0};
   if (n > K) {
+    const int64_t nseg = (n - K + kSeg - 1) / kSeg;
     Scratch<double> part(kReduceGrid, s);
+    Scratch<int32_t> prm(2, s);
+    Scratch<long long> Q((size_t)kMaxBinades * nseg, s), PQ((size_t)kMaxBinades * (nseg + 1), s);
+    Scratch<int32_t> F((size_t)kMaxBinades * nseg, s), PF((size_t)kMaxBinades * (nseg + 1), s);
     k_tree_partial<<<kReduceGrid, kBlock, 0, s>>>(d_x, K, n, part.p);
-    Scratch<double> tot(1, s);
-    std::vector<double> hp(kReduceGrid);
-    GH_CUDA(cudaMemcpyAsync(hp.data(), part.p, sizeof(double) * kReduceGrid, cudaMemcpyDeviceToHost, s));
-    GH_CUDA(cudaMemcpyAsync(h, acc.p, sizeof(double), cudaMemcpyDeviceToHost, s));
-    GH_CUDA(cudaStreamSynchronize(s));
-    nl += 1;
-    double rest = 0.0;  // an upper bound only (bounds the binades the walk can visit)
-    for (double v : hp) rest += v;
-    const double s0 = h[0];
-    const int e0 = s0 > 0.0 ? std::ilogb(s0) : 0;
-    const int e1 = std::ilogb((s0 + rest) * (1.0 + 1.0 / (1 << 20)) + 1e-300);
-    const int nb = e1 - e0 + 1;
-    Scratch<int32_t> fail(1, s);
-    GH_CUDA(cudaMemsetAsync(fail.p, 0, sizeof(int32_t), s));
-    if (!(s0 > 0.0) || nb < 1 || nb > kMaxBinades) {
-      k_seq<<<1, 32, 0, s>>>(d_x, K, n, acc.p);  // pathological ranges: plain sequential
-      nl += 1;
-    } else {
-      const int64_t nseg = (n - K + kSeg - 1) / kSeg;
-      Scratch<long long> Q((size_t)nb * nseg, s), PQ((size_t)nb * (nseg + 1), s);
-      Scratch<int32_t> F((size_t)nb * nseg, s), PF((size_t)nb * (nseg + 1), s);
-      k_segments<<<(unsigned)std::min<int64_t>(nseg, 148 * 16), kSeg, 0, s>>>(d_x, K, n, nseg, e0, nb, Q.p, F.p);
-      k_prefix<<<nb, 1024, 0, s>>>(Q.p, F.p, nseg, PQ.p, PF.p);
-      k_walk<<<1, 32, 0, s>>>(d_x, K, n, nseg, e0, nb, PQ.p, PF.p, acc.p, fail.p);
-      GH_LAUNCH_CHECK();
-      nl += 3;
-    }
+    k_binades<<<1, 1024, 0, s>>>(part.p, kReduceGrid, acc.p, prm.p);
+    k_segments<<<(unsigned)std::min<int64_t>(nseg, 148 * 32), kSegThreads, 0, s>>>(d_x, K, n, nseg, prm.p, Q.p, F.p);
+    k_prefix<<<kMaxBinades, 1024, 0, s>>>(Q.p, F.p, nseg, prm.p, PQ.p, PF.p);
+    k_walk<<<1, kWalkThreads, 0, s>>>(d_x, K, n, nseg, prm.p, PQ.p, PF.p, acc.p);
+    nl += 5;
   }
-  GH_CUDA(cudaMemcpyAsync(h, acc.p, sizeof(double), cudaMemcpyDeviceToHost, s));
+  GH_LAUNCH_CHECK();
+  double h = 0.0;
+  GH_CUDA(cudaMemcpyAsync(&h, acc.p, sizeof(double), cudaMemcpyDeviceToHost, s));
   GH_CUDA(cudaStreamSynchronize(s));
   if (launches) *launches += nl;
-  return h[0];
+  return h;
 }
 
 double deterministic_sum_dev(const double* d_x, int64_t n, cudaStream_t s) {
@@ -247,7 +344,7 @@ double deterministic_sum_dev(const double* d_x, int64_t n, cudaStream_t s) {
   if (!h) return sequential_sum_nonneg(d_x, n, s, nullptr);
   Scratch<double> acc(1, s);
   GH_CUDA(cudaMemsetAsync(acc.p, 0, sizeof(double), s));
-  k_seq<<<1, 32, 0, s>>>(d_x, 0, n, acc.p);
+  k_seq_block<<<1, kWalkThreads, 0, s>>>(d_x, 0, n, acc.p);
   GH_LAUNCH_CHECK();
   double out = 0.0;
   GH_CUDA(cudaMemcpyAsync(&out, acc.p, sizeof(out), cudaMemcpyDeviceToHost, s));

@@ -37,6 +37,20 @@ def test_ties_and_binade_jumps(gpu):
     assert g.deterministic_sum(z) == seq(z)
 
 
+def test_prefix_saturation_and_mixed_scales(gpu):
+    """Terms just below the first binade's top make that binade's integer
+    prefix pass 2^63 (saturated, must stay monotone); mixed scales force
+    many binade changes."""
+    g = gpu.geoheat
+    x = np.concatenate([np.ones(4096), np.full(300_000, 4095.9)])
+    assert g.deterministic_sum(x) == seq(x)
+    rng = np.random.RandomState(11)
+    y = rng.uniform(0, 1, 500_000) * 10.0 ** rng.randint(-8, 8, 500_000)
+    assert g.deterministic_sum(y) == seq(y)
+    z = np.concatenate([np.full(4096, 1e-12), rng.uniform(0, 1, 1_000_000)])
+    assert g.deterministic_sum(z) == seq(z)
+
+
 def test_negative_terms_take_the_ordered_path(gpu):
     g = gpu.geoheat
     rng = np.random.RandomState(3)
