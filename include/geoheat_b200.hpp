@@ -511,6 +511,13 @@ inline TriMesh midpoint_subdivide(const TriMesh& mesh, int levels) {
   return TriMesh(h);
 }
 
+/// deterministic_sum (parallel.hpp:50-54): left-to-right, bit-identical, on the device.
+inline double deterministic_sum(const std::vector<double>& terms) {
+  double out = 0.0;
+  detail::check(gh_deterministic_sum(terms.data(), static_cast<std::int64_t>(terms.size()), &out));
+  return out;
+}
+
 /// triangulation_quality (mesh.hpp:297-310).
 inline double triangulation_quality(const TriMesh& mesh) {
   double tau = 0.0;
