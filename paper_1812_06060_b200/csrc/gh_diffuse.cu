@@ -485,21 +485,18 @@ T read_scalar(const T* d, cudaStream_t s) {
   return v;
 }
 
-// r_j = A_j u_j - t * sum theta (u_k - u_j) - u0_j (diffusion.hpp:41-47)
+// r_j = A_j u_j - t * sum theta (u_k - u_j) - u0_j (diffusion.hpp:41-47); sq_j = r_j^2
 __global__ void k_residual(const int32_t* __restrict__ vv_off, const int32_t* __restrict__ vv_idx,
                            const double* __restrict__ vv_w, const double* __restrict__ va,
                            const int32_t* __restrict__ level, const double* __restrict__ u, double t, int64_t nv,
-                           double* __restrict__ part) {
-  double s = 0.0;
+                           double* __restrict__ sq) {
   for (int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; j < nv; j += (int64_t)gridDim.x * blockDim.x) {
     double lap = 0.0;
     const double uj = u[j];
     for (int32_t i = vv_off[j]; i < vv_off[j + 1]; ++i) lap += vv_w[i] * (u[vv_idx[i]] - uj);
     const double r = va[j] * uj - t * lap - (level[j] == 0 ? 1.0 : 0.0);
-    s += r * r;
+    sq[j] = r * r;
   }
-  s = ghd::block_sum<B>(s);
-  if (threadIdx.x == 0) part[blockIdx.x] = s;
 }
 
 }  // namespace
@@ -660,12 +657,13 @@ double diffuse_bands_dev(gh_levels* L, std::vector<Band*>& bands, double t, int3
 double diffusion_residual_dev(gh_levels* L, const double* d_u, double t) {
   gh_mesh* m = L->mesh;
   // u0 from the level-0 flags: sources are exactly D_0 (diffusion.hpp:38-39)
-  k_residual<<<kReduceGrid, B, 0, m->stream>>>(m->vv_offset.p, m->vv_index.p, m->vv_weight.p, m->vertex_area.p,
-                                               L->level.p, d_u, t, m->nv, m->partials.p);
+  Scratch<double> sq(m->nv, m->stream);
+  k_residual<<<grid_for(m->nv), B, 0, m->stream>>>(m->vv_offset.p, m->vv_index.p, m->vv_weight.p,
+                                                   m->vertex_area.p, L->level.p, d_u, t, m->nv, sq.p);
   GH_LAUNCH_CHECK();
   m->launches++;
-  reduce_partials(m, m->scalars.p + 3);
-  return std::sqrt(read_scalar(m->scalars.p + 3, m->stream));
+  // sqrt(deterministic_sum(sq)) (diffusion.hpp:48): the left-to-right sum, bit for bit
+  return std::sqrt(sequential_sum_nonneg(sq.p, m->nv, m->stream, &m->launches));
 }
 
 }  // namespace gh

@@ -59,7 +59,7 @@ def test_golden_case_bitwise(gpu, case):
     assert_same(lv.offsets, g["offsets"], "ring offsets")
     assert lv.unreachable_count == int(g["unreachable"])
     t, sweeps, iters = float(g["t"]), int(g["sweeps"]), int(g["admm_iters"])
-    assert gh.average_edge_length(mesh) == pytest.approx(float(g["avg_edge_length"]), rel=1e-13)
+    assert gh.average_edge_length(mesh) == float(g["avg_edge_length"])  # left-to-right sum, bit for bit
     u = gh.gs_diffuse(mesh, lv, t, gh.DiffusionConfig(sweeps=sweeps))
     assert_same(u, g["u"], "u")
     nh = gh.normalized_target_gradients(mesh, u)
@@ -84,7 +84,7 @@ def test_golden_case_bitwise(gpu, case):
         u2 = gh.gs_diffuse(mesh, lv, t, gh.DiffusionConfig(sweeps=3), initial=u)
         assert_same(u2, g["u_warm3"], "warm start")
     e1 = gh.diffusion_residual(mesh, u, t, g["sources"], levels=lv)
-    assert e1 == pytest.approx(float(g["e1"]), rel=1e-12, abs=1e-300)
+    assert e1 == float(g["e1"])  # left-to-right sum, bit for bit
     # the fused device-resident chain equals the stage-by-stage results
     for method, key in (("face", "d_face"), ("edge", "d_edge")):
         d, rep = gh.distance(lv, method, sweeps, t, admm=cfg)
@@ -219,8 +219,8 @@ TOL_CASES = sorted(os.path.basename(p)[:-4] for p in glob.glob(os.path.join(GOLD
 @pytest.mark.parametrize("case", TOL_CASES)
 def test_residual_tolerance_early_stop(gpu, case):
     """gs_diffuse with residual_tolerance (diffusion.hpp:110-117): same stop sweep, bitwise u,
-    E1 history within 1e-12 (device tree sum vs the reference's left-to-right sum), and the
-    stop decision is not within 1e-9 of the threshold on either side."""
+    and the E1 history bit-identical (the reference's left-to-right sum of r^2 is
+    reproduced exactly on the device)."""
     gh = gpu
     g = np.load(os.path.join(GOLDEN, "tol", case + ".npz"))
     mesh = gh.build_mesh(g["positions"], g["faces"])
@@ -230,10 +230,7 @@ def test_residual_tolerance_early_stop(gpu, case):
     u = gh.gs_diffuse(mesh, lv, float(g["t"]), cfg, rep)
     assert rep.iterations == int(g["iterations"]) and rep.converged == bool(g["converged"])
     assert_same(u, g["u"], "u")
-    check_history(rep.residual_history, g["residual_history"], "E1")
-    tol = float(g["tolerance"])
-    for e1 in rep.residual_history:
-        assert abs(e1 / tol - 1.0) > 1e-9
+    assert_same(np.asarray(rep.residual_history), g["residual_history"], "E1 history")
 
 
 @pytest.mark.parametrize("nbands", [2, 3, 4, 8])

@@ -51,6 +51,19 @@ def test_prefix_saturation_and_mixed_scales(gpu):
     assert g.deterministic_sum(z) == seq(z)
 
 
+def test_many_windows(gpu):
+    """Terms spanning hundreds of binades (the running sum climbs through
+    several 48-binade windows), tiny leading terms, denormal sums."""
+    g = gpu.geoheat
+    rng = np.random.RandomState(5)
+    x = 10.0 ** rng.uniform(-300, 0, 400_000)
+    assert g.deterministic_sum(x) == seq(x)
+    y = np.concatenate([np.full(100_000, 1e-310), 10.0 ** np.linspace(-300, 300, 200_000)])
+    assert g.deterministic_sum(y) == seq(y)
+    z = np.sort(10.0 ** rng.uniform(-250, 250, 300_000))  # ascending: a new window every few segments
+    assert g.deterministic_sum(z) == seq(z)
+
+
 def test_negative_terms_take_the_ordered_path(gpu):
     g = gpu.geoheat
     rng = np.random.RandomState(3)
