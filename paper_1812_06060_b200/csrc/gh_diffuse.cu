@@ -22,7 +22,8 @@
 //    with cp.async.bulk + mbarrier complete_tx into a ring of tiles, running
 //    ahead across steps (the CSR is read-only);
 //  * 8 consumer warps each take 2 chunks of a tile, gather the neighbour u
-//    values from L2 (ld.global.cg) with all 12-16 gathers in flight, store u;
+//    values (ld.global.ca: L1, then L2) with all 12-16 gathers in flight,
+//    store u;
 //  * no grid barrier: a chunk of level L at step tau waits (acquire) on
 //    per-level row counters of L-1, L, L+1; blocks publish their rows per
 //    level after each step (release). Each task depends only on earlier
@@ -355,6 +356,12 @@ __global__ void __launch_bounds__(kTmaThreads, 2) k_diffuse_tma(const __grid_con
         live[i] = cb + j * kTileChunks + q < ce;
         Lq[i] = live[i] ? hdr[32 + q] : -1;
       }
+      // The u gathers below are L1-cached loads (ld.global.ca). That is safe
+      // because every warp passes this check at the start of every step (tau
+      // changes) and the acquire loads here are followed by CCTL.IVALL, which
+      // drops the SM's whole L1: every value the step reads was published
+      // before that acquire, so an L1 line is either refilled from L2 after it
+      // or was filled after it — never older than the data the step needs.
       if (Lq[0] != seen_L || Lq[kChunksPerWarp - 1] != seen_L2 || tau != seen_tau) {
         // operands: wait for levels L-1, L, L+1 of each chunk (lanes 3i..3i+2)
         const int i = lane / 3;
@@ -412,7 +419,7 @@ __global__ void __launch_bounds__(kTmaThreads, 2) k_diffuse_tma(const __grid_con
         for (int k = 0; k < kUnroll; ++k)
           if (fast[i] && k < d[i]) {
             const int32_t cc = scol[32 * k];
-            v[i][k] = __ldcg((cc < 0 ? cur[i] : prev[i]) + (cc & 0x7fffffff));
+            v[i][k] = __ldca((cc < 0 ? cur[i] : prev[i]) + (cc & 0x7fffffff));  // L1-cached, see below
           }
       }
 #pragma unroll
@@ -430,7 +437,7 @@ __global__ void __launch_bounds__(kTmaThreads, 2) k_diffuse_tma(const __grid_con
           for (int32_t k = 0; k < d[i]; ++k) {
             const int32_t cc = __ldg(vba->col + q0 + 32 * (int64_t)k);
             const double w = __ldg(vba->wt + q0 + 32 * (int64_t)k);
-            num[i] += w * __ldcg((cc < 0 ? cur[i] : prev[i]) + (cc & 0x7fffffff));
+            num[i] += w * __ldca((cc < 0 ? cur[i] : prev[i]) + (cc & 0x7fffffff));
           }
         }
         if (on[i]) {
