@@ -95,10 +95,12 @@ T read_scalar(const T* d, cudaStream_t s) {
 namespace gh {
 
 Band::~Band() {
-  if (ubuf || rows_done) cudaSetDevice(device);
-  if (ubuf) cudaFree(ubuf);
-  if (rows_done) cudaFree(rows_done);
-  if (stalled) cudaFree(stalled);
+  if (ubuf || rows_done || stalled) cudaSetDevice(device);
+  for (void* p : {(void*)ubuf, (void*)rows_done, (void*)stalled}) {
+    if (!p) continue;
+    if (ipc) cudaFree(p);
+    else cudaFreeAsync(p, astream);
+  }
 }
 
 uint64_t Band::device_bytes() const {
@@ -222,9 +224,14 @@ void band_build(gh_levels* L, Band* b, int32_t lb, int32_t le) {
   b->den.alloc(b->nrows, s);
   b->den_t = 0.0;
   if (!b->ubuf) {
-    GH_CUDA(cudaMalloc(&b->ubuf, sizeof(double) * 2 * (size_t)b->nrows));
-    GH_CUDA(cudaMalloc(&b->rows_done, sizeof(unsigned long long) * nlev));
-    GH_CUDA(cudaMalloc(&b->stalled, sizeof(int32_t)));
+    b->astream = s;
+    const size_t sizes[3] = {sizeof(double) * 2 * (size_t)b->nrows, sizeof(unsigned long long) * nlev, sizeof(int32_t)};
+    void** ptrs[3] = {reinterpret_cast<void**>(&b->ubuf), reinterpret_cast<void**>(&b->rows_done),
+                      reinterpret_cast<void**>(&b->stalled)};
+    for (int i = 0; i < 3; ++i) {
+      if (b->ipc) GH_CUDA(cudaMalloc(ptrs[i], sizes[i]));  // IPC handles need driver allocations
+      else GH_CUDA(cudaMallocAsync(ptrs[i], sizes[i], s));
+    }
   }
   m->launches += 4;
   GH_CUDA(cudaStreamSynchronize(s));

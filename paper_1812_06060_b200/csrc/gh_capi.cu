@@ -979,6 +979,7 @@ gh_status gh_band_create(gh_levels* levels, int32_t rank, int32_t nranks, gh_ban
     b->levels = levels;
     b->rank = rank;
     b->nranks = nranks;
+    b->band.ipc = true;  // its buffers are exported to the neighbour processes
     gh::band_build(levels, &b->band, cut[rank], cut[rank + 1]);
     *out = b.release();
   });

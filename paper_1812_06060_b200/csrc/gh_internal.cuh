@@ -155,7 +155,10 @@ struct Band {
   DevBuf<double> wt;            // cotan weights in the reference's row order
   DevBuf<double> area_r, wsum_r, den;
   double den_t = 0.0;
-  // state shared with neighbour bands: plain cudaMalloc so it can be IPC-exported
+  // state shared with neighbour bands: plain cudaMalloc when it is IPC-exported
+  // (ipc), else from the stream-ordered pool like every other buffer
+  bool ipc = false;
+  cudaStream_t astream = nullptr;
   double* ubuf = nullptr;                   // [2][nrows] sweep-parity buffers
   unsigned long long* rows_done = nullptr;  // [nlev] rows finished per level over all sweeps
   int32_t* stalled = nullptr;               // dependency-timeout flag of the last launch
