@@ -209,6 +209,15 @@ __global__ void k_count_i32(const int32_t* __restrict__ idx, int64_t n, int32_t*
     atomicAdd(&cnt[idx[i]], 1);
 }
 
+// vertex -> corner keys: vertex * H + h (bucket = vertex, order = corner)
+__global__ void k_corner_keys(const int32_t* __restrict__ faces, int64_t n, uint64_t* __restrict__ key,
+                              int32_t* __restrict__ val) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+    key[i] = (uint64_t)faces[i] * (uint64_t)n + (uint64_t)i;
+    val[i] = (int32_t)i;
+  }
+}
+
 __global__ void k_iota_u32(uint32_t* __restrict__ keys, const int32_t* __restrict__ src, int32_t* __restrict__ val,
                            int64_t n) {
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
@@ -325,19 +334,90 @@ void radix_sort_pairs(K*& keys, K*& keys_alt, int32_t*& vals, int32_t*& vals_alt
   if (vb.Current() != vals) std::swap(vals, vals_alt);
 }
 
-void exclusive_scan(const int32_t* in, int32_t* out, int64_t n, cudaStream_t s) {
-  size_t tmp = 0;
-  GH_CUDA(cub::DeviceScan::ExclusiveSum(nullptr, tmp, in, out, (int)n, s));
-  gh::Scratch<char> t(tmp, s);
-  GH_CUDA(cub::DeviceScan::ExclusiveSum(t.p, tmp, in, out, (int)n, s));
-}
-
 template <class T>
 T read_scalar(const T* d, cudaStream_t s) {
   T v;
   GH_CUDA(cudaMemcpyAsync(&v, d, sizeof(T), cudaMemcpyDeviceToHost, s));
   GH_CUDA(cudaStreamSynchronize(s));
   return v;
+}
+
+// ---- bucketed sort for mesh keys key = bucket * div + rest with small buckets
+// (a vertex's incident halfedges / neighbours): count, scan, scatter, then each
+// bucket is insertion-sorted by (key, value) by one thread. The result equals
+// the stable radix sort's (equal keys keep ascending value = input order).
+constexpr int kMaxBucket = 64;
+
+__global__ void k_bucket_count(const uint64_t* __restrict__ key, int64_t n, uint64_t div, int32_t* __restrict__ cnt,
+                               int32_t* __restrict__ maxb) {
+  int32_t mx = 0;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+    const int32_t c = atomicAdd(&cnt[key[i] / div], 1) + 1;
+    mx = c > mx ? c : mx;
+  }
+  for (int o = 16; o > 0; o >>= 1) mx = max(mx, __shfl_down_sync(0xffffffffu, mx, o));
+  if ((threadIdx.x & 31) == 0 && mx) atomicMax(maxb, mx);
+}
+
+__global__ void k_bucket_scatter(const uint64_t* __restrict__ key, const int32_t* __restrict__ val, int64_t n,
+                                 uint64_t div, const int32_t* __restrict__ off, int32_t* __restrict__ cur,
+                                 uint64_t* __restrict__ key_out, int32_t* __restrict__ val_out) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+    const uint64_t k = key[i];
+    const uint64_t b = k / div;
+    const int32_t pos = off[b] + atomicAdd(&cur[b], 1);
+    key_out[pos] = k;
+    val_out[pos] = val[i];
+  }
+}
+
+__global__ void k_bucket_sort(const int32_t* __restrict__ off, int64_t nb, uint64_t* __restrict__ key,
+                              int32_t* __restrict__ val) {
+  for (int64_t b = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; b < nb; b += (int64_t)gridDim.x * blockDim.x) {
+    const int32_t s = off[b], e = off[b + 1];
+    for (int32_t i = s + 1; i < e; ++i) {  // insertion sort by (key, value)
+      const uint64_t k = key[i];
+      const int32_t v = val[i];
+      int32_t j = i - 1;
+      while (j >= s && (key[j] > k || (key[j] == k && val[j] > v))) {
+        key[j + 1] = key[j];
+        val[j + 1] = val[j];
+        --j;
+      }
+      key[j + 1] = k;
+      val[j + 1] = v;
+    }
+  }
+}
+
+void exclusive_scan(const int32_t* in, int32_t* out, int64_t n, cudaStream_t s);
+
+// Sorts (keys, vals) into (keys_out, vals_out) by (key, val); nb buckets of
+// key / div. Returns false (outputs untouched) when a bucket exceeds
+// kMaxBucket, for the caller's radix sort.
+bool bucket_sort_pairs(const uint64_t* keys, const int32_t* vals, int64_t n, uint64_t div, int64_t nb,
+                       uint64_t* keys_out, int32_t* vals_out, cudaStream_t s, int32_t* offsets_out = nullptr) {
+  gh::Scratch<int32_t> cnt(nb + 1, s), off(nb + 1, s), cur(nb + 1, s), maxb(1, s);
+  GH_CUDA(cudaMemsetAsync(cnt.p, 0, sizeof(int32_t) * (nb + 1), s));
+  GH_CUDA(cudaMemsetAsync(cur.p, 0, sizeof(int32_t) * (nb + 1), s));
+  GH_CUDA(cudaMemsetAsync(maxb.p, 0, sizeof(int32_t), s));
+  k_bucket_count<<<gh::grid_for(n), B, 0, s>>>(keys, n, div, cnt.p, maxb.p);
+  GH_LAUNCH_CHECK();
+  const int32_t mb = read_scalar(maxb.p, s);
+  if (mb > kMaxBucket) return false;
+  exclusive_scan(cnt.p, off.p, nb + 1, s);
+  k_bucket_scatter<<<gh::grid_for(n), B, 0, s>>>(keys, vals, n, div, off.p, cur.p, keys_out, vals_out);
+  k_bucket_sort<<<gh::grid_for(nb), B, 0, s>>>(off.p, nb, keys_out, vals_out);
+  GH_LAUNCH_CHECK();
+  if (offsets_out) GH_CUDA(cudaMemcpyAsync(offsets_out, off.p, sizeof(int32_t) * (nb + 1), cudaMemcpyDeviceToDevice, s));
+  return true;
+}
+
+void exclusive_scan(const int32_t* in, int32_t* out, int64_t n, cudaStream_t s) {
+  size_t tmp = 0;
+  GH_CUDA(cub::DeviceScan::ExclusiveSum(nullptr, tmp, in, out, (int)n, s));
+  gh::Scratch<char> t(tmp, s);
+  GH_CUDA(cub::DeviceScan::ExclusiveSum(t.p, tmp, in, out, (int)n, s));
 }
 
 // Host restatement of one face's checks, only to word the error message of the
@@ -451,7 +531,13 @@ void mesh_build(gh_mesh* m, const double* h_pos, const int32_t* h_faces) {
     if (H) {
       k_he_keys<<<grid_for(H), B, 0, s>>>(m->faces.p, H, nvu, ka, va);
       GH_LAUNCH_CHECK();
-      radix_sort_pairs(ka, kb, va, vb, H, end_bit, s);
+      if (bucket_sort_pairs(ka, va, H, nvu, V, kb, vb, s)) {
+        std::swap(ka, kb);
+        std::swap(va, vb);
+        m->launches += 4;
+      } else {
+        radix_sort_pairs(ka, kb, va, vb, H, end_bit, s);
+      }
     }
     Scratch<int32_t> flag(H + 1, s), eid(H + 1, s);
     if (H) {
@@ -533,10 +619,21 @@ void mesh_build(gh_mesh* m, const double* h_pos, const int32_t* h_faces) {
     uint32_t *ka = k0.p, *kb = k1.p;
     int32_t *va = m->vc_corner.p, *vb = v1.p;
     if (H) {
-      k_iota_u32<<<grid_for(H), B, 0, s>>>(ka, m->faces.p, va, H);
-      GH_LAUNCH_CHECK();
-      radix_sort_pairs(ka, kb, va, vb, H, bits_for(nvu), s);
-      if (va != m->vc_corner.p) GH_CUDA(cudaMemcpyAsync(m->vc_corner.p, va, sizeof(int32_t) * H, cudaMemcpyDeviceToDevice, s));
+      bool done = false;
+      {
+        Scratch<uint64_t> wk(H, s), wk2(H, s);
+        Scratch<int32_t> wv(H, s);
+        k_corner_keys<<<grid_for(H), B, 0, s>>>(m->faces.p, H, wk.p, wv.p);
+        GH_LAUNCH_CHECK();
+        done = bucket_sort_pairs(wk.p, wv.p, H, (uint64_t)H, V, wk2.p, m->vc_corner.p, s);
+      }
+      if (!done) {
+        k_iota_u32<<<grid_for(H), B, 0, s>>>(ka, m->faces.p, va, H);
+        GH_LAUNCH_CHECK();
+        radix_sort_pairs(ka, kb, va, vb, H, bits_for(nvu), s);
+        if (va != m->vc_corner.p)
+          GH_CUDA(cudaMemcpyAsync(m->vc_corner.p, va, sizeof(int32_t) * H, cudaMemcpyDeviceToDevice, s));
+      }
     }
     if (V) k_vertex_area<<<grid_for(V), B, 0, s>>>(m->vc_offset.p, m->vc_corner.p, m->face_area.p, V, m->vertex_area.p);
     GH_LAUNCH_CHECK();
@@ -559,7 +656,12 @@ void mesh_build(gh_mesh* m, const double* h_pos, const int32_t* h_faces) {
     if (E) {
       k_vv_keys<<<grid_for(E), B, 0, s>>>(m->edge_v.p, E, nvu, ka, va, degree.p);
       GH_LAUNCH_CHECK();
-      radix_sort_pairs(ka, kb, va, vb, 2 * E, end_bit, s);
+      if (bucket_sort_pairs(ka, va, 2 * E, nvu, V, kb, vb, s)) {
+        std::swap(ka, kb);
+        std::swap(va, vb);
+      } else {
+        radix_sort_pairs(ka, kb, va, vb, 2 * E, end_bit, s);
+      }
     }
     exclusive_scan(degree.p, m->vv_offset.p, V + 1, s);
     if (E) {
