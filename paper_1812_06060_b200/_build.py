@@ -111,10 +111,45 @@ def build_cli(force: bool = False) -> str:
     return CLI_BIN
 
 
+REF = "/root/reference/proj"
+
+
+def build_test_programs(force: bool = False) -> list:
+    """Test infrastructure, not product: the C++ programs the GPU tests run.
+
+    lib/wrapper_parity       the reference's run_pipelines chain on include/geoheat_b200.hpp
+    lib/dropin_run_pipeline  that chain on the reference's own functions and on
+                             geoheat::b200 with the reference's types (needs the
+                             reference headers, so only where /root/reference exists)
+    """
+    lib = build_cuda()
+    meshgen = build_meshgen()
+    inc = os.path.join(ROOT, "include")
+    built = []
+    jobs = [("wrapper_parity", ["g++", "-std=c++20", "-O2", "-Wall", "-I", inc], ["-lgh_meshgen"], True)]
+    if os.path.isdir(os.path.join(REF, "include", "geoheat")):
+        jobs.append(("dropin_run_pipeline",
+                     ["g++", "-std=gnu++20", "-O2", "-fopenmp", "-ffp-contract=off", "-I",
+                      os.path.join(ROOT, "oracle", "eigen_shim"), "-I", REF + "/include", "-I", REF + "/tests", "-I", inc],
+                     [], True))
+    for name, head, extra, _ in jobs:
+        src = os.path.join(ROOT, "tests", "cpp", name + ".cpp")
+        exe = os.path.join(LIBDIR, name)
+        if force or not _newer(exe, [src, lib, meshgen, os.path.join(inc, "geoheat_b200.hpp")]):
+            r = subprocess.run(head + [src, "-o", exe + ".tmp", "-L", LIBDIR, "-lgeoheat_b200", *extra,
+                                       "-Wl,-rpath,$ORIGIN"], capture_output=True, text=True)
+            if r.returncode != 0:
+                raise RuntimeError(f"{name} build failed:\n{r.stderr[-3000:]}")
+            os.replace(exe + ".tmp", exe)
+        built.append(exe)
+    return built
+
+
 def build_all(force: bool = False) -> None:
     build_meshgen(force)
     build_cuda(force)
     build_cli(force)
+    build_test_programs(force)
 
 
 if __name__ == "__main__":
