@@ -36,6 +36,14 @@ __global__ void k_band_renumber(const int32_t* __restrict__ order, const int32_t
   }
 }
 
+__global__ void k_deg_big(const int32_t* __restrict__ perm, const int32_t* __restrict__ vv_off, int64_t nrows,
+                          int32_t* __restrict__ deg) {
+  for (int64_t r = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; r < nrows; r += (int64_t)gridDim.x * blockDim.x) {
+    const int32_t v = perm[r];
+    deg[r] = v >= 0 ? vv_off[v + 1] - vv_off[v] : 0;
+  }
+}
+
 // per own chunk: its level, width = longest row, and the row lengths
 __global__ void k_chunk_meta(const int32_t* __restrict__ perm, const int32_t* __restrict__ level,
                              const int32_t* __restrict__ vv_off, int64_t nchunks, int32_t* __restrict__ chunk_level,
@@ -53,7 +61,7 @@ __global__ void k_chunk_meta(const int32_t* __restrict__ perm, const int32_t* __
     if (lane == 0) {
       width[c] = 32 * (int64_t)m;
       chunk_level[c] = level[perm[c * 32]];  // levels are chunk aligned: row 0 of a chunk is real
-      if (m > 65535) atomicMax(maxdeg, m);
+      if (m >= 65535) atomicMax(maxdeg, m);
     }
   }
 }
@@ -105,6 +113,7 @@ Band::~Band() {
 
 uint64_t Band::device_bytes() const {
   return pstart.bytes() + pend.bytes() + perm.bytes() + chunk_level.bytes() + chunk_ptr.bytes() + deg.bytes() +
+         deg_big.bytes() +
          col.bytes() + wt.bytes() + area_r.bytes() + wsum_r.bytes() + den.bytes() + 2 * sizeof(double) * nrows +
          sizeof(unsigned long long) * nlev;
 }
@@ -192,7 +201,13 @@ void band_build(gh_levels* L, Band* b, int32_t lb, int32_t le) {
                                                                        b->own_chunks, b->chunk_level.p, width.p,
                                                                        b->deg.p, maxdeg.p);
     GH_LAUNCH_CHECK();
-    if (read_scalar(maxdeg.p, s) > 65535) fail(GH_ERR_INVALID, "vertex valence above 65535 is not supported");
+    if (read_scalar(maxdeg.p, s) >= 65535) {
+      // valences past the 16-bit row length: the kernel reads these rows' true
+      // length here (deg holds the 65535 marker)
+      b->deg_big.alloc(b->nrows, s);
+      k_deg_big<<<grid_for(b->nrows), B, 0, s>>>(b->perm.p, m->vv_offset.p, b->nrows, b->deg_big.p);
+      GH_LAUNCH_CHECK();
+    }
     size_t tmp = 0;
     GH_CUDA(cub::DeviceScan::ExclusiveSum(nullptr, tmp, width.p, b->chunk_ptr.p, b->own_chunks + 1, s));
     Scratch<char> t(tmp, s);

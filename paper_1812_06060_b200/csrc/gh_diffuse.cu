@@ -84,6 +84,7 @@ struct BandArgs {
   const int32_t* chunk_level;
   const int64_t* chunk_ptr;
   const uint16_t* deg;
+  const int32_t* deg_big;         // true row lengths where deg holds 65535 (else null)
   const int32_t* col;
   const double* wt;
   const double* den;
@@ -408,6 +409,7 @@ __global__ void __launch_bounds__(kTmaThreads, 2) k_diffuse_tma(const __grid_con
         prev[i] = vba->ubuf + ((sweep & 1) ^ 1) * vba->nrows;
         den[i] = reinterpret_cast<const double*>(sb + kDenOff)[q * 32 + lane];
         d[i] = on[i] ? reinterpret_cast<const uint16_t*>(sb + kDegOff)[q * 32 + lane] : 0;
+        if (d[i] == 65535 && vba->deg_big) d[i] = vba->deg_big[r];  // valence past 16 bits
         fast[i] = fits && d[i] <= kUnroll;
         num[i] = 0.0;
       }
@@ -519,6 +521,7 @@ BandArgs band_args(const Band& b) {
   x.chunk_level = b.chunk_level.p;
   x.chunk_ptr = b.chunk_ptr.p;
   x.deg = b.deg.p;
+  x.deg_big = b.deg_big.p;
   x.col = b.col.p;
   x.wt = b.wt.p;
   x.den = b.den.p;

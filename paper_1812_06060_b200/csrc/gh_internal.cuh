@@ -150,7 +150,8 @@ struct Band {
   DevBuf<int32_t> perm;         // row -> original vertex (-1 for padding)
   DevBuf<int32_t> chunk_level;  // level of each own chunk (a chunk holds one level)
   DevBuf<int64_t> chunk_ptr;    // SELL-32 chunk offsets (own chunks)
-  DevBuf<uint16_t> deg;         // row lengths
+  DevBuf<uint16_t> deg;         // row lengths (65535: look in deg_big)
+  DevBuf<int32_t> deg_big;      // full row lengths, only when some valence >= 65535
   DevBuf<int32_t> col;          // local row of the neighbour | 0x80000000 if one level closer to the sources
   DevBuf<double> wt;            // cotan weights in the reference's row order
   DevBuf<double> area_r, wsum_r, den;

@@ -287,3 +287,42 @@ def test_dropin_reference_program_bitwise(gpu):
     r = subprocess.run([exe], capture_output=True, text=True, timeout=600)
     assert r.returncode == 0, r.stdout + r.stderr
     assert r.stdout.count("identical") == 6, r.stdout
+
+
+def _fan(n):
+    """A two-ring disc around one hub vertex of valence n (past 16 bits for
+    n > 65535): hub 0, inner ring 1..n, outer ring n+1..2n."""
+    a = np.arange(n)
+    th = 2 * np.pi * a / n
+    inner = np.stack([np.cos(th), np.sin(th), 0.1 * np.sin(3 * th)], 1)
+    outer = np.stack([2 * np.cos(th + np.pi / n), 2 * np.sin(th + np.pi / n), np.zeros(n)], 1)
+    P = np.concatenate([[[0.0, 0.0, 0.3]], inner, outer])
+    i0, i1 = 1 + a, 1 + (a + 1) % n
+    o0, o1 = 1 + n + a, 1 + n + (a + 1) % n
+    F = np.concatenate([np.stack([np.zeros(n, np.int64), i0, i1], 1), np.stack([i0, o0, i1], 1),
+                        np.stack([i1, o0, o1], 1)]).astype(np.int32)
+    return P, F
+
+
+@pytest.mark.parametrize("n,source", [(70_000, "outer"), (70_000, "hub"), (65_535, "outer"), (131_072, "inner")])
+def test_high_valence_hub_bitwise(gpu, port_oracle, n, source):
+    """A vertex whose valence does not fit the 16-bit row length of the
+    diffusion layout (deg_big path): every stage bitwise vs the C oracle, one
+    launch and band-sharded."""
+    from types import SimpleNamespace
+    from paper_1812_06060_b200 import bands
+    gh = gpu
+    P, F = _fan(n)
+    src = np.array([{"outer": n + 1, "hub": 0, "inner": 1}[source]], np.int32)
+    w = SimpleNamespace(positions=P, faces=F, sources=src, m=1.0)
+    ref = _oracle_chain(port_oracle, w, 60, None)
+    mesh = gh.build_mesh(P, F)
+    lv = gh.bfs_levels(mesh, src)
+    assert_same(lv.level_of_vertex, ref["level"], "level")
+    u = gh.gs_diffuse(mesh, lv, ref["t"], gh.DiffusionConfig(sweeps=60))
+    assert_same(u, ref["u"], "u")
+    for method, key in (("face", "d_face"), ("edge", "d_edge")):
+        d, rep = gh.distance(lv, method, 60, ref["t"])
+        assert_same(d, ref[key], f"fan {n} {method} distances")
+    if len(lv.offsets) - 1 >= 2:
+        assert_same(bands.gs_diffuse_bands(mesh, lv, 2, ref["t"], 60), ref["u"], "fan with 2 bands")
