@@ -70,7 +70,7 @@ __global__ void k_sell_fill(const int32_t* __restrict__ perm, const int32_t* __r
                             const int32_t* __restrict__ local, const int32_t* __restrict__ vv_off,
                             const int32_t* __restrict__ vv_idx, const double* __restrict__ vv_w,
                             const double* __restrict__ va, const double* __restrict__ wsum,
-                            const int64_t* __restrict__ chunk_ptr, int64_t own_rows, int32_t* __restrict__ col,
+                            const int64_t* __restrict__ chunk_ptr, int64_t own_rows, uint32_t* __restrict__ col,
                             double* __restrict__ wt, double* __restrict__ area_r, double* __restrict__ wsum_r) {
   for (int64_t r = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; r < own_rows;
        r += (int64_t)gridDim.x * blockDim.x) {
@@ -81,8 +81,9 @@ __global__ void k_sell_fill(const int32_t* __restrict__ perm, const int32_t* __r
     const int32_t a0 = vv_off[v], a1 = vv_off[v + 1];
     for (int32_t a = a0; a < a1; ++a) {
       const int32_t nb = vv_idx[a];
-      const uint32_t flag = level[nb] == L - 1 ? 0x80000000u : 0u;
-      col[base + 32 * (int64_t)(a - a0)] = (int32_t)((uint32_t)local[nb] | flag);
+      // the neighbour's slot in the sweep buffers: parity bit 0 = the sweep being
+      // written (one level closer to the sources), 1 = the previous sweep
+      col[base + 32 * (int64_t)(a - a0)] = gh::uidx((uint32_t)local[nb], level[nb] == L - 1 ? 0u : 1u);
       wt[base + 32 * (int64_t)(a - a0)] = vv_w[a];
     }
     area_r[r] = va[v];
@@ -169,7 +170,7 @@ void band_build(gh_levels* L, Band* b, int32_t lb, int32_t le) {
     b->h_pend[g] = (int32_t)cursor;
     cursor = (cursor + 31) & ~int64_t(31);
   }
-  if (cursor > 0x7fffffffLL) fail(GH_ERR_INVALID, "mesh too large for the diffusion layout");
+  if (cursor > 0x3fffffffLL) fail(GH_ERR_INVALID, "mesh too large for the diffusion layout");  // uidx < 2^31
   b->nrows = (int32_t)cursor;
   b->own_chunks = b->own_rows / 32;
   b->pstart.alloc(nlev, s);
@@ -223,7 +224,7 @@ void band_build(gh_levels* L, Band* b, int32_t lb, int32_t le) {
   b->col.alloc(nnz, s);
   b->wt.alloc(nnz, s);
   if (nnz) {
-    GH_CUDA(cudaMemsetAsync(b->col.p, 0, sizeof(int32_t) * nnz, s));
+    GH_CUDA(cudaMemsetAsync(b->col.p, 0, sizeof(uint32_t) * nnz, s));
     GH_CUDA(cudaMemsetAsync(b->wt.p, 0, sizeof(double) * nnz, s));
   }
   b->area_r.alloc(b->nrows, s);

@@ -51,8 +51,8 @@ __global__ void k_init_buffers(const int32_t* __restrict__ perm, const int32_t* 
     const int32_t v = perm[r];
     double x = 0.0;
     if (v >= 0) x = initial ? initial[v] : (level[v] == 0 ? 1.0 : 0.0);
-    ubuf[r] = x;
-    ubuf[nrows + r] = x;
+    ubuf[gh::uidx((uint32_t)r, 0)] = x;
+    ubuf[gh::uidx((uint32_t)r, 1)] = x;
   }
 }
 
@@ -63,11 +63,11 @@ __global__ void k_init_orig(const int32_t* __restrict__ level, const double* __r
 }
 
 // own rows of a band -> original vertex order
-__global__ void k_scatter(const int32_t* __restrict__ perm, const double* __restrict__ src, int64_t nrows,
-                          double* __restrict__ u) {
+__global__ void k_scatter(const int32_t* __restrict__ perm, const double* __restrict__ ubuf, uint32_t parity,
+                          int64_t nrows, double* __restrict__ u) {
   for (int64_t r = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; r < nrows; r += (int64_t)gridDim.x * blockDim.x) {
     const int32_t v = perm[r];
-    if (v >= 0) u[v] = src[r];
+    if (v >= 0) u[v] = ubuf[gh::uidx((uint32_t)r, parity)];
   }
 }
 
@@ -85,17 +85,16 @@ struct BandArgs {
   const int64_t* chunk_ptr;
   const uint16_t* deg;
   const int32_t* deg_big;         // true row lengths where deg holds 65535 (else null)
-  const int32_t* col;
+  const uint32_t* col;            // gh::uidx(neighbour row, 1 unless one level closer to the sources)
   const double* wt;
   const double* den;
-  double* ubuf;                   // [2][nrows]
+  double* ubuf;                   // both sweep parities, gh::uidx layout
   unsigned long long* rows_done;  // [nlev]
   double* lo_ubuf;                // lower neighbour (holds our level lb as a ghost), or null
   unsigned long long* lo_done;
   double* hi_ubuf;                // upper neighbour (holds our level le-1 as a ghost), or null
   unsigned long long* hi_done;
   int32_t* stalled;               // set when a dependency never arrives (a dead peer): the kernel bails out
-  int64_t nrows, lo_nrows, hi_nrows;
   int32_t lo_ghost, hi_ghost;     // first row of the ghost copy inside the neighbour
   int32_t lb, le;                 // own levels
 };
@@ -186,6 +185,21 @@ __device__ __forceinline__ bool step_range(int32_t sweeps, int32_t lb, int32_t l
   return true;
 }
 
+// Make n more rows of level X (this band) visible to every waiter: after a
+// release fence, the band's own counter and, for a boundary level, the
+// neighbour band's copy of it (system scope: the neighbour is another GPU).
+__device__ __forceinline__ void publish_rows(const BandArgs* vba, int32_t band_lb, int32_t band_le, int32_t X,
+                                             unsigned long long n) {
+  unsigned long long* lo_done = vba->lo_done;
+  unsigned long long* hi_done = vba->hi_done;
+  const bool to_lo = X == band_lb && lo_done, to_hi = X == band_le - 1 && hi_done;
+  if (to_lo || to_hi) __threadfence_system();
+  else __threadfence();
+  atomicAdd(vba->rows_done + X, n);
+  if (to_lo) atomicAdd_system(lo_done + X, n);
+  if (to_hi) atomicAdd_system(hi_done + X, n);
+}
+
 // slot layout: header 256 B (int32: chunk offsets [0..kTileChunks], fits [31], chunk levels [32..])
 //              | den kTileChunks x 256 B | deg kTileChunks x 64 B | columns | weights
 constexpr int kHdr = 256;
@@ -195,7 +209,9 @@ constexpr int kColOff = kDegOff + kTileChunks * 64;
 
 // kUnroll: rows up to this valence are gathered fully unrolled (6 covers
 // icosphere and torus meshes and saves the registers of two more gathers).
-template <int kUnroll>
+// kTable: the pstart/pend tables are copied into shared memory (separate
+// instances so every shared-memory access compiles to LDS, not a generic load).
+template <int kUnroll, bool kTable>
 __global__ void __launch_bounds__(kTmaThreads, 2) k_diffuse_tma(const __grid_constant__ TmaArgs a) {
   extern __shared__ __align__(128) unsigned char smem[];
   // this block's band and its rank inside the band
@@ -213,9 +229,11 @@ __global__ void __launch_bounds__(kTmaThreads, 2) k_diffuse_tma(const __grid_con
   uint64_t* empty = full + a.nslots;
   int32_t* sh_pend = reinterpret_cast<int32_t*>(empty + a.nslots);
   int32_t* sh_pstart = sh_pend + a.nlev;
-  const size_t table_bytes = a.table_in_smem ? ((2 * sizeof(int32_t) * a.nlev + 127) & ~size_t(127)) : 0;
-  unsigned char* slots = reinterpret_cast<unsigned char*>(empty + a.nslots) + table_bytes;
-  slots = reinterpret_cast<unsigned char*>((reinterpret_cast<uintptr_t>(slots) + 127) & ~uintptr_t(127));
+  const uint32_t table_bytes = kTable ? ((8u * (uint32_t)a.nlev + 127u) & ~127u) : 0u;
+  // slots start 128-byte aligned in the shared window (offsets from smem keep
+  // the accesses in the shared address space)
+  const uint32_t slots_at = 16u * (uint32_t)a.nslots + table_bytes;
+  unsigned char* slots = smem + slots_at + ((128u - ((smem_u32(smem) + slots_at) & 127u)) & 127u);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   if (threadIdx.x == 0) {
     for (int i = 0; i < a.nslots; ++i) {
@@ -224,16 +242,14 @@ __global__ void __launch_bounds__(kTmaThreads, 2) k_diffuse_tma(const __grid_con
     }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
-  const int32_t* pend = sba.pend;
-  const int32_t* pstart = sba.pstart;
-  if (a.table_in_smem) {
+  if (kTable) {
     for (int i = threadIdx.x; i < a.nlev; i += blockDim.x) {
       sh_pend[i] = sba.pend[i];
       sh_pstart[i] = sba.pstart[i];
     }
-    pend = sh_pend;
-    pstart = sh_pstart;
   }
+  const int32_t* pend = kTable ? sh_pend : sba.pend;
+  const int32_t* pstart = kTable ? sh_pstart : sba.pstart;
   __syncthreads();
 
   const int32_t nsteps = (band_le - 1) + 2 * (a.sweeps - 1) + 1;
@@ -283,13 +299,14 @@ __global__ void __launch_bounds__(kTmaThreads, 2) k_diffuse_tma(const __grid_con
       const int32_t cbase = cb + t0 * kTileChunks;
       for (int j = 0; j < kTilesPerBatch && t0 + j < ntile; ++j) {
         if (issued >= a.nslots) mbar_wait(empty + slot, use ^ 1u);
-        const int32_t c0 = cbase + j * kTileChunks;
+        const int off = j * kTileChunks;  // the tile's lanes in the batch
+        const int32_t c0 = cbase + off;
         const int nch = (int)(ce - c0 < kTileChunks ? ce - c0 : kTileChunks);
-        const int64_t base = __shfl_sync(0xffffffffu, p0, j * kTileChunks);
-        const int src = j * kTileChunks + (lane <= kTileChunks ? lane : 0);
+        const int64_t base = __shfl_sync(0xffffffffu, p0, off);
+        const int src = off + (lane <= kTileChunks ? lane : 0);
         int64_t pi = __shfl_sync(0xffffffffu, p0, src < 32 ? src : 31);
-        const int32_t li = __shfl_sync(0xffffffffu, lv0, (j * kTileChunks + (lane & (kTileChunks - 1))) & 31);
-        if (j * kTileChunks + lane == 32) pi = p_last;
+        const int32_t li = __shfl_sync(0xffffffffu, lv0, (off + (lane & (kTileChunks - 1))) & 31);
+        if (off + lane == 32) pi = p_last;
         int32_t* hdr = reinterpret_cast<int32_t*>(slots + (size_t)slot * a.slot_bytes);
         if (lane <= nch) hdr[lane] = (int32_t)(pi - base);
         if (lane < kTileChunks) hdr[32 + lane] = li;
@@ -396,63 +413,76 @@ __global__ void __launch_bounds__(kTmaThreads, 2) k_diffuse_tma(const __grid_con
       double num[kChunksPerWarp], den[kChunksPerWarp], v[kChunksPerWarp][kUnroll];
       int32_t d[kChunksPerWarp];
       bool on[kChunksPerWarp], fast[kChunksPerWarp];
-      double* cur[kChunksPerWarp];
-      const double* prev[kChunksPerWarp];
+      uint32_t px[kChunksPerWarp];  // sweep parity of the step, as the uidx xor mask
+      double* const ub = vba->ubuf;
 #pragma unroll
       for (int i = 0; i < kChunksPerWarp; ++i) {
         const int q = warp + kConsumerWarps * i;
         const int32_t c = cb + j * kTileChunks + q;
         const int32_t r = c * 32 + lane;
         on[i] = live[i] && r < pend[Lq[i]];
-        const int32_t sweep = (int32_t)((tau - Lq[i]) >> 1);
-        cur[i] = vba->ubuf + (sweep & 1) * vba->nrows;
-        prev[i] = vba->ubuf + ((sweep & 1) ^ 1) * vba->nrows;
+        px[i] = (uint32_t)((tau - Lq[i]) >> 1 & 1) << 5;
         den[i] = reinterpret_cast<const double*>(sb + kDenOff)[q * 32 + lane];
         d[i] = on[i] ? reinterpret_cast<const uint16_t*>(sb + kDegOff)[q * 32 + lane] : 0;
         if (d[i] == 65535 && vba->deg_big) d[i] = vba->deg_big[r];  // valence past 16 bits
         fast[i] = fits && d[i] <= kUnroll;
         num[i] = 0.0;
       }
-      // all gathers of both chunks in flight together
+      // all gathers of both chunks in flight together; u gathers are L1-cached
+      // (see the dependency check above)
 #pragma unroll
       for (int i = 0; i < kChunksPerWarp; ++i) {
-        const int32_t* scol = reinterpret_cast<const int32_t*>(sb + kColOff) + hdr[warp + kConsumerWarps * i] + lane;
+        const uint32_t* scol = reinterpret_cast<const uint32_t*>(sb + kColOff) + hdr[warp + kConsumerWarps * i] + lane;
 #pragma unroll
         for (int k = 0; k < kUnroll; ++k)
-          if (fast[i] && k < d[i]) {
-            const int32_t cc = scol[32 * k];
-            v[i][k] = __ldca((cc < 0 ? cur[i] : prev[i]) + (cc & 0x7fffffff));  // L1-cached, see below
+          if (fast[i] && k < d[i]) v[i][k] = __ldca(ub + (scol[32 * k] ^ px[i]));
+      }
+      // row sums, each left to right (diffusion.hpp:79). The branch keeps the
+      // scheduler from pulling products above the later gathers; the common
+      // case interleaves the two rows' dependent chains.
+      const double* swt[kChunksPerWarp];
+#pragma unroll
+      for (int i = 0; i < kChunksPerWarp; ++i)
+        swt[i] = reinterpret_cast<const double*>(sb + kColOff + (size_t)col_cap * 4u) +
+                 hdr[warp + kConsumerWarps * i] + lane;
+      if (fast[0] && fast[kChunksPerWarp - 1]) {
+#pragma unroll
+        for (int k = 0; k < kUnroll; ++k)
+#pragma unroll
+          for (int i = 0; i < kChunksPerWarp; ++i)
+            if (k < d[i]) num[i] += swt[i][32 * k] * v[i][k];
+      } else {
+#pragma unroll
+        for (int i = 0; i < kChunksPerWarp; ++i)
+          if (fast[i]) {
+#pragma unroll
+            for (int k = 0; k < kUnroll; ++k)
+              if (k < d[i]) num[i] += swt[i][32 * k] * v[i][k];
           }
       }
 #pragma unroll
       for (int i = 0; i < kChunksPerWarp; ++i) {
         const int q = warp + kConsumerWarps * i;
         const int32_t c = cb + j * kTileChunks + q;
-        if (fast[i]) {
-          const double* swt =
-              reinterpret_cast<const double*>(sb + kColOff + (size_t)col_cap * 4u) + hdr[q] + lane;
-#pragma unroll
-          for (int k = 0; k < kUnroll; ++k)
-            if (k < d[i]) num[i] += swt[32 * k] * v[i][k];  // diffusion.hpp:79
-        } else if (on[i]) {
+        if (!fast[i] && on[i]) {  // wide rows or a tile past the slot: straight from global memory
           const int64_t q0 = __ldg(vba->chunk_ptr + c) + lane;
           for (int32_t k = 0; k < d[i]; ++k) {
-            const int32_t cc = __ldg(vba->col + q0 + 32 * (int64_t)k);
+            const uint32_t cc = __ldg(vba->col + q0 + 32 * (int64_t)k);
             const double w = __ldg(vba->wt + q0 + 32 * (int64_t)k);
-            num[i] += w * __ldca((cc < 0 ? cur[i] : prev[i]) + (cc & 0x7fffffff));
+            num[i] += w * __ldca(ub + (cc ^ px[i]));
           }
         }
         if (on[i]) {
           const int32_t r = c * 32 + lane;
           const double u0 = Lq[i] == 0 ? 1.0 : 0.0;
           const double un = (u0 + a.t * num[i]) / den[i];  // diffusion.hpp:82
-          __stcg(cur[i] + r, un);
+          const uint32_t par = px[i] >> 5;
+          __stcg(ub + gh::uidx((uint32_t)r, par), un);
           // boundary levels also land in the neighbour band's ghost copy
-          const int64_t par = ((tau - Lq[i]) >> 1) & 1;
           if (Lq[i] == band_lb && vba->lo_ubuf)
-            __stcg(vba->lo_ubuf + par * vba->lo_nrows + vba->lo_ghost + (r - pstart[Lq[i]]), un);
+            __stcg(vba->lo_ubuf + gh::uidx((uint32_t)(vba->lo_ghost + (r - pstart[Lq[i]])), par), un);
           if (Lq[i] == band_le - 1 && vba->hi_ubuf)
-            __stcg(vba->hi_ubuf + par * vba->hi_nrows + vba->hi_ghost + (r - pstart[Lq[i]]), un);
+            __stcg(vba->hi_ubuf + gh::uidx((uint32_t)(vba->hi_ghost + (r - pstart[Lq[i]])), par), un);
         }
       }
       __syncwarp();
@@ -470,17 +500,7 @@ __global__ void __launch_bounds__(kTmaThreads, 2) k_diffuse_tma(const __grid_con
       for (int32_t X = lv_first + 2 * lane; X <= lv_last; X += 64) {
         const int32_t lo = cb * 32 > pstart[X] ? cb * 32 : pstart[X];
         const int32_t hi = ce * 32 < pend[X] ? ce * 32 : pend[X];
-        if (hi > lo) {
-          const unsigned long long n = (unsigned long long)(hi - lo);
-          unsigned long long* lo_done = vba->lo_done;
-          unsigned long long* hi_done = vba->hi_done;
-          const bool to_lo = X == band_lb && lo_done, to_hi = X == band_le - 1 && hi_done;
-          if (to_lo || to_hi) __threadfence_system();
-          else __threadfence();
-          atomicAdd(vba->rows_done + X, n);
-          if (to_lo) atomicAdd_system(lo_done + X, n);
-          if (to_hi) atomicAdd_system(hi_done + X, n);
-        }
+        if (hi > lo) publish_rows(vba, band_lb, band_le, X, (unsigned long long)(hi - lo));
       }
     }
   }
@@ -532,9 +552,6 @@ BandArgs band_args(const Band& b) {
   x.lo_done = b.lo_done;
   x.hi_ubuf = b.hi_ubuf;
   x.hi_done = b.hi_done;
-  x.nrows = b.nrows;
-  x.lo_nrows = b.lo_nrows;
-  x.hi_nrows = b.hi_nrows;
   x.lo_ghost = b.lo_ghost;
   x.hi_ghost = b.hi_ghost;
   x.lb = b.lb;
@@ -589,7 +606,8 @@ double bands_launch(gh_levels* L, std::vector<Band*>& bands, double t, int32_t s
   }
   if (nslots < 2) nslots = 2;
   const size_t shmem = 16 * (size_t)nslots + table_bytes + 128 + (size_t)nslots * slot_bytes;
-  void* fn = wmax <= 6 ? (void*)k_diffuse_tma<6> : (void*)k_diffuse_tma<8>;
+  void* fn = wmax <= 6 ? (table ? (void*)k_diffuse_tma<6, true> : (void*)k_diffuse_tma<6, false>)
+                       : (table ? (void*)k_diffuse_tma<8, true> : (void*)k_diffuse_tma<8, false>);
   GH_CUDA(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)shmem));
   int nsm = 0, per_sm = 0;
   GH_CUDA(cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, m->device));
@@ -629,8 +647,8 @@ double bands_launch(gh_levels* L, std::vector<Band*>& bands, double t, int32_t s
     GH_CUDA(cudaMemcpyAsync(&stalled, b->stalled, sizeof(int32_t), cudaMemcpyDeviceToHost, s));
     GH_CUDA(cudaStreamSynchronize(s));
     if (stalled) fail(GH_ERR_INTERNAL, "diffusion: a band dependency never arrived (neighbour band not running?)");
-    const double* result = b->ubuf + ((sweeps - 1) & 1) * (int64_t)b->nrows;
-    k_scatter<<<grid_for(b->own_rows), B, 0, s>>>(b->perm.p, result, b->own_rows, L->u_orig.p);
+    k_scatter<<<grid_for(b->own_rows), B, 0, s>>>(b->perm.p, b->ubuf, (uint32_t)((sweeps - 1) & 1), b->own_rows,
+                                                  L->u_orig.p);
     GH_LAUNCH_CHECK();
     m->launches++;
   }

@@ -39,6 +39,12 @@ struct Error {
 constexpr int kBlock = 256;
 constexpr int kReduceGrid = 4096;  // fixed partial count => reproducible reductions
 
+// Sweep buffers: rows in blocks of 32, each block holding parity 0 then parity 1,
+// so a gather's parity is one xor with (sweep & 1) << 5 of the stored column.
+__host__ __device__ __forceinline__ uint32_t uidx(uint32_t row, uint32_t parity) {
+  return ((row >> 5) << 6) | (parity << 5) | (row & 31u);
+}
+
 inline unsigned grid_for(int64_t n, int block = kBlock, int64_t cap = 148 * 32) {
   int64_t g = (n + block - 1) / block;
   if (g < 1) g = 1;
@@ -152,7 +158,7 @@ struct Band {
   DevBuf<int64_t> chunk_ptr;    // SELL-32 chunk offsets (own chunks)
   DevBuf<uint16_t> deg;         // row lengths (65535: look in deg_big)
   DevBuf<int32_t> deg_big;      // full row lengths, only when some valence >= 65535
-  DevBuf<int32_t> col;          // local row of the neighbour | 0x80000000 if one level closer to the sources
+  DevBuf<uint32_t> col;         // uidx(local row of the neighbour, 0 if one level closer to the sources else 1)
   DevBuf<double> wt;            // cotan weights in the reference's row order
   DevBuf<double> area_r, wsum_r, den;
   double den_t = 0.0;
@@ -160,7 +166,7 @@ struct Band {
   // (ipc), else from the stream-ordered pool like every other buffer
   bool ipc = false;
   cudaStream_t astream = nullptr;
-  double* ubuf = nullptr;                   // [2][nrows] sweep-parity buffers
+  double* ubuf = nullptr;                   // both sweep parities of every row, uidx layout
   unsigned long long* rows_done = nullptr;  // [nlev] rows finished per level over all sweeps
   int32_t* stalled = nullptr;               // dependency-timeout flag of the last launch
   // links to the neighbours' copies of this band's boundary levels
