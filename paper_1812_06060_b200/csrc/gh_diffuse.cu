@@ -475,7 +475,14 @@ __global__ void __launch_bounds__(kTmaThreads, 2) k_diffuse_tma(const __grid_con
         if (on[i]) {
           const int32_t r = c * 32 + lane;
           const double u0 = Lq[i] == 0 ? 1.0 : 0.0;
-          const double un = (u0 + a.t * num[i]) / den[i];  // diffusion.hpp:82
+          // (u0 + t num) / den (diffusion.hpp:82). Far from the sources the
+          // numerator is exactly 0 for many sweeps (underflow), and a zero
+          // quotient sends the IEEE division down its slow path; 0 / den with
+          // den > 0 is that same zero, so skip the division there.
+          const double nz = u0 + a.t * num[i];
+          double un = nz;
+          if (!(nz == 0.0 && den[i] > 0.0))  // asm volatile: keeps the division under the branch
+            asm volatile("div.rn.f64 %0, %1, %2;" : "=d"(un) : "d"(nz), "d"(den[i]));
           const uint32_t par = px[i] >> 5;
           __stcg(ub + gh::uidx((uint32_t)r, par), un);
           // boundary levels also land in the neighbour band's ghost copy

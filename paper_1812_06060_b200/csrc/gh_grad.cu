@@ -101,8 +101,8 @@ __device__ __forceinline__ void face_y_update(int64_t i, int32_t f1, int32_t f2,
   const v3 ed = ld3(edir, i);
   const double mismatch = dot(ed, sub(q2, q1));
   const v3 shift = mk(ed.x * mismatch, ed.y * mismatch, ed.z * mismatch);
-  st3(Y, 2 * i, add(q1, scale(a2 / (a1 + a2), shift)));
-  st3(Y, 2 * i + 1, sub(q2, scale(a1 / (a1 + a2), shift)));
+  st3(Y, 2 * i, add(q1, scale(ddiv(a2, a1 + a2), shift)));
+  st3(Y, 2 * i + 1, sub(q2, scale(ddiv(a1, a1 + a2), shift)));
 }
 
 __global__ void k_face_first_y(const int32_t* __restrict__ ef, const double* __restrict__ area,
@@ -208,7 +208,7 @@ __global__ void k_edge_init_edges(const int32_t* __restrict__ edge_he, const dou
       ++deg;
     }
     tsum[e] = s;
-    x[e] = s / (double)deg;
+    x[e] = ddiv(s, (double)deg);
   }
 }
 
@@ -218,10 +218,10 @@ __device__ __forceinline__ void edge_w_update(int64_t f, const int32_t* __restri
                                               const int8_t* __restrict__ sgn, double mu, double* __restrict__ w) {
   double v[3], dotv = 0.0;
   for (int k = 0; k < 3; ++k) {
-    v[k] = x[he_edge[3 * f + k]] - l[k] / mu;
+    v[k] = x[he_edge[3 * f + k]] - ddiv(l[k], mu);
     dotv += (double)sgn[3 * f + k] * v[k];
   }
-  const double shift = dotv / 3.0;
+  const double shift = ddiv(dotv, 3.0);
   for (int k = 0; k < 3; ++k) w[3 * f + k] = v[k] - shift * (double)sgn[3 * f + k];
 }
 
@@ -246,7 +246,7 @@ __global__ void k_edge_x(const int32_t* __restrict__ edge_he, const double* __re
     if (h0 >= 0) sum += lam[h0] + mu * w[h0];
     if (h1 >= 0) sum += lam[h1] + mu * w[h1];
     const double deg = (h0 >= 0 && h1 >= 0) ? 2.0 : 1.0;
-    const double xn = sum / (deg * (1.0 + mu));
+    const double xn = ddiv(sum, deg * (1.0 + mu));
     x[e] = xn;
     const double d = xn - xold;
     const double tt = deg * d * d;

@@ -49,7 +49,7 @@ __global__ void k_inc_face(const int32_t* __restrict__ order, const int32_t* __r
       sum += dot(ld3(g, h / 3), step);
       ++count;
     }
-    inc[i] = sum / (double)count;
+    inc[i] = ddiv(sum, (double)count);
   }
 }
 

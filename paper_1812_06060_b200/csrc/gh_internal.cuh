@@ -288,7 +288,17 @@ __device__ __forceinline__ void st3(double* p, int64_t i, v3 a) {
 __device__ __forceinline__ v3 sub(v3 a, v3 b) { return v3{a.x - b.x, a.y - b.y, a.z - b.z}; }
 __device__ __forceinline__ v3 add(v3 a, v3 b) { return v3{a.x + b.x, a.y + b.y, a.z + b.z}; }
 __device__ __forceinline__ v3 scale(double s, v3 a) { return v3{s * a.x, s * a.y, s * a.z}; }
-__device__ __forceinline__ v3 divs(v3 a, double s) { return v3{a.x / s, a.y / s, a.z / s}; }
+// n / d, IEEE round to nearest. A zero numerator (common: zero gradients,
+// zero multipliers, underflowed heat) sends the inline division down its slow
+// path, so that case returns the signed zero directly; the asm keeps the
+// division itself under the branch instead of being computed speculatively.
+__device__ __forceinline__ double ddiv(double n, double d) {
+  if (n == 0.0 && d != 0.0 && d == d) return (__double_as_longlong(n) ^ __double_as_longlong(d)) < 0 ? -0.0 : 0.0;
+  double q;
+  asm volatile("div.rn.f64 %0, %1, %2;" : "=d"(q) : "d"(n), "d"(d));
+  return q;
+}
+__device__ __forceinline__ v3 divs(v3 a, double s) { return v3{ddiv(a.x, s), ddiv(a.y, s), ddiv(a.z, s)}; }
 // Eigen size-3 dot order: (x0*y0 + x1*y1) + x2*y2
 __device__ __forceinline__ double dot(v3 a, v3 b) { return (a.x * b.x + a.y * b.y) + a.z * b.z; }
 __device__ __forceinline__ double sqnorm(v3 a) { return dot(a, a); }

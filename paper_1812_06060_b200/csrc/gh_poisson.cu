@@ -79,7 +79,7 @@ __global__ void k_cg_init(Op op, const double* __restrict__ rhs, double* __restr
   double rz = 0.0, rr = 0.0;
   GRID_STRIDE(i, op.n) {
     const double ri = rhs[i], di = op.diag(i);
-    const double zi = ri / di;
+    const double zi = ddiv(ri, di);
     x[i] = 0.0;
     r[i] = ri;
     diag[i] = di;
@@ -161,7 +161,7 @@ __global__ void k_cg_update(int64_t n, const double* __restrict__ p, const doubl
     x[i] += alpha * p[i];
     const double ri = r[i] - alpha * q[i];
     r[i] = ri;
-    const double zi = ri / diag[i];
+    const double zi = ddiv(ri, diag[i]);
     z[i] = zi;
     rr += ri * ri;
     rz += ri * zi;
