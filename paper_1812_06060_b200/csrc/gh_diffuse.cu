@@ -424,8 +424,7 @@ __global__ void __launch_bounds__(kTmaThreads, 2) k_diffuse_tma(const __grid_con
         px[i] = (uint32_t)((tau - Lq[i]) >> 1 & 1) << 5;
         den[i] = reinterpret_cast<const double*>(sb + kDenOff)[q * 32 + lane];
         d[i] = on[i] ? reinterpret_cast<const uint16_t*>(sb + kDegOff)[q * 32 + lane] : 0;
-        if (d[i] == 65535 && vba->deg_big) d[i] = vba->deg_big[r];  // valence past 16 bits
-        fast[i] = fits && d[i] <= kUnroll;
+        fast[i] = fits && d[i] <= kUnroll;  // 65535 (valence past 16 bits) always takes the slow path
         num[i] = 0.0;
       }
       // all gathers of both chunks in flight together; u gathers are L1-cached
@@ -466,7 +465,10 @@ __global__ void __launch_bounds__(kTmaThreads, 2) k_diffuse_tma(const __grid_con
         const int32_t c = cb + j * kTileChunks + q;
         if (!fast[i] && on[i]) {  // wide rows or a tile past the slot: straight from global memory
           const int64_t q0 = __ldg(vba->chunk_ptr + c) + lane;
-          for (int32_t k = 0; k < d[i]; ++k) {
+          // (a global load here, not above: a load in the fast path would share a
+          // scoreboard with the gathers and serialise the two chunks)
+          const int32_t dd = d[i] == 65535 && vba->deg_big ? vba->deg_big[c * 32 + lane] : d[i];
+          for (int32_t k = 0; k < dd; ++k) {
             const uint32_t cc = __ldg(vba->col + q0 + 32 * (int64_t)k);
             const double w = __ldg(vba->wt + q0 + 32 * (int64_t)k);
             num[i] += w * __ldca(ub + (cc ^ px[i]));
