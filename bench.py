@@ -362,7 +362,7 @@ def main():
                      "scope": "per GPU (rank 0)" if world > 1 else "whole launch"},
         "e2e": {"value": e2e_value, "unit": "vertex-updates/s", "seconds": e2e_sec,
                 "h2d_bytes_per_step": nbytes_p + nbytes_f + S.nbytes, "d2h_bytes_per_step": nbytes_d,
-                "stages_ms": stages, "parity": parity, **e2e_extra},
+                "stages_ms": stages, "parity": parity, "samples_s": [round(x, 6) for x in e2e_s], **e2e_extra},
         "gpu_launches": launches,
         "clocks": clk.summary(),
         "cpu_baseline": cpu,

@@ -118,7 +118,8 @@ __global__ void k_face_first_y(const int32_t* __restrict__ ef, const double* __r
 __global__ void k_face_g(const int32_t* __restrict__ slot, const double* __restrict__ area,
                          const double* __restrict__ h, const double* __restrict__ Y, const double* __restrict__ lam,
                          int64_t nf, double mu, double* __restrict__ g, double* __restrict__ part,
-                         double* __restrict__ term) {
+                         double* __restrict__ term, const int32_t* __restrict__ halt) {
+  if (*halt) return;  // the device stop rule ended the loop (see admm_loop)
   double s = 0.0;
   GRID_STRIDE(f, nf) {
     const double A = area[f];
@@ -148,7 +149,8 @@ __global__ void k_face_g(const int32_t* __restrict__ slot, const double* __restr
 __global__ void k_face_lambda_y(const int32_t* __restrict__ ef, const double* __restrict__ area,
                                 const double* __restrict__ g, const double* __restrict__ edir, int64_t ni, double mu,
                                 double* __restrict__ Y, double* __restrict__ lam, double* __restrict__ part,
-                                double* __restrict__ term) {
+                                double* __restrict__ term, const int32_t* __restrict__ halt) {
+  if (*halt) return;
   double s = 0.0;
   GRID_STRIDE(i, ni) {
     const int32_t f1 = ef[2 * i], f2 = ef[2 * i + 1];
@@ -237,7 +239,9 @@ __global__ void k_edge_first_w(const int32_t* __restrict__ he_edge, const double
 // X-update per edge (143-149) + dual partials (163-164, 117-123)
 __global__ void k_edge_x(const int32_t* __restrict__ edge_he, const double* __restrict__ tsum,
                          const double* __restrict__ lam, const double* __restrict__ w, int64_t ne, double mu,
-                         double* __restrict__ x, double* __restrict__ part, double* __restrict__ term) {
+                         double* __restrict__ x, double* __restrict__ part, double* __restrict__ term,
+                         const int32_t* __restrict__ halt) {
+  if (*halt) return;
   double s = 0.0;
   GRID_STRIDE(e, ne) {
     const double xold = x[e];
@@ -260,7 +264,9 @@ __global__ void k_edge_x(const int32_t* __restrict__ edge_he, const double* __re
 // lambda-update + primal (151-158), then the next W-update per face
 __global__ void k_edge_lambda_w(const int32_t* __restrict__ he_edge, const double* __restrict__ x,
                                 const int8_t* __restrict__ sgn, int64_t nf, double mu, double* __restrict__ w,
-                                double* __restrict__ lam, double* __restrict__ part, double* __restrict__ term) {
+                                double* __restrict__ lam, double* __restrict__ part, double* __restrict__ term,
+                                const int32_t* __restrict__ halt) {
+  if (*halt) return;
   double s = 0.0;
   GRID_STRIDE(f, nf) {
     double l[3], rs = 0.0;
@@ -279,10 +285,47 @@ __global__ void k_edge_lambda_w(const int32_t* __restrict__ he_edge, const doubl
   if (threadIdx.x == 0) part[blockIdx.x] = s;
 }
 
-__global__ void k_sqrt_pair(const double* __restrict__ sums, double mu, double* __restrict__ out) {
+// Fixed-order sum of kReduceGrid partials by one 1024-thread block (the same
+// order as k_reduce_block below).
+__device__ double block_reduce_1024(const double* __restrict__ part, double* sh) {
+  double s = 0.0;
+  for (int i = threadIdx.x; i < (int)G; i += 1024) s += part[i];
+  sh[threadIdx.x] = s;
+  __syncthreads();
+  for (int k = 512; k > 0; k >>= 1) {
+    if (threadIdx.x < k) sh[threadIdx.x] += sh[threadIdx.x + k];
+    __syncthreads();
+  }
+  const double r = sh[0];
+  __syncthreads();
+  return r;
+}
+
+// Stop rule of iteration `it` on the device: residual norms from the partials
+// (primal = sqrt(sum), dual = mu sqrt(sum), grad_face.hpp:170-177 /
+// grad_edge.hpp:163-170), recorded in hist[2 it], hist[2 it + 1]. halt = 1 when
+// both thresholds are met, 2 when either norm is inside the guard band where
+// the tree sum might decide differently from the reference's left-to-right sum
+// (the host then decides from the exact sums), and stays 0 otherwise. Once set,
+// the later iterations' kernels return at once, so the state is that of `it`.
+__global__ void k_admm_stop(const double* __restrict__ part_primal, const double* __restrict__ part_dual, double mu,
+                            double thr1, double thr2, double gp, double gd, int32_t it, double* __restrict__ hist,
+                            double* __restrict__ halted_at, int32_t* __restrict__ halt) {
+  __shared__ double sh[1024];
+  if (*halt) return;
+  const double sp = block_reduce_1024(part_primal, sh);
+  const double sd = block_reduce_1024(part_dual, sh);
   if (threadIdx.x == 0) {
-    out[0] = sqrt(sums[0]);       // primal
-    out[1] = mu * sqrt(sums[1]);  // dual
+    const double primal = sqrt(sp), dual = mu * sqrt(sd);
+    hist[2 * it] = primal;
+    hist[2 * it + 1] = dual;
+    const bool near1 = fabs(primal - thr1) <= gp * fmax(fabs(primal), thr1);
+    const bool near2 = fabs(dual - thr2) <= gd * fmax(fabs(dual), thr2);
+    const int32_t state = (near1 || near2) ? 2 : (primal <= thr1 && dual <= thr2) ? 1 : 0;
+    if (state) {
+      *halt = state;
+      *halted_at = (double)it;  // read back with the history
+    }
   }
 }
 
@@ -341,20 +384,17 @@ namespace {
 // counts and converged flags equal the reference's by construction; the
 // reported residuals are the tree values (within ~1e-14 of the reference's)
 // except where the band forced the exact sums.
+double guard(int64_t n) { return (double)(n + 64) * 2.220446049250313e-16; }
+
 bool stop_rule(gh_mesh* m, AdmmResult& res, int it, const gh_admm_config& cfg, double scale, double mu,
-               const double* term_p, int64_t np, const double* term_d, int64_t nd) {
-  double primal = m->pinned_scalars[0], dual = m->pinned_scalars[1];
+               double primal, double dual, const double* term_p, int64_t np, const double* term_d, int64_t nd) {
   const double thr1 = scale * cfg.eps1, thr2 = scale * cfg.eps2;
-  const double gp = (double)(np + 64) * 2.220446049250313e-16, gd = (double)(nd + 64) * 2.220446049250313e-16;
+  const double gp = guard(np), gd = guard(nd);
   auto near = [](double v, double thr, double g) { return std::fabs(v - thr) <= g * std::fmax(std::fabs(v), thr); };
-  bool exact = false;
-  auto make_exact = [&] {
-    if (exact) return;
+  if (near(primal, thr1, gp) || near(dual, thr2, gd)) {
     primal = std::sqrt(sequential_sum_nonneg(term_p, np, m->stream, &m->launches));
     dual = mu * std::sqrt(sequential_sum_nonneg(term_d, nd, m->stream, &m->launches));
-    exact = true;
-  };
-  if (near(primal, thr1, gp) || near(dual, thr2, gd)) make_exact();
+  }
   const bool met = primal <= thr1 && dual <= thr2;
   res.primal.push_back(primal);
   res.dual.push_back(dual);
@@ -364,6 +404,46 @@ bool stop_rule(gh_mesh* m, AdmmResult& res, int it, const gh_admm_config& cfg, d
   res.converged = met;
   (void)it;
   return met;
+}
+
+// The iteration loop without a host round trip per iteration: all remaining
+// iterations are enqueued at once, each followed by k_admm_stop; the first
+// iteration whose stop rule fires (or lands in the guard band) halts the rest
+// on the device. One read-back then gives the history; a guard-band iteration
+// is decided on the host from the exact sums (stop_rule) and the loop resumes
+// after it if the thresholds are not met.
+template <class Iterate>
+void admm_loop(gh_mesh* m, AdmmResult& res, const gh_admm_config& cfg, double scale, double mu,
+               const double* term_p, int64_t np, const double* term_d, int64_t nd, Iterate iterate) {
+  const int32_t imax = cfg.max_iterations;
+  if (imax <= 0) return;
+  cudaStream_t s = m->stream;
+  Scratch<double> hist(2 * (size_t)imax + 1, s);
+  Scratch<int32_t> halt(1, s);
+  std::vector<double> h(2 * (size_t)imax + 1);
+  const double thr1 = scale * cfg.eps1, thr2 = scale * cfg.eps2;
+  int32_t it0 = 0;
+  while (it0 < imax) {
+    GH_CUDA(cudaMemsetAsync(halt.p, 0, sizeof(int32_t), s));
+    for (int32_t it = it0; it < imax; ++it) {
+      iterate(halt.p);
+      k_admm_stop<<<1, 1024, 0, s>>>(m->partials.p + G, m->partials.p, mu, thr1, thr2, guard(np), guard(nd), it,
+                                     hist.p, hist.p + 2 * (size_t)imax, halt.p);
+      GH_LAUNCH_CHECK();
+      m->launches += 3;
+    }
+    int32_t state = 0;
+    GH_CUDA(cudaMemcpyAsync(h.data(), hist.p, sizeof(double) * h.size(), cudaMemcpyDeviceToHost, s));
+    GH_CUDA(cudaMemcpyAsync(&state, halt.p, sizeof(int32_t), cudaMemcpyDeviceToHost, s));
+    GH_CUDA(cudaStreamSynchronize(s));
+    const int32_t last = state ? (int32_t)h[2 * (size_t)imax] : imax - 1;  // iteration that halted (or the final one)
+    for (int32_t it = it0; it < last; ++it) {  // cleared both thresholds' guard bands, not met
+      res.primal.push_back(h[2 * it]);
+      res.dual.push_back(h[2 * it + 1]);
+    }
+    if (stop_rule(m, res, last, cfg, scale, mu, h[2 * last], h[2 * last + 1], term_p, np, term_d, nd)) return;
+    it0 = last + 1;
+  }
 }
 
 }  // namespace
@@ -377,10 +457,8 @@ AdmmResult admm_face_dev(gh_mesh* m, const double* d_h, const gh_admm_config& cf
   Scratch<double> Y(6 * NI + 6, s), lam(6 * NI + 6, s), edir(3 * NI + 3, s);
   Scratch<int32_t> ef(2 * NI + 2, s), slot(3 * F + 3, s);
   res.state_bytes = sizeof(double) * (3 * F /*g*/ + 3 * F /*targets*/ + 15 * NI) + sizeof(int32_t) * (2 * NI + 3 * F);
-  double* part_dual = m->partials.p;
+  double* part_dual = m->partials.p;  // admm_loop's k_admm_stop reads both halves
   double* part_primal = m->partials.p + G;
-  double* sums = m->scalars.p + 8;  // [primal_sum, dual_sum]
-  double* pr = m->scalars.p + 10;   // [primal, dual]
   EventTimer timer(s);
   timer.start();
   GH_CUDA(cudaMemcpyAsync(d_g, d_h, sizeof(double) * 3 * F, cudaMemcpyDeviceToDevice, s));  // g = h
@@ -399,19 +477,12 @@ AdmmResult admm_face_dev(gh_mesh* m, const double* d_h, const gh_admm_config& cf
     GH_LAUNCH_CHECK();
     m->launches++;
   }
-  for (int it = 0; it < cfg.max_iterations; ++it) {
-    k_face_g<<<G, B, 0, s>>>(slot.p, m->face_area.p, d_h, Y.p, lam.p, F, mu, d_g, part_dual, term_d.p);
-    k_face_lambda_y<<<G, B, 0, s>>>(ef.p, m->face_area.p, d_g, edir.p, NI, mu, Y.p, lam.p, part_primal, term_p.p);
-    GH_LAUNCH_CHECK();
-    reduce_into(m, part_primal, sums);
-    reduce_into(m, part_dual, sums + 1);
-    k_sqrt_pair<<<1, 32, 0, s>>>(sums, mu, pr);
-    GH_LAUNCH_CHECK();
-    m->launches += 3;
-    GH_CUDA(cudaMemcpyAsync(m->pinned_scalars, pr, 2 * sizeof(double), cudaMemcpyDeviceToHost, s));
-    GH_CUDA(cudaStreamSynchronize(s));
-    if (stop_rule(m, res, it, cfg, scale, mu, term_p.p, NI, term_d.p, F)) break;  // grad_face.hpp:175-177
-  }
+  // grad_face.hpp:175-177
+  admm_loop(m, res, cfg, scale, mu, term_p.p, NI, term_d.p, F, [&](const int32_t* halt) {
+    k_face_g<<<G, B, 0, s>>>(slot.p, m->face_area.p, d_h, Y.p, lam.p, F, mu, d_g, part_dual, term_d.p, halt);
+    k_face_lambda_y<<<G, B, 0, s>>>(ef.p, m->face_area.p, d_g, edir.p, NI, mu, Y.p, lam.p, part_primal, term_p.p,
+                                    halt);
+  });
   timer.stop();
   res.device_ms = timer.ms();
   return res;
@@ -426,10 +497,8 @@ AdmmResult admm_edge_dev(gh_mesh* m, const double* d_h, const gh_admm_config& cf
   Scratch<double> w(3 * F + 3, s), lam(3 * F + 3, s), tsum(E + 1, s);
   Scratch<int8_t> sgn(3 * F + 3, s);
   res.state_bytes = sizeof(double) * (2 * E + 6 * F) + 3 * F;  // x, target_sum, w, lambda, sign
-  double* part_dual = m->partials.p;
+  double* part_dual = m->partials.p;  // admm_loop's k_admm_stop reads both halves
   double* part_primal = m->partials.p + G;
-  double* sums = m->scalars.p + 8;
-  double* pr = m->scalars.p + 10;
   const double scale = std::sqrt(3.0 * (double)F);  // ||R||_F (grad_edge.hpp:79)
   EventTimer timer(s);
   timer.start();
@@ -443,19 +512,11 @@ AdmmResult admm_edge_dev(gh_mesh* m, const double* d_h, const gh_admm_config& cf
     m->launches++;
   }
   Scratch<double> term_p(F + 1, s), term_d(E + 1, s);  // per-element residual terms
-  for (int it = 0; it < cfg.max_iterations; ++it) {
-    k_edge_x<<<G, B, 0, s>>>(m->edge_he.p, tsum.p, lam.p, w.p, E, mu, d_x, part_dual, term_d.p);
-    k_edge_lambda_w<<<G, B, 0, s>>>(m->he_edge.p, d_x, sgn.p, F, mu, w.p, lam.p, part_primal, term_p.p);
-    GH_LAUNCH_CHECK();
-    reduce_into(m, part_primal, sums);
-    reduce_into(m, part_dual, sums + 1);
-    k_sqrt_pair<<<1, 32, 0, s>>>(sums, mu, pr);
-    GH_LAUNCH_CHECK();
-    m->launches += 3;
-    GH_CUDA(cudaMemcpyAsync(m->pinned_scalars, pr, 2 * sizeof(double), cudaMemcpyDeviceToHost, s));
-    GH_CUDA(cudaStreamSynchronize(s));
-    if (stop_rule(m, res, it, cfg, scale, mu, term_p.p, F, term_d.p, E)) break;  // grad_edge.hpp:168-170
-  }
+  // grad_edge.hpp:168-170
+  admm_loop(m, res, cfg, scale, mu, term_p.p, F, term_d.p, E, [&](const int32_t* halt) {
+    k_edge_x<<<G, B, 0, s>>>(m->edge_he.p, tsum.p, lam.p, w.p, E, mu, d_x, part_dual, term_d.p, halt);
+    k_edge_lambda_w<<<G, B, 0, s>>>(m->he_edge.p, d_x, sgn.p, F, mu, w.p, lam.p, part_primal, term_p.p, halt);
+  });
   timer.stop();
   res.device_ms = timer.ms();
   return res;

@@ -22,7 +22,24 @@ for ptr, nb in ((pp, P.nbytes), (pf, F.nbytes), (pd, 8 * P.shape[0])):
 C.memmove(pp, P.ctypes.data, P.nbytes)
 C.memmove(pf, F.ctypes.data, F.nbytes)
 pcfg = G._pipeline_config(w.method, w.sweeps, w.t, w.m, G.AdmmConfig())
-for it in range(3):
+try:  # the default memory pool's reserved / used bytes (stream-ordered allocations)
+    _rt = C.CDLL("/usr/local/cuda/lib64/libcudart.so.12")
+except OSError:
+    _rt = None
+
+
+def pool_gb():
+    if _rt is None:
+        return ""
+    pool = C.c_void_p()
+    _rt.cudaDeviceGetDefaultMemPool(C.byref(pool), 0)
+    out = []
+    for attr in (5, 7):  # cudaMemPoolAttrReservedMemCurrent, cudaMemPoolAttrUsedMemCurrent
+        v = C.c_uint64()
+        _rt.cudaMemPoolGetAttribute(pool, attr, C.byref(v))
+        out.append(v.value / 1e9)
+    return f" pool reserved {out[0]:.2f} GB used {out[1]:.2f} GB"
+for it in range(int(sys.argv[2]) if len(sys.argv) > 2 else 3):
     t0 = time.perf_counter()
     m = C.c_void_p()
     G._check(L.gh_mesh_create(pp, P.shape[0], pf, F.shape[0], C.byref(m)))
@@ -45,4 +62,5 @@ for it in range(3):
     rr = G.gh_run_report()
     G._check(L.gh_distance_host(pp, P.shape[0], pf, F.shape[0], S.ctypes.data_as(C.c_void_p), S.size, C.byref(pcfg),
                                 pd, C.byref(rr)))
-    print(f"   distance_host {1e3*(time.perf_counter()-t0):.1f} ms (report total {rr.total_ms:.1f})", flush=True)
+    print(f"   distance_host {1e3*(time.perf_counter()-t0):.1f} ms (report total {rr.total_ms:.1f}, "
+          f"admm {rr.optimization_ms:.1f}){pool_gb()}", flush=True)
