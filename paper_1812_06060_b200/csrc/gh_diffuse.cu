@@ -193,8 +193,9 @@ __device__ __forceinline__ void publish_rows(const BandArgs* vba, int32_t band_l
   unsigned long long* lo_done = vba->lo_done;
   unsigned long long* hi_done = vba->hi_done;
   const bool to_lo = X == band_lb && lo_done, to_hi = X == band_le - 1 && hi_done;
-  if (to_lo || to_hi) __threadfence_system();
-  else __threadfence();
+  // release: acq_rel fences (not the sequentially consistent __threadfence)
+  if (to_lo || to_hi) asm volatile("fence.acq_rel.sys;" ::: "memory");
+  else asm volatile("fence.acq_rel.gpu;" ::: "memory");
   atomicAdd(vba->rows_done + X, n);
   if (to_lo) atomicAdd_system(lo_done + X, n);
   if (to_hi) atomicAdd_system(hi_done + X, n);
@@ -512,6 +513,9 @@ __global__ void __launch_bounds__(kTmaThreads, 2) k_diffuse_tma(const __grid_con
         if (hi > lo) publish_rows(vba, band_lb, band_le, X, (unsigned long long)(hi - lo));
       }
     }
+    // the block's own rows are published before any warp starts the next step:
+    // otherwise the first tile of the next step polls for them
+    asm volatile("bar.sync 1, %0;" ::"r"(32 * kConsumerWarps) : "memory");
   }
 }
 
