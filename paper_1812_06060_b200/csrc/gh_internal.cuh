@@ -324,10 +324,12 @@ __device__ __forceinline__ unsigned ld_acquire_u32(const unsigned* p) {
 __device__ __forceinline__ void grid_barrier(unsigned* counter, unsigned k) {
   __syncthreads();
   if (threadIdx.x == 0) {
-    __threadfence();
-    atomicAdd(counter, 1u);
+    // release arrival (cumulative over the block's writes ordered by the
+    // __syncthreads), acquire polling: no sequentially consistent fence
+    asm volatile("red.release.gpu.global.add.u32 [%0], 1;" ::"l"(counter) : "memory");
     const unsigned target = (k + 1) * gridDim.x;
-    while (ld_acquire_u32(counter) < target) __nanosleep(32);
+    while (ld_acquire_u32(counter) < target) {
+    }
   }
   __syncthreads();
 }
