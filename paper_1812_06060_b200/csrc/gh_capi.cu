@@ -92,23 +92,23 @@ void keep_pool_memory(int device) {
   done[device] = true;
 }
 
-// One non-blocking stream and a small pinned scratch per (host thread, device),
-// created on first use and kept for the life of the thread: creating and
-// destroying them per mesh cost up to hundreds of ms per end-to-end solve.
-void thread_context(int device, cudaStream_t* stream, double** pinned) {
+// Two non-blocking streams per (host thread, device) — the work stream and
+// one for uploads that overlap it — created on first use and kept for the
+// life of the thread: creating and destroying them per mesh cost up to
+// hundreds of ms per end-to-end solve.
+void thread_context(int device, cudaStream_t* stream, cudaStream_t* copy_stream) {
   struct Ctx {
-    cudaStream_t stream = nullptr;
-    double* pinned = nullptr;
+    cudaStream_t stream = nullptr, copy = nullptr;
   };
   thread_local Ctx ctx[64];
   if (device < 0 || device >= 64) gh::fail(GH_ERR_CUDA, "device ordinal out of range");
   Ctx& c = ctx[device];
   if (!c.stream) {
     GH_CUDA(cudaStreamCreateWithFlags(&c.stream, cudaStreamNonBlocking));
-    GH_CUDA(cudaMallocHost(&c.pinned, 8 * sizeof(double)));
+    GH_CUDA(cudaStreamCreateWithFlags(&c.copy, cudaStreamNonBlocking));
   }
   *stream = c.stream;
-  *pinned = c.pinned;
+  if (copy_stream) *copy_stream = c.copy;
 }
 
 int take_launches(gh_mesh* m) {
@@ -164,7 +164,7 @@ static std::unique_ptr<gh_mesh> new_mesh() {
   if (g_device >= 0) GH_CUDA(cudaSetDevice(g_device));
   GH_CUDA(cudaGetDevice(&m->device));
   keep_pool_memory(m->device);
-  thread_context(m->device, &m->stream, &m->pinned_scalars);
+  thread_context(m->device, &m->stream, &m->copy_stream);
   return m;
 }
 
@@ -862,8 +862,7 @@ gh_status gh_error_metrics(const double* d, const double* d_ref, int64_t n, cons
     int dev = 0;
     GH_CUDA(cudaGetDevice(&dev));
     cudaStream_t s;
-    double* pinned;
-    thread_context(dev, &s, &pinned);
+    thread_context(dev, &s, nullptr);
     gh::errors_dev(s, d, d_ref, n, sources, ns, mean_rel_error, excluded, e2);
   });
 }
@@ -881,8 +880,7 @@ gh_status gh_deterministic_sum(const double* terms, int64_t n, double* sum_out) 
     GH_CUDA(cudaGetDevice(&dev));
     keep_pool_memory(dev);
     cudaStream_t s;
-    double* pinned;
-    thread_context(dev, &s, &pinned);
+    thread_context(dev, &s, nullptr);
     gh::Scratch<double> x(n, s);
     if (n) GH_CUDA(cudaMemcpyAsync(x.p, terms, sizeof(double) * n, cudaMemcpyHostToDevice, s));
     *sum_out = gh::deterministic_sum_dev(x.p, n, s);

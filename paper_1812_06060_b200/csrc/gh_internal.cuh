@@ -94,6 +94,17 @@ struct Scratch {
   Scratch& operator=(const Scratch&) = delete;
 };
 
+struct Event {  // an ordering-only event
+  cudaEvent_t e = nullptr;
+  Event() { GH_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming)); }
+  ~Event() {
+    if (e) cudaEventDestroy(e);
+  }
+  Event(const Event&) = delete;
+  Event& operator=(const Event&) = delete;
+  void record(cudaStream_t s) { GH_CUDA(cudaEventRecord(e, s)); }
+};
+
 struct EventTimer {
   cudaEvent_t a = nullptr, b = nullptr;
   cudaStream_t s;
@@ -129,7 +140,7 @@ struct gh_mesh {
   gh::DevBuf<uint8_t> on_boundary;
   // reduction scratch: kReduceGrid partials + result slots
   gh::DevBuf<double> partials, scalars;
-  double* pinned_scalars = nullptr;  // host mirror for per-iteration stop checks
+  cudaStream_t copy_stream = nullptr;  // the thread's second stream: uploads overlapping kernels
   int launches = 0;                  // kernels launched since the counter was last read
   int level_refs = 0;                // live gh_levels built on this mesh
   bool destroy_pending = false;      // gh_mesh_destroy called while levels were alive

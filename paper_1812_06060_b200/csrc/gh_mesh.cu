@@ -90,6 +90,17 @@ __global__ void k_faces(const double* __restrict__ pos, const int32_t* __restric
   }
 }
 
+// the index part of the face checks (mesh.hpp:133-137): first face with a
+// vertex out of range or repeated; needs no positions
+__global__ void k_face_indices(const int32_t* __restrict__ faces, int64_t nf, int32_t nv,
+                               int32_t* __restrict__ err_face) {
+  for (int64_t f = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; f < nf; f += (int64_t)gridDim.x * blockDim.x) {
+    const int32_t a = faces[3 * f], b = faces[3 * f + 1], c = faces[3 * f + 2];
+    if (a < 0 || a >= nv || b < 0 || b >= nv || c < 0 || c >= nv || a == b || b == c || a == c)
+      atomicMin(err_face, (int32_t)f);
+  }
+}
+
 // halfedge keys: (vmin * nv + vmax, h) (mesh.hpp:147-158)
 __global__ void k_he_keys(const int32_t* __restrict__ faces, int64_t nh, uint64_t nv, uint64_t* __restrict__ key,
                           int32_t* __restrict__ val) {
@@ -474,51 +485,90 @@ void reduce_partials(gh_mesh* m, double* d_result_slot) {
   m->launches++;
 }
 
+// The upload is split so the face-only topology work (halfedge sort, edges,
+// interior edges, the corner and adjacency orderings) runs while the
+// positions are still crossing PCIe: faces first on the mesh stream,
+// positions behind them on the thread's copy stream. Errors keep the
+// reference's precedence: every face check (mesh.hpp:128-145) before any
+// edge check (170-183).
 void mesh_build(gh_mesh* m, const double* h_pos, const int32_t* h_faces) {
   cudaStream_t s = m->stream;
   const int64_t V = m->nv, F = m->nf, H = 3 * F;
   const uint64_t nvu = (uint64_t)(V > 0 ? V : 1);
   m->partials.alloc(kReduceGrid * 6, s);
   m->scalars.alloc(16, s);
+  Event pos_ready;  // positions on the device (recorded on the copy stream)
+  bool pos_pending = false;
   // h_pos == h_faces == nullptr: the loader already decoded the arrays into
   // m->pos / m->faces on the device.
   if (h_pos || h_faces || m->pos.n != (size_t)(3 * V) || m->faces.n != (size_t)(3 * F)) {
     m->pos.alloc(3 * V, s);
     m->faces.alloc(3 * F, s);
-    if (V) GH_CUDA(cudaMemcpyAsync(m->pos.p, h_pos, sizeof(double) * 3 * V, cudaMemcpyHostToDevice, s));
     if (F) GH_CUDA(cudaMemcpyAsync(m->faces.p, h_faces, sizeof(int32_t) * 3 * F, cudaMemcpyHostToDevice, s));
+    if (V) {
+      Event faces_done;
+      faces_done.record(s);  // also orders the pos allocation before the copy stream uses it
+      GH_CUDA(cudaStreamWaitEvent(m->copy_stream, faces_done.e, 0));
+      GH_CUDA(cudaMemcpyAsync(m->pos.p, h_pos, sizeof(double) * 3 * V, cudaMemcpyHostToDevice, m->copy_stream));
+      pos_ready.record(m->copy_stream);
+      pos_pending = true;
+    }
   }
-
-  // bbox -> degenerate threshold
-  const unsigned gb = grid_for(V, B, 512);
-  k_bbox_partial<<<gb, B, 0, s>>>(m->pos.p, V, m->partials.p);
-  k_bbox_final<<<1, 32, 0, s>>>(m->partials.p, (int)gb, V, m->scalars.p);
-  GH_LAUNCH_CHECK();
-
-  // faces
+  auto wait_pos = [&] {
+    if (pos_pending) GH_CUDA(cudaStreamWaitEvent(s, pos_ready.e, 0));
+    pos_pending = false;
+  };
+  // on an early exit, the buffers freed on the mesh stream must not be reused
+  // before the upload into them has landed
+  struct PosGuard {
+    cudaStream_t s;
+    cudaEvent_t e;
+    bool& pending;
+    ~PosGuard() {
+      if (pending) cudaStreamWaitEvent(s, e, 0);
+    }
+  } pos_guard{s, pos_ready.e, pos_pending};
   m->face_area.alloc(F, s);
   m->face_normal.alloc(3 * F, s);
-  Scratch<int32_t> err_face(1, s);
   const int32_t big = 0x7fffffff;
-  GH_CUDA(cudaMemcpyAsync(err_face.p, &big, sizeof(int32_t), cudaMemcpyHostToDevice, s));
-  if (F) {
-    k_faces<<<grid_for(F), B, 0, s>>>(m->pos.p, m->faces.p, F, m->nv, m->scalars.p, m->face_area.p,
-                                      m->face_normal.p, err_face.p);
+  Scratch<int32_t> err_face(1, s);
+  // the face checks in full (range, repeat, degenerate; first failing face
+  // wins), then fail with the reference's message
+  auto face_checks = [&] {
+    wait_pos();
+    const unsigned gb = grid_for(V, B, 512);
+    k_bbox_partial<<<gb, B, 0, s>>>(m->pos.p, V, m->partials.p);
+    k_bbox_final<<<1, 32, 0, s>>>(m->partials.p, (int)gb, V, m->scalars.p);
     GH_LAUNCH_CHECK();
+    GH_CUDA(cudaMemcpyAsync(err_face.p, &big, sizeof(int32_t), cudaMemcpyHostToDevice, s));
+    if (F) {
+      k_faces<<<grid_for(F), B, 0, s>>>(m->pos.p, m->faces.p, F, m->nv, m->scalars.p, m->face_area.p,
+                                        m->face_normal.p, err_face.p);
+      GH_LAUNCH_CHECK();
+    }
+    m->launches += 3;
+    const int32_t bad_face = read_scalar(err_face.p, s);
+    if (bad_face != big) {
+      int32_t t[3];
+      GH_CUDA(cudaMemcpyAsync(t, m->faces.p + 3 * (int64_t)bad_face, sizeof(t), cudaMemcpyDeviceToHost, s));
+      GH_CUDA(cudaStreamSynchronize(s));
+      DeviceCorners ctx{m->pos.p, s, {0, 0, 0}};
+      fail(GH_ERR_MESH, face_error(t, bad_face, m->nv, device_corner, &ctx));
+    }
+  };
+  // indices first: the topology kernels need them in range
+  if (F) {
+    GH_CUDA(cudaMemcpyAsync(err_face.p, &big, sizeof(int32_t), cudaMemcpyHostToDevice, s));
+    k_face_indices<<<grid_for(F), B, 0, s>>>(m->faces.p, F, m->nv, err_face.p);
+    GH_LAUNCH_CHECK();
+    m->launches++;
+    if (read_scalar(err_face.p, s) != big) face_checks();  // fails (an earlier degenerate face may win)
   }
-  const int32_t bad_face = read_scalar(err_face.p, s);
-  if (bad_face != big) {
-    int32_t t[3];
-    GH_CUDA(cudaMemcpyAsync(t, m->faces.p + 3 * (int64_t)bad_face, sizeof(t), cudaMemcpyDeviceToHost, s));
-    GH_CUDA(cudaStreamSynchronize(s));
-    DeviceCorners ctx{m->pos.p, s, {0, 0, 0}};
-    fail(GH_ERR_MESH, face_error(t, bad_face, m->nv, device_corner, &ctx));
-  }
-  m->launches += 3;
 
-  // edges: stable radix sort of halfedge keys
+  // edges: stable sort of halfedge keys
   const int end_bit = bits_for(nvu * nvu - 1 > 0 ? nvu * nvu - 1 : 1);
   int64_t E = 0;
+  std::string edge_error;  // reported after the face checks (reference order)
   m->he_twin.alloc(H, s);
   m->he_edge.alloc(H, s);
   GH_CUDA(cudaMemsetAsync(m->he_twin.p, 0xff, sizeof(int32_t) * H, s));
@@ -568,11 +618,15 @@ void mesh_build(gh_mesh* m, const double* h_pos, const int32_t* h_faces) {
         GH_CUDA(cudaMemcpyAsync(ev, m->edge_v.p + 2 * e, sizeof(ev), cudaMemcpyDeviceToHost, s));
         GH_CUDA(cudaStreamSynchronize(s));
         const std::string pair = "(" + std::to_string(ev[0]) + "," + std::to_string(ev[1]) + ")";
-        if (code == 1) fail(GH_ERR_MESH, "non-manifold edge " + pair + ": " + std::to_string(inc) + " incident faces");
-        fail(GH_ERR_MESH, "inconsistent winding across edge " + pair);
+        edge_error = code == 1 ? "non-manifold edge " + pair + ": " + std::to_string(inc) + " incident faces"
+                               : "inconsistent winding across edge " + pair;
       }
       m->launches += 4;
     }
+  }
+  if (!edge_error.empty()) {
+    face_checks();  // a face error anywhere takes precedence
+    fail(GH_ERR_MESH, edge_error);
   }
 
   // interior edges (mesh.hpp:194-201)
@@ -594,21 +648,9 @@ void mesh_build(gh_mesh* m, const double* h_pos, const int32_t* h_faces) {
     }
   }
 
-  // cotangents, weights, boundary flags
-  m->he_cot.alloc(H, s);
-  m->edge_weight.alloc(E, s);
-  m->on_boundary.alloc(V, s);
-  if (V) GH_CUDA(cudaMemsetAsync(m->on_boundary.p, 0, V, s));
-  if (F) k_cot<<<grid_for(F), B, 0, s>>>(m->pos.p, m->faces.p, F, m->he_cot.p);
-  if (E) k_edge_weight<<<grid_for(E), B, 0, s>>>(m->edge_he.p, m->edge_v.p, m->he_cot.p, E, m->edge_weight.p,
-                                                  m->on_boundary.p);
-  GH_LAUNCH_CHECK();
-  m->launches += 2;
-
-  // vertex -> corner CSR (mesh.hpp:272-283) and vertex areas (222-224)
+  // vertex -> corner CSR (mesh.hpp:272-283): faces only
   m->vc_offset.alloc(V + 1, s);
   m->vc_corner.alloc(H, s);
-  m->vertex_area.alloc(V, s);
   {
     Scratch<int32_t> cnt(V + 1, s);
     GH_CUDA(cudaMemsetAsync(cnt.p, 0, sizeof(int32_t) * (V + 1), s));
@@ -635,44 +677,67 @@ void mesh_build(gh_mesh* m, const double* h_pos, const int32_t* h_faces) {
           GH_CUDA(cudaMemcpyAsync(m->vc_corner.p, va, sizeof(int32_t) * H, cudaMemcpyDeviceToDevice, s));
       }
     }
-    if (V) k_vertex_area<<<grid_for(V), B, 0, s>>>(m->vc_offset.p, m->vc_corner.p, m->face_area.p, V, m->vertex_area.p);
-    GH_LAUNCH_CHECK();
-    m->launches += 3;
+    m->launches += 2;
   }
 
-  // vertex adjacency CSR, rows sorted by neighbour (mesh.hpp:234-266) + row sums (267-270)
+  // vertex adjacency ordering (mesh.hpp:234-266): rows sorted by neighbour
   m->vv_offset.alloc(V + 1, s);
   m->vv_index.alloc(2 * E, s);
   m->vv_edge.alloc(2 * E, s);
   m->vv_weight.alloc(2 * E, s);
   m->vertex_weight_sum.alloc(V, s);
+  Scratch<uint64_t> vk0(2 * E, s), vk1(2 * E, s);
+  Scratch<int32_t> vv0(2 * E, s), vv1(2 * E, s);
+  uint64_t* vka = vk0.p;
+  int32_t* vva = vv0.p;
   {
     Scratch<int32_t> degree(V + 1, s);
     GH_CUDA(cudaMemsetAsync(degree.p, 0, sizeof(int32_t) * (V + 1), s));
-    Scratch<uint64_t> k0(2 * E, s), k1(2 * E, s);
-    Scratch<int32_t> v0(2 * E, s), v1(2 * E, s);
-    uint64_t *ka = k0.p, *kb = k1.p;
-    int32_t *va = v0.p, *vb = v1.p;
+    uint64_t* kb = vk1.p;
+    int32_t* vb = vv1.p;
     if (E) {
-      k_vv_keys<<<grid_for(E), B, 0, s>>>(m->edge_v.p, E, nvu, ka, va, degree.p);
+      k_vv_keys<<<grid_for(E), B, 0, s>>>(m->edge_v.p, E, nvu, vka, vva, degree.p);
       GH_LAUNCH_CHECK();
-      if (bucket_sort_pairs(ka, va, 2 * E, nvu, V, kb, vb, s)) {
-        std::swap(ka, kb);
-        std::swap(va, vb);
+      if (bucket_sort_pairs(vka, vva, 2 * E, nvu, V, kb, vb, s)) {
+        std::swap(vka, kb);
+        std::swap(vva, vb);
       } else {
-        radix_sort_pairs(ka, kb, va, vb, 2 * E, end_bit, s);
+        radix_sort_pairs(vka, kb, vva, vb, 2 * E, end_bit, s);
       }
     }
     exclusive_scan(degree.p, m->vv_offset.p, V + 1, s);
-    if (E) {
-      k_vv_fill<<<grid_for(2 * E), B, 0, s>>>(ka, va, 2 * E, nvu, m->edge_weight.p, m->vv_index.p, m->vv_edge.p,
-                                               m->vv_weight.p);
-      GH_LAUNCH_CHECK();
-    }
-    if (V) k_row_sum<<<grid_for(V), B, 0, s>>>(m->vv_offset.p, m->vv_weight.p, V, m->vertex_weight_sum.p);
-    GH_LAUNCH_CHECK();
-    m->launches += 3;
+    m->launches += 2;
   }
+
+  // ---- geometry: needs the positions
+  face_checks();
+
+  // cotangents, weights, boundary flags
+  m->he_cot.alloc(H, s);
+  m->edge_weight.alloc(E, s);
+  m->on_boundary.alloc(V, s);
+  if (V) GH_CUDA(cudaMemsetAsync(m->on_boundary.p, 0, V, s));
+  if (F) k_cot<<<grid_for(F), B, 0, s>>>(m->pos.p, m->faces.p, F, m->he_cot.p);
+  if (E) k_edge_weight<<<grid_for(E), B, 0, s>>>(m->edge_he.p, m->edge_v.p, m->he_cot.p, E, m->edge_weight.p,
+                                                  m->on_boundary.p);
+  GH_LAUNCH_CHECK();
+  m->launches += 2;
+
+  // vertex areas (mesh.hpp:222-224)
+  m->vertex_area.alloc(V, s);
+  if (V) k_vertex_area<<<grid_for(V), B, 0, s>>>(m->vc_offset.p, m->vc_corner.p, m->face_area.p, V, m->vertex_area.p);
+  GH_LAUNCH_CHECK();
+  m->launches++;
+
+  // adjacency weights + row sums (mesh.hpp:259-270)
+  if (E) {
+    k_vv_fill<<<grid_for(2 * E), B, 0, s>>>(vka, vva, 2 * E, nvu, m->edge_weight.p, m->vv_index.p, m->vv_edge.p,
+                                             m->vv_weight.p);
+    GH_LAUNCH_CHECK();
+  }
+  if (V) k_row_sum<<<grid_for(V), B, 0, s>>>(m->vv_offset.p, m->vv_weight.p, V, m->vertex_weight_sum.p);
+  GH_LAUNCH_CHECK();
+  m->launches += 2;
 
   // boundary vertex count (for gh_mesh_info)
   if (V) {
