@@ -15,6 +15,7 @@
 // is reproducible run to run but not the reference's left-to-right sum; the
 // stop rule compares them against thresholds with the same formulas.
 
+#include <algorithm>
 #include <cmath>
 
 #include "gh_internal.cuh"
@@ -415,17 +416,21 @@ bool stop_rule(gh_mesh* m, AdmmResult& res, int it, const gh_admm_config& cfg, d
 template <class Iterate>
 void admm_loop(gh_mesh* m, AdmmResult& res, const gh_admm_config& cfg, double scale, double mu,
                const double* term_p, int64_t np, const double* term_d, int64_t nd, Iterate iterate) {
+  constexpr int32_t kBatch = 16;  // iterations enqueued per host check (no-ops after a halt)
   const int32_t imax = cfg.max_iterations;
   if (imax <= 0) return;
   cudaStream_t s = m->stream;
-  Scratch<double> hist(2 * (size_t)imax + 1, s);
+  Scratch<double> hist(2 * (size_t)imax + 1, s);  // [primal, dual] per iteration, then the halting iteration
   Scratch<int32_t> halt(1, s);
   std::vector<double> h(2 * (size_t)imax + 1);
   const double thr1 = scale * cfg.eps1, thr2 = scale * cfg.eps2;
   int32_t it0 = 0;
+  bool armed = false;
   while (it0 < imax) {
-    GH_CUDA(cudaMemsetAsync(halt.p, 0, sizeof(int32_t), s));
-    for (int32_t it = it0; it < imax; ++it) {
+    if (!armed) GH_CUDA(cudaMemsetAsync(halt.p, 0, sizeof(int32_t), s));
+    armed = true;
+    const int32_t end = std::min(imax, it0 + kBatch);
+    for (int32_t it = it0; it < end; ++it) {
       iterate(halt.p);
       k_admm_stop<<<1, 1024, 0, s>>>(m->partials.p + G, m->partials.p, mu, thr1, thr2, guard(np), guard(nd), it,
                                      hist.p, hist.p + 2 * (size_t)imax, halt.p);
@@ -433,16 +438,28 @@ void admm_loop(gh_mesh* m, AdmmResult& res, const gh_admm_config& cfg, double sc
       m->launches += 3;
     }
     int32_t state = 0;
-    GH_CUDA(cudaMemcpyAsync(h.data(), hist.p, sizeof(double) * h.size(), cudaMemcpyDeviceToHost, s));
+    GH_CUDA(cudaMemcpyAsync(h.data() + 2 * (size_t)it0, hist.p + 2 * (size_t)it0, sizeof(double) * 2 * (end - it0),
+                            cudaMemcpyDeviceToHost, s));
+    GH_CUDA(cudaMemcpyAsync(h.data() + 2 * (size_t)imax, hist.p + 2 * (size_t)imax, sizeof(double),
+                            cudaMemcpyDeviceToHost, s));
     GH_CUDA(cudaMemcpyAsync(&state, halt.p, sizeof(int32_t), cudaMemcpyDeviceToHost, s));
     GH_CUDA(cudaStreamSynchronize(s));
+    if (!state && end < imax) {  // the whole batch cleared both guard bands without meeting the rule
+      for (int32_t it = it0; it < end; ++it) {
+        res.primal.push_back(h[2 * it]);
+        res.dual.push_back(h[2 * it + 1]);
+      }
+      it0 = end;
+      continue;
+    }
     const int32_t last = state ? (int32_t)h[2 * (size_t)imax] : imax - 1;  // iteration that halted (or the final one)
-    for (int32_t it = it0; it < last; ++it) {  // cleared both thresholds' guard bands, not met
+    for (int32_t it = it0; it < last; ++it) {
       res.primal.push_back(h[2 * it]);
       res.dual.push_back(h[2 * it + 1]);
     }
     if (stop_rule(m, res, last, cfg, scale, mu, h[2 * last], h[2 * last + 1], term_p, np, term_d, nd)) return;
     it0 = last + 1;
+    armed = false;  // the guard-band halt is cleared before resuming
   }
 }
 

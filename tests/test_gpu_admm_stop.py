@@ -49,14 +49,15 @@ def test_stop_rule_cases(gpu, torus, method):
     assert rep.iterations == 12 and not rep.converged
     rep = _run(gpu, torus, method, 12, 1e30, 1e30)
     assert rep.iterations == 1 and rep.converged
-    # thresholds between two iterations' residuals: stops in the middle
-    full = _run(gpu, torus, method, 30, 1e-30, 1e-30)
+    # thresholds between two iterations' residuals: stops in the middle, in
+    # the first batch of enqueued iterations or a later one (16 per batch)
+    full = _run(gpu, torus, method, 60, 1e-30, 1e-30)
     scale = torus["face_scale" if method == "face" else "edge_scale"]
-    k = 6
-    eps1 = max(full.primal_history[:k + 1]) / scale * (1 + 1e-6)
-    eps2 = max(full.dual_history[:k + 1]) / scale * (1 + 1e-6)
-    rep = _run(gpu, torus, method, 30, eps1, eps2)
-    assert rep.converged and rep.iterations <= k + 1
+    for k in (6, 20, 40):
+        eps1 = full.primal_history[k] / scale * (1 + 1e-6)  # iteration k meets both
+        eps2 = full.dual_history[k] / scale * (1 + 1e-6)
+        rep = _run(gpu, torus, method, 60, eps1, eps2)
+        assert rep.converged and rep.iterations <= k + 1
 
 
 @pytest.mark.parametrize("method", ["face", "edge"])
