@@ -82,7 +82,7 @@ typedef struct {
   int32_t level_count;       /* BfsLevels::level_count()        */
   int32_t unreachable_count; /* BfsLevels::unreachable_count    */
   int32_t max_level_width;   /* widest ring                     */
-  int32_t reserved;
+  int32_t column_bits;       /* columns the last gs_diffuse streamed: 16 or 32 (0 before the first) */
 } gh_levels_info;
 
 /* AdmmConfig (grad_face.hpp:15-26). */

@@ -21,7 +21,7 @@ class gh_mesh_info(C.Structure):
 
 class gh_levels_info(C.Structure):
     _fields_ = [("level_count", C.c_int32), ("unreachable_count", C.c_int32), ("max_level_width", C.c_int32),
-                ("reserved", C.c_int32)]
+                ("column_bits", C.c_int32)]
 
 
 class gh_admm_config(C.Structure):

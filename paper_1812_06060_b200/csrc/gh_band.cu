@@ -16,6 +16,7 @@
 #include <cub/device/device_scan.cuh>
 
 #include <algorithm>
+#include <cstdlib>
 
 #include "gh_internal.cuh"
 
@@ -91,6 +92,57 @@ __global__ void k_sell_fill(const int32_t* __restrict__ perm, const int32_t* __r
   }
 }
 
+// 16-bit columns of one chunk per warp: the entries of a chunk point into two
+// windows, its own level (same parity half) and levels L-1, L+1 (the other
+// half, adjacent there); each window gets a 64-aligned uidx base and the
+// entries keep the low 15 bits of their offset (parity bit included). A chunk
+// whose window spans reach span_limit keeps only its 32-bit columns.
+__global__ void k_col16(const int32_t* __restrict__ chunk_level, const int32_t* __restrict__ pstart,
+                        const int32_t* __restrict__ pend, const int64_t* __restrict__ chunk_ptr,
+                        const uint16_t* __restrict__ deg, const int32_t* __restrict__ deg_big,
+                        const uint32_t* __restrict__ col, int64_t nchunks, uint32_t span_limit,
+                        uint16_t* __restrict__ col16, int2* __restrict__ cbase,
+                        unsigned long long* __restrict__ nwide) {
+  const int lane = threadIdx.x & 31;
+  const int64_t warp = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+  const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  for (int64_t c = warp; c < nchunks; c += nwarps) {
+    const int32_t L = chunk_level[c];
+    const uint32_t lo = (uint32_t)pstart[L], hi = (uint32_t)pend[L];
+    const int64_t p0 = chunk_ptr[c], w = (chunk_ptr[c + 1] - p0) / 32;
+    int64_t d = deg[c * 32 + lane];
+    if (d == 65535 && deg_big) d = deg_big[c * 32 + lane];
+    uint32_t mn[2] = {0xffffffffu, 0xffffffffu}, mx[2] = {0u, 0u};
+    for (int64_t k = 0; k < d; ++k) {
+      const uint32_t u = col[p0 + 32 * k + lane];
+      const uint32_t row = (u >> 6) << 5 | (u & 31u);
+      const int o = row >= lo && row < hi ? 0 : 1;
+      mn[o] = min(mn[o], u);
+      mx[o] = max(mx[o], u);
+    }
+    for (int o = 0; o < 2; ++o)
+      for (int x = 16; x > 0; x >>= 1) {
+        mn[o] = min(mn[o], __shfl_xor_sync(0xffffffffu, mn[o], x));
+        mx[o] = max(mx[o], __shfl_xor_sync(0xffffffffu, mx[o], x));
+      }
+    const uint32_t b0 = mn[0] == 0xffffffffu ? 0u : mn[0] & ~63u, b1 = mn[1] == 0xffffffffu ? 0u : mn[1] & ~63u;
+    const bool fits = (mn[0] == 0xffffffffu || mx[0] - b0 < span_limit) && (mn[1] == 0xffffffffu || mx[1] - b1 < span_limit);
+    for (int64_t k = 0; k < w; ++k) {
+      uint16_t e = 0;
+      if (fits && k < d) {
+        const uint32_t u = col[p0 + 32 * k + lane];
+        const uint32_t row = (u >> 6) << 5 | (u & 31u);
+        e = row >= lo && row < hi ? (uint16_t)(u - b0) : (uint16_t)(0x8000u | (u - b1));
+      }
+      col16[p0 + 32 * k + lane] = e;
+    }
+    if (lane == 0) {
+      cbase[c] = fits ? make_int2((int32_t)b0, (int32_t)b1) : make_int2(-1, -1);
+      if (!fits) atomicAdd(nwide, 1ull);
+    }
+  }
+}
+
 template <class T>
 T read_scalar(const T* d, cudaStream_t s) {
   T v;
@@ -115,7 +167,7 @@ Band::~Band() {
 uint64_t Band::device_bytes() const {
   return pstart.bytes() + pend.bytes() + perm.bytes() + chunk_level.bytes() + chunk_ptr.bytes() + deg.bytes() +
          deg_big.bytes() +
-         col.bytes() + wt.bytes() + area_r.bytes() + wsum_r.bytes() + den.bytes() + 2 * sizeof(double) * nrows +
+         col.bytes() + col16.bytes() + cbase.bytes() + wt.bytes() + area_r.bytes() + wsum_r.bytes() + den.bytes() + 2 * sizeof(double) * nrows +
          sizeof(unsigned long long) * nlev;
 }
 
@@ -237,6 +289,21 @@ void band_build(gh_levels* L, Band* b, int32_t lb, int32_t le) {
                                                     b->chunk_ptr.p, b->own_rows, b->col.p, b->wt.p, b->area_r.p,
                                                     b->wsum_r.p);
   GH_LAUNCH_CHECK();
+  b->col16.alloc(nnz, s);
+  b->cbase.alloc(b->own_chunks, s);
+  b->wide_chunks = 0;
+  if (b->own_chunks) {
+    // GH_COL16_SPAN (tests only) lowers the 15-bit window limit to force the 32-bit fallback
+    const char* env = getenv("GH_COL16_SPAN");
+    const uint32_t span = env ? (uint32_t)std::max(1, std::min(32768, atoi(env))) : 32768u;
+    Scratch<unsigned long long> nwide(1, s);
+    GH_CUDA(cudaMemsetAsync(nwide.p, 0, sizeof(unsigned long long), s));
+    k_col16<<<grid_for((int64_t)b->own_chunks * 32), B, 0, s>>>(b->chunk_level.p, b->pstart.p, b->pend.p,
+                                                                b->chunk_ptr.p, b->deg.p, b->deg_big.p, b->col.p,
+                                                                b->own_chunks, span, b->col16.p, b->cbase.p, nwide.p);
+    GH_LAUNCH_CHECK();
+    b->wide_chunks = (int64_t)read_scalar(nwide.p, s);
+  }
   b->den.alloc(b->nrows, s);
   b->den_t = 0.0;
   if (!b->ubuf) {
@@ -249,7 +316,7 @@ void band_build(gh_levels* L, Band* b, int32_t lb, int32_t le) {
       else GH_CUDA(cudaMallocAsync(ptrs[i], sizes[i], s));
     }
   }
-  m->launches += 4;
+  m->launches += 5;
   GH_CUDA(cudaStreamSynchronize(s));
 }
 

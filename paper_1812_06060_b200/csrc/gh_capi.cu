@@ -460,7 +460,7 @@ gh_status gh_bfs_get_info(const gh_levels* levels, gh_levels_info* info) {
     info->level_count = levels->nlev;
     info->unreachable_count = levels->unreachable;
     info->max_level_width = levels->max_width;
-    info->reserved = 0;
+    info->column_bits = levels->last_col16 ? 16 : levels->u_valid ? 32 : 0;
   });
 }
 

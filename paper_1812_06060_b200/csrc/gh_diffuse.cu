@@ -30,6 +30,7 @@
 //    steps and all blocks are co-resident, so the schedule cannot deadlock.
 
 #include <algorithm>
+#include <cstdlib>
 
 #include "gh_internal.cuh"
 
@@ -86,6 +87,8 @@ struct BandArgs {
   const uint16_t* deg;
   const int32_t* deg_big;         // true row lengths where deg holds 65535 (else null)
   const uint32_t* col;            // gh::uidx(neighbour row, 1 unless one level closer to the sources)
+  const uint16_t* col16;          // the same columns in 16 bits against per-chunk bases (gh::Band::col16)
+  const int2* cbase;
   const double* wt;
   const double* den;
   double* ubuf;                   // both sweep parities, gh::uidx layout
@@ -201,9 +204,11 @@ __device__ __forceinline__ void publish_rows(const BandArgs* vba, int32_t band_l
   if (to_hi) atomicAdd_system(hi_done + X, n);
 }
 
-// slot layout: header 256 B (int32: chunk offsets [0..kTileChunks], fits [31], chunk levels [32..])
+// slot layout: header 512 B (int32: chunk offsets [0..kTileChunks], fits [31], chunk levels [32..],
+//              16-bit column bases [64 + 2q], [65 + 2q])
 //              | den kTileChunks x 256 B | deg kTileChunks x 64 B | columns | weights
-constexpr int kHdr = 256;
+constexpr int kHdr = 512;
+constexpr int kBaseHdr = 64;
 constexpr int kDenOff = kHdr;
 constexpr int kDegOff = kDenOff + kTileChunks * 256;
 constexpr int kColOff = kDegOff + kTileChunks * 64;
@@ -212,7 +217,9 @@ constexpr int kColOff = kDegOff + kTileChunks * 64;
 // icosphere and torus meshes and saves the registers of two more gathers).
 // kTable: the pstart/pend tables are copied into shared memory (separate
 // instances so every shared-memory access compiles to LDS, not a generic load).
-template <int kUnroll, bool kTable>
+// kCol16: columns are streamed as 16-bit offsets (gh::Band::col16), 12 B less
+// per row; chunks without 16-bit columns take the global-memory path.
+template <int kUnroll, bool kTable, bool kCol16>
 __global__ void __launch_bounds__(kTmaThreads, 2) k_diffuse_tma(const __grid_constant__ TmaArgs a) {
   extern __shared__ __align__(128) unsigned char smem[];
   // this block's band and its rank inside the band
@@ -255,6 +262,7 @@ __global__ void __launch_bounds__(kTmaThreads, 2) k_diffuse_tma(const __grid_con
 
   const int32_t nsteps = (band_le - 1) + 2 * (a.sweeps - 1) + 1;
   const uint32_t col_cap = (uint32_t)kTileChunks * 32u * a.wcap;  // entries
+  constexpr uint32_t kColBytes = kCol16 ? 2u : 4u;
   // ring position: slot index and its use parity advance tile by tile
   int slot = 0;
   uint32_t use = 0;
@@ -280,23 +288,26 @@ __global__ void __launch_bounds__(kTmaThreads, 2) k_diffuse_tma(const __grid_con
       }
       return true;
     };
-    auto load = [&](int32_t xcb, int32_t xce, int32_t xt0, int64_t& p0, int32_t& lv0, int64_t& plast) {
+    auto load = [&](int32_t xcb, int32_t xce, int32_t xt0, int64_t& p0, int32_t& lv0, int64_t& plast, int2& cb0) {
       const int32_t cbase = xcb + xt0 * kTileChunks;
       const int32_t cl = cbase + lane < xce ? cbase + lane : xce;
       p0 = __ldg(vba->chunk_ptr + cl);
       lv0 = cbase + lane < xce ? __ldg(vba->chunk_level + cl) : 0;
+      if (kCol16) cb0 = cbase + lane < xce ? __ldg(vba->cbase + cl) : make_int2(-1, -1);
       plast = __ldg(vba->chunk_ptr + (cbase + 32 < xce ? cbase + 32 : xce));
     };
     int64_t p0 = 0, p_last = 0;
     int32_t lv0 = 0;
+    int2 cb0 = make_int2(-1, -1);
     bool have = advance(tau, cb, ce, ntile, t0);
-    if (have) load(cb, ce, t0, p0, lv0, p_last);
+    if (have) load(cb, ce, t0, p0, lv0, p_last, cb0);
     while (have) {
       int32_t ntau = tau, ncb = cb, nce = ce, nnt = ntile, nt0 = t0;
       int64_t np0 = 0, np_last = 0;
       int32_t nlv0 = 0;
+      int2 ncb0 = make_int2(-1, -1);
       const bool have_next = advance(ntau, ncb, nce, nnt, nt0);
-      if (have_next) load(ncb, nce, nt0, np0, nlv0, np_last);
+      if (have_next) load(ncb, nce, nt0, np0, nlv0, np_last, ncb0);
       const int32_t cbase = cb + t0 * kTileChunks;
       for (int j = 0; j < kTilesPerBatch && t0 + j < ntile; ++j) {
         if (issued >= a.nslots) mbar_wait(empty + slot, use ^ 1u);
@@ -311,6 +322,14 @@ __global__ void __launch_bounds__(kTmaThreads, 2) k_diffuse_tma(const __grid_con
         int32_t* hdr = reinterpret_cast<int32_t*>(slots + (size_t)slot * a.slot_bytes);
         if (lane <= nch) hdr[lane] = (int32_t)(pi - base);
         if (lane < kTileChunks) hdr[32 + lane] = li;
+        if (kCol16) {
+          const int qs = (off + (lane & (kTileChunks - 1))) & 31;
+          const int32_t bx = __shfl_sync(0xffffffffu, cb0.x, qs), by = __shfl_sync(0xffffffffu, cb0.y, qs);
+          if (lane < kTileChunks) {
+            hdr[kBaseHdr + 2 * lane] = bx;
+            hdr[kBaseHdr + 2 * lane + 1] = by;
+          }
+        }
         const int64_t pend_tile = __shfl_sync(0xffffffffu, pi, nch);
         const uint32_t ncol = (uint32_t)(pend_tile - base);
         const bool fits = ncol <= col_cap;
@@ -318,14 +337,15 @@ __global__ void __launch_bounds__(kTmaThreads, 2) k_diffuse_tma(const __grid_con
         __syncwarp();
         if (lane == 0) {
           unsigned char* sb = reinterpret_cast<unsigned char*>(hdr);
-          const uint32_t bytes = (uint32_t)nch * (256u + 64u) + (fits ? ncol * 12u : 0u);
+          const uint32_t bytes = (uint32_t)nch * (256u + 64u) + (fits ? ncol * (kColBytes + 8u) : 0u);
           mbar_expect_tx(full + slot, bytes);
           const uint64_t pol = l2_evict_first_policy();
           bulk_g2s(sb + kDenOff, vba->den + (int64_t)c0 * 32, (uint32_t)nch * 256u, full + slot, pol);
           bulk_g2s(sb + kDegOff, vba->deg + (int64_t)c0 * 32, (uint32_t)nch * 64u, full + slot, pol);
           if (fits && ncol) {
-            bulk_g2s(sb + kColOff, vba->col + base, ncol * 4u, full + slot, pol);
-            bulk_g2s(sb + kColOff + col_cap * 4u, vba->wt + base, ncol * 8u, full + slot, pol);
+            if (kCol16) bulk_g2s(sb + kColOff, vba->col16 + base, ncol * 2u, full + slot, pol);
+            else bulk_g2s(sb + kColOff, vba->col + base, ncol * 4u, full + slot, pol);
+            bulk_g2s(sb + kColOff + col_cap * kColBytes, vba->wt + base, ncol * 8u, full + slot, pol);
           }
         }
         __syncwarp();
@@ -336,7 +356,7 @@ __global__ void __launch_bounds__(kTmaThreads, 2) k_diffuse_tma(const __grid_con
         }
       }
       tau = ntau, cb = ncb, ce = nce, ntile = nnt, t0 = nt0;
-      p0 = np0, p_last = np_last, lv0 = nlv0;
+      p0 = np0, p_last = np_last, lv0 = nlv0, cb0 = ncb0;
       have = have_next;
     }
     return;
@@ -416,6 +436,8 @@ __global__ void __launch_bounds__(kTmaThreads, 2) k_diffuse_tma(const __grid_con
       bool on[kChunksPerWarp], fast[kChunksPerWarp];
       uint32_t px[kChunksPerWarp];  // sweep parity of the step, as the uidx xor mask
       double* const ub = vba->ubuf;
+      const double* ubs[kChunksPerWarp];  // 16-bit columns: u at the chunk's same-level base
+      int32_t dlt[kChunksPerWarp];        // other-half base - same-level base - 0x8000
 #pragma unroll
       for (int i = 0; i < kChunksPerWarp; ++i) {
         const int q = warp + kConsumerWarps * i;
@@ -426,16 +448,34 @@ __global__ void __launch_bounds__(kTmaThreads, 2) k_diffuse_tma(const __grid_con
         den[i] = reinterpret_cast<const double*>(sb + kDenOff)[q * 32 + lane];
         d[i] = on[i] ? reinterpret_cast<const uint16_t*>(sb + kDegOff)[q * 32 + lane] : 0;
         fast[i] = fits && d[i] <= kUnroll;  // 65535 (valence past 16 bits) always takes the slow path
+        if (kCol16) {
+          const int32_t bs = hdr[kBaseHdr + 2 * q], bo = hdr[kBaseHdr + 2 * q + 1];
+          fast[i] = fast[i] && bs >= 0;
+          ubs[i] = ub + bs;
+          dlt[i] = bo - bs - 0x8000;
+        }
         num[i] = 0.0;
       }
       // all gathers of both chunks in flight together; u gathers are L1-cached
       // (see the dependency check above)
 #pragma unroll
       for (int i = 0; i < kChunksPerWarp; ++i) {
-        const uint32_t* scol = reinterpret_cast<const uint32_t*>(sb + kColOff) + hdr[warp + kConsumerWarps * i] + lane;
+        if (kCol16) {
+          // e ^ px keeps bit 15; the same-level base is 64-aligned, so the parity
+          // xor commutes with adding it: u index = base(e >> 15) + (e & 0x7fff) ^ px
+          const uint16_t* scol = reinterpret_cast<const uint16_t*>(sb + kColOff) + hdr[warp + kConsumerWarps * i] + lane;
 #pragma unroll
-        for (int k = 0; k < kUnroll; ++k)
-          if (fast[i] && k < d[i]) v[i][k] = __ldca(ub + (scol[32 * k] ^ px[i]));
+          for (int k = 0; k < kUnroll; ++k)
+            if (fast[i] && k < d[i]) {
+              const int32_t e = (int32_t)((uint32_t)scol[32 * k] ^ px[i]);
+              v[i][k] = __ldca(ubs[i] + ((e >> 15) * dlt[i] + e));
+            }
+        } else {
+          const uint32_t* scol = reinterpret_cast<const uint32_t*>(sb + kColOff) + hdr[warp + kConsumerWarps * i] + lane;
+#pragma unroll
+          for (int k = 0; k < kUnroll; ++k)
+            if (fast[i] && k < d[i]) v[i][k] = __ldca(ub + (scol[32 * k] ^ px[i]));
+        }
       }
       // row sums, each left to right (diffusion.hpp:79). The branch keeps the
       // scheduler from pulling products above the later gathers; the common
@@ -443,7 +483,7 @@ __global__ void __launch_bounds__(kTmaThreads, 2) k_diffuse_tma(const __grid_con
       const double* swt[kChunksPerWarp];
 #pragma unroll
       for (int i = 0; i < kChunksPerWarp; ++i)
-        swt[i] = reinterpret_cast<const double*>(sb + kColOff + (size_t)col_cap * 4u) +
+        swt[i] = reinterpret_cast<const double*>(sb + kColOff + (size_t)col_cap * kColBytes) +
                  hdr[warp + kConsumerWarps * i] + lane;
       if (fast[0] && fast[kChunksPerWarp - 1]) {
 #pragma unroll
@@ -556,6 +596,8 @@ BandArgs band_args(const Band& b) {
   x.deg = b.deg.p;
   x.deg_big = b.deg_big.p;
   x.col = b.col.p;
+  x.col16 = b.col16.p;
+  x.cbase = b.cbase.p;
   x.wt = b.wt.p;
   x.den = b.den.p;
   x.ubuf = b.ubuf;
@@ -601,14 +643,23 @@ double bands_launch(gh_levels* L, std::vector<Band*>& bands, double t, int32_t s
   gh_mesh* m = L->mesh;
   cudaStream_t s = m->stream;
   int32_t wmax = 1;
-  int64_t rows = 0;
+  int64_t rows = 0, chunks = 0, wide = 0;
+  bool have16 = true;
   for (Band* b : bands) {
     wmax = std::max(wmax, b->max_chunk_width);
     rows += b->own_rows;
+    chunks += b->own_chunks;
+    wide += b->wide_chunks;
+    have16 = have16 && (b->col16.p || !b->own_chunks);
   }
-  // slot = 256 B header + per chunk (den 256 B + deg 64 B + wcap x 32 x 12 B of columns/weights)
+  // 16-bit columns unless more than 1/64 of the chunks would fall back to the
+  // global-memory path (GH_DIFFUSE_COL32 forces 32-bit columns, for tests)
+  // (GH_DIFFUSE_COL16 forces them, so tests can mix in fallback chunks)
+  const bool col16 =
+      have16 && !getenv("GH_DIFFUSE_COL32") && (wide * 64 <= chunks || getenv("GH_DIFFUSE_COL16"));
+  // slot = 512 B header + per chunk (den 256 B + deg 64 B + wcap x 32 x (2 or 4 + 8) B of columns/weights)
   const int32_t wcap = std::min<int32_t>(wmax, 16);
-  const int32_t slot_bytes = ((kColOff + kTileChunks * 32 * wcap * 12) + 127) & ~127;
+  const int32_t slot_bytes = ((kColOff + kTileChunks * 32 * wcap * (col16 ? 10 : 12)) + 127) & ~127;
   const bool table = L->nlev <= kMaxSmemLevels;
   const size_t table_bytes = table ? ((2 * sizeof(int32_t) * L->nlev + 127) & ~size_t(127)) : 0;
   // two blocks per SM with a ring of >= 2 slots each (228 KB per SM, 1 KB reserved per block)
@@ -619,8 +670,14 @@ double bands_launch(gh_levels* L, std::vector<Band*>& bands, double t, int32_t s
   }
   if (nslots < 2) nslots = 2;
   const size_t shmem = 16 * (size_t)nslots + table_bytes + 128 + (size_t)nslots * slot_bytes;
-  void* fn = wmax <= 6 ? (table ? (void*)k_diffuse_tma<6, true> : (void*)k_diffuse_tma<6, false>)
-                       : (table ? (void*)k_diffuse_tma<8, true> : (void*)k_diffuse_tma<8, false>);
+  void* fn;
+  if (col16)
+    fn = wmax <= 6 ? (table ? (void*)k_diffuse_tma<6, true, true> : (void*)k_diffuse_tma<6, false, true>)
+                   : (table ? (void*)k_diffuse_tma<8, true, true> : (void*)k_diffuse_tma<8, false, true>);
+  else
+    fn = wmax <= 6 ? (table ? (void*)k_diffuse_tma<6, true, false> : (void*)k_diffuse_tma<6, false, false>)
+                   : (table ? (void*)k_diffuse_tma<8, true, false> : (void*)k_diffuse_tma<8, false, false>);
+  L->last_col16 = col16 ? 1 : 0;
   GH_CUDA(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)shmem));
   int nsm = 0, per_sm = 0;
   GH_CUDA(cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, m->device));

@@ -171,6 +171,13 @@ struct Band {
   DevBuf<int32_t> deg_big;      // full row lengths, only when some valence >= 65535
   DevBuf<uint32_t> col;         // uidx(local row of the neighbour, 0 if one level closer to the sources else 1)
   DevBuf<double> wt;            // cotan weights in the reference's row order
+  // 16-bit copy of col: bit 15 = the neighbour is one level
+  // away (the other parity half), bits 0-14 = its uidx minus the chunk's base
+  // for that half. cbase per own chunk: (same-level base, other-half base), or
+  // x = -1 where the chunk's neighbours span more than 15 bits (kept 32-bit).
+  DevBuf<uint16_t> col16;
+  DevBuf<int2> cbase;
+  int64_t wide_chunks = 0;  // own chunks with cbase.x == -1
   DevBuf<double> area_r, wsum_r, den;
   double den_t = 0.0;
   // state shared with neighbour bands: plain cudaMalloc when it is IPC-exported
@@ -207,6 +214,7 @@ struct gh_levels {
   gh::Band main;                                       // the whole level range
   int32_t u_valid = 0;
   int32_t u_sweeps = 0;
+  int32_t last_col16 = 0;  // the last diffusion launch streamed 16-bit columns
   gh::DevBuf<double> u_orig;  // last diffusion result, original order [V]
   uint64_t device_bytes() const;
 };

@@ -337,6 +337,13 @@ class BfsLevels:
         self.max_level_width = info.max_level_width
         self._cache = None
 
+    @property
+    def column_bits(self) -> int:
+        """Column width (16 or 32) the last diffusion on these levels streamed; 0 before one ran."""
+        info = gh_levels_info()
+        _check(self._lib.gh_bfs_get_info(self._h, C.byref(info)))
+        return info.column_bits
+
     def __del__(self):
         h = getattr(self, "_h", None)
         if h and not _SHUTTING_DOWN[0]:

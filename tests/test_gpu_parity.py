@@ -326,3 +326,41 @@ def test_high_valence_hub_bitwise(gpu, port_oracle, n, source):
         assert_same(d, ref[key], f"fan {n} {method} distances")
     if len(lv.offsets) - 1 >= 2:
         assert_same(bands.gs_diffuse_bands(mesh, lv, 2, ref["t"], 60), ref["u"], "fan with 2 bands")
+
+
+@pytest.mark.parametrize("mode", ["col16", "col32", "col16_mixed"])
+def test_diffusion_column_formats_bitwise(gpu, port_oracle, monkeypatch, mode):
+    """The diffusion kernel streams 16-bit column offsets against per-chunk
+    bases (chunks whose neighbour windows do not fit keep 32-bit columns and
+    take the global-memory path); both formats, and a mix forced by a tiny
+    window limit, give u bit-identical to the reference on every fixture and on
+    reduced configs 2-5, single band and 3 bands."""
+    from paper_1812_06060_b200 import bands, meshgen
+    gh = gpu
+    if mode == "col32":
+        monkeypatch.setenv("GH_DIFFUSE_COL32", "1")
+    if mode == "col16_mixed":
+        monkeypatch.setenv("GH_COL16_SPAN", "96")
+        monkeypatch.setenv("GH_DIFFUSE_COL16", "1")
+    want_bits = 32 if mode == "col32" else 16
+    for case in CASES:
+        g = np.load(os.path.join(GOLDEN, case + ".npz"))
+        if int(g["sweeps"]) == 0:
+            continue
+        mesh = gh.build_mesh(g["positions"], g["faces"])
+        lv = gh.bfs_levels(mesh, g["sources"])
+        u = gh.gs_diffuse(mesh, lv, float(g["t"]), gh.DiffusionConfig(sweeps=int(g["sweeps"])))
+        assert_same(u, g["u"], f"{case} ({mode})")
+        if lv.unreachable_count < mesh.vertex_count():
+            assert lv.column_bits == want_bits, case
+    for config, scale, sweeps in ((2, 8, 300), (3, 16, 300), (4, 64, 200), (5, 128, 100)):
+        w = meshgen.config(config, scale=scale)
+        om = port_oracle.build_mesh(w.positions, w.faces)
+        ol = om.bfs(w.sources)
+        t = om.diffusion_time(1.0) if w.t is None else w.t
+        ref, _ = om.gs_diffuse(ol, t, sweeps)
+        mesh = gh.build_mesh(w.positions, w.faces)
+        lv = gh.bfs_levels(mesh, w.sources)
+        assert_same(gh.gs_diffuse(mesh, lv, t, gh.DiffusionConfig(sweeps=sweeps)), ref, f"C{config} ({mode})")
+        assert lv.column_bits == want_bits
+        assert_same(bands.gs_diffuse_bands(mesh, lv, 3, t, sweeps), ref, f"C{config} 3 bands ({mode})")
