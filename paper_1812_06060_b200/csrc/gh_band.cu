@@ -101,7 +101,7 @@ __global__ void k_col16(const int32_t* __restrict__ chunk_level, const int32_t* 
                         const int32_t* __restrict__ pend, const int64_t* __restrict__ chunk_ptr,
                         const uint16_t* __restrict__ deg, const int32_t* __restrict__ deg_big,
                         const uint32_t* __restrict__ col, int64_t nchunks, uint32_t span_limit,
-                        uint16_t* __restrict__ col16, int2* __restrict__ cbase,
+                        uint16_t* __restrict__ col16, int2* __restrict__ cbase, uint8_t* __restrict__ deg4,
                         unsigned long long* __restrict__ nwide) {
   const int lane = threadIdx.x & 31;
   const int64_t warp = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
@@ -112,6 +112,10 @@ __global__ void k_col16(const int32_t* __restrict__ chunk_level, const int32_t* 
     const int64_t p0 = chunk_ptr[c], w = (chunk_ptr[c + 1] - p0) / 32;
     int64_t d = deg[c * 32 + lane];
     if (d == 65535 && deg_big) d = deg_big[c * 32 + lane];
+    // row lengths as nibbles, lane pairs to one byte (15: the kernel reads deg)
+    const uint32_t nib = (uint32_t)(d < 15 ? d : 15);
+    const uint32_t hi_nib = __shfl_down_sync(0xffffffffu, nib, 1);
+    if ((lane & 1) == 0) deg4[c * 16 + (lane >> 1)] = (uint8_t)(nib | hi_nib << 4);
     uint32_t mn[2] = {0xffffffffu, 0xffffffffu}, mx[2] = {0u, 0u};
     for (int64_t k = 0; k < d; ++k) {
       const uint32_t u = col[p0 + 32 * k + lane];
@@ -167,7 +171,7 @@ Band::~Band() {
 uint64_t Band::device_bytes() const {
   return pstart.bytes() + pend.bytes() + perm.bytes() + chunk_level.bytes() + chunk_ptr.bytes() + deg.bytes() +
          deg_big.bytes() +
-         col.bytes() + col16.bytes() + cbase.bytes() + wt.bytes() + area_r.bytes() + wsum_r.bytes() + den.bytes() + 2 * sizeof(double) * nrows +
+         col.bytes() + col16.bytes() + cbase.bytes() + deg4.bytes() + wt.bytes() + area_r.bytes() + wsum_r.bytes() + den.bytes() + 2 * sizeof(double) * nrows +
          sizeof(unsigned long long) * nlev;
 }
 
@@ -291,6 +295,7 @@ void band_build(gh_levels* L, Band* b, int32_t lb, int32_t le) {
   GH_LAUNCH_CHECK();
   b->col16.alloc(nnz, s);
   b->cbase.alloc(b->own_chunks, s);
+  b->deg4.alloc((size_t)b->own_chunks * 16, s);
   b->wide_chunks = 0;
   if (b->own_chunks) {
     // GH_COL16_SPAN (tests only) lowers the 15-bit window limit to force the 32-bit fallback
@@ -300,7 +305,8 @@ void band_build(gh_levels* L, Band* b, int32_t lb, int32_t le) {
     GH_CUDA(cudaMemsetAsync(nwide.p, 0, sizeof(unsigned long long), s));
     k_col16<<<grid_for((int64_t)b->own_chunks * 32), B, 0, s>>>(b->chunk_level.p, b->pstart.p, b->pend.p,
                                                                 b->chunk_ptr.p, b->deg.p, b->deg_big.p, b->col.p,
-                                                                b->own_chunks, span, b->col16.p, b->cbase.p, nwide.p);
+                                                                b->own_chunks, span, b->col16.p, b->cbase.p, b->deg4.p,
+                                                                nwide.p);
     GH_LAUNCH_CHECK();
     b->wide_chunks = (int64_t)read_scalar(nwide.p, s);
   }

@@ -86,6 +86,7 @@ struct BandArgs {
   const int64_t* chunk_ptr;
   const uint16_t* deg;
   const int32_t* deg_big;         // true row lengths where deg holds 65535 (else null)
+  const uint8_t* deg4;            // row lengths as nibbles, 16 B per chunk (15: look in deg)
   const uint32_t* col;            // gh::uidx(neighbour row, 1 unless one level closer to the sources)
   const uint16_t* col16;          // the same columns in 16 bits against per-chunk bases (gh::Band::col16)
   const int2* cbase;
@@ -337,11 +338,12 @@ __global__ void __launch_bounds__(kTmaThreads, 2) k_diffuse_tma(const __grid_con
         __syncwarp();
         if (lane == 0) {
           unsigned char* sb = reinterpret_cast<unsigned char*>(hdr);
-          const uint32_t bytes = (uint32_t)nch * (256u + 64u) + (fits ? ncol * (kColBytes + 8u) : 0u);
+          const uint32_t bytes = (uint32_t)nch * (256u + (kCol16 ? 16u : 64u)) + (fits ? ncol * (kColBytes + 8u) : 0u);
           mbar_expect_tx(full + slot, bytes);
           const uint64_t pol = l2_evict_first_policy();
           bulk_g2s(sb + kDenOff, vba->den + (int64_t)c0 * 32, (uint32_t)nch * 256u, full + slot, pol);
-          bulk_g2s(sb + kDegOff, vba->deg + (int64_t)c0 * 32, (uint32_t)nch * 64u, full + slot, pol);
+          if (kCol16) bulk_g2s(sb + kDegOff, vba->deg4 + (int64_t)c0 * 16, (uint32_t)nch * 16u, full + slot, pol);
+          else bulk_g2s(sb + kDegOff, vba->deg + (int64_t)c0 * 32, (uint32_t)nch * 64u, full + slot, pol);
           if (fits && ncol) {
             if (kCol16) bulk_g2s(sb + kColOff, vba->col16 + base, ncol * 2u, full + slot, pol);
             else bulk_g2s(sb + kColOff, vba->col + base, ncol * 4u, full + slot, pol);
@@ -446,7 +448,12 @@ __global__ void __launch_bounds__(kTmaThreads, 2) k_diffuse_tma(const __grid_con
         on[i] = live[i] && r < pend[Lq[i]];
         px[i] = (uint32_t)((tau - Lq[i]) >> 1 & 1) << 5;
         den[i] = reinterpret_cast<const double*>(sb + kDenOff)[q * 32 + lane];
-        d[i] = on[i] ? reinterpret_cast<const uint16_t*>(sb + kDegOff)[q * 32 + lane] : 0;
+        if (kCol16) {  // nibbles; 15 (a valence of 15 or more) takes the slow path, which reads deg
+          const uint32_t nb = reinterpret_cast<const uint8_t*>(sb + kDegOff)[q * 16 + (lane >> 1)];
+          d[i] = on[i] ? (int32_t)((nb >> ((lane & 1) << 2)) & 15u) : 0;
+        } else {
+          d[i] = on[i] ? reinterpret_cast<const uint16_t*>(sb + kDegOff)[q * 32 + lane] : 0;
+        }
         fast[i] = fits && d[i] <= kUnroll;  // 65535 (valence past 16 bits) always takes the slow path
         if (kCol16) {
           const int32_t bs = hdr[kBaseHdr + 2 * q], bo = hdr[kBaseHdr + 2 * q + 1];
@@ -508,7 +515,9 @@ __global__ void __launch_bounds__(kTmaThreads, 2) k_diffuse_tma(const __grid_con
           const int64_t q0 = __ldg(vba->chunk_ptr + c) + lane;
           // (a global load here, not above: a load in the fast path would share a
           // scoreboard with the gathers and serialise the two chunks)
-          const int32_t dd = d[i] == 65535 && vba->deg_big ? vba->deg_big[c * 32 + lane] : d[i];
+          int32_t dd = d[i];
+          if (kCol16) dd = vba->deg[c * 32 + lane];
+          if (dd == 65535 && vba->deg_big) dd = vba->deg_big[c * 32 + lane];
           for (int32_t k = 0; k < dd; ++k) {
             const uint32_t cc = __ldg(vba->col + q0 + 32 * (int64_t)k);
             const double w = __ldg(vba->wt + q0 + 32 * (int64_t)k);
@@ -595,6 +604,7 @@ BandArgs band_args(const Band& b) {
   x.chunk_ptr = b.chunk_ptr.p;
   x.deg = b.deg.p;
   x.deg_big = b.deg_big.p;
+  x.deg4 = b.deg4.p;
   x.col = b.col.p;
   x.col16 = b.col16.p;
   x.cbase = b.cbase.p;

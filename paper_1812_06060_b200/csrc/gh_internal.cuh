@@ -177,6 +177,7 @@ struct Band {
   // x = -1 where the chunk's neighbours span more than 15 bits (kept 32-bit).
   DevBuf<uint16_t> col16;
   DevBuf<int2> cbase;
+  DevBuf<uint8_t> deg4;  // row lengths as nibbles (min(deg, 15)), 16 B per own chunk
   int64_t wide_chunks = 0;  // own chunks with cbase.x == -1
   DevBuf<double> area_r, wsum_r, den;
   double den_t = 0.0;
