@@ -94,48 +94,61 @@ __global__ void k_face_init_edges(const double* __restrict__ pos, const int32_t*
 }
 
 // Y-update for interior edge i (grad_face.hpp:126-137 + y_update_edge 31-36)
-__device__ __forceinline__ void face_y_update(int64_t i, int32_t f1, int32_t f2, double a1, double a2, double mu,
-                                              const double* __restrict__ g, const double* __restrict__ edir,
-                                              const v3 l1, const v3 l2, double* __restrict__ Y) {
-  const v3 q1 = sub(ld3(g, f1), divs(l1, mu * sqrt(a1)));
-  const v3 q2 = sub(ld3(g, f2), divs(l2, mu * sqrt(a2)));
+// from the two side faces' g and lambda; d = lambda / (mu sqrt(A)) per side is
+// returned too (the G-update adds the same quotient, grad_face.hpp:150).
+__device__ __forceinline__ void face_y_update(int64_t i, v3 g1, v3 g2, double a1, double a2, double mu,
+                                              const double* __restrict__ edir, v3 l1, v3 l2, v3& y1, v3& y2, v3& d1,
+                                              v3& d2) {
+  d1 = divs(l1, mu * sqrt(a1));
+  d2 = divs(l2, mu * sqrt(a2));
+  const v3 q1 = sub(g1, d1);
+  const v3 q2 = sub(g2, d2);
   const v3 ed = ld3(edir, i);
   const double mismatch = dot(ed, sub(q2, q1));
   const v3 shift = mk(ed.x * mismatch, ed.y * mismatch, ed.z * mismatch);
-  st3(Y, 2 * i, add(q1, scale(ddiv(a2, a1 + a2), shift)));
-  st3(Y, 2 * i + 1, sub(q2, scale(ddiv(a1, a1 + a2), shift)));
+  y1 = add(q1, scale(ddiv(a2, a1 + a2), shift));
+  y2 = sub(q2, scale(ddiv(a1, a1 + a2), shift));
 }
 
-__global__ void k_face_first_y(const int32_t* __restrict__ ef, const double* __restrict__ area,
+// The face kernel needs, per slot (interior edge i, side), only
+// c = y + lambda / (mu sqrt(A_side)) (grad_face.hpp:150): the edge kernel writes
+// c instead of Y, and recomputes Y from the previous g (kept in a second
+// buffer) and lambda when it needs it. 48 B per face less to read, no Y
+// round trip; every value is the reference's expression, so bits are unchanged.
+__global__ void k_face_first_c(const int32_t* __restrict__ ef, const double* __restrict__ area,
                                const double* __restrict__ g, const double* __restrict__ edir,
-                               const double* __restrict__ lam, int64_t ni, double mu, double* __restrict__ Y) {
+                               const double* __restrict__ lam, int64_t ni, double mu, double* __restrict__ C) {
   GRID_STRIDE(i, ni) {
     const int32_t f1 = ef[2 * i], f2 = ef[2 * i + 1];
-    face_y_update(i, f1, f2, area[f1], area[f2], mu, g, edir, ld3(lam, 2 * i), ld3(lam, 2 * i + 1), Y);
+    v3 y1, y2, d1, d2;
+    face_y_update(i, ld3(g, f1), ld3(g, f2), area[f1], area[f2], mu, edir, ld3(lam, 2 * i), ld3(lam, 2 * i + 1), y1,
+                  y2, d1, d2);
+    st3(C, 2 * i, add(y1, d1));
+    st3(C, 2 * i + 1, add(y2, d2));
   }
 }
 
-// G-update per face (grad_face.hpp:139-155) + dual partials (170-171, 104-111)
+// G-update per face (grad_face.hpp:139-155) + dual partials (170-171, 104-111):
+// g_out = (2h + mu sum_k c_k) / (2 + mu count), dual term from g_out - g_in
 __global__ void k_face_g(const int32_t* __restrict__ slot, const double* __restrict__ area,
-                         const double* __restrict__ h, const double* __restrict__ Y, const double* __restrict__ lam,
-                         int64_t nf, double mu, double* __restrict__ g, double* __restrict__ part,
+                         const double* __restrict__ h, const double* __restrict__ C, int64_t nf, double mu,
+                         const double* __restrict__ gin, double* __restrict__ gout, double* __restrict__ part,
                          double* __restrict__ term, const int32_t* __restrict__ halt) {
   if (*halt) return;  // the device stop rule ended the loop (see admm_loop)
   double s = 0.0;
   GRID_STRIDE(f, nf) {
     const double A = area[f];
-    const double alpha = sqrt(A);
     v3 sum = mk(0.0, 0.0, 0.0);
     int count = 0;
     for (int k = 0; k < 3; ++k) {
       const int32_t sl = slot[3 * f + k];
       if (sl < 0) continue;
-      sum = add(sum, add(ld3(Y, sl), divs(ld3(lam, sl), mu * alpha)));
+      sum = add(sum, ld3(C, sl));
       ++count;
     }
-    const v3 gold = ld3(g, f);
+    const v3 gold = ld3(gin, f);
     const v3 gnew = divs(add(scale(2.0, ld3(h, f)), scale(mu, sum)), 2.0 + mu * (double)count);
-    st3(g, f, gnew);
+    st3(gout, f, gnew);
     const v3 dg = sub(gnew, gold);
     const double tt = (double)count * A * sqnorm(dg);
     term[f] = tt;
@@ -145,19 +158,25 @@ __global__ void k_face_g(const int32_t* __restrict__ slot, const double* __restr
   if (threadIdx.x == 0) part[blockIdx.x] = s;
 }
 
-// lambda-update + primal rows per interior edge (grad_face.hpp:158-168), then
-// the next iteration's Y-update from the same registers.
-__global__ void k_face_lambda_y(const int32_t* __restrict__ ef, const double* __restrict__ area,
-                                const double* __restrict__ g, const double* __restrict__ edir, int64_t ni, double mu,
-                                double* __restrict__ Y, double* __restrict__ lam, double* __restrict__ part,
-                                double* __restrict__ term, const int32_t* __restrict__ halt) {
+// lambda-update + primal rows per interior edge (grad_face.hpp:158-168) with
+// this iteration's Y recomputed from g_in (the previous g) and the old lambda,
+// then the next iteration's Y and c from the same registers.
+__global__ void __launch_bounds__(B, 4) k_face_lambda_c(const int32_t* __restrict__ ef, const double* __restrict__ area,
+                                const double* __restrict__ gin, const double* __restrict__ gout,
+                                const double* __restrict__ edir, int64_t ni, double mu, double* __restrict__ C,
+                                double* __restrict__ lam, double* __restrict__ part, double* __restrict__ term,
+                                const int32_t* __restrict__ halt) {
   if (*halt) return;
   double s = 0.0;
   GRID_STRIDE(i, ni) {
     const int32_t f1 = ef[2 * i], f2 = ef[2 * i + 1];
     const double a1 = area[f1], a2 = area[f2];
-    const v3 r1 = scale(sqrt(a1), sub(ld3(Y, 2 * i), ld3(g, f1)));
-    const v3 r2 = scale(sqrt(a2), sub(ld3(Y, 2 * i + 1), ld3(g, f2)));
+    v3 y1, y2, d1, d2;
+    face_y_update(i, ld3(gin, f1), ld3(gin, f2), a1, a2, mu, edir, ld3(lam, 2 * i), ld3(lam, 2 * i + 1), y1, y2, d1,
+                  d2);
+    const v3 g1 = ld3(gout, f1), g2 = ld3(gout, f2);
+    const v3 r1 = scale(sqrt(a1), sub(y1, g1));
+    const v3 r2 = scale(sqrt(a2), sub(y2, g2));
     const v3 l1 = add(ld3(lam, 2 * i), scale(mu, r1));
     const v3 l2 = add(ld3(lam, 2 * i + 1), scale(mu, r2));
     st3(lam, 2 * i, l1);
@@ -165,7 +184,9 @@ __global__ void k_face_lambda_y(const int32_t* __restrict__ ef, const double* __
     const double tt = sqnorm(r1) + sqnorm(r2);
     term[i] = tt;
     s += tt;
-    face_y_update(i, f1, f2, a1, a2, mu, g, edir, l1, l2, Y);
+    face_y_update(i, g1, g2, a1, a2, mu, edir, l1, l2, y1, y2, d1, d2);
+    st3(C, 2 * i, add(y1, d1));
+    st3(C, 2 * i + 1, add(y2, d2));
   }
   s = block_sum<B>(s);
   if (threadIdx.x == 0) part[blockIdx.x] = s;
@@ -431,7 +452,7 @@ void admm_loop(gh_mesh* m, AdmmResult& res, const gh_admm_config& cfg, double sc
     armed = true;
     const int32_t end = std::min(imax, it0 + kBatch);
     for (int32_t it = it0; it < end; ++it) {
-      iterate(halt.p);
+      iterate(it, halt.p);
       k_admm_stop<<<1, 1024, 0, s>>>(m->partials.p + G, m->partials.p, mu, thr1, thr2, guard(np), guard(nd), it,
                                      hist.p, hist.p + 2 * (size_t)imax, halt.p);
       GH_LAUNCH_CHECK();
@@ -471,14 +492,18 @@ AdmmResult admm_face_dev(gh_mesh* m, const double* d_h, const gh_admm_config& cf
   const int64_t F = m->nf, NI = m->ni;
   const double mu = cfg.mu;
   AdmmResult res;
-  Scratch<double> Y(6 * NI + 6, s), lam(6 * NI + 6, s), edir(3 * NI + 3, s);
+  Scratch<double> Cs(6 * NI + 6, s), lam(6 * NI + 6, s), edir(3 * NI + 3, s), gtmp(3 * F + 3, s);
   Scratch<int32_t> ef(2 * NI + 2, s), slot(3 * F + 3, s);
   res.state_bytes = sizeof(double) * (3 * F /*g*/ + 3 * F /*targets*/ + 15 * NI) + sizeof(int32_t) * (2 * NI + 3 * F);
   double* part_dual = m->partials.p;  // admm_loop's k_admm_stop reads both halves
   double* part_primal = m->partials.p + G;
   EventTimer timer(s);
   timer.start();
+  // g ping-pongs between d_g and gtmp: iteration it reads gbuf[(it + 1) & 1] and
+  // writes gbuf[it & 1]; g = h starts in gbuf[1] (and in d_g for 0 iterations)
+  double* gbuf[2] = {d_g, gtmp.p};
   GH_CUDA(cudaMemcpyAsync(d_g, d_h, sizeof(double) * 3 * F, cudaMemcpyDeviceToDevice, s));  // g = h
+  GH_CUDA(cudaMemcpyAsync(gtmp.p, d_h, sizeof(double) * 3 * F, cudaMemcpyDeviceToDevice, s));
   if (F) k_face_slots<<<G, B, 0, s>>>(m->he_edge.p, m->interior_edge_index.p, m->edge_he.p, F, slot.p);
   Scratch<double> term_p(NI + 1, s), term_d(F + 1, s);  // per-element residual terms
   k_face_init_edges<<<G, B, 0, s>>>(m->pos.p, m->interior_edges.p, m->edge_v.p, m->edge_he.p, m->face_area.p, NI,
@@ -490,16 +515,21 @@ AdmmResult admm_face_dev(gh_mesh* m, const double* d_h, const gh_admm_config& cf
   if (cfg.max_iterations > 0 && NI) {
     // y1, y2 start at H of the side faces (grad_face.hpp:82-83) == Y-update from
     // g = h, lambda = 0 of iteration 0 (computed here exactly like later ones)
-    k_face_first_y<<<G, B, 0, s>>>(ef.p, m->face_area.p, d_g, edir.p, lam.p, NI, mu, Y.p);
+    k_face_first_c<<<G, B, 0, s>>>(ef.p, m->face_area.p, d_g, edir.p, lam.p, NI, mu, Cs.p);
     GH_LAUNCH_CHECK();
     m->launches++;
   }
   // grad_face.hpp:175-177
-  admm_loop(m, res, cfg, scale, mu, term_p.p, NI, term_d.p, F, [&](const int32_t* halt) {
-    k_face_g<<<G, B, 0, s>>>(slot.p, m->face_area.p, d_h, Y.p, lam.p, F, mu, d_g, part_dual, term_d.p, halt);
-    k_face_lambda_y<<<G, B, 0, s>>>(ef.p, m->face_area.p, d_g, edir.p, NI, mu, Y.p, lam.p, part_primal, term_p.p,
-                                    halt);
+  admm_loop(m, res, cfg, scale, mu, term_p.p, NI, term_d.p, F, [&](int32_t it, const int32_t* halt) {
+    const double* gin = gbuf[(it + 1) & 1];
+    double* gout = gbuf[it & 1];
+    k_face_g<<<G, B, 0, s>>>(slot.p, m->face_area.p, d_h, Cs.p, F, mu, gin, gout, part_dual, term_d.p, halt);
+    k_face_lambda_c<<<G, B, 0, s>>>(ef.p, m->face_area.p, gin, gout, edir.p, NI, mu, Cs.p, lam.p, part_primal,
+                                    term_p.p, halt);
   });
+  // the last iteration's g: odd iterations wrote gtmp
+  if (res.iterations > 0 && ((res.iterations - 1) & 1))
+    GH_CUDA(cudaMemcpyAsync(d_g, gtmp.p, sizeof(double) * 3 * F, cudaMemcpyDeviceToDevice, s));
   timer.stop();
   res.device_ms = timer.ms();
   return res;
@@ -530,7 +560,7 @@ AdmmResult admm_edge_dev(gh_mesh* m, const double* d_h, const gh_admm_config& cf
   }
   Scratch<double> term_p(F + 1, s), term_d(E + 1, s);  // per-element residual terms
   // grad_edge.hpp:168-170
-  admm_loop(m, res, cfg, scale, mu, term_p.p, F, term_d.p, E, [&](const int32_t* halt) {
+  admm_loop(m, res, cfg, scale, mu, term_p.p, F, term_d.p, E, [&](int32_t, const int32_t* halt) {
     k_edge_x<<<G, B, 0, s>>>(m->edge_he.p, tsum.p, lam.p, w.p, E, mu, d_x, part_dual, term_d.p, halt);
     k_edge_lambda_w<<<G, B, 0, s>>>(m->he_edge.p, d_x, sgn.p, F, mu, w.p, lam.p, part_primal, term_p.p, halt);
   });
