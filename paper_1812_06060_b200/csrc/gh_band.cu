@@ -92,23 +92,27 @@ __global__ void k_sell_fill(const int32_t* __restrict__ perm, const int32_t* __r
   }
 }
 
-// 16-bit columns of one chunk per warp: the entries of a chunk point into two
-// windows, its own level (same parity half) and levels L-1, L+1 (the other
-// half, adjacent there); each window gets a 64-aligned uidx base and the
-// entries keep the low 15 bits of their offset (parity bit included). A chunk
-// whose window spans reach span_limit keeps only its 32-bit columns.
+// 16-bit columns of one chunk per warp (format: gh::Band::col16). With 2
+// windows the entries point into the chunk's own level (same parity half) or
+// levels L-1, L+1 (adjacent in the other half); with 3 windows into L, L-1 and
+// L+1 separately (for rings so wide that L-1 and L+1 are far apart in the
+// other half). Each window gets a 64-aligned uidx base; an entry keeps its
+// offset (parity bit included) below the window bits. A chunk whose window
+// spans reach the limit keeps only its 32-bit columns.
 __global__ void k_col16(const int32_t* __restrict__ chunk_level, const int32_t* __restrict__ pstart,
                         const int32_t* __restrict__ pend, const int64_t* __restrict__ chunk_ptr,
                         const uint16_t* __restrict__ deg, const int32_t* __restrict__ deg_big,
-                        const uint32_t* __restrict__ col, int64_t nchunks, uint32_t span_limit,
-                        uint16_t* __restrict__ col16, int2* __restrict__ cbase, uint8_t* __restrict__ deg4,
+                        const uint32_t* __restrict__ col, int64_t nchunks, int windows, uint32_t span_limit,
+                        uint16_t* __restrict__ col16, int4* __restrict__ cbase, uint8_t* __restrict__ deg4,
                         unsigned long long* __restrict__ nwide) {
   const int lane = threadIdx.x & 31;
   const int64_t warp = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
   const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  const uint32_t limit = min(span_limit, windows == 2 ? 32768u : 16384u);
   for (int64_t c = warp; c < nchunks; c += nwarps) {
     const int32_t L = chunk_level[c];
     const uint32_t lo = (uint32_t)pstart[L], hi = (uint32_t)pend[L];
+    const uint32_t lo1 = L > 0 ? (uint32_t)pstart[L - 1] : 0u, hi1 = L > 0 ? (uint32_t)pend[L - 1] : 0u;
     const int64_t p0 = chunk_ptr[c], w = (chunk_ptr[c + 1] - p0) / 32;
     int64_t d = deg[c * 32 + lane];
     if (d == 65535 && deg_big) d = deg_big[c * 32 + lane];
@@ -116,33 +120,50 @@ __global__ void k_col16(const int32_t* __restrict__ chunk_level, const int32_t* 
     const uint32_t nib = (uint32_t)(d < 15 ? d : 15);
     const uint32_t hi_nib = __shfl_down_sync(0xffffffffu, nib, 1);
     if ((lane & 1) == 0) deg4[c * 16 + (lane >> 1)] = (uint8_t)(nib | hi_nib << 4);
-    uint32_t mn[2] = {0xffffffffu, 0xffffffffu}, mx[2] = {0u, 0u};
+    // window of a neighbour: 0 = level L; else 1 (2 windows: the other half;
+    // 3 windows: level L-1) or 2 (level L+1)
+    auto window = [&](uint32_t u) -> int {
+      const uint32_t row = (u >> 6) << 5 | (u & 31u);
+      if (row >= lo && row < hi) return 0;
+      if (windows == 2) return 1;
+      return row >= lo1 && row < hi1 ? 1 : 2;
+    };
+    uint32_t mn[3] = {0xffffffffu, 0xffffffffu, 0xffffffffu}, mx[3] = {0u, 0u, 0u};
     for (int64_t k = 0; k < d; ++k) {
       const uint32_t u = col[p0 + 32 * k + lane];
-      const uint32_t row = (u >> 6) << 5 | (u & 31u);
-      const int o = row >= lo && row < hi ? 0 : 1;
+      const int o = window(u);
       mn[o] = min(mn[o], u);
       mx[o] = max(mx[o], u);
     }
-    for (int o = 0; o < 2; ++o)
+    bool fits = true;
+    uint32_t base[3];
+    for (int o = 0; o < 3; ++o) {
       for (int x = 16; x > 0; x >>= 1) {
         mn[o] = min(mn[o], __shfl_xor_sync(0xffffffffu, mn[o], x));
         mx[o] = max(mx[o], __shfl_xor_sync(0xffffffffu, mx[o], x));
       }
-    const uint32_t b0 = mn[0] == 0xffffffffu ? 0u : mn[0] & ~63u, b1 = mn[1] == 0xffffffffu ? 0u : mn[1] & ~63u;
-    const bool fits = (mn[0] == 0xffffffffu || mx[0] - b0 < span_limit) && (mn[1] == 0xffffffffu || mx[1] - b1 < span_limit);
+      base[o] = mn[o] == 0xffffffffu ? 0u : mn[o] & ~63u;
+      fits = fits && (mn[o] == 0xffffffffu || mx[o] - base[o] < limit);
+    }
+    const int shift = windows == 2 ? 15 : 14;
     for (int64_t k = 0; k < w; ++k) {
       uint16_t e = 0;
       if (fits && k < d) {
         const uint32_t u = col[p0 + 32 * k + lane];
-        const uint32_t row = (u >> 6) << 5 | (u & 31u);
-        e = row >= lo && row < hi ? (uint16_t)(u - b0) : (uint16_t)(0x8000u | (u - b1));
+        const int o = window(u);
+        e = (uint16_t)((uint32_t)o << shift | (u - base[o]));
       }
       col16[p0 + 32 * k + lane] = e;
     }
     if (lane == 0) {
-      cbase[c] = fits ? make_int2((int32_t)b0, (int32_t)b1) : make_int2(-1, -1);
-      if (!fits) atomicAdd(nwide, 1ull);
+      if (!fits) {
+        cbase[c] = make_int4(-1, 0, 0, 0);
+        atomicAdd(nwide, 1ull);
+      } else if (windows == 2) {
+        cbase[c] = make_int4((int32_t)base[0], (int32_t)base[1], 0, 0);
+      } else {
+        cbase[c] = make_int4((int32_t)base[0], (int32_t)base[1] - (1 << 14), (int32_t)base[2] - (2 << 14), 0);
+      }
     }
   }
 }
@@ -297,18 +318,30 @@ void band_build(gh_levels* L, Band* b, int32_t lb, int32_t le) {
   b->cbase.alloc(b->own_chunks, s);
   b->deg4.alloc((size_t)b->own_chunks * 16, s);
   b->wide_chunks = 0;
+  b->col16_windows = 0;
   if (b->own_chunks) {
-    // GH_COL16_SPAN (tests only) lowers the 15-bit window limit to force the 32-bit fallback
+    // 2 windows if at most 1/64 of the chunks fall back to 32 bits, else 3,
+    // else none. Tests: GH_COL16_WINDOWS=2|3 forces a format, GH_COL16_SPAN
+    // lowers the window limit (forcing fallback chunks).
     const char* env = getenv("GH_COL16_SPAN");
     const uint32_t span = env ? (uint32_t)std::max(1, std::min(32768, atoi(env))) : 32768u;
+    const char* force = getenv("GH_COL16_WINDOWS");
+    const int forced = force ? atoi(force) : 0;
     Scratch<unsigned long long> nwide(1, s);
-    GH_CUDA(cudaMemsetAsync(nwide.p, 0, sizeof(unsigned long long), s));
-    k_col16<<<grid_for((int64_t)b->own_chunks * 32), B, 0, s>>>(b->chunk_level.p, b->pstart.p, b->pend.p,
-                                                                b->chunk_ptr.p, b->deg.p, b->deg_big.p, b->col.p,
-                                                                b->own_chunks, span, b->col16.p, b->cbase.p, b->deg4.p,
-                                                                nwide.p);
-    GH_LAUNCH_CHECK();
-    b->wide_chunks = (int64_t)read_scalar(nwide.p, s);
+    for (int windows : {2, 3}) {
+      if (forced && windows != forced) continue;
+      GH_CUDA(cudaMemsetAsync(nwide.p, 0, sizeof(unsigned long long), s));
+      k_col16<<<grid_for((int64_t)b->own_chunks * 32), B, 0, s>>>(
+          b->chunk_level.p, b->pstart.p, b->pend.p, b->chunk_ptr.p, b->deg.p, b->deg_big.p, b->col.p, b->own_chunks,
+          windows, span, b->col16.p, b->cbase.p, b->deg4.p, nwide.p);
+      GH_LAUNCH_CHECK();
+      m->launches++;
+      b->wide_chunks = (int64_t)read_scalar(nwide.p, s);
+      if (forced || b->wide_chunks * 64 <= b->own_chunks) {
+        b->col16_windows = windows;
+        break;
+      }
+    }
   }
   b->den.alloc(b->nrows, s);
   b->den_t = 0.0;
@@ -322,7 +355,7 @@ void band_build(gh_levels* L, Band* b, int32_t lb, int32_t le) {
       else GH_CUDA(cudaMallocAsync(ptrs[i], sizes[i], s));
     }
   }
-  m->launches += 5;
+  m->launches += 4;
   GH_CUDA(cudaStreamSynchronize(s));
 }
 

@@ -26,23 +26,31 @@ __global__ void k_bfs_init(int32_t* __restrict__ level, int64_t nv) {
     level[v] = -1;
 }
 
-__global__ void k_bfs_seed(int32_t* __restrict__ level, const int32_t* __restrict__ src, int32_t ns) {
-  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < ns; i += gridDim.x * blockDim.x) level[src[i]] = 0;
+// D_0: level 0 and the first frontier (vertex, row begin, row end)
+__global__ void k_bfs_seed(const int32_t* __restrict__ vv_off, int32_t* __restrict__ level,
+                           const int32_t* __restrict__ src, int32_t ns, int4* __restrict__ frontier) {
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < ns; i += gridDim.x * blockDim.x) {
+    const int32_t v = src[i];
+    level[v] = 0;
+    frontier[i] = make_int4(v, vv_off[v], vv_off[v + 1], 0);
+  }
 }
 
 // One ring per iteration; level_size[d] counts ring d. Returns nlev in *out.
+// Frontier entries carry their row bounds (read by the claiming thread while
+// its append slot is reserved), so expanding a ring starts at vv_idx.
 constexpr int kBfsBlock = 512;
 __global__ void __launch_bounds__(kBfsBlock) k_bfs(const int32_t* __restrict__ vv_off, const int32_t* __restrict__ vv_idx,
-                                                   int32_t* __restrict__ level, int32_t* __restrict__ fa,
-                                                   int32_t* __restrict__ fb, int32_t* __restrict__ level_size,
+                                                   int32_t* __restrict__ level, int4* __restrict__ fa,
+                                                   int4* __restrict__ fb, int32_t* __restrict__ level_size,
                                                    int32_t* __restrict__ out, unsigned* __restrict__ bar) {
   // 8 lanes per frontier vertex, one neighbour each, so a ring costs a few
   // dependent memory round trips instead of one per neighbour
   const int64_t tid = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   const int64_t groups = ((int64_t)gridDim.x * blockDim.x) >> 3;
   const int sub = threadIdx.x & 7, lane = threadIdx.x & 31;
-  int32_t* cur = fa;
-  int32_t* nxt = fb;
+  int4* cur = fa;
+  int4* nxt = fb;
   int32_t ncur = __ldcg(level_size);
   int32_t depth = 1;
   for (;;) {
@@ -51,28 +59,32 @@ __global__ void __launch_bounds__(kBfsBlock) k_bfs(const int32_t* __restrict__ v
       const int64_t i = (tid >> 3) + k * groups;
       int32_t a = 0, a1 = 0;
       if (i < ncur) {
-        const int32_t v = __ldcg(cur + i);
-        a = vv_off[v] + sub;
-        a1 = vv_off[v + 1];
+        const int4 e = __ldcg(cur + i);
+        a = e.y + sub;
+        a1 = e.z;
       }
       for (; __any_sync(0xffffffffu, a < a1); a += 8) {
         bool claimed = false;
-        int32_t w = 0;
+        int32_t w = 0, w0 = 0, w1 = 0;
         if (a < a1) {
           w = vv_idx[a];
           claimed = atomicCAS(level + w, -1, depth) == -1;
+        }
+        if (claimed) {
+          w0 = vv_off[w];
+          w1 = vv_off[w + 1];
         }
         const unsigned mask = __ballot_sync(0xffffffffu, claimed);
         int32_t base = 0;
         if (lane == 0 && mask) base = atomicAdd(level_size + depth, __popc(mask));
         base = __shfl_sync(0xffffffffu, base, 0);
-        if (claimed) nxt[base + __popc(mask & ((1u << lane) - 1u))] = w;
+        if (claimed) nxt[base + __popc(mask & ((1u << lane) - 1u))] = make_int4(w, w0, w1, 0);
       }
     }
     ghd::grid_barrier(bar, (unsigned)(depth - 1));
     const int32_t nn = __ldcg(level_size + depth);
     if (nn == 0) break;
-    int32_t* t = cur;
+    int4* t = cur;
     cur = nxt;
     nxt = t;
     ncur = nn;
@@ -133,13 +145,13 @@ void bfs_build(gh_levels* L, const int32_t* h_sources, int32_t ns) {
 
   L->level.alloc(V, s);
   L->parent.alloc(V, s);
-  Scratch<int32_t> fa(V + 1, s), fb(V + 1, s), level_size(V + 2, s), dsrc(n0, s), nlev_d(2, s);
+  Scratch<int4> fa(V + 1, s), fb(V + 1, s);
+  Scratch<int32_t> level_size(V + 2, s), dsrc(n0, s), nlev_d(2, s);
   GH_CUDA(cudaMemsetAsync(level_size.p, 0, sizeof(int32_t) * (V + 2), s));
   GH_CUDA(cudaMemcpyAsync(level_size.p, &n0, sizeof(int32_t), cudaMemcpyHostToDevice, s));
   GH_CUDA(cudaMemcpyAsync(dsrc.p, src.data(), sizeof(int32_t) * n0, cudaMemcpyHostToDevice, s));
-  GH_CUDA(cudaMemcpyAsync(fa.p, src.data(), sizeof(int32_t) * n0, cudaMemcpyHostToDevice, s));
   k_bfs_init<<<grid_for(V), B, 0, s>>>(L->level.p, V);
-  k_bfs_seed<<<grid_for(n0), B, 0, s>>>(L->level.p, dsrc.p, n0);
+  k_bfs_seed<<<grid_for(n0), B, 0, s>>>(m->vv_offset.p, L->level.p, dsrc.p, n0, fa.p);
   GH_LAUNCH_CHECK();
 
   // cooperative ring expansion
@@ -152,8 +164,8 @@ void bfs_build(gh_levels* L, const int32_t* h_sources, int32_t ns) {
     const int32_t* vo = m->vv_offset.p;
     const int32_t* vi = m->vv_index.p;
     int32_t* lv = L->level.p;
-    int32_t* pa = fa.p;
-    int32_t* pb = fb.p;
+    int4* pa = fa.p;
+    int4* pb = fb.p;
     int32_t* ls = level_size.p;
     int32_t* out = nlev_d.p;
     unsigned* bar = reinterpret_cast<unsigned*>(nlev_d.p + 1);

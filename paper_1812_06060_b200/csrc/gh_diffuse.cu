@@ -89,7 +89,7 @@ struct BandArgs {
   const uint8_t* deg4;            // row lengths as nibbles, 16 B per chunk (15: look in deg)
   const uint32_t* col;            // gh::uidx(neighbour row, 1 unless one level closer to the sources)
   const uint16_t* col16;          // the same columns in 16 bits against per-chunk bases (gh::Band::col16)
-  const int2* cbase;
+  const int4* cbase;              // per chunk: window bases (gh::Band::cbase)
   const double* wt;
   const double* den;
   double* ubuf;                   // both sweep parities, gh::uidx layout
@@ -206,7 +206,7 @@ __device__ __forceinline__ void publish_rows(const BandArgs* vba, int32_t band_l
 }
 
 // slot layout: header 512 B (int32: chunk offsets [0..kTileChunks], fits [31], chunk levels [32..],
-//              16-bit column bases [64 + 2q], [65 + 2q])
+//              16-bit column window bases [64 + 4q .. 67 + 4q])
 //              | den kTileChunks x 256 B | deg kTileChunks x 64 B | columns | weights
 constexpr int kHdr = 512;
 constexpr int kBaseHdr = 64;
@@ -218,9 +218,10 @@ constexpr int kColOff = kDegOff + kTileChunks * 64;
 // icosphere and torus meshes and saves the registers of two more gathers).
 // kTable: the pstart/pend tables are copied into shared memory (separate
 // instances so every shared-memory access compiles to LDS, not a generic load).
-// kCol16: columns are streamed as 16-bit offsets (gh::Band::col16), 12 B less
-// per row; chunks without 16-bit columns take the global-memory path.
-template <int kUnroll, bool kTable, bool kCol16>
+// kWin: 0 = 32-bit columns; 2 or 3 = columns streamed as 16-bit offsets into
+// 2 or 3 per-chunk windows (gh::Band::col16), 12 B less per
+// row; chunks without 16-bit columns take the global-memory path.
+template <int kUnroll, bool kTable, int kWin>
 __global__ void __launch_bounds__(kTmaThreads, 2) k_diffuse_tma(const __grid_constant__ TmaArgs a) {
   extern __shared__ __align__(128) unsigned char smem[];
   // this block's band and its rank inside the band
@@ -263,6 +264,7 @@ __global__ void __launch_bounds__(kTmaThreads, 2) k_diffuse_tma(const __grid_con
 
   const int32_t nsteps = (band_le - 1) + 2 * (a.sweeps - 1) + 1;
   const uint32_t col_cap = (uint32_t)kTileChunks * 32u * a.wcap;  // entries
+  constexpr bool kCol16 = kWin != 0;
   constexpr uint32_t kColBytes = kCol16 ? 2u : 4u;
   // ring position: slot index and its use parity advance tile by tile
   int slot = 0;
@@ -289,24 +291,24 @@ __global__ void __launch_bounds__(kTmaThreads, 2) k_diffuse_tma(const __grid_con
       }
       return true;
     };
-    auto load = [&](int32_t xcb, int32_t xce, int32_t xt0, int64_t& p0, int32_t& lv0, int64_t& plast, int2& cb0) {
+    auto load = [&](int32_t xcb, int32_t xce, int32_t xt0, int64_t& p0, int32_t& lv0, int64_t& plast, int4& cb0) {
       const int32_t cbase = xcb + xt0 * kTileChunks;
       const int32_t cl = cbase + lane < xce ? cbase + lane : xce;
       p0 = __ldg(vba->chunk_ptr + cl);
       lv0 = cbase + lane < xce ? __ldg(vba->chunk_level + cl) : 0;
-      if (kCol16) cb0 = cbase + lane < xce ? __ldg(vba->cbase + cl) : make_int2(-1, -1);
+      if (kCol16) cb0 = cbase + lane < xce ? __ldg(vba->cbase + cl) : make_int4(-1, 0, 0, 0);
       plast = __ldg(vba->chunk_ptr + (cbase + 32 < xce ? cbase + 32 : xce));
     };
     int64_t p0 = 0, p_last = 0;
     int32_t lv0 = 0;
-    int2 cb0 = make_int2(-1, -1);
+    int4 cb0 = make_int4(-1, 0, 0, 0);
     bool have = advance(tau, cb, ce, ntile, t0);
     if (have) load(cb, ce, t0, p0, lv0, p_last, cb0);
     while (have) {
       int32_t ntau = tau, ncb = cb, nce = ce, nnt = ntile, nt0 = t0;
       int64_t np0 = 0, np_last = 0;
       int32_t nlv0 = 0;
-      int2 ncb0 = make_int2(-1, -1);
+      int4 ncb0 = make_int4(-1, 0, 0, 0);
       const bool have_next = advance(ntau, ncb, nce, nnt, nt0);
       if (have_next) load(ncb, nce, nt0, np0, nlv0, np_last, ncb0);
       const int32_t cbase = cb + t0 * kTileChunks;
@@ -326,9 +328,11 @@ __global__ void __launch_bounds__(kTmaThreads, 2) k_diffuse_tma(const __grid_con
         if (kCol16) {
           const int qs = (off + (lane & (kTileChunks - 1))) & 31;
           const int32_t bx = __shfl_sync(0xffffffffu, cb0.x, qs), by = __shfl_sync(0xffffffffu, cb0.y, qs);
+          const int32_t bz = __shfl_sync(0xffffffffu, cb0.z, qs);
           if (lane < kTileChunks) {
-            hdr[kBaseHdr + 2 * lane] = bx;
-            hdr[kBaseHdr + 2 * lane + 1] = by;
+            hdr[kBaseHdr + 4 * lane] = bx;
+            hdr[kBaseHdr + 4 * lane + 1] = by;
+            hdr[kBaseHdr + 4 * lane + 2] = bz;
           }
         }
         const int64_t pend_tile = __shfl_sync(0xffffffffu, pi, nch);
@@ -438,8 +442,9 @@ __global__ void __launch_bounds__(kTmaThreads, 2) k_diffuse_tma(const __grid_con
       bool on[kChunksPerWarp], fast[kChunksPerWarp];
       uint32_t px[kChunksPerWarp];  // sweep parity of the step, as the uidx xor mask
       double* const ub = vba->ubuf;
-      const double* ubs[kChunksPerWarp];  // 16-bit columns: u at the chunk's same-level base
-      int32_t dlt[kChunksPerWarp];        // other-half base - same-level base - 0x8000
+      const double* ubs[kChunksPerWarp];  // 2 windows: u at the chunk's same-level base
+      int32_t dlt[kChunksPerWarp];        // 2 windows: other-half base - same-level base - 0x8000
+      const int32_t* wtab[kChunksPerWarp];  // 3 windows: the chunk's base table (base_c - c * 2^14)
 #pragma unroll
       for (int i = 0; i < kChunksPerWarp; ++i) {
         const int q = warp + kConsumerWarps * i;
@@ -456,10 +461,11 @@ __global__ void __launch_bounds__(kTmaThreads, 2) k_diffuse_tma(const __grid_con
         }
         fast[i] = fits && d[i] <= kUnroll;  // 65535 (valence past 16 bits) always takes the slow path
         if (kCol16) {
-          const int32_t bs = hdr[kBaseHdr + 2 * q], bo = hdr[kBaseHdr + 2 * q + 1];
+          const int32_t bs = hdr[kBaseHdr + 4 * q], bo = hdr[kBaseHdr + 4 * q + 1];
           fast[i] = fast[i] && bs >= 0;
           ubs[i] = ub + bs;
           dlt[i] = bo - bs - 0x8000;
+          wtab[i] = hdr + kBaseHdr + 4 * q;
         }
         num[i] = 0.0;
       }
@@ -467,7 +473,7 @@ __global__ void __launch_bounds__(kTmaThreads, 2) k_diffuse_tma(const __grid_con
       // (see the dependency check above)
 #pragma unroll
       for (int i = 0; i < kChunksPerWarp; ++i) {
-        if (kCol16) {
+        if (kWin == 2) {
           // e ^ px keeps bit 15; the same-level base is 64-aligned, so the parity
           // xor commutes with adding it: u index = base(e >> 15) + (e & 0x7fff) ^ px
           const uint16_t* scol = reinterpret_cast<const uint16_t*>(sb + kColOff) + hdr[warp + kConsumerWarps * i] + lane;
@@ -476,6 +482,16 @@ __global__ void __launch_bounds__(kTmaThreads, 2) k_diffuse_tma(const __grid_con
             if (fast[i] && k < d[i]) {
               const int32_t e = (int32_t)((uint32_t)scol[32 * k] ^ px[i]);
               v[i][k] = __ldca(ubs[i] + ((e >> 15) * dlt[i] + e));
+            }
+        } else if (kWin == 3) {
+          // window c = e >> 14 (same level, L-1, L+1); table entry c holds
+          // base_c - c * 2^14, so u index = table[e >> 14] + e ^ px
+          const uint16_t* scol = reinterpret_cast<const uint16_t*>(sb + kColOff) + hdr[warp + kConsumerWarps * i] + lane;
+#pragma unroll
+          for (int k = 0; k < kUnroll; ++k)
+            if (fast[i] && k < d[i]) {
+              const int32_t e = (int32_t)((uint32_t)scol[32 * k] ^ px[i]);
+              v[i][k] = __ldca(ub + (wtab[i][e >> 14] + e));
             }
         } else {
           const uint32_t* scol = reinterpret_cast<const uint32_t*>(sb + kColOff) + hdr[warp + kConsumerWarps * i] + lane;
@@ -653,20 +669,19 @@ double bands_launch(gh_levels* L, std::vector<Band*>& bands, double t, int32_t s
   gh_mesh* m = L->mesh;
   cudaStream_t s = m->stream;
   int32_t wmax = 1;
-  int64_t rows = 0, chunks = 0, wide = 0;
-  bool have16 = true;
+  int64_t rows = 0;
+  int32_t win = -1;  // the bands' common 16-bit column format (0: some band has none)
   for (Band* b : bands) {
     wmax = std::max(wmax, b->max_chunk_width);
     rows += b->own_rows;
-    chunks += b->own_chunks;
-    wide += b->wide_chunks;
-    have16 = have16 && (b->col16.p || !b->own_chunks);
+    if (!b->own_chunks) continue;
+    win = win < 0 || win == b->col16_windows ? b->col16_windows : 0;
   }
-  // 16-bit columns unless more than 1/64 of the chunks would fall back to the
-  // global-memory path (GH_DIFFUSE_COL32 forces 32-bit columns, for tests)
-  // (GH_DIFFUSE_COL16 forces them, so tests can mix in fallback chunks)
-  const bool col16 =
-      have16 && !getenv("GH_DIFFUSE_COL32") && (wide * 64 <= chunks || getenv("GH_DIFFUSE_COL16"));
+  // 16-bit columns when every band has them in one format (gh::band_build
+  // picks one only if at most 1/64 of its chunks fall back to 32 bits);
+  // GH_DIFFUSE_COL32 forces 32-bit columns (tests)
+  if (win < 0 || getenv("GH_DIFFUSE_COL32")) win = 0;
+  const bool col16 = win != 0;
   // slot = 512 B header + per chunk (den 256 B + deg 64 B + wcap x 32 x (2 or 4 + 8) B of columns/weights)
   const int32_t wcap = std::min<int32_t>(wmax, 16);
   const int32_t slot_bytes = ((kColOff + kTileChunks * 32 * wcap * (col16 ? 10 : 12)) + 127) & ~127;
@@ -680,14 +695,12 @@ double bands_launch(gh_levels* L, std::vector<Band*>& bands, double t, int32_t s
   }
   if (nslots < 2) nslots = 2;
   const size_t shmem = 16 * (size_t)nslots + table_bytes + 128 + (size_t)nslots * slot_bytes;
-  void* fn;
-  if (col16)
-    fn = wmax <= 6 ? (table ? (void*)k_diffuse_tma<6, true, true> : (void*)k_diffuse_tma<6, false, true>)
-                   : (table ? (void*)k_diffuse_tma<8, true, true> : (void*)k_diffuse_tma<8, false, true>);
-  else
-    fn = wmax <= 6 ? (table ? (void*)k_diffuse_tma<6, true, false> : (void*)k_diffuse_tma<6, false, false>)
-                   : (table ? (void*)k_diffuse_tma<8, true, false> : (void*)k_diffuse_tma<8, false, false>);
-  L->last_col16 = col16 ? 1 : 0;
+#define GH_DIFFUSE_FN(W)                                                                                 \
+  (wmax <= 6 ? (table ? (void*)k_diffuse_tma<6, true, W> : (void*)k_diffuse_tma<6, false, W>)           \
+             : (table ? (void*)k_diffuse_tma<8, true, W> : (void*)k_diffuse_tma<8, false, W>))
+  void* fn = win == 2 ? GH_DIFFUSE_FN(2) : win == 3 ? GH_DIFFUSE_FN(3) : GH_DIFFUSE_FN(0);
+#undef GH_DIFFUSE_FN
+  L->last_col16 = win;
   GH_CUDA(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)shmem));
   int nsm = 0, per_sm = 0;
   GH_CUDA(cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, m->device));

@@ -171,14 +171,19 @@ struct Band {
   DevBuf<int32_t> deg_big;      // full row lengths, only when some valence >= 65535
   DevBuf<uint32_t> col;         // uidx(local row of the neighbour, 0 if one level closer to the sources else 1)
   DevBuf<double> wt;            // cotan weights in the reference's row order
-  // 16-bit copy of col: bit 15 = the neighbour is one level
-  // away (the other parity half), bits 0-14 = its uidx minus the chunk's base
-  // for that half. cbase per own chunk: (same-level base, other-half base), or
-  // x = -1 where the chunk's neighbours span more than 15 bits (kept 32-bit).
+  // 16-bit copy of col, in one of two formats:
+  //  2 windows: bit 15 = the neighbour is one level away (the other parity
+  //    half), bits 0-14 = its uidx minus the chunk's base for that half;
+  //    cbase = (same-level base, other-half base, -, -);
+  //  3 windows: bits 14-15 = window (0 same level, 1 level L-1, 2 level L+1),
+  //    bits 0-13 = uidx minus the window's base; cbase = (base_0, base_1 - 2^14,
+  //    base_2 - 2^15, -).
+  // cbase.x = -1 marks a chunk whose windows do not fit (kept 32-bit).
   DevBuf<uint16_t> col16;
-  DevBuf<int2> cbase;
-  DevBuf<uint8_t> deg4;  // row lengths as nibbles (min(deg, 15)), 16 B per own chunk
-  int64_t wide_chunks = 0;  // own chunks with cbase.x == -1
+  DevBuf<int4> cbase;
+  DevBuf<uint8_t> deg4;       // row lengths as nibbles (min(deg, 15)), 16 B per own chunk
+  int32_t col16_windows = 0;  // format of col16: 2, 3, or 0 when too many chunks do not fit
+  int64_t wide_chunks = 0;    // own chunks with cbase.x == -1
   DevBuf<double> area_r, wsum_r, den;
   double den_t = 0.0;
   // state shared with neighbour bands: plain cudaMalloc when it is IPC-exported

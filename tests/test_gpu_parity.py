@@ -328,20 +328,21 @@ def test_high_valence_hub_bitwise(gpu, port_oracle, n, source):
         assert_same(bands.gs_diffuse_bands(mesh, lv, 2, ref["t"], 60), ref["u"], "fan with 2 bands")
 
 
-@pytest.mark.parametrize("mode", ["col16", "col32", "col16_mixed"])
+@pytest.mark.parametrize("mode", ["auto", "col32", "win2", "win3", "win2_mixed", "win3_mixed"])
 def test_diffusion_column_formats_bitwise(gpu, port_oracle, monkeypatch, mode):
-    """The diffusion kernel streams 16-bit column offsets against per-chunk
-    bases (chunks whose neighbour windows do not fit keep 32-bit columns and
-    take the global-memory path); both formats, and a mix forced by a tiny
-    window limit, give u bit-identical to the reference on every fixture and on
+    """The diffusion kernel streams 16-bit column offsets into 2 or 3 per-chunk
+    windows (chunks whose windows do not fit keep 32-bit columns and take the
+    global-memory path); every format, and mixes forced by a tiny window
+    limit, give u bit-identical to the reference on every fixture and on
     reduced configs 2-5, single band and 3 bands."""
     from paper_1812_06060_b200 import bands, meshgen
     gh = gpu
     if mode == "col32":
         monkeypatch.setenv("GH_DIFFUSE_COL32", "1")
-    if mode == "col16_mixed":
+    if mode.startswith("win"):
+        monkeypatch.setenv("GH_COL16_WINDOWS", mode[3])
+    if mode.endswith("mixed"):
         monkeypatch.setenv("GH_COL16_SPAN", "96")
-        monkeypatch.setenv("GH_DIFFUSE_COL16", "1")
     want_bits = 32 if mode == "col32" else 16
     for case in CASES:
         g = np.load(os.path.join(GOLDEN, case + ".npz"))
