@@ -261,7 +261,8 @@ void band_build(gh_levels* L, Band* b, int32_t lb, int32_t le) {
   const int32_t glo = std::max(lb - 1, 0), ghi = std::min(le, nlev - 1);
   const int64_t pb = off[glo], pe = off[ghi + 1];
   if (pe > pb) {
-    k_band_renumber<<<grid_for(pe - pb), B, 0, s>>>(L->order.p, L->level.p, pb, pe, L->offsets.p, b->pstart.p,
+    const int32_t* ord = L->layout_order.p ? L->layout_order.p : L->order.p;
+    k_band_renumber<<<grid_for(pe - pb), B, 0, s>>>(ord, L->level.p, pb, pe, L->offsets.p, b->pstart.p,
                                                     b->perm.p, local.p);
     GH_LAUNCH_CHECK();
   }

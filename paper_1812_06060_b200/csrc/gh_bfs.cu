@@ -14,6 +14,8 @@
 #include <cub/device/device_scan.cuh>
 
 #include <algorithm>
+#include <cstdlib>
+#include <cstring>
 
 #include "gh_internal.cuh"
 
@@ -110,6 +112,39 @@ __global__ void k_parent(const int32_t* __restrict__ vv_off, const int32_t* __re
       }
     parent[v] = p;
     key[v] = L >= 0 ? (uint32_t)L : unreach_key;
+    val[v] = (int32_t)v;
+  }
+}
+
+// Spatial order inside each ring for the diffusion layout: key = (level,
+// 30-bit Morton code of the position in the mesh's bounding box). Rows of a
+// ring keep their arithmetic (each row sums its neighbours in the reference's
+// order, whatever its position); only which rows share a chunk changes.
+__device__ __forceinline__ uint64_t spread3(uint32_t x) {
+  uint64_t r = 0;
+  for (int b = 0; b < 10; ++b) r |= (uint64_t)((x >> b) & 1u) << (3 * b);
+  return r;
+}
+__global__ void k_morton_keys(const double* __restrict__ pos, const int32_t* __restrict__ level,
+                              const double* __restrict__ box, int64_t nv, uint64_t* __restrict__ key,
+                              int32_t* __restrict__ val) {
+  const double lo[3] = {box[0], box[1], box[2]};
+  double ext = 0.0;
+  for (int k = 0; k < 3; ++k) ext = fmax(ext, box[3 + k] - box[k]);
+  const double sc = ext > 0.0 ? 1023.0 / ext : 0.0;
+  for (int64_t v = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; v < nv; v += (int64_t)gridDim.x * blockDim.x) {
+    const int32_t L = level[v];
+    uint64_t k = ~0ull;
+    if (L >= 0) {
+      uint64_t m = 0;
+      for (int a = 0; a < 3; ++a) {
+        const double q = (pos[3 * v + a] - lo[a]) * sc;
+        const uint32_t qi = q > 0.0 ? (q < 1023.0 ? (uint32_t)q : 1023u) : 0u;
+        m |= spread3(qi) << a;
+      }
+      k = (uint64_t)L << 32 | m;
+    }
+    key[v] = k;
     val[v] = (int32_t)v;
   }
 }
@@ -215,6 +250,36 @@ void bfs_build(gh_levels* L, const int32_t* h_sources, int32_t ns) {
   m->launches += 4;
   // diffusion layout of the whole level range (one band, no ghosts)
   band_build(L, &L->main, 0, nlev);
+  // Rings in vertex-id order are spatially coherent on grid-like numberings;
+  // when they are not (ring neighbours scattered over the ring, as with the
+  // icosphere's subdivision numbering) no 16-bit column format fits, and the
+  // layout is rebuilt with each ring in Morton order (GH_LAYOUT=id|morton
+  // forces one, for tests).
+  const char* lay = getenv("GH_LAYOUT");
+  const bool force_morton = lay && std::strcmp(lay, "morton") == 0;
+  const bool force_id = lay && std::strcmp(lay, "id") == 0;
+  L->layout_order.release();
+  if (L->nreach > 0 && (force_morton || (!force_id && L->main.col16_windows == 0))) {
+    L->layout_order.alloc(V, s);
+    {
+      Scratch<uint64_t> k0(V, s), k1(V, s);
+      Scratch<int32_t> v1(V, s);
+      k_morton_keys<<<grid_for(V), B, 0, s>>>(m->pos.p, L->level.p, m->scalars.p + 5, V, k0.p, L->layout_order.p);
+      GH_LAUNCH_CHECK();
+      int end_bit = 33;
+      while (end_bit < 64 && ((uint64_t)nlev >> (end_bit - 32)) != 0) ++end_bit;
+      cub::DoubleBuffer<uint64_t> kb(k0.p, k1.p);
+      cub::DoubleBuffer<int32_t> vb(L->layout_order.p, v1.p);
+      size_t tmp = 0;
+      GH_CUDA(cub::DeviceRadixSort::SortPairs(nullptr, tmp, kb, vb, (int)V, 0, end_bit, s));
+      Scratch<char> t(tmp, s);
+      GH_CUDA(cub::DeviceRadixSort::SortPairs(t.p, tmp, kb, vb, (int)V, 0, end_bit, s));
+      if (vb.Current() != L->layout_order.p)
+        GH_CUDA(cudaMemcpyAsync(L->layout_order.p, vb.Current(), sizeof(int32_t) * V, cudaMemcpyDeviceToDevice, s));
+    }
+    m->launches += 2;
+    band_build(L, &L->main, 0, nlev);
+  }
 }
 
 }  // namespace gh

@@ -65,6 +65,10 @@ __global__ void k_bbox_final(const double* __restrict__ part, int nparts, int64_
   v3 d = sub(mk(hi[0], hi[1], hi[2]), mk(lo[0], lo[1], lo[2]));
   const double diag2 = nv > 0 ? sqnorm(d) : 0.0;
   out[0] = 1e-14 * diag2;
+  for (int k = 0; k < 3; ++k) {  // the box itself (the diffusion layout's spatial order, gh_bfs.cu)
+    out[5 + k] = lo[k];
+    out[8 + k] = hi[k];
+  }
 }
 
 // face checks + area + unit normal (mesh.hpp:128-145); first failing face via atomicMin

@@ -328,15 +328,21 @@ def test_high_valence_hub_bitwise(gpu, port_oracle, n, source):
         assert_same(bands.gs_diffuse_bands(mesh, lv, 2, ref["t"], 60), ref["u"], "fan with 2 bands")
 
 
-@pytest.mark.parametrize("mode", ["auto", "col32", "win2", "win3", "win2_mixed", "win3_mixed"])
+@pytest.mark.parametrize("mode", ["auto", "col32", "win2", "win3", "win2_mixed", "win3_mixed", "morton",
+                                  "morton_win3_mixed", "morton_col32"])
 def test_diffusion_column_formats_bitwise(gpu, port_oracle, monkeypatch, mode):
     """The diffusion kernel streams 16-bit column offsets into 2 or 3 per-chunk
     windows (chunks whose windows do not fit keep 32-bit columns and take the
     global-memory path); every format, and mixes forced by a tiny window
     limit, give u bit-identical to the reference on every fixture and on
-    reduced configs 2-5, single band and 3 bands."""
+    reduced configs 2-5, single band and 3 bands. The "morton" modes lay each
+    ring out in spatial order (the layout picked when vertex-id order leaves no
+    16-bit format usable), which moves rows between chunks but not their sums."""
     from paper_1812_06060_b200 import bands, meshgen
     gh = gpu
+    if mode.startswith("morton"):
+        monkeypatch.setenv("GH_LAYOUT", "morton")
+        mode = mode[7:] or "auto"
     if mode == "col32":
         monkeypatch.setenv("GH_DIFFUSE_COL32", "1")
     if mode.startswith("win"):
