@@ -114,6 +114,7 @@ struct TmaArgs {
   int32_t nslots;      // ring slots per block
   int32_t slot_bytes;
   int32_t table_in_smem;
+  int32_t stream_resident;  // the CSR stream fits in L2: keep it (evict_last) instead of evict_first
   double t;
 };
 
@@ -141,6 +142,12 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
 __device__ __forceinline__ uint64_t l2_evict_first_policy() {
   uint64_t p;
   asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(p));
+  return p;
+}
+// ... unless the whole stream fits in L2 next to u: then it stays there
+__device__ __forceinline__ uint64_t l2_evict_last_policy() {
+  uint64_t p;
+  asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(p));
   return p;
 }
 __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar, uint64_t policy) {
@@ -344,7 +351,7 @@ __global__ void __launch_bounds__(kTmaThreads, 2) k_diffuse_tma(const __grid_con
           unsigned char* sb = reinterpret_cast<unsigned char*>(hdr);
           const uint32_t bytes = (uint32_t)nch * (256u + (kCol16 ? 16u : 64u)) + (fits ? ncol * (kColBytes + 8u) : 0u);
           mbar_expect_tx(full + slot, bytes);
-          const uint64_t pol = l2_evict_first_policy();
+          const uint64_t pol = a.stream_resident ? l2_evict_last_policy() : l2_evict_first_policy();
           bulk_g2s(sb + kDenOff, vba->den + (int64_t)c0 * 32, (uint32_t)nch * 256u, full + slot, pol);
           if (kCol16) bulk_g2s(sb + kDegOff, vba->deg4 + (int64_t)c0 * 16, (uint32_t)nch * 16u, full + slot, pol);
           else bulk_g2s(sb + kDegOff, vba->deg + (int64_t)c0 * 32, (uint32_t)nch * 64u, full + slot, pol);
@@ -727,6 +734,17 @@ double bands_launch(gh_levels* L, std::vector<Band*>& bands, double t, int32_t s
   a.slot_bytes = slot_bytes;
   a.table_in_smem = table ? 1 : 0;
   a.t = t;
+  {
+    // stream + both u buffers against L2 (GH_STREAM_L2=0|1 forces, for experiments): config 2 -2 %
+    int l2 = 0;
+    GH_CUDA(cudaDeviceGetAttribute(&l2, cudaDevAttrL2CacheSize, m->device));
+    uint64_t bytes = 0;
+    for (Band* b : bands) bytes += b->den.bytes() + b->deg4.bytes() + b->col16.bytes() + b->wt.bytes() + 16ull * b->nrows;
+    if (!col16)
+      for (Band* b : bands) bytes += b->col.bytes() - b->col16.bytes() + b->deg.bytes();
+    const char* env = getenv("GH_STREAM_L2");
+    a.stream_resident = env ? atoi(env) : (bytes <= (uint64_t)l2 ? 1 : 0);
+  }
   void* kargs[] = {&a};
   EventTimer timer(s);
   timer.start();
