@@ -17,8 +17,9 @@
 //    32-row aligned, so a step's active rows are one contiguous range and a
 //    32-row chunk holds one level; CSR in SELL-32 (entry k of lane j at
 //    chunk_ptr + 32k + j).
-//  * per block, a producer warp streams the step's chunk share (den, deg,
-//    columns, weights: ~86 of the ~100 B per update) HBM -> shared memory
+//  * per block, a producer warp streams the step's chunk share (den, row
+//    lengths, columns, weights: 68.5 B per update with 16-bit columns, 82 B
+//    with 32-bit ones, of the ~100 algorithmic B) HBM -> shared memory
 //    with cp.async.bulk + mbarrier complete_tx into a ring of tiles, running
 //    ahead across steps (the CSR is read-only);
 //  * 8 consumer warps each take 2 chunks of a tile, gather the neighbour u
@@ -214,7 +215,8 @@ __device__ __forceinline__ void publish_rows(const BandArgs* vba, int32_t band_l
 
 // slot layout: header 512 B (int32: chunk offsets [0..kTileChunks], fits [31], chunk levels [32..],
 //              16-bit column window bases [64 + 4q .. 67 + 4q])
-//              | den kTileChunks x 256 B | deg kTileChunks x 64 B | columns | weights
+//              | den kTileChunks x 256 B | row lengths kTileChunks x 64 B (u16; nibbles use 16 B)
+//              | columns (u32, or u16 with kWin) | weights
 constexpr int kHdr = 512;
 constexpr int kBaseHdr = 64;
 constexpr int kDenOff = kHdr;
