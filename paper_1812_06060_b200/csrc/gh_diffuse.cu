@@ -38,7 +38,7 @@
 namespace {
 
 constexpr int B = gh::kBlock;
-constexpr int kMaxSmemLevels = 6 * 1024;  // pstart/pend tables in shared memory (48 KB)
+constexpr int kMaxSmemLevels = 12 * 1024;  // pend table in shared memory (48 KB; pstart is derived from it)
 
 __global__ void k_den(const double* __restrict__ area, const double* __restrict__ wsum, double t, int64_t n,
                       double* __restrict__ den) {
@@ -102,6 +102,8 @@ struct BandArgs {
   int32_t* stalled;               // set when a dependency never arrives (a dead peer): the kernel bails out
   int32_t lo_ghost, hi_ghost;     // first row of the ghost copy inside the neighbour
   int32_t lb, le;                 // own levels
+  int32_t half2;                  // first row of the odd-level half
+  int32_t gs_lo, gs_hi;           // first rows of the ghost levels lb-1, le (this band)
 };
 
 constexpr int kMaxBands = 8;  // bands per launch (one per GPU in production; more when emulated)
@@ -184,7 +186,8 @@ __device__ __forceinline__ unsigned long long ld_done(const unsigned long long* 
 }
 
 // rows [rb, re) of the band's own levels active at step tau (L = tau - 2s, 0 <= s < S)
-__device__ __forceinline__ bool step_range(int32_t sweeps, int32_t lb, int32_t le, const int32_t* pstart,
+template <class PStart>
+__device__ __forceinline__ bool step_range(int32_t sweeps, int32_t lb, int32_t le, PStart pstart,
                                            const int32_t* pend, int32_t tau, int32_t& rb, int32_t& re) {
   int32_t lhi = tau < le - 1 ? tau : le - 1;
   if ((lhi ^ tau) & 1) --lhi;
@@ -192,7 +195,7 @@ __device__ __forceinline__ bool step_range(int32_t sweeps, int32_t lb, int32_t l
   if (llo < lb) llo = lb;
   if ((llo ^ tau) & 1) ++llo;
   if (llo > lhi) return false;
-  rb = pstart[llo];
+  rb = pstart(llo);
   re = pend[lhi];
   return true;
 }
@@ -221,12 +224,15 @@ constexpr int kHdr = 512;
 constexpr int kBaseHdr = 64;
 constexpr int kDenOff = kHdr;
 constexpr int kDegOff = kDenOff + kTileChunks * 256;
-constexpr int kColOff = kDegOff + kTileChunks * 64;
+constexpr int kColOff32 = kDegOff + kTileChunks * 64;  // u16 row lengths
+constexpr int kColOff16 = kDegOff + kTileChunks * 16;  // nibbles (16-bit-column kernels)
 
 // kUnroll: rows up to this valence are gathered fully unrolled (6 covers
 // icosphere and torus meshes and saves the registers of two more gathers).
-// kTable: the pstart/pend tables are copied into shared memory (separate
-// instances so every shared-memory access compiles to LDS, not a generic load).
+// kTable: the pend table is copied into shared memory (separate instances so
+// every shared-memory access compiles to LDS, not a generic load); pstart is
+// derived from it (levels of a parity half are consecutive, 32-row aligned),
+// which halves the table and leaves room for a third ring slot.
 // kWin: 0 = 32-bit columns; 2 or 3 = columns streamed as 16-bit offsets into
 // 2 or 3 per-chunk windows (gh::Band::col16), 12 B less per
 // row; chunks without 16-bit columns take the global-memory path.
@@ -247,8 +253,7 @@ __global__ void __launch_bounds__(kTmaThreads, 2) k_diffuse_tma(const __grid_con
   uint64_t* full = reinterpret_cast<uint64_t*>(smem);
   uint64_t* empty = full + a.nslots;
   int32_t* sh_pend = reinterpret_cast<int32_t*>(empty + a.nslots);
-  int32_t* sh_pstart = sh_pend + a.nlev;
-  const uint32_t table_bytes = kTable ? ((8u * (uint32_t)a.nlev + 127u) & ~127u) : 0u;
+  const uint32_t table_bytes = kTable ? ((4u * (uint32_t)a.nlev + 127u) & ~127u) : 0u;
   // slots start 128-byte aligned in the shared window (offsets from smem keep
   // the accesses in the shared address space)
   const uint32_t slots_at = 16u * (uint32_t)a.nslots + table_bytes;
@@ -264,16 +269,26 @@ __global__ void __launch_bounds__(kTmaThreads, 2) k_diffuse_tma(const __grid_con
   if (kTable) {
     for (int i = threadIdx.x; i < a.nlev; i += blockDim.x) {
       sh_pend[i] = sba.pend[i];
-      sh_pstart[i] = sba.pstart[i];
     }
   }
   const int32_t* pend = kTable ? sh_pend : sba.pend;
-  const int32_t* pstart = kTable ? sh_pstart : sba.pstart;
+  // first row of level X: the even and the odd half start at 0 and half2, a
+  // later level right after the previous one of its half (rounded up to 32),
+  // ghosts where the layout put them
+  const int32_t half2 = sba.half2, gs_lo = sba.gs_lo, gs_hi = sba.gs_hi;
+  auto pstart = [&](int32_t X) -> int32_t {
+    if (!kTable) return sba.pstart[X];
+    if (X < band_lb) return gs_lo;
+    if (X >= band_le) return gs_hi;
+    if (X <= band_lb + 1) return (X & 1) ? half2 : 0;
+    return (pend[X - 2] + 31) & ~31;
+  };
   __syncthreads();
 
   const int32_t nsteps = (band_le - 1) + 2 * (a.sweeps - 1) + 1;
   const uint32_t col_cap = (uint32_t)kTileChunks * 32u * a.wcap;  // entries
   constexpr bool kCol16 = kWin != 0;
+  constexpr int kColOff = kCol16 ? kColOff16 : kColOff32;
   constexpr uint32_t kColBytes = kCol16 ? 2u : 4u;
   // ring position: slot index and its use parity advance tile by tile
   int slot = 0;
@@ -424,7 +439,7 @@ __global__ void __launch_bounds__(kTmaThreads, 2) k_diffuse_tma(const __grid_con
           const int32_t X = Li - 1 + lane % 3;
           if (X >= 0 && X < a.nlev) {
             const unsigned long long need =
-                (unsigned long long)((tau - X + 1) >> 1) * (unsigned long long)(pend[X] - pstart[X]);
+                (unsigned long long)((tau - X + 1) >> 1) * (unsigned long long)(pend[X] - pstart(X));
             const bool ghost = X < band_lb || X >= band_le;
             if (ld_done(vba->rows_done + X, ghost) < need) {
               const long long t0 = clock64();
@@ -564,9 +579,9 @@ __global__ void __launch_bounds__(kTmaThreads, 2) k_diffuse_tma(const __grid_con
           __stcg(ub + gh::uidx((uint32_t)r, par), un);
           // boundary levels also land in the neighbour band's ghost copy
           if (Lq[i] == band_lb && vba->lo_ubuf)
-            __stcg(vba->lo_ubuf + gh::uidx((uint32_t)(vba->lo_ghost + (r - pstart[Lq[i]])), par), un);
+            __stcg(vba->lo_ubuf + gh::uidx((uint32_t)(vba->lo_ghost + (r - pstart(Lq[i]))), par), un);
           if (Lq[i] == band_le - 1 && vba->hi_ubuf)
-            __stcg(vba->hi_ubuf + gh::uidx((uint32_t)(vba->hi_ghost + (r - pstart[Lq[i]])), par), un);
+            __stcg(vba->hi_ubuf + gh::uidx((uint32_t)(vba->hi_ghost + (r - pstart(Lq[i]))), par), un);
         }
       }
       __syncwarp();
@@ -582,7 +597,8 @@ __global__ void __launch_bounds__(kTmaThreads, 2) k_diffuse_tma(const __grid_con
       lv_first = __shfl_sync(0xffffffffu, lv_first, 0);
       lv_last = __shfl_sync(0xffffffffu, lv_last, 0);
       for (int32_t X = lv_first + 2 * lane; X <= lv_last; X += 64) {
-        const int32_t lo = cb * 32 > pstart[X] ? cb * 32 : pstart[X];
+        const int32_t px0 = pstart(X);
+        const int32_t lo = cb * 32 > px0 ? cb * 32 : px0;
         const int32_t hi = ce * 32 < pend[X] ? ce * 32 : pend[X];
         if (hi > lo) publish_rows(vba, band_lb, band_le, X, (unsigned long long)(hi - lo));
       }
@@ -624,6 +640,11 @@ namespace {
 BandArgs band_args(const Band& b) {
   BandArgs x{};
   x.pstart = b.pstart.p;
+  x.half2 = 0;
+  for (int32_t l = b.lb; l < b.le && l <= b.lb + 1; ++l)
+    if (l & 1) x.half2 = b.h_pstart[l];
+  x.gs_lo = b.lb > 0 ? b.h_pstart[b.lb - 1] : 0;
+  x.gs_hi = b.le < b.nlev ? b.h_pstart[b.le] : 0;
   x.pend = b.pend.p;
   x.chunk_level = b.chunk_level.p;
   x.chunk_ptr = b.chunk_ptr.p;
@@ -693,9 +714,9 @@ double bands_launch(gh_levels* L, std::vector<Band*>& bands, double t, int32_t s
   const bool col16 = win != 0;
   // slot = 512 B header + per chunk (den 256 B + deg 64 B + wcap x 32 x (2 or 4 + 8) B of columns/weights)
   const int32_t wcap = std::min<int32_t>(wmax, 16);
-  const int32_t slot_bytes = ((kColOff + kTileChunks * 32 * wcap * (col16 ? 10 : 12)) + 127) & ~127;
+  const int32_t slot_bytes = (((col16 ? kColOff16 : kColOff32) + kTileChunks * 32 * wcap * (col16 ? 10 : 12)) + 127) & ~127;
   const bool table = L->nlev <= kMaxSmemLevels;
-  const size_t table_bytes = table ? ((2 * sizeof(int32_t) * L->nlev + 127) & ~size_t(127)) : 0;
+  const size_t table_bytes = table ? ((sizeof(int32_t) * L->nlev + 127) & ~size_t(127)) : 0;
   // two blocks per SM with a ring of >= 2 slots each (228 KB per SM, 1 KB reserved per block)
   int32_t nslots = 0;
   for (int per = 2; per >= 1 && nslots < 2; --per) {
