@@ -191,9 +191,8 @@ Band::~Band() {
 
 uint64_t Band::device_bytes() const {
   return pstart.bytes() + pend.bytes() + perm.bytes() + chunk_level.bytes() + chunk_ptr.bytes() + deg.bytes() +
-         deg_big.bytes() +
-         col.bytes() + col16.bytes() + cbase.bytes() + deg4.bytes() + wt.bytes() + area_r.bytes() + wsum_r.bytes() + den.bytes() + 2 * sizeof(double) * nrows +
-         sizeof(unsigned long long) * nlev;
+         deg_big.bytes() + col.bytes() + col16.bytes() + cbase.bytes() + deg4.bytes() + wt.bytes() + area_r.bytes() +
+         wsum_r.bytes() + den.bytes() + 2 * sizeof(double) * nrows + sizeof(unsigned long long) * nlev;
 }
 
 // Cut levels into nbands contiguous bands of about equal row counts; band r

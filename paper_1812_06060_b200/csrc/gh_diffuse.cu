@@ -714,7 +714,8 @@ double bands_launch(gh_levels* L, std::vector<Band*>& bands, double t, int32_t s
   const bool col16 = win != 0;
   // slot = 512 B header + per chunk (den 256 B + deg 64 B + wcap x 32 x (2 or 4 + 8) B of columns/weights)
   const int32_t wcap = std::min<int32_t>(wmax, 16);
-  const int32_t slot_bytes = (((col16 ? kColOff16 : kColOff32) + kTileChunks * 32 * wcap * (col16 ? 10 : 12)) + 127) & ~127;
+  const int32_t col_off = col16 ? kColOff16 : kColOff32;
+  const int32_t slot_bytes = ((col_off + kTileChunks * 32 * wcap * (col16 ? 10 : 12)) + 127) & ~127;
   const bool table = L->nlev <= kMaxSmemLevels;
   const size_t table_bytes = table ? ((sizeof(int32_t) * L->nlev + 127) & ~size_t(127)) : 0;
   // two blocks per SM with a ring of >= 2 slots each (228 KB per SM, 1 KB reserved per block)
@@ -762,7 +763,8 @@ double bands_launch(gh_levels* L, std::vector<Band*>& bands, double t, int32_t s
     int l2 = 0;
     GH_CUDA(cudaDeviceGetAttribute(&l2, cudaDevAttrL2CacheSize, m->device));
     uint64_t bytes = 0;
-    for (Band* b : bands) bytes += b->den.bytes() + b->deg4.bytes() + b->col16.bytes() + b->wt.bytes() + 16ull * b->nrows;
+    for (Band* b : bands)
+      bytes += b->den.bytes() + b->deg4.bytes() + b->col16.bytes() + b->wt.bytes() + 16ull * b->nrows;
     if (!col16)
       for (Band* b : bands) bytes += b->col.bytes() - b->col16.bytes() + b->deg.bytes();
     const char* env = getenv("GH_STREAM_L2");
