@@ -56,6 +56,19 @@ inline unsigned grid_for(int64_t n, int block = kBlock, int64_t cap = 148 * 32) 
 // stream from the device's default memory pool, whose release threshold is
 // raised once per device (gh_mesh_create) so freed handle memory stays cached
 // for the next solve instead of going back to the driver.
+// Stream-ordered allocation with an exact-size cache for large blocks
+// (gh_alloc.cu). The default pool keeps freed memory (release threshold
+// raised), but it fragments: an end-to-end solve that repeats the previous
+// one's allocations still made the pool map new memory now and then (one
+// 134 MB request taking 134 ms). Blocks of 1 MB and more are therefore kept
+// by size on free (with an event recorded on the freeing stream) and handed
+// back to the next request of exactly that size (the requesting stream waits
+// on the event). The cache is bounded (half of device memory, oldest
+// blocks go back to the pool first) and flushed when an allocation fails.
+void* dev_alloc(size_t bytes, cudaStream_t s);
+void dev_free(void* p, size_t bytes, cudaStream_t s);
+void dev_cache_flush();
+
 template <class T>
 struct DevBuf {
   T* p = nullptr;
@@ -69,10 +82,10 @@ struct DevBuf {
     release();
     n = count;
     s = stream;
-    if (count) GH_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&p), sizeof(T) * count, stream));
+    if (count) p = static_cast<T*>(dev_alloc(sizeof(T) * count, stream));
   }
   void release() {
-    if (p) cudaFreeAsync(p, s);
+    if (p) dev_free(p, sizeof(T) * n, s);
     p = nullptr;
     n = 0;
   }
@@ -83,12 +96,13 @@ struct DevBuf {
 template <class T>
 struct Scratch {
   T* p = nullptr;
+  size_t bytes = 0;
   cudaStream_t s = nullptr;
-  Scratch(size_t count, cudaStream_t stream) : s(stream) {
-    if (count) GH_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&p), sizeof(T) * count, stream));
+  Scratch(size_t count, cudaStream_t stream) : bytes(sizeof(T) * count), s(stream) {
+    if (count) p = static_cast<T*>(dev_alloc(bytes, stream));
   }
   ~Scratch() {
-    if (p) cudaFreeAsync(p, s);
+    if (p) dev_free(p, bytes, s);
   }
   Scratch(const Scratch&) = delete;
   Scratch& operator=(const Scratch&) = delete;
