@@ -70,28 +70,6 @@ __global__ void k_face_slots(const int32_t* __restrict__ he_edge, const int32_t*
   }
 }
 
-// ctor (grad_face.hpp:76-85): edge_dir, incident faces, scale partials
-__global__ void k_face_init_edges(const double* __restrict__ pos, const int32_t* __restrict__ interior_edges,
-                                  const int32_t* __restrict__ edge_v, const int32_t* __restrict__ edge_he,
-                                  const double* __restrict__ area, int64_t ni, double* __restrict__ edir,
-                                  int32_t* __restrict__ ef, double* __restrict__ lam, double* __restrict__ part,
-                                  double* __restrict__ term) {
-  double s = 0.0;
-  GRID_STRIDE(i, ni) {
-    const int32_t e = interior_edges[i];
-    st3(edir, i, normalized(sub(ld3(pos, edge_v[2 * e + 1]), ld3(pos, edge_v[2 * e]))));
-    const int32_t f1 = edge_he[2 * e] / 3, f2 = edge_he[2 * e + 1] / 3;
-    ef[2 * i] = f1;
-    ef[2 * i + 1] = f2;
-    st3(lam, 2 * i, mk(0.0, 0.0, 0.0));
-    st3(lam, 2 * i + 1, mk(0.0, 0.0, 0.0));
-    const double tt = area[f1] + area[f2];  // scale2 += A1 + A2 (grad_face.hpp:83)
-    term[i] = tt;
-    s += tt;
-  }
-  s = block_sum<B>(s);
-  if (threadIdx.x == 0) part[blockIdx.x] = s;
-}
 
 // Y-update for interior edge i (grad_face.hpp:126-137 + y_update_edge 31-36)
 // from the two side faces' g and lambda; d = lambda / (mu sqrt(A)) per side is
@@ -110,23 +88,46 @@ __device__ __forceinline__ void face_y_update(int64_t i, v3 g1, v3 g2, double a1
   y2 = sub(q2, scale(ddiv(a1, a1 + a2), shift));
 }
 
+// ctor (grad_face.hpp:76-85): edge_dir, incident faces, lambda = 0, scale
+// partials; with C set, also the first iteration's c per slot: y1, y2 start
+// at h of the side faces (grad_face.hpp:82-83), which is the Y-update from
+// g = h, lambda = 0 (computed exactly like later ones, see k_face_lambda_c)
+__global__ void k_face_init_edges(const double* __restrict__ pos, const int32_t* __restrict__ interior_edges,
+                                  const int32_t* __restrict__ edge_v, const int32_t* __restrict__ edge_he,
+                                  const double* __restrict__ area, const double* __restrict__ h, int64_t ni,
+                                  double mu, double* __restrict__ edir, int32_t* __restrict__ ef,
+                                  double* __restrict__ lam, double* __restrict__ C, double* __restrict__ part,
+                                  double* __restrict__ term) {
+  double s = 0.0;
+  GRID_STRIDE(i, ni) {
+    const int32_t e = interior_edges[i];
+    st3(edir, i, normalized(sub(ld3(pos, edge_v[2 * e + 1]), ld3(pos, edge_v[2 * e]))));
+    const int32_t f1 = edge_he[2 * e] / 3, f2 = edge_he[2 * e + 1] / 3;
+    ef[2 * i] = f1;
+    ef[2 * i + 1] = f2;
+    const v3 zero = mk(0.0, 0.0, 0.0);
+    st3(lam, 2 * i, zero);
+    st3(lam, 2 * i + 1, zero);
+    const double a1 = area[f1], a2 = area[f2];
+    const double tt = a1 + a2;  // scale2 += A1 + A2 (grad_face.hpp:83)
+    term[i] = tt;
+    s += tt;
+    if (C) {
+      v3 y1, y2, d1, d2;
+      face_y_update(i, ld3(h, f1), ld3(h, f2), a1, a2, mu, edir, zero, zero, y1, y2, d1, d2);
+      st3(C, 2 * i, add(y1, d1));
+      st3(C, 2 * i + 1, add(y2, d2));
+    }
+  }
+  s = block_sum<B>(s);
+  if (threadIdx.x == 0) part[blockIdx.x] = s;
+}
+
 // The face kernel needs, per slot (interior edge i, side), only
 // c = y + lambda / (mu sqrt(A_side)) (grad_face.hpp:150): the edge kernel writes
 // c instead of Y, and recomputes Y from the previous g (kept in a second
 // buffer) and lambda when it needs it. 48 B per face less to read, no Y
 // round trip; every value is the reference's expression, so bits are unchanged.
-__global__ void k_face_first_c(const int32_t* __restrict__ ef, const double* __restrict__ area,
-                               const double* __restrict__ g, const double* __restrict__ edir,
-                               const double* __restrict__ lam, int64_t ni, double mu, double* __restrict__ C) {
-  GRID_STRIDE(i, ni) {
-    const int32_t f1 = ef[2 * i], f2 = ef[2 * i + 1];
-    v3 y1, y2, d1, d2;
-    face_y_update(i, ld3(g, f1), ld3(g, f2), area[f1], area[f2], mu, edir, ld3(lam, 2 * i), ld3(lam, 2 * i + 1), y1,
-                  y2, d1, d2);
-    st3(C, 2 * i, add(y1, d1));
-    st3(C, 2 * i + 1, add(y2, d2));
-  }
-}
 
 // G-update per face (grad_face.hpp:139-155) + dual partials (170-171, 104-111):
 // g_out = (2h + mu sum_k c_k) / (2 + mu count), dual term from g_out - g_in
@@ -506,19 +507,13 @@ AdmmResult admm_face_dev(gh_mesh* m, const double* d_h, const gh_admm_config& cf
   GH_CUDA(cudaMemcpyAsync(gtmp.p, d_h, sizeof(double) * 3 * F, cudaMemcpyDeviceToDevice, s));
   if (F) k_face_slots<<<G, B, 0, s>>>(m->he_edge.p, m->interior_edge_index.p, m->edge_he.p, F, slot.p);
   Scratch<double> term_p(NI + 1, s), term_d(F + 1, s);  // per-element residual terms
-  k_face_init_edges<<<G, B, 0, s>>>(m->pos.p, m->interior_edges.p, m->edge_v.p, m->edge_he.p, m->face_area.p, NI,
-                                    edir.p, ef.p, lam.p, part_primal, term_p.p);
+  k_face_init_edges<<<G, B, 0, s>>>(m->pos.p, m->interior_edges.p, m->edge_v.p, m->edge_he.p, m->face_area.p, d_h,
+                                    NI, mu, edir.p, ef.p, lam.p, cfg.max_iterations > 0 ? Cs.p : nullptr,
+                                    part_primal, term_p.p);
   GH_LAUNCH_CHECK();
   m->launches += 2;
   // ||M||_F (grad_face.hpp:85): the reference's left-to-right sum, exactly
   const double scale = std::sqrt(sequential_sum_nonneg(term_p.p, NI, s, &m->launches));
-  if (cfg.max_iterations > 0 && NI) {
-    // y1, y2 start at H of the side faces (grad_face.hpp:82-83) == Y-update from
-    // g = h, lambda = 0 of iteration 0 (computed here exactly like later ones)
-    k_face_first_c<<<G, B, 0, s>>>(ef.p, m->face_area.p, d_g, edir.p, lam.p, NI, mu, Cs.p);
-    GH_LAUNCH_CHECK();
-    m->launches++;
-  }
   // grad_face.hpp:175-177
   admm_loop(m, res, cfg, scale, mu, term_p.p, NI, term_d.p, F, [&](int32_t it, const int32_t* halt) {
     const double* gin = gbuf[(it + 1) & 1];

@@ -371,3 +371,21 @@ def test_diffusion_column_formats_bitwise(gpu, port_oracle, monkeypatch, mode):
         assert_same(gh.gs_diffuse(mesh, lv, t, gh.DiffusionConfig(sweeps=sweeps)), ref, f"C{config} ({mode})")
         assert lv.column_bits == want_bits
         assert_same(bands.gs_diffuse_bands(mesh, lv, 3, t, sweeps), ref, f"C{config} 3 bands ({mode})")
+
+
+def test_repeated_solves_reuse_cached_blocks(gpu):
+    """Device blocks are recycled by exact size across solves (gh_alloc.cu):
+    end-to-end solves of two meshes, interleaved and repeated (handles created
+    and destroyed every time, so every large block comes from the cache after
+    the first round), return the first round's distances bit for bit."""
+    from paper_1812_06060_b200 import meshgen
+    gh = gpu
+    ws = [meshgen.config(2, scale=8), meshgen.config(3, scale=16)]
+    first = []
+    for rnd in range(3):
+        for k, w in enumerate(ws):
+            d, rep = gh.distance_host(w.positions, w.faces, w.sources, w.method, 200, w.t, w.m)
+            if rnd == 0:
+                first.append(d)
+            else:
+                assert_same(d, first[k], f"round {rnd}, mesh {k}")
