@@ -27,6 +27,7 @@ fixed); the roofline is rank 0's own band.
 from __future__ import annotations
 
 import argparse
+import gc
 import json
 import os
 import subprocess
@@ -289,6 +290,12 @@ def main():
     achieved = bytes_per_sweep * w.sweeps / (step_ms * 1e-3) / 1e9
     traffic, traffic_src = recorded_traffic(workload, w.sweeps) if world == 1 else (None, None)
 
+    # the device-resident solve's handles go before the end-to-end calls build
+    # their own (config 5 holds ~70 GB per mesh + levels)
+    n_levels, max_width = lv.level_count(), lv.max_level_width
+    band = lv = mesh = None
+    gc.collect()
+
     # ---- e2e: host arrays in -> distances out through the C ABI, pinned buffers
     P = np.ascontiguousarray(w.positions, dtype=np.float64)
     Fc = np.ascontiguousarray(w.faces, dtype=np.int32)
@@ -351,7 +358,7 @@ def main():
         "warmup": a.warmup, "ms_per_step": step_ms_max, "higher_is_better": True,
         "scaling": "weak" if world == 1 else "strong", "vs_baseline": None, "dtype": "f64",
         "data": "synthetic (seeded BASELINE config mesh, DESIGN.md §5)",
-        "config": dict(base_cfg, t=t, levels=lv.level_count(), max_level_width=lv.max_level_width,
+        "config": dict(base_cfg, t=t, levels=n_levels, max_level_width=max_width,
                        parallelism="single-gpu" if world == 1 else f"bfs-bands x{world}",
                        **({} if band is None else {"band_levels_rank0": [band.lb, band.le],
                                                    "band_rows_rank0": rows_mine})),

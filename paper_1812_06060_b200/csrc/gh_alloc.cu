@@ -10,6 +10,7 @@
 // request is a cache hit and the pool never has to map new memory mid-solve.
 
 #include <cstdio>
+#include <cstdlib>
 #include <list>
 #include <mutex>
 
@@ -19,7 +20,10 @@ namespace gh {
 
 namespace {
 
-constexpr size_t kCacheMin = size_t(1) << 20;
+constexpr size_t kCacheMin = size_t(1) << 20;  // smaller blocks: the pool directly
+constexpr size_t kCacheMax = size_t(2) << 30;  // larger ones too: a cache holding them kept the
+                                               // pool from reusing that memory for other sizes
+                                               // (config 5: every call ran out of memory once)
 
 struct Block {
   void* p;
@@ -32,7 +36,7 @@ struct Cache {
   std::mutex mu;
   std::list<Block> blocks;    // oldest first
   size_t bytes[64] = {};      // cached bytes per device
-  size_t limit[64] = {};      // half of the device memory, set on first use
+  size_t limit[64] = {};      // an eighth of the device memory, set on first use
   std::vector<cudaEvent_t> spare_events;
 };
 
@@ -67,7 +71,7 @@ void* dev_alloc(size_t bytes, cudaStream_t s) {
   int dev = 0;
   GH_CUDA(cudaGetDevice(&dev));
   Cache& c = cache();
-  if (bytes >= kCacheMin && dev >= 0 && dev < 64) {
+  if (bytes >= kCacheMin && bytes <= kCacheMax && dev >= 0 && dev < 64) {
     std::lock_guard<std::mutex> lock(c.mu);
     for (auto it = c.blocks.begin(); it != c.blocks.end(); ++it) {
       if (it->bytes != bytes || it->device != dev) continue;
@@ -81,9 +85,21 @@ void* dev_alloc(size_t bytes, cudaStream_t s) {
   }
   void* p = nullptr;
   cudaError_t e = cudaMallocAsync(&p, bytes, s);
-  if (e == cudaErrorMemoryAllocation) {  // hand the cached blocks back and retry once
+  if (e == cudaErrorMemoryAllocation && getenv("GH_ALLOC_TRACE"))
+    fprintf(stderr, "[gh_alloc] %zu B: pool allocation failed, flushing the cache\n", bytes);
+  if (e == cudaErrorMemoryAllocation) {  // hand the cached blocks back to the pool and retry
     (void)cudaGetLastError();
     dev_cache_flush();
+    e = cudaMallocAsync(&p, bytes, s);
+  }
+  if (e == cudaErrorMemoryAllocation) {
+    // the pool's free blocks are too fragmented for this request: let it return
+    // what it holds unused to the driver (slow: the memory is mapped again), retry
+    (void)cudaGetLastError();
+    cudaMemPool_t pool;
+    if (cudaDeviceSynchronize() == cudaSuccess && cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess)
+      cudaMemPoolTrimTo(pool, 0);
+    (void)cudaGetLastError();
     e = cudaMallocAsync(&p, bytes, s);
   }
   GH_CUDA(e);
@@ -94,7 +110,7 @@ void dev_free(void* p, size_t bytes, cudaStream_t s) {
   if (!p) return;
   // the block's own device (a handle may be destroyed with another device current)
   cudaPointerAttributes attr{};
-  if (bytes < kCacheMin || cudaPointerGetAttributes(&attr, p) != cudaSuccess || attr.device < 0 ||
+  if (bytes < kCacheMin || bytes > kCacheMax || cudaPointerGetAttributes(&attr, p) != cudaSuccess || attr.device < 0 ||
       attr.device >= 64) {
     (void)cudaGetLastError();
     cudaFreeAsync(p, s);
@@ -106,7 +122,7 @@ void dev_free(void* p, size_t bytes, cudaStream_t s) {
   if (!c.limit[dev]) {
     size_t free_b = 0, total_b = 0;
     if (cudaMemGetInfo(&free_b, &total_b) != cudaSuccess) total_b = 0;
-    c.limit[dev] = total_b / 2;
+    c.limit[dev] = total_b / 8;
   }
   cudaEvent_t ev = nullptr;
   try {

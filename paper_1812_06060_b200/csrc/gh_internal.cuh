@@ -56,14 +56,14 @@ inline unsigned grid_for(int64_t n, int block = kBlock, int64_t cap = 148 * 32) 
 // stream from the device's default memory pool, whose release threshold is
 // raised once per device (gh_mesh_create) so freed handle memory stays cached
 // for the next solve instead of going back to the driver.
-// Stream-ordered allocation with an exact-size cache for large blocks
+// Stream-ordered allocation with an exact-size cache for mid-size blocks
 // (gh_alloc.cu). The default pool keeps freed memory (release threshold
 // raised), but it fragments: an end-to-end solve that repeats the previous
 // one's allocations still made the pool map new memory now and then (one
-// 134 MB request taking 134 ms). Blocks of 1 MB and more are therefore kept
+// 134 MB request taking 134 ms). Blocks from 1 MB to 2 GB are therefore kept
 // by size on free (with an event recorded on the freeing stream) and handed
 // back to the next request of exactly that size (the requesting stream waits
-// on the event). The cache is bounded (half of device memory, oldest
+// on the event). The cache is bounded (an eighth of device memory, oldest
 // blocks go back to the pool first) and flushed when an allocation fails.
 void* dev_alloc(size_t bytes, cudaStream_t s);
 void dev_free(void* p, size_t bytes, cudaStream_t s);
