@@ -45,13 +45,15 @@ __global__ void k_deg_big(const int32_t* __restrict__ perm, const int32_t* __res
   }
 }
 
-// per own chunk: its level, width = longest row, and the row lengths
+// per own chunk: its level, width = longest row, and the row lengths; *maxdeg
+// = the longest row of the band (one atomic per block)
 __global__ void k_chunk_meta(const int32_t* __restrict__ perm, const int32_t* __restrict__ level,
                              const int32_t* __restrict__ vv_off, int64_t nchunks, int32_t* __restrict__ chunk_level,
                              int64_t* __restrict__ width, uint16_t* __restrict__ deg, int32_t* __restrict__ maxdeg) {
   const int lane = threadIdx.x & 31;
   const int64_t warp = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
   const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  int32_t wm = 0;
   for (int64_t c = warp; c < nchunks; c += nwarps) {
     const int64_t r = c * 32 + lane;
     const int32_t v = perm[r];
@@ -59,12 +61,18 @@ __global__ void k_chunk_meta(const int32_t* __restrict__ perm, const int32_t* __
     int32_t m = d;
     for (int o = 16; o > 0; o >>= 1) m = max(m, __shfl_xor_sync(0xffffffffu, m, o));
     deg[r] = (uint16_t)(d > 65535 ? 65535 : d);
+    wm = max(wm, m);
     if (lane == 0) {
       width[c] = 32 * (int64_t)m;
       chunk_level[c] = level[perm[c * 32]];  // levels are chunk aligned: row 0 of a chunk is real
-      if (m >= 65535) atomicMax(maxdeg, m);
     }
   }
+  __shared__ int32_t sm;
+  if (threadIdx.x == 0) sm = 0;
+  __syncthreads();
+  if (lane == 0 && wm) atomicMax(&sm, wm);
+  __syncthreads();
+  if (threadIdx.x == 0 && sm) atomicMax(maxdeg, sm);
 }
 
 __global__ void k_sell_fill(const int32_t* __restrict__ perm, const int32_t* __restrict__ level,
@@ -279,7 +287,8 @@ void band_build(gh_levels* L, Band* b, int32_t lb, int32_t le) {
                                                                        b->own_chunks, b->chunk_level.p, width.p,
                                                                        b->deg.p, maxdeg.p);
     GH_LAUNCH_CHECK();
-    if (read_scalar(maxdeg.p, s) >= 65535) {
+    b->max_chunk_width = read_scalar(maxdeg.p, s);  // the widest chunk = the longest row
+    if (b->max_chunk_width >= 65535) {
       // valences past the 16-bit row length: the kernel reads these rows' true
       // length here (deg holds the 65535 marker)
       b->deg_big.alloc(b->nrows, s);
@@ -291,13 +300,7 @@ void band_build(gh_levels* L, Band* b, int32_t lb, int32_t le) {
     Scratch<char> t(tmp, s);
     GH_CUDA(cub::DeviceScan::ExclusiveSum(t.p, tmp, width.p, b->chunk_ptr.p, b->own_chunks + 1, s));
   }
-  std::vector<int64_t> cp(b->own_chunks + 1);
-  GH_CUDA(cudaMemcpyAsync(cp.data(), b->chunk_ptr.p, sizeof(int64_t) * cp.size(), cudaMemcpyDeviceToHost, s));
-  GH_CUDA(cudaStreamSynchronize(s));
-  int64_t wmax = 0;
-  for (int32_t c = 0; c < b->own_chunks; ++c) wmax = std::max(wmax, (cp[c + 1] - cp[c]) / 32);
-  b->max_chunk_width = (int32_t)wmax;
-  const int64_t nnz = cp[b->own_chunks];
+  const int64_t nnz = read_scalar(b->chunk_ptr.p + b->own_chunks, s);
   b->col.alloc(nnz, s);
   b->wt.alloc(nnz, s);
   if (nnz) {
