@@ -188,6 +188,7 @@ def cpu_reference_rate(w, sample_sweeps: int, steps: int, warmup: int):
     build_s = time.time() - t0
     t = w.t if w.t is not None else mesh.diffusion_time(w.m)
     reach = mesh.nv - lv.unreachable
+    shape = {"t": t, "levels": lv.nlev, "max_level_width": int(np.diff(lv.offsets).max()) if lv.nlev else 0}
     if sample_sweeps <= 0:
         u, rep = mesh.gs_diffuse(lv, t, 1)
         per = max(rep.wall_seconds, 1e-6)
@@ -199,7 +200,7 @@ def cpu_reference_rate(w, sample_sweeps: int, steps: int, warmup: int):
             rates.append(reach * sample_sweeps / rep.wall_seconds)
     info = {"kind": kind, "cores": cores, "sample": f"{sample_sweeps} gs_diffuse sweeps of {w.name} "
             f"({reach} reachable vertices), mesh built outside the timed region ({build_s:.1f} s)",
-            "sample_sweeps": sample_sweeps}
+            "sample_sweeps": sample_sweeps, "shape": shape}
     return rates, info
 
 
@@ -208,6 +209,16 @@ def main():
     a = parse()
     rank, world, local, dist = dist_setup(a.gpus)
     from paper_1812_06060_b200 import meshgen
+    if a.impl == "reference":
+        if rank != 0:
+            return
+        # the same workload source built under oracle/_ref: this process maps
+        # nothing of the product (only the reference and its test harness)
+        from oracle import oracle as orc
+        gen = os.path.join(orc.REF_DIR, "libgh_meshgen.so")
+        if not os.path.exists(gen):
+            orc.build()
+        meshgen.use_library(gen)
     w = meshgen.config(a.config)
     w.sweeps = a.sweeps
     workload = f"C{a.config} {w.name} {w.method}, {w.sweeps} sweeps, {w.admm_iters} ADMM iters"
@@ -216,15 +227,13 @@ def main():
                 "l2": "inputs larger than L2 (CSR+u >= 0.8 GB vs 126 MB)" if a.config >= 3 else "working set may fit L2"}
 
     if a.impl == "reference":
-        if rank != 0:
-            return
         rates, info = cpu_reference_rate(w, a.cpu_sample_sweeps, a.steps, a.warmup)
         v = float(np.mean(rates))
         line = {"metric": METRIC, "value": v, "unit": "vertex-updates/s", "n_gpus": world, "steps": a.steps,
                 "warmup": a.warmup, "ms_per_step": 1e3 * info["sample_sweeps"] * (w.positions.shape[0]) / v,
                 "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
-                "data": "synthetic (seeded BASELINE config mesh)", "impl": "reference",
-                "config": dict(base_cfg, parallelism="cpu-openmp"),
+                "data": "synthetic (seeded BASELINE config mesh, DESIGN.md §5)", "impl": "reference",
+                "config": dict(base_cfg, **info["shape"]), "parallelism": f"cpu-openmp x{info['cores']}",
                 "cpu_baseline": {"value": v, "unit": "vertex-updates/s", "cores": info["cores"], "kind": info["kind"],
                                  "sample": info["sample"]},
                 "e2e": {"value": v, "unit": "vertex-updates/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
@@ -267,6 +276,10 @@ def main():
             band.prepare(t)
             barrier(dist)  # every rank's counters are zeroed before any kernel runs
             band.launch(t, w.sweeps, rep, copy_out=False)
+            # the upper neighbour's last task writes into this band's ghost rows and
+            # counters after this band's own kernel may have finished: nobody
+            # prepares the next solve until every rank's kernel has returned
+            barrier(dist)
 
     launches = 0
     for _ in range(a.warmup):
@@ -293,6 +306,7 @@ def main():
     # the device-resident solve's handles go before the end-to-end calls build
     # their own (config 5 holds ~70 GB per mesh + levels)
     n_levels, max_width = lv.level_count(), lv.max_level_width
+    band_info = None if band is None else [band.lb, band.le]
     band = lv = mesh = None
     gc.collect()
 
@@ -358,10 +372,9 @@ def main():
         "warmup": a.warmup, "ms_per_step": step_ms_max, "higher_is_better": True,
         "scaling": "weak" if world == 1 else "strong", "vs_baseline": None, "dtype": "f64",
         "data": "synthetic (seeded BASELINE config mesh, DESIGN.md §5)",
-        "config": dict(base_cfg, t=t, levels=n_levels, max_level_width=max_width,
-                       parallelism="single-gpu" if world == 1 else f"bfs-bands x{world}",
-                       **({} if band is None else {"band_levels_rank0": [band.lb, band.le],
-                                                   "band_rows_rank0": rows_mine})),
+        "config": dict(base_cfg, t=t, levels=n_levels, max_level_width=max_width),
+        "parallelism": "single-gpu" if world == 1 else f"bfs-bands x{world}",
+        **({} if band_info is None else {"band_levels_rank0": band_info[:2], "band_rows_rank0": rows_mine}),
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
                      "traffic": traffic, "peak_source": peak_src, "kernel": "k_diffuse_tma",
                      "algorithmic_bytes_per_launch": bytes_per_sweep * w.sweeps,

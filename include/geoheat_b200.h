@@ -15,8 +15,12 @@
  *   - every function returns a gh_status; gh_last_error() gives the message
  *     of the last failure on the calling thread.
  *   - handles own device memory on the device that was current (or chosen by
- *     gh_set_device) at creation, and one CUDA stream each. Thread-compatible:
- *     one handle per host thread, not internally re-entrant.
+ *     gh_set_device) at creation, and one CUDA stream each. Thread-safe: calls
+ *     on one mesh (or on levels / bands built on it) from several host threads
+ *     are serialised by a per-mesh lock (the reference's functions are pure on
+ *     const objects, so concurrent calls must not corrupt each other); calls on
+ *     different meshes run concurrently. Every call restores the calling
+ *     thread's current CUDA device before it returns.
  *   - host buffers are caller-owned; outputs are written before return.
  */
 #ifndef GEOHEAT_B200_H
@@ -320,6 +324,11 @@ gh_status gh_band_info(const gh_band* band, int32_t* lb, int32_t* le, int32_t* o
 gh_status gh_band_export(const gh_band* band, void* blob, int32_t capacity, int32_t* size);
 /* lower_blob / upper_blob NULL for the first / last band. */
 gh_status gh_band_connect(gh_band* band, const void* lower_blob, const void* upper_blob);
+/* Every rank prepares before any rank launches (a barrier between), and no rank
+   prepares the next solve until every rank's gh_band_launch of the previous one
+   has returned (a barrier after the launch): the upper neighbour's last sweep
+   writes into this band's ghost rows and counters after this band's own kernel
+   may have finished, and prepare re-initialises both. */
 gh_status gh_band_prepare(gh_band* band, double t, const double* initial);
 /* u_out (host [V], may be NULL): this band's vertices hold the result. */
 gh_status gh_band_launch(gh_band* band, double t, int32_t sweeps, double* u_out, gh_solver_report* report);

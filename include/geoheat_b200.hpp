@@ -203,6 +203,7 @@ struct BfsLevels {
       parent_of_vertex = std::move(o.parent_of_vertex);
       unreachable_count = o.unreachable_count;
       h_ = std::exchange(o.h_, nullptr);
+      mesh_ = std::exchange(o.mesh_, nullptr);
     }
     return *this;
   }
@@ -212,10 +213,17 @@ struct BfsLevels {
     if (h_) gh_bfs_destroy(h_);
   }
   gh_levels* handle() const { return h_; }
+  /// The levels' device layout belongs to the mesh they were built on; the
+  /// solvers reject another mesh (the Python mirror raises the same way).
+  void require_mesh(const TriMesh& mesh, const char* fn) const {
+    if (mesh.handle() != mesh_)
+      throw std::invalid_argument(std::string(fn) + ": levels were built on a different mesh");
+  }
 
  private:
   friend BfsLevels bfs_levels(const TriMesh&, std::span<const Index>);
   gh_levels* h_ = nullptr;
+  gh_mesh* mesh_ = nullptr;
 };
 
 /// build_mesh (mesh.hpp:113-286) with device preprocessing.
@@ -252,6 +260,7 @@ inline FaceField face_gradient(const TriMesh& mesh, const VertexScalarField& u) 
 inline BfsLevels bfs_levels(const TriMesh& mesh, std::span<const Index> sources) {
   BfsLevels out;
   detail::check(gh_bfs_create(mesh.handle(), sources.data(), static_cast<std::int32_t>(sources.size()), &out.h_));
+  out.mesh_ = mesh.handle();
   gh_levels_info info{};
   detail::check(gh_bfs_get_info(out.h_, &info));
   const std::size_t nv = static_cast<std::size_t>(mesh.vertex_count());
@@ -273,6 +282,7 @@ inline VertexScalarField gs_diffuse(const TriMesh& mesh, const BfsLevels& levels
                                     const DiffusionConfig& config, SolverReport* report = nullptr,
                                     const VertexScalarField* initial = nullptr) {
   config.validate();
+  levels.require_mesh(mesh, "gs_diffuse");
   VertexScalarField u(static_cast<std::size_t>(mesh.vertex_count()));
   gh_solver_report r{};
   std::vector<double> hist(static_cast<std::size_t>(config.sweeps > 0 ? config.sweeps : 1));
@@ -294,7 +304,9 @@ inline VertexScalarField gs_diffuse(const TriMesh& mesh, const BfsLevels& levels
 }
 
 /// diffusion_residual (diffusion.hpp:35-49); `levels` must be the BFS of `sources`.
-inline double diffusion_residual(const TriMesh&, const VertexScalarField& u, double t, const BfsLevels& levels) {
+inline double diffusion_residual(const TriMesh& mesh, const VertexScalarField& u, double t,
+                                 const BfsLevels& levels) {
+  levels.require_mesh(mesh, "diffusion_residual");
   double e1 = 0.0;
   detail::check(gh_diffusion_residual(levels.handle(), u.data(), t, &e1));
   return e1;
@@ -364,6 +376,7 @@ inline EdgeAdmmResult admm_edge_optimize(const TriMesh& mesh, const FaceField& t
 /// integrate_face_gradients (integrate.hpp:40-59).
 inline VertexScalarField integrate_face_gradients(const TriMesh& mesh, const BfsLevels& levels,
                                                   const FaceField& gradients) {
+  levels.require_mesh(mesh, "integrate_face_gradients");
   VertexScalarField d(static_cast<std::size_t>(mesh.vertex_count()));
   detail::check(gh_integrate_face_gradients(levels.handle(), detail::flat(gradients), d.data()));
   return d;
@@ -372,6 +385,7 @@ inline VertexScalarField integrate_face_gradients(const TriMesh& mesh, const Bfs
 /// integrate_edge_differences (integrate.hpp:64-75).
 inline VertexScalarField integrate_edge_differences(const TriMesh& mesh, const BfsLevels& levels,
                                                     const EdgeDiffField& differences) {
+  levels.require_mesh(mesh, "integrate_edge_differences");
   VertexScalarField d(static_cast<std::size_t>(mesh.vertex_count()));
   detail::check(gh_integrate_edge_differences(levels.handle(), differences.data(), d.data()));
   return d;

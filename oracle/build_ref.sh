@@ -1,6 +1,8 @@
 #!/usr/bin/env bash
 # TEST INFRASTRUCTURE ONLY. Builds the two oracle libraries into oracle/_ref/:
 #   libgeoheat_port.so  the C restatement (oracle/geoheat_oracle.c); always built.
+#   libgh_meshgen.so    the seeded BASELINE workload generators (workloads/meshgen.c),
+#                       so bench.py's CPU reference arm maps no product library.
 #   libgeoheat_ref.so   the unmodified reference headers compiled in place from
 #                       /root/reference/proj/{include,tests} with the Eigen shim;
 #                       built only when /root/reference exists (this container).
@@ -15,6 +17,10 @@ REF="${GEOHEAT_REFERENCE:-/root/reference/proj}"
 gcc -std=gnu11 -O2 -DNDEBUG -fopenmp -ffp-contract=off -fPIC -shared \
     -o "$out/libgeoheat_port.so.tmp" "$here/geoheat_oracle.c" -lm
 mv "$out/libgeoheat_port.so.tmp" "$out/libgeoheat_port.so"
+
+gcc -std=gnu11 -O2 -fPIC -shared -ffp-contract=off \
+    -o "$out/libgh_meshgen.so.tmp" "$here/../workloads/meshgen.c" -lm
+mv "$out/libgh_meshgen.so.tmp" "$out/libgh_meshgen.so"
 
 if [ -d "$REF/include/geoheat" ]; then
   g++ -std=gnu++20 -O2 -DNDEBUG -fopenmp -ffp-contract=off -fPIC -shared \

@@ -3,7 +3,7 @@
   lib/libgeoheat_b200.so   the CUDA path: csrc/*.cu for sm_100a, fp64 with
                            FMA contraction off (-fmad=false) so element values
                            match the reference bit for bit.
-  lib/libgh_meshgen.so     host C mesh generators for the BASELINE configs.
+  lib/libgh_meshgen.so     host C mesh generators for the BASELINE configs (workloads/meshgen.c).
 
 The libraries are built in place (not pip-installed) so they travel with the
 repo snapshot to the GPU box.
@@ -22,6 +22,9 @@ CSRC = os.path.join(PKG, "csrc")
 LIBDIR = os.path.join(PKG, "lib")
 CUDA_LIB = os.path.join(LIBDIR, "libgeoheat_b200.so")
 MESHGEN_LIB = os.path.join(LIBDIR, "libgh_meshgen.so")
+# the seeded BASELINE workloads (not the solver path): shared with the CPU
+# reference arm, which builds its own copy under oracle/_ref/
+MESHGEN_SRC = os.path.join(ROOT, "workloads", "meshgen.c")
 CLI_BIN = os.path.join(LIBDIR, "geoheat_b200")
 CLI_SRC = os.path.join(PKG, "cli", "geoheat_cli.cpp")
 
@@ -48,7 +51,7 @@ def _newer(target: str, sources) -> bool:
 
 def build_meshgen(force: bool = False) -> str:
     os.makedirs(LIBDIR, exist_ok=True)
-    src = os.path.join(CSRC, "meshgen.c")
+    src = MESHGEN_SRC
     if force or not _newer(MESHGEN_LIB, [src]):
         tmp = MESHGEN_LIB + ".tmp"
         subprocess.run(["gcc", "-std=gnu11", "-O2", "-fPIC", "-shared", "-ffp-contract=off", "-o", tmp, src, "-lm"],

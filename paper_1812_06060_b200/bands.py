@@ -14,6 +14,9 @@ Multi-process use (one process per GPU, torch.distributed for the plumbing):
     band.prepare(t)                   # every rank
     dist.barrier()                    # all counters zeroed before any kernel runs
     u = band.launch(t, sweeps)        # this rank's vertices of u
+    dist.barrier()                    # before the next prepare: a neighbour's last
+                                      # sweep still writes into our ghost rows and
+                                      # counters after our own kernel returned
 
 `gs_diffuse_bands` runs the same schedule with all bands on one GPU in one
 launch (the single-GPU emulation used by the tests).

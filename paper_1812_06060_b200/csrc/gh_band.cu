@@ -189,12 +189,16 @@ T read_scalar(const T* d, cudaStream_t s) {
 namespace gh {
 
 Band::~Band() {
-  if (ubuf || rows_done || stalled) cudaSetDevice(device);
+  if (!ubuf && !rows_done && !stalled) return;
+  int prev = -1;
+  if (cudaGetDevice(&prev) != cudaSuccess) prev = -1;
+  if (prev != device) cudaSetDevice(device);
   for (void* p : {(void*)ubuf, (void*)rows_done, (void*)stalled}) {
     if (!p) continue;
     if (ipc) cudaFree(p);
     else cudaFreeAsync(p, astream);
   }
+  if (prev >= 0 && prev != device) cudaSetDevice(prev);  // the caller's current device stays
 }
 
 uint64_t Band::device_bytes() const {

@@ -47,7 +47,15 @@ void require(bool ok, const char* what) {
   if (!ok) gh::fail(GH_ERR_INVALID, what);
 }
 
-void use_device_of(const gh_mesh* m) { GH_CUDA(cudaSetDevice(m->device)); }
+// One C-ABI call's hold on a handle: the mesh's device for the call (the
+// caller's current device restored on return) and the mesh's lock, so calls
+// from several host threads on one mesh (or its levels / bands) run one after
+// another (gh_mesh::mtx).
+struct Use {
+  gh::DeviceScope dev;
+  std::lock_guard<std::recursive_mutex> lock;
+  explicit Use(const gh_mesh* m) : dev(m->device), lock(m->mtx) {}
+};
 
 template <class T>
 void to_host(T* dst, const T* src, size_t n, cudaStream_t s) {
@@ -279,7 +287,7 @@ gh_status gh_mesh_serialize(gh_mesh* mesh, int32_t format, const double* quality
     require(mesh && data && bytes, "gh_mesh_serialize: null argument");
     require(format == GH_FORMAT_OBJ || format == GH_FORMAT_PLY, "gh_mesh_serialize: unknown format");
     require(!quality || format == GH_FORMAT_PLY, "gh_mesh_serialize: quality is written by PLY only");
-    use_device_of(mesh);
+    Use use_(mesh);
     *data = to_malloc(gh::serialize_mesh(mesh, format, quality), bytes);
   });
 }
@@ -287,7 +295,7 @@ gh_status gh_mesh_serialize(gh_mesh* mesh, int32_t format, const double* quality
 gh_status gh_mesh_save(gh_mesh* mesh, const char* path, const double* quality) {
   return guarded([&] {
     require(mesh && path, "gh_mesh_save: null argument");
-    use_device_of(mesh);
+    Use use_(mesh);
     // save_mesh opens the file before it infers the format (mesh_io.hpp:321-326)
     FILE* probe = std::fopen(path, "wb");
     if (!probe) gh::fail(GH_ERR_MESH, std::string("cannot open output file '") + path + "'");
@@ -326,7 +334,7 @@ gh_status gh_write_distances(const char* path, const double* d, int64_t n, int32
 void gh_free(void* p) { std::free(p); }
 
 static void free_mesh(gh_mesh* mesh) {
-  cudaSetDevice(mesh->device);
+  gh::DeviceScope dev(mesh->device);
   cudaStreamSynchronize(mesh->stream);
   delete mesh;  // buffers return to the stream-ordered pool; stream and pinned scratch are per thread
 }
@@ -358,7 +366,7 @@ gh_status gh_mesh_get_info(const gh_mesh* mesh, gh_mesh_info* info) {
 gh_status gh_mesh_download(const gh_mesh* mesh, int32_t which, void* host_out, int64_t count) {
   return guarded([&] {
     require(mesh && host_out, "gh_mesh_download: null argument");
-    use_device_of(mesh);
+    Use use_(mesh);
     const void* src = nullptr;
     size_t n = 0, es = 0;
     const gh_mesh& m = *mesh;
@@ -403,7 +411,7 @@ gh_status gh_mesh_download(const gh_mesh* mesh, int32_t which, void* host_out, i
 gh_status gh_average_edge_length(gh_mesh* mesh, double* h_out) {
   return guarded([&] {
     require(mesh && h_out, "gh_average_edge_length: null argument");
-    use_device_of(mesh);
+    Use use_(mesh);
     *h_out = gh::mesh_average_edge_length(mesh);
   });
 }
@@ -412,7 +420,7 @@ gh_status gh_diffusion_time(gh_mesh* mesh, double m, double* t_out) {
   return guarded([&] {
     require(mesh && t_out, "gh_diffusion_time: null argument");
     if (!(m > 0.0)) gh::fail(GH_ERR_INVALID, "diffusion_time: m must be positive");
-    use_device_of(mesh);
+    Use use_(mesh);
     const double h = gh::mesh_average_edge_length(mesh);
     *t_out = m * h * h;  // diffusion.hpp:30-31
   });
@@ -421,7 +429,7 @@ gh_status gh_diffusion_time(gh_mesh* mesh, double m, double* t_out) {
 gh_status gh_face_gradient(gh_mesh* mesh, const double* u, double* grad_out) {
   return guarded([&] {
     require(mesh && u && grad_out, "gh_face_gradient: null argument");
-    use_device_of(mesh);
+    Use use_(mesh);
     cudaStream_t s = mesh->stream;
     gh::Scratch<double> du(mesh->nv, s), dg(3 * (size_t)mesh->nf, s);
     GH_CUDA(cudaMemcpyAsync(du.p, u, sizeof(double) * mesh->nv, cudaMemcpyHostToDevice, s));
@@ -434,7 +442,7 @@ gh_status gh_bfs_create(gh_mesh* mesh, const int32_t* sources, int32_t ns, gh_le
   return guarded([&] {
     require(mesh && out, "gh_bfs_create: null argument");
     require(ns == 0 || sources, "gh_bfs_create: null sources");
-    use_device_of(mesh);
+    Use use_(mesh);
     std::unique_ptr<gh_levels> L(new gh_levels());
     L->mesh = mesh;
     gh::bfs_build(L.get(), sources, ns);
@@ -447,9 +455,12 @@ gh_status gh_bfs_destroy(gh_levels* levels) {
   return guarded([&] {
     if (!levels) return;
     gh_mesh* m = levels->mesh;
-    cudaSetDevice(m->device);
-    cudaStreamSynchronize(m->stream);
-    delete levels;
+    gh::DeviceScope dev(m->device);
+    {
+      std::lock_guard<std::recursive_mutex> lock(m->mtx);
+      cudaStreamSynchronize(m->stream);
+      delete levels;
+    }
     if (--m->level_refs == 0 && m->destroy_pending) free_mesh(m);
   });
 }
@@ -469,7 +480,7 @@ gh_status gh_bfs_download(const gh_levels* levels, int32_t* level_of_vertex, int
   return guarded([&] {
     require(levels != nullptr, "gh_bfs_download: null levels");
     const gh_mesh* m = levels->mesh;
-    use_device_of(m);
+    Use use_(m);
     cudaStream_t s = m->stream;
     if (level_of_vertex) to_host(level_of_vertex, levels->level.p, m->nv, s);
     if (parent_of_vertex) to_host(parent_of_vertex, levels->parent.p, m->nv, s);
@@ -483,7 +494,7 @@ gh_status gh_gs_diffuse(gh_levels* levels, double t, int32_t sweeps, const doubl
   return guarded([&] {
     require(levels != nullptr, "gh_gs_diffuse: null levels");
     gh_mesh* m = levels->mesh;
-    use_device_of(m);
+    Use use_(m);
     cudaStream_t s = m->stream;
     const double w0 = now_s();
     take_launches(m);
@@ -508,7 +519,7 @@ gh_status gh_gs_diffuse_tol(gh_levels* levels, double t, int32_t sweeps, double 
   return guarded([&] {
     require(levels != nullptr, "gh_gs_diffuse_tol: null levels");
     gh_mesh* m = levels->mesh;
-    use_device_of(m);
+    Use use_(m);
     cudaStream_t s = m->stream;
     const double w0 = now_s();
     take_launches(m);
@@ -549,7 +560,7 @@ gh_status gh_diffusion_residual(gh_levels* levels, const double* u, double t, do
   return guarded([&] {
     require(levels && u && e1_out, "gh_diffusion_residual: null argument");
     gh_mesh* m = levels->mesh;
-    use_device_of(m);
+    Use use_(m);
     gh::Scratch<double> du(m->nv, m->stream);
     GH_CUDA(cudaMemcpyAsync(du.p, u, sizeof(double) * m->nv, cudaMemcpyHostToDevice, m->stream));
     *e1_out = gh::diffusion_residual_dev(levels, du.p, t);
@@ -559,7 +570,7 @@ gh_status gh_diffusion_residual(gh_levels* levels, const double* u, double t, do
 gh_status gh_normalized_target_gradients(gh_mesh* mesh, const double* u, double* h_out, int32_t* zero_count) {
   return guarded([&] {
     require(mesh && u && h_out, "gh_normalized_target_gradients: null argument");
-    use_device_of(mesh);
+    Use use_(mesh);
     cudaStream_t s = mesh->stream;
     gh::Scratch<double> du(mesh->nv, s), dh(3 * (size_t)mesh->nf, s);
     GH_CUDA(cudaMemcpyAsync(du.p, u, sizeof(double) * mesh->nv, cudaMemcpyHostToDevice, s));
@@ -573,7 +584,7 @@ gh_status gh_admm_face_optimize(gh_mesh* mesh, const double* h, const gh_admm_co
                                 gh_solver_report* report) {
   return guarded([&] {
     require(mesh && h && config && g_out, "gh_admm_face_optimize: null argument");
-    use_device_of(mesh);
+    Use use_(mesh);
     cudaStream_t s = mesh->stream;
     const double w0 = now_s();
     take_launches(mesh);
@@ -589,7 +600,7 @@ gh_status gh_admm_edge_optimize(gh_mesh* mesh, const double* h, const gh_admm_co
                                 gh_solver_report* report) {
   return guarded([&] {
     require(mesh && h && config && x_out, "gh_admm_edge_optimize: null argument");
-    use_device_of(mesh);
+    Use use_(mesh);
     cudaStream_t s = mesh->stream;
     const double w0 = now_s();
     take_launches(mesh);
@@ -612,7 +623,7 @@ gh_status gh_integrate_face_gradients(gh_levels* levels, const double* g, double
   return guarded([&] {
     require(levels && g && d_out, "gh_integrate_face_gradients: null argument");
     gh_mesh* m = levels->mesh;
-    use_device_of(m);
+    Use use_(m);
     cudaStream_t s = m->stream;
     gh::Scratch<double> dg(3 * (size_t)m->nf, s), dd(m->nv, s);
     GH_CUDA(cudaMemcpyAsync(dg.p, g, sizeof(double) * 3 * m->nf, cudaMemcpyHostToDevice, s));
@@ -625,7 +636,7 @@ gh_status gh_integrate_edge_differences(gh_levels* levels, const double* x, doub
   return guarded([&] {
     require(levels && x && d_out, "gh_integrate_edge_differences: null argument");
     gh_mesh* m = levels->mesh;
-    use_device_of(m);
+    Use use_(m);
     cudaStream_t s = m->stream;
     gh::Scratch<double> dx(m->ne, s), dd(m->nv, s);
     GH_CUDA(cudaMemcpyAsync(dx.p, x, sizeof(double) * m->ne, cudaMemcpyHostToDevice, s));
@@ -711,7 +722,7 @@ gh_status gh_distance(gh_levels* levels, const gh_pipeline_config* config, doubl
   return guarded([&] {
     require(levels && config && d_out, "gh_distance: null argument");
     gh_mesh* m = levels->mesh;
-    use_device_of(m);
+    Use use_(m);
     cudaStream_t s = m->stream;
     take_launches(m);
     if (report) std::memset(report, 0, sizeof(*report));
@@ -766,7 +777,7 @@ gh_status gh_poisson_heat_method(gh_levels* levels, double t, double cg_tol, dou
     require(levels && d_out, "gh_poisson_heat_method: null argument");
     require(t > 0.0 && cg_tol > 0.0, "gh_poisson_heat_method: t and cg_tol must be positive");
     gh_mesh* m = levels->mesh;
-    use_device_of(m);
+    Use use_(m);
     take_launches(m);
     gh::Scratch<double> dd(m->nv, m->stream);
     const gh::PoissonOut po = gh::poisson_heat_dev(levels, t, cg_tol, dd.p);
@@ -787,7 +798,7 @@ gh_status gh_poisson_heat_method(gh_levels* levels, double t, double cg_tol, dou
 gh_status gh_triangulation_quality(gh_mesh* mesh, double* tau_out) {
   return guarded([&] {
     require(mesh && tau_out, "gh_triangulation_quality: null argument");
-    use_device_of(mesh);
+    Use use_(mesh);
     *tau_out = gh::triangulation_quality_dev(mesh);
   });
 }
@@ -795,7 +806,7 @@ gh_status gh_triangulation_quality(gh_mesh* mesh, double* tau_out) {
 gh_status gh_mesh_subdivide(gh_mesh* mesh, int32_t levels, gh_mesh** out) {
   return guarded([&] {
     require(mesh && out, "gh_mesh_subdivide: null argument");
-    use_device_of(mesh);
+    Use use_(mesh);
     std::unique_ptr<gh_mesh> cur = new_mesh();
     if (levels <= 0) {
       gh::copy_mesh_arrays(mesh, cur.get());  // midpoint_subdivide(mesh, 0) returns the mesh
@@ -824,7 +835,7 @@ gh_status gh_analytic_distance(gh_mesh* mesh, int32_t kind, const int32_t* sourc
     require(mesh && d_out, "gh_analytic_distance: null argument");
     require(kind == GH_SURFACE_PLANE || kind == GH_SURFACE_SPHERE, "gh_analytic_distance: unknown surface");
     check_sources(mesh, sources, ns);
-    use_device_of(mesh);
+    Use use_(mesh);
     cudaStream_t s = mesh->stream;
     gh::Scratch<int32_t> src(ns, s);
     gh::Scratch<double> d(mesh->nv, s);
@@ -838,7 +849,7 @@ gh_status gh_dijkstra_distance(gh_mesh* mesh, const int32_t* sources, int32_t ns
   return guarded([&] {
     require(mesh && d_out, "gh_dijkstra_distance: null argument");
     check_sources(mesh, sources, ns);
-    use_device_of(mesh);
+    Use use_(mesh);
     cudaStream_t s = mesh->stream;
     gh::Scratch<int32_t> src(ns, s);
     gh::Scratch<double> d(mesh->nv, s);
@@ -939,7 +950,7 @@ gh_status gh_gs_diffuse_bands(gh_levels* levels, int32_t nbands, double t, int32
   return guarded([&] {
     require(levels != nullptr, "gh_gs_diffuse_bands: null levels");
     gh_mesh* m = levels->mesh;
-    use_device_of(m);
+    Use use_(m);
     cudaStream_t s = m->stream;
     const double w0 = now_s();
     take_launches(m);
@@ -971,7 +982,7 @@ gh_status gh_band_create(gh_levels* levels, int32_t rank, int32_t nranks, gh_ban
   return guarded([&] {
     require(levels && out, "gh_band_create: null argument");
     require(nranks >= 1 && rank >= 0 && rank < nranks, "gh_band_create: bad rank");
-    use_device_of(levels->mesh);
+    Use use_(levels->mesh);
     const std::vector<int32_t> cut = gh::plan_bands(levels->h_offsets, nranks);
     std::unique_ptr<gh_band> b(new gh_band());
     b->levels = levels;
@@ -986,7 +997,7 @@ gh_status gh_band_create(gh_levels* levels, int32_t rank, int32_t nranks, gh_ban
 gh_status gh_band_destroy(gh_band* band) {
   return guarded([&] {
     if (!band) return;
-    cudaSetDevice(band->levels->mesh->device);
+    Use use_(band->levels->mesh);
     cudaStreamSynchronize(band->levels->mesh->stream);
     for (void* p : band->opened) cudaIpcCloseMemHandle(p);
     delete band;
@@ -1010,7 +1021,7 @@ gh_status gh_band_export(const gh_band* band, void* blob, int32_t capacity, int3
     require(capacity >= (int32_t)sizeof(BandBlob), "gh_band_export: blob buffer too small");
     const gh::Band& b = band->band;
     BandBlob x{};
-    GH_CUDA(cudaSetDevice(b.device));
+    Use use_(band->levels->mesh);
     GH_CUDA(cudaIpcGetMemHandle(&x.ubuf, b.ubuf));
     GH_CUDA(cudaIpcGetMemHandle(&x.done, b.rows_done));
     x.nrows = b.nrows;
@@ -1028,7 +1039,7 @@ gh_status gh_band_connect(gh_band* band, const void* lower_blob, const void* upp
   return guarded([&] {
     require(band != nullptr, "gh_band_connect: null band");
     gh::Band& b = band->band;
-    GH_CUDA(cudaSetDevice(b.device));
+    Use use_(band->levels->mesh);
     auto open = [&](const cudaIpcMemHandle_t& h) {
       void* p = nullptr;
       GH_CUDA(cudaIpcOpenMemHandle(&p, h, cudaIpcMemLazyEnablePeerAccess));
@@ -1061,7 +1072,7 @@ gh_status gh_band_prepare(gh_band* band, double t, const double* initial) {
     require(band != nullptr, "gh_band_prepare: null band");
     if (!(t > 0.0)) gh::fail(GH_ERR_INVALID, "gs_diffuse: t must be positive");
     gh_mesh* m = band->levels->mesh;
-    use_device_of(m);
+    Use use_(m);
     cudaStream_t s = m->stream;
     gh::Scratch<double> dinit(initial ? m->nv : 0, s);
     if (initial) GH_CUDA(cudaMemcpyAsync(dinit.p, initial, sizeof(double) * m->nv, cudaMemcpyHostToDevice, s));
@@ -1076,7 +1087,7 @@ gh_status gh_band_launch(gh_band* band, double t, int32_t sweeps, double* u_out,
     require(band != nullptr, "gh_band_launch: null band");
     require(sweeps >= 1, "gh_band_launch: sweeps must be >= 1");
     gh_mesh* m = band->levels->mesh;
-    use_device_of(m);
+    Use use_(m);
     cudaStream_t s = m->stream;
     const double w0 = now_s();
     take_launches(m);

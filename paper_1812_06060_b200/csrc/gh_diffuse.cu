@@ -804,6 +804,9 @@ double diffuse_bands_dev(gh_levels* L, std::vector<Band*>& bands, double t, int3
   gh_mesh* m = L->mesh;
   cudaStream_t s = m->stream;
   if (sweeps < 0) fail(GH_ERR_INVALID, "DiffusionConfig: sweeps must be >= 0");
+  // the pipeline's step index tau < nlev + 2 * sweeps is an int32
+  if ((int64_t)L->nlev + 2 * (int64_t)sweeps >= 0x7fffffffLL)
+    fail(GH_ERR_INVALID, "gs_diffuse: sweeps must be below (2^31 - levels) / 2 for the sweep pipeline");
   if (!(t > 0.0)) fail(GH_ERR_INVALID, "gs_diffuse: t must be positive");
   k_init_orig<<<grid_for(m->nv), B, 0, s>>>(L->level.p, d_initial, m->nv, L->u_orig.p);
   GH_LAUNCH_CHECK();

@@ -11,6 +11,7 @@
 
 #include <cstdint>
 #include <cstdio>
+#include <mutex>
 #include <stdexcept>
 #include <string>
 #include <vector>
@@ -158,8 +159,42 @@ struct gh_mesh {
   int launches = 0;                  // kernels launched since the counter was last read
   int level_refs = 0;                // live gh_levels built on this mesh
   bool destroy_pending = false;      // gh_mesh_destroy called while levels were alive
+  // Every C-ABI entry point holds this while it uses the handle (or a gh_levels /
+  // gh_band built on it): the per-call state above (reduction scratch, launch
+  // counter, the levels' u buffers) and the one work stream are shared, so two
+  // host threads calling into the same mesh are serialised instead of
+  // interleaving on the stream (the reference's functions are pure on const
+  // objects, so concurrent calls must stay safe).
+  mutable std::recursive_mutex mtx;
   uint64_t device_bytes() const;
 };
+
+namespace gh {
+// Sets a device for the scope and restores the caller's current device after
+// (a host application or torch on another GPU keeps its own current device).
+struct DeviceScope {
+  int prev = -1;
+  explicit DeviceScope(int device) {
+    if (cudaGetDevice(&prev) != cudaSuccess) {
+      (void)cudaGetLastError();
+      prev = -1;
+    }
+    if (device != prev) {
+      const cudaError_t e = cudaSetDevice(device);
+      if (e != cudaSuccess) {
+        (void)cudaGetLastError();
+        throw Error{GH_ERR_CUDA, std::string("cudaSetDevice: ") + cudaGetErrorString(e)};
+      }
+    }
+  }
+  ~DeviceScope() {
+    int cur = -1;
+    if (prev >= 0 && cudaGetDevice(&cur) == cudaSuccess && cur != prev) cudaSetDevice(prev);
+  }
+  DeviceScope(const DeviceScope&) = delete;
+  DeviceScope& operator=(const DeviceScope&) = delete;
+};
+}  // namespace gh
 
 namespace gh {
 

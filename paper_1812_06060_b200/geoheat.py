@@ -591,6 +591,9 @@ def distance_host(positions, faces, sources, method: str = "face", sweeps: int =
     P = _f64(positions).reshape(-1, 3)
     Fc = np.ascontiguousarray(faces, dtype=np.int32).reshape(-1, 3)
     S = np.ascontiguousarray(sources, dtype=np.int32)
+    if out is not None and not (isinstance(out, np.ndarray) and out.dtype == np.float64 and out.ndim == 1
+                                and out.size == P.shape[0] and out.flags.c_contiguous and out.flags.writeable):
+        raise ValueError(f"distance_host: out must be a writeable C-contiguous float64 array of {P.shape[0]} values")
     d = out if out is not None else np.empty(P.shape[0], np.float64)
     cfg = _pipeline_config(method, sweeps, t, m, admm)
     rep = gh_run_report()

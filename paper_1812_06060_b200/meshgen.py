@@ -1,9 +1,13 @@
-"""Seeded synthetic meshes for BASELINE.json configs 1-5 (host C, csrc/meshgen.c).
+"""Seeded synthetic meshes for BASELINE.json configs 1-5 (host C, workloads/meshgen.c).
 
 The reference measures no public dataset; these generators stand in for the
 paper's scanned models with the shapes, sizes and value distributions
 BASELINE.json names. Both the GPU path and the CPU oracle consume the same
 arrays. Formulas and seeds: DESIGN.md §5.
+
+The generator library is lib/libgh_meshgen.so by default; the CPU reference
+arm of bench.py calls use_library() with its own build of the same source
+(oracle/_ref/libgh_meshgen.so), so that process maps nothing of the product.
 """
 from __future__ import annotations
 
@@ -19,14 +23,25 @@ from . import _build
 SEEDS = {k: 1812060600 + k for k in range(1, 6)}
 
 _lib = None
+_lib_path = None
+
+
+def use_library(path: str) -> None:
+    """Load the generators from `path` (a build of workloads/meshgen.c) instead."""
+    global _lib, _lib_path
+    if _lib is not None and _lib_path != path:
+        raise RuntimeError("meshgen: a generator library is already loaded")
+    _lib_path = path
 
 
 def _load():
-    global _lib
+    global _lib, _lib_path
     if _lib is None:
-        if not os.path.exists(_build.MESHGEN_LIB):
-            _build.build_meshgen()
-        L = C.CDLL(_build.MESHGEN_LIB)
+        if _lib_path is None:
+            if not os.path.exists(_build.MESHGEN_LIB):
+                _build.build_meshgen()
+            _lib_path = _build.MESHGEN_LIB
+        L = C.CDLL(_lib_path)
         PP = C.POINTER(C.POINTER(C.c_double))
         PI = C.POINTER(C.POINTER(C.c_int32))
         i32p = C.POINTER(C.c_int32)

@@ -2,11 +2,14 @@
 // run_pipelines) written against geoheat::b200 instead of geoheat, on config 1
 // (icosphere_mesh(5), source 0). argv[1] = t as a C99 hex float (the
 // reference's t, from tests/golden). Exit 0 iff both distance hashes equal the
-// reference's and a malformed mesh throws MeshError.
+// reference's, a malformed mesh throws MeshError, levels
+// of another mesh are rejected, and four host threads solving on the one mesh
+// at once all get the single-thread result (the per-mesh lock of the C ABI).
 #include "geoheat_b200.hpp"
 
 #include <cstdio>
 #include <cstdlib>
+#include <thread>
 
 extern "C" int gh_gen_icosphere(int32_t, double, double**, int32_t*, int32_t**, int32_t*);
 extern "C" void gh_gen_free(void*);
@@ -47,7 +50,41 @@ int main(int argc, char** argv) {
   } catch (const b200::MeshError& e) {
     threw = std::string(e.what()) == "non-manifold edge (0,1): 3 incident faces";
   }
-  const bool ok = hf == 0xcca540701b66bfd5ull && he == 0xa8e56e8b98582eb9ull && h.zero_count == 5560 && threw;
+  // levels built on another mesh: std::invalid_argument, as the Python mirror
+  bool mismatch = false;
+  {
+    b200::TriMesh other = b200::build_mesh(positions, faces);
+    try {
+      b200::gs_diffuse(other, levels, t, dc);
+    } catch (const std::invalid_argument& e) {
+      mismatch = std::string(e.what()) == "gs_diffuse: levels were built on a different mesh";
+    }
+  }
+  // concurrent solves on one mesh + levels from four threads
+  std::vector<std::uint64_t> got(4, 0);
+  {
+    std::vector<std::thread> th;
+    for (int i = 0; i < 4; ++i)
+      th.emplace_back([&, i] {
+        try {
+          b200::DiffusionConfig c;
+          c.sweeps = 300 + 100 * (i & 1);
+          got[i] = b200::field_hash(b200::gs_diffuse(mesh, levels, t, c));
+        } catch (...) {
+          got[i] = 1;
+        }
+      });
+    for (auto& x : th) x.join();
+  }
+  bool threads_ok = true;
+  for (int i = 0; i < 4; ++i) {
+    b200::DiffusionConfig c;
+    c.sweeps = 300 + 100 * (i & 1);
+    threads_ok = threads_ok && got[i] == b200::field_hash(b200::gs_diffuse(mesh, levels, t, c));
+  }
+  std::printf("mismatch rejected %d, threads %d\n", (int)mismatch, (int)threads_ok);
+  const bool ok = hf == 0xcca540701b66bfd5ull && he == 0xa8e56e8b98582eb9ull && h.zero_count == 5560 && threw &&
+                  mismatch && threads_ok;
   std::printf("%s\n", ok ? "PASS" : "FAIL");
   return ok ? 0 : 1;
 }

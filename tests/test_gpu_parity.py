@@ -152,17 +152,17 @@ def test_configs_reduced_size_vs_oracle(gpu, port_oracle, config, scale, sweeps)
 
 
 def test_config1_full_with_device_t(gpu, port_oracle):
-    """Config 1 end to end with t from the device mean edge length: distances agree
-    with the reference within 1e-9 relative (t differs from the reference's
-    sequential sum by a few ulps) and the error vs the great-circle geodesic
-    equals the reference's."""
+    """Config 1 end to end with t from the device mean edge length: t is the
+    reference's left-to-right sum bit for bit (gh_seqsum.cu), so the distances
+    are bit-identical, and the error vs the great-circle geodesic equals the
+    reference's."""
     from paper_1812_06060_b200 import meshgen
     gh = gpu
     w = meshgen.config(1)
     g = np.load(os.path.join(GOLDEN, "icosphere5_config1.npz"))
     d, rep = gh.distance_host(w.positions, w.faces, w.sources, "face", 1000, None, 1.0)
-    assert rep.t == pytest.approx(float(g["t"]), rel=1e-13)
-    np.testing.assert_allclose(d, g["d_face"], rtol=1e-9, atol=0)
+    assert np.float64(rep.t).view(np.uint64) == np.float64(g["t"]).view(np.uint64), (rep.t, float(g["t"]))
+    assert_same(d, g["d_face"], "C1 distances with the device t")
     P = w.positions
     exact = np.arccos(np.clip(P @ P[0] / (np.linalg.norm(P, axis=1) * np.linalg.norm(P[0])), -1, 1))
     mask = np.arange(len(d)) != 0
@@ -389,3 +389,47 @@ def test_repeated_solves_reuse_cached_blocks(gpu):
                 first.append(d)
             else:
                 assert_same(d, first[k], f"round {rnd}, mesh {k}")
+
+
+def _strip(nx: int, wobble: float = 0.013):
+    """A 2 x nx triangle strip (a ladder): a source at one end gives ~nx BFS rings."""
+    i = np.arange(nx, dtype=np.float64)
+    P = np.zeros((2 * nx, 3))
+    P[0::2, 0] = i
+    P[1::2, 0] = i + 0.5 * np.sin(i)  # irregular cotan weights
+    P[1::2, 1] = 1.0
+    P[:, 2] = wobble * np.cos(0.7 * np.arange(2 * nx))
+    a = 2 * np.arange(nx - 1, dtype=np.int32)
+    F = np.concatenate([np.stack([a, a + 2, a + 3], 1), np.stack([a, a + 3, a + 1], 1)]).astype(np.int32)
+    return P, F
+
+
+@pytest.mark.parametrize("nbands", [1, 3])
+def test_more_levels_than_the_shared_table(gpu, port_oracle, nbands):
+    """More than 12,288 BFS rings (gh_diffuse.cu kMaxSmemLevels): the level table
+    stays in global memory (k_diffuse_tma<*, false, *>); u bitwise vs the oracle,
+    single band and the 3-band emulation, and the chain's distances bitwise."""
+    gh = gpu
+    from paper_1812_06060_b200 import bands as GB
+    P, F = _strip(13_000)
+    src = np.array([0], np.int32)
+    mesh = gh.build_mesh(P, F)
+    lv = gh.bfs_levels(mesh, src)
+    assert lv.level_count() > 12 * 1024
+    om = port_oracle.build_mesh(P, F)
+    ol = om.bfs(src)
+    assert_same(lv.level_of_vertex, ol.level_of_vertex, "level")
+    t = om.diffusion_time(1.0)
+    for sweeps in (1, 2, 37):
+        want, _ = om.gs_diffuse(ol, t, sweeps)
+        if nbands == 1:
+            got = gh.gs_diffuse(mesh, lv, t, gh.DiffusionConfig(sweeps=sweeps))
+        else:
+            got = GB.gs_diffuse_bands(mesh, lv, nbands, t, sweeps)
+        assert_same(got, want, f"u after {sweeps} sweeps, {nbands} band(s)")
+    if nbands == 1:
+        u, _ = om.gs_diffuse(ol, t, 37)
+        H, _ = om.normalized_target_gradients(u)
+        X, _ = om.admm_edge(H, 10)
+        d, _ = gh.distance(lv, "edge", 37, t)
+        assert_same(d, om.integrate_edge(ol, X), "edge-method distances")

@@ -63,3 +63,30 @@ def test_config4_sh_displacement_bounds():
     r = np.linalg.norm(w.positions, axis=1)
     assert r.min() >= 0.95 - 1e-12 and r.max() <= 1.05 + 1e-12
     assert max(abs(r.max() - 1.0), abs(r.min() - 1.0)) == pytest.approx(0.05, rel=1e-9)
+
+
+def test_reference_arm_generator_build_matches():
+    """bench.py --impl reference generates its workload with oracle/_ref's build
+    of workloads/meshgen.c (so the reference process maps no product library):
+    the arrays are bit-identical to the product build's, config by config."""
+    import hashlib
+    import subprocess
+    import sys
+
+    from conftest import ROOT
+    from oracle import oracle as orc
+    gen = os.path.join(orc.REF_DIR, "libgh_meshgen.so")
+    if not os.path.exists(gen):
+        orc.build()
+    code = ("import sys, hashlib; sys.path.insert(0, %r)\n"
+            "from paper_1812_06060_b200 import meshgen\n"
+            "meshgen.use_library(%r)\n"
+            "for k, s in ((1, 1), (2, 16), (3, 32), (4, 128), (5, 128)):\n"
+            "    w = meshgen.config(k, scale=s)\n"
+            "    print(hashlib.sha256(w.positions.tobytes() + w.faces.tobytes() + w.sources.tobytes()).hexdigest())\n"
+            "print(meshgen._lib_path)\n") % (ROOT, gen)
+    out = subprocess.run([sys.executable, "-c", code], capture_output=True, text=True, check=True).stdout.split()
+    assert out[-1] == gen
+    for (k, s), h in zip(((1, 1), (2, 16), (3, 32), (4, 128), (5, 128)), out):
+        w = meshgen.config(k, scale=s)
+        assert h == hashlib.sha256(w.positions.tobytes() + w.faces.tobytes() + w.sources.tobytes()).hexdigest(), k
