@@ -341,13 +341,13 @@ def main():
     e2e_sec = max_over_ranks(dist, float(np.mean(e2e_s)), local)
     e2e_value = reach * w.sweeps / e2e_sec
     # the distances of the last timed call vs the reference chain's field_hash
-    # recorded for this config (tools/e2e_parity.py -> profiles/r1_e2e_parity.json)
+    # recorded for this config (tools/e2e_parity.py -> profiles/reference_hashes.json)
     d_out = np.ctypeslib.as_array(C.cast(pd, C.POINTER(C.c_double)), shape=(P.shape[0],))
     parity = {"field_hash": f"{G.field_hash(d_out):016x}", "reference_field_hash": None, "identical": None,
-              "source": "profiles/r1_e2e_parity.json"}
+              "source": "profiles/reference_hashes.json (tools/e2e_parity.py: the reference's own chain)"}
     try:
-        with open(os.path.join(ROOT, "profiles", "r1_e2e_parity.json")) as f:
-            rec = next(r for r in json.load(f)
+        with open(os.path.join(ROOT, "profiles", "reference_hashes.json")) as f:
+            rec = next(r for r in json.load(f)["records"]
                        if r["config"] == a.config and r["method"] == w.method and r["sweeps"] == w.sweeps)
         parity["reference_field_hash"] = rec["hash_reference"]
         parity["identical"] = parity["field_hash"] == rec["hash_reference"]

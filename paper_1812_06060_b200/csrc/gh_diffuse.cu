@@ -117,9 +117,19 @@ struct TmaArgs {
   int32_t nslots;      // ring slots per block
   int32_t slot_bytes;
   int32_t table_in_smem;
-  int32_t stream_resident;  // the CSR stream fits in L2: keep it (evict_last) instead of evict_first
+  int32_t stream_policy;    // L2 policy of the CSR stream copies: 0 evict_first, 1 evict_last, 2 evict_normal
+  // Sweep groups: sweeps [gK, gK + K) run as one pipeline
+  // over the levels, group g starting at step g * P. K = sweeps, P = huge is
+  // the plain pipeline (step tau = L + 2s).
+  int32_t group_sweeps, group_period;
   double t;
 };
+
+// step tau -> group g, local step tl = tau - g * P
+__device__ __forceinline__ void step_group(const TmaArgs& a, int32_t tau, int32_t& g, int32_t& tl) {
+  g = tau / a.group_period;
+  tl = tau - g * a.group_period;
+}
 
 __device__ __forceinline__ uint32_t smem_u32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
 
@@ -151,6 +161,11 @@ __device__ __forceinline__ uint64_t l2_evict_first_policy() {
 __device__ __forceinline__ uint64_t l2_evict_last_policy() {
   uint64_t p;
   asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(p));
+  return p;
+}
+__device__ __forceinline__ uint64_t l2_evict_normal_policy() {
+  uint64_t p;
+  asm volatile("createpolicy.fractional.L2::evict_normal.b64 %0, 1.0;" : "=l"(p));
   return p;
 }
 __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar, uint64_t policy) {
@@ -185,15 +200,22 @@ __device__ __forceinline__ unsigned long long ld_done(const unsigned long long* 
   return ghost ? ld_acquire_sys_u64(p) : ld_acquire_gpu_u64(p);
 }
 
-// rows [rb, re) of the band's own levels active at step tau (L = tau - 2s, 0 <= s < S)
+// rows [rb, re) of the band's own levels active at step tau: in group g
+// (sweeps gK .. gK + Kg - 1) at local step tl, level L runs sweep
+// gK + (tl - L) / 2 for tl - L even, 0 <= tl - L < 2 Kg
 template <class PStart>
-__device__ __forceinline__ bool step_range(int32_t sweeps, int32_t lb, int32_t le, PStart pstart,
+__device__ __forceinline__ bool step_range(const TmaArgs& a, int32_t lb, int32_t le, PStart pstart,
                                            const int32_t* pend, int32_t tau, int32_t& rb, int32_t& re) {
-  int32_t lhi = tau < le - 1 ? tau : le - 1;
-  if ((lhi ^ tau) & 1) --lhi;
-  int32_t llo = tau - 2 * (sweeps - 1);
+  int32_t g, tl;
+  step_group(a, tau, g, tl);
+  const int32_t s0 = g * a.group_sweeps;
+  if (s0 >= a.sweeps) return false;
+  const int32_t kg = a.sweeps - s0 < a.group_sweeps ? a.sweeps - s0 : a.group_sweeps;
+  int32_t lhi = tl < le - 1 ? tl : le - 1;
+  if ((lhi ^ tl) & 1) --lhi;
+  int32_t llo = tl - 2 * (kg - 1);
   if (llo < lb) llo = lb;
-  if ((llo ^ tau) & 1) ++llo;
+  if ((llo ^ tl) & 1) ++llo;
   if (llo > lhi) return false;
   rb = pstart(llo);
   re = pend[lhi];
@@ -285,7 +307,9 @@ __global__ void __launch_bounds__(kTmaThreads, 2) k_diffuse_tma(const __grid_con
   };
   __syncthreads();
 
-  const int32_t nsteps = (band_le - 1) + 2 * (a.sweeps - 1) + 1;
+  // the last group's last task: (band_le - 1) + 2 (kg - 1) steps after its start
+  const int32_t last_g = (a.sweeps - 1) / a.group_sweeps;
+  const int32_t nsteps = last_g * a.group_period + (band_le - 1) + 2 * (a.sweeps - 1 - last_g * a.group_sweeps) + 1;
   const uint32_t col_cap = (uint32_t)kTileChunks * 32u * a.wcap;  // entries
   constexpr bool kCol16 = kWin != 0;
   constexpr int kColOff = kCol16 ? kColOff16 : kColOff32;
@@ -309,7 +333,7 @@ __global__ void __launch_bounds__(kTmaThreads, 2) k_diffuse_tma(const __grid_con
         int32_t rb, re;
         xt0 = 0;
         xnt = 0;
-        if (!step_range(a.sweeps, band_lb, band_le, pstart, pend, xtau, rb, re)) continue;
+        if (!step_range(a, band_lb, band_le, pstart, pend, xtau, rb, re)) continue;
         block_share(rb >> 5, (re + 31) >> 5, b, nb, xcb, xce);
         xnt = (xce - xcb + kTileChunks - 1) / kTileChunks;
       }
@@ -368,7 +392,9 @@ __global__ void __launch_bounds__(kTmaThreads, 2) k_diffuse_tma(const __grid_con
           unsigned char* sb = reinterpret_cast<unsigned char*>(hdr);
           const uint32_t bytes = (uint32_t)nch * (256u + (kCol16 ? 16u : 64u)) + (fits ? ncol * (kColBytes + 8u) : 0u);
           mbar_expect_tx(full + slot, bytes);
-          const uint64_t pol = a.stream_resident ? l2_evict_last_policy() : l2_evict_first_policy();
+          const uint64_t pol = a.stream_policy == 1   ? l2_evict_last_policy()
+                               : a.stream_policy == 2 ? l2_evict_normal_policy()
+                                                      : l2_evict_first_policy();
           bulk_g2s(sb + kDenOff, vba->den + (int64_t)c0 * 32, (uint32_t)nch * 256u, full + slot, pol);
           if (kCol16) bulk_g2s(sb + kDegOff, vba->deg4 + (int64_t)c0 * 16, (uint32_t)nch * 16u, full + slot, pol);
           else bulk_g2s(sb + kDegOff, vba->deg + (int64_t)c0 * 32, (uint32_t)nch * 64u, full + slot, pol);
@@ -402,7 +428,11 @@ __global__ void __launch_bounds__(kTmaThreads, 2) k_diffuse_tma(const __grid_con
   int32_t seen_tau = -1;
   for (int32_t tau = 0; tau < nsteps; ++tau) {
     int32_t rb, re;
-    if (!step_range(a.sweeps, band_lb, band_le, pstart, pend, tau, rb, re)) continue;
+    if (!step_range(a, band_lb, band_le, pstart, pend, tau, rb, re)) continue;
+    // sweep of level L at this step: s_base - L / 2 (tl - L is even)
+    int32_t grp, tl;
+    step_group(a, tau, grp, tl);
+    const int32_t s_base = grp * a.group_sweeps + (tl >> 1);
     int32_t cb, ce;
     block_share(rb >> 5, (re + 31) >> 5, b, nb, cb, ce);
     const int32_t ntile = (ce - cb + kTileChunks - 1) / kTileChunks;
@@ -438,8 +468,10 @@ __global__ void __launch_bounds__(kTmaThreads, 2) k_diffuse_tma(const __grid_con
         if (i < kChunksPerWarp && Li >= 0) {
           const int32_t X = Li - 1 + lane % 3;
           if (X >= 0 && X < a.nlev) {
+            // level L-1 through sweep s, levels L and L+1 through sweep s-1
+            const int32_t s = s_base - (Li >> 1);
             const unsigned long long need =
-                (unsigned long long)((tau - X + 1) >> 1) * (unsigned long long)(pend[X] - pstart(X));
+                (unsigned long long)(s + (X < Li ? 1 : 0)) * (unsigned long long)(pend[X] - pstart(X));
             const bool ghost = X < band_lb || X >= band_le;
             if (ld_done(vba->rows_done + X, ghost) < need) {
               const long long t0 = clock64();
@@ -475,7 +507,7 @@ __global__ void __launch_bounds__(kTmaThreads, 2) k_diffuse_tma(const __grid_con
         const int32_t c = cb + j * kTileChunks + q;
         const int32_t r = c * 32 + lane;
         on[i] = live[i] && r < pend[Lq[i]];
-        px[i] = (uint32_t)((tau - Lq[i]) >> 1 & 1) << 5;
+        px[i] = (uint32_t)((s_base - (Lq[i] >> 1)) & 1) << 5;
         den[i] = reinterpret_cast<const double*>(sb + kDenOff)[q * 32 + lane];
         if (kCol16) {  // nibbles; 15 (a valence of 15 or more) takes the slow path, which reads deg
           const uint32_t nb = reinterpret_cast<const uint8_t*>(sb + kDegOff)[q * 16 + (lane >> 1)];
@@ -758,8 +790,24 @@ double bands_launch(gh_levels* L, std::vector<Band*>& bands, double t, int32_t s
   a.slot_bytes = slot_bytes;
   a.table_in_smem = table ? 1 : 0;
   a.t = t;
+  // sweep groups: one pipeline of all sweeps unless GH_SWEEP_GROUP=K (then
+  // groups of K sweeps, each starting GH_SWEEP_PERIOD steps after the last,
+  // at least nlev + 2K - 1 so that the groups never share a step)
+  a.group_sweeps = sweeps;
+  a.group_period = 0x3fffffff;
+  if (const char* gk = getenv("GH_SWEEP_GROUP")) {
+    const int32_t k = std::max(1, std::min(sweeps, atoi(gk)));
+    if (k < sweeps) {
+      const int64_t pmin = (int64_t)L->nlev + 2 * (int64_t)k - 1;
+      const char* gp = getenv("GH_SWEEP_PERIOD");
+      const int64_t p = std::max<int64_t>(pmin, gp ? atoll(gp) : 0);
+      if ((int64_t)((sweeps - 1) / k + 1) * p >= 0x7fffffffLL) fail(GH_ERR_INVALID, "GH_SWEEP_GROUP: too many steps");
+      a.group_sweeps = k;
+      a.group_period = (int32_t)p;
+    }
+  }
   {
-    // stream + both u buffers against L2 (GH_STREAM_L2=0|1 forces, for experiments): config 2 -2 %
+    // stream + both u buffers against L2 (GH_STREAM_L2=0|1|2 forces, for experiments): config 2 -2 %
     int l2 = 0;
     GH_CUDA(cudaDeviceGetAttribute(&l2, cudaDevAttrL2CacheSize, m->device));
     uint64_t bytes = 0;
@@ -768,7 +816,7 @@ double bands_launch(gh_levels* L, std::vector<Band*>& bands, double t, int32_t s
     if (!col16)
       for (Band* b : bands) bytes += b->col.bytes() - b->col16.bytes() + b->deg.bytes();
     const char* env = getenv("GH_STREAM_L2");
-    a.stream_resident = env ? atoi(env) : (bytes <= (uint64_t)l2 ? 1 : 0);
+    a.stream_policy = env ? atoi(env) : (bytes <= (uint64_t)l2 ? 1 : 0);
   }
   void* kargs[] = {&a};
   EventTimer timer(s);

@@ -20,8 +20,12 @@
 //      would carry s out of it; the segments before it are added exactly as
 //      integers, that segment is added term by term in double (exactly the
 //      reference's operations), and the walk goes on from the next one.
-// The walk stops once per binade change or flagged segment; everything else
-// is a parallel pass over the terms plus one scan per 1024 segments.
+// Ties do not stop the walk: their rounding depends only on the parity of
+// the running count, so every term, segment and run of segments is a 2-state
+// transducer (quanta added and outgoing parity per incoming parity), and the
+// sums are scans of those (see Tx below). The walk stops once per binade
+// change; everything else is a parallel pass over the terms plus one scan per
+// 1024 segments.
 
 #include <cmath>
 
@@ -88,13 +92,69 @@ __global__ void __launch_bounds__(kSegThreads) k_seg_sums(const double* __restri
   }
 }
 
+// Ties: fl(s + x) with x / u = m + 1/2 rounds to the even multiple of u, so
+// it adds m + ((A + m) & 1) quanta (A = s / u) and leaves an even count. A
+// term's effect on the integer running count is therefore a function of the
+// incoming parity only: (q(p), out(p)) for p in {0, 1}, with q the quanta
+// added and out the parity after (a tie: q(p) = m + ((p + m) & 1), out = 0;
+// else q = rint(x / u), out = p ^ (q & 1)). These 2-state transducers compose
+// associatively, so a segment (and a run of segments) reduces to one, and the
+// walk scans them in parallel: ties never stop it, only a change of binade.
+// saturating non-negative int64 sums (cap 2^62: a saturated count is past any binade)
+constexpr unsigned long long kCap = 1ull << 62;
+__device__ __forceinline__ unsigned long long sat_add(unsigned long long a, unsigned long long b) {
+  const unsigned long long c = a + b;  // both <= 2^62: no wrap
+  return c < kCap ? c : kCap;
+}
+
+struct Tx {
+  unsigned long long q0, q1;  // quanta added for incoming parity 0 / 1 (saturating at 2^62)
+  uint32_t o;                 // bit p: outgoing parity for incoming parity p
+};
+__device__ __forceinline__ Tx tx_identity() { return Tx{0ull, 0ull, 2u}; }
+// a then b
+__device__ __forceinline__ Tx tx_then(const Tx& a, const Tx& b) {
+  const uint32_t a0 = a.o & 1u, a1 = (a.o >> 1) & 1u;
+  Tx r;
+  r.q0 = sat_add(a.q0, a0 ? b.q1 : b.q0);
+  r.q1 = sat_add(a.q1, a1 ? b.q1 : b.q0);
+  r.o = ((b.o >> a0) & 1u) | (((b.o >> a1) & 1u) << 1);
+  return r;
+}
+__device__ __forceinline__ Tx tx_shfl_down(const Tx& t, int d) {
+  return Tx{__shfl_down_sync(0xffffffffu, t.q0, d), __shfl_down_sync(0xffffffffu, t.q1, d),
+            __shfl_down_sync(0xffffffffu, t.o, d)};
+}
+__device__ __forceinline__ Tx tx_shfl_up(const Tx& t, int d) {
+  return Tx{__shfl_up_sync(0xffffffffu, t.q0, d), __shfl_up_sync(0xffffffffu, t.q1, d),
+            __shfl_up_sync(0xffffffffu, t.o, d)};
+}
+// the transducer of term x in binade e; *flag when x >= 2^e (leaves the binade)
+__device__ __forceinline__ Tx tx_term(double x, int e, double lim, bool& flag) {
+  if (x >= lim) {
+    flag = true;
+    return tx_identity();
+  }
+  const double y = scale2(x, 52 - e);  // exact
+  const double m = floor(y);
+  const unsigned long long mi = (unsigned long long)m;
+  if (y - m == 0.5) {
+    const unsigned long long odd = mi & 1ull;
+    return Tx{mi + odd, mi + (odd ^ 1ull), 0u};
+  }
+  const unsigned long long q = (unsigned long long)rint(y);
+  const uint32_t b = (uint32_t)(q & 1ull);
+  return Tx{q, q, b | ((1u ^ b) << 1)};
+}
+
 // step 2b: candidate binades from the bounded prefix, then per candidate the
-// segment's integer sum and flag
+// segment's transducer and a flag (a term that leaves the binade). Thread t
+// takes the 4 consecutive terms 4t .. 4t+3 of the segment.
 __global__ void __launch_bounds__(kSegThreads) k_seg_q(const double* __restrict__ x, int64_t b, int64_t n, int64_t nseg,
                                                        const double* __restrict__ P, const double* __restrict__ acc,
                                                        double rel, int32_t* __restrict__ elo,
-                                                       long long* __restrict__ Q, int32_t* __restrict__ F) {
-  __shared__ long long sq[kSegThreads / 32][2];
+                                                       Tx* __restrict__ Q, int32_t* __restrict__ F) {
+  __shared__ Tx sq[kSegThreads / 32][2];
   __shared__ int32_t sf[kSegThreads / 32][2];
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
   for (int64_t g = blockIdx.x; g < nseg; g += gridDim.x) {
@@ -106,35 +166,37 @@ __global__ void __launch_bounds__(kSegThreads) k_seg_q(const double* __restrict_
     bool in[kPerThread];
 #pragma unroll
     for (int i = 0; i < kPerThread; ++i) {
-      const int64_t k = b + g * kSeg + i * kSegThreads + threadIdx.x;
+      const int64_t k = b + g * kSeg + kPerThread * threadIdx.x + i;
       in[i] = k < n;
       xv[i] = in[i] ? x[k] : 0.0;
     }
     for (int c = 0; c < 2; ++c) {
       const int e = e0 + c;
       const double lim = ok ? ldexp(1.0, e + (e == -1022 ? 1 : 0)) : 0.0;  // the lowest "binade" ends at 2^-1021
-      long long q = 0;
+      Tx t = tx_identity();
       bool flag = !ok;
+      if (ok) {
 #pragma unroll
-      for (int i = 0; i < kPerThread; ++i) {
-        const double y = ok ? scale2(xv[i], 52 - e) : 0.0;  // exact scaling
-        const bool f = in[i] && (xv[i] >= lim || y - floor(y) == 0.5);
-        flag |= f;
-        q += f ? 0 : (long long)rint(y);
+        for (int i = 0; i < kPerThread; ++i)
+          if (in[i]) t = tx_then(t, tx_term(xv[i], e, lim, flag));
       }
-      for (int o = 16; o > 0; o >>= 1) q += __shfl_down_sync(0xffffffffu, q, o);
+      // ordered warp reduction: lane l composes with lanes above it
+      for (int o = 1; o < 32; o <<= 1) {
+        const Tx up = tx_shfl_down(t, o);
+        if ((lane & (2 * o - 1)) == 0) t = tx_then(t, up);
+      }
       const unsigned any = __ballot_sync(0xffffffffu, flag);
       if (lane == 0) {
-        sq[w][c] = q;
+        sq[w][c] = t;
         sf[w][c] = any ? 1 : 0;
       }
     }
     __syncthreads();
     if (threadIdx.x < 2) {
-      long long tq = 0;
+      Tx tq = tx_identity();
       int32_t tf = 0;
       for (int v = 0; v < kSegThreads / 32; ++v) {
-        tq += sq[v][threadIdx.x];
+        tq = tx_then(tq, sq[v][threadIdx.x]);
         tf |= sf[v][threadIdx.x];
       }
       Q[2 * g + threadIdx.x] = tq;
@@ -145,40 +207,35 @@ __global__ void __launch_bounds__(kSegThreads) k_seg_q(const double* __restrict_
   }
 }
 
-// block-wide inclusive scan of saturating non-negative int64 (cap 2^62)
-constexpr unsigned long long kCap = 1ull << 62;
-__device__ __forceinline__ unsigned long long sat_add(unsigned long long a, unsigned long long b) {
-  const unsigned long long c = a + b;  // both <= 2^62: no wrap
-  return c < kCap ? c : kCap;
-}
-__device__ unsigned long long block_scan_sat(unsigned long long v, unsigned long long* wsum) {
+// block-wide inclusive scan of transducers in thread order
+__device__ Tx block_scan_tx(Tx v, Tx* wsum) {
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
   for (int o = 1; o < 32; o <<= 1) {
-    const unsigned long long t = __shfl_up_sync(0xffffffffu, v, o);
-    if (lane >= o) v = sat_add(v, t);
+    const Tx t = tx_shfl_up(v, o);
+    if (lane >= o) v = tx_then(t, v);
   }
   __syncthreads();
   if (lane == 31) wsum[w] = v;
   __syncthreads();
   if (w == 0) {
-    unsigned long long a = wsum[lane];
+    Tx a = wsum[lane];
     for (int o = 1; o < 32; o <<= 1) {
-      const unsigned long long t = __shfl_up_sync(0xffffffffu, a, o);
-      if (lane >= o) a = sat_add(a, t);
+      const Tx t = tx_shfl_up(a, o);
+      if (lane >= o) a = tx_then(t, a);
     }
     wsum[lane] = a;
   }
   __syncthreads();
-  return w ? sat_add(v, wsum[w - 1]) : v;
+  return w ? tx_then(wsum[w - 1], v) : v;
 }
 
 // step 3: one block of 1024 threads
 __global__ void __launch_bounds__(kWalkThreads) k_walk(const double* __restrict__ x, int64_t b, int64_t n,
                                                        int64_t nseg, const int32_t* __restrict__ elo,
-                                                       const long long* __restrict__ Q, const int32_t* __restrict__ F,
+                                                       const Tx* __restrict__ Q, const int32_t* __restrict__ F,
                                                        double* __restrict__ acc) {
   __shared__ double sh[kWalkThreads];
-  __shared__ unsigned long long wsum[32];
+  __shared__ Tx wsum[32];
   __shared__ double s_sh;
   __shared__ int64_t stop_at;
   __shared__ unsigned long long cum_before;
@@ -195,17 +252,19 @@ __global__ void __launch_bounds__(kWalkThreads) k_walk(const double* __restrict_
     const int e = has ? binade_of(sc) : kNoBinade;
     const double u = has ? ldexp(1.0, e - 52) : 0.0;
     const unsigned long long A = has ? (unsigned long long)scale2(sc, 52 - e) : 0;  // s / u, exact
+    const uint32_t p0 = (uint32_t)(A & 1ull);
     const int64_t gi = g + threadIdx.x;
     bool simple = false;
-    unsigned long long q = 0;
+    Tx q = tx_identity();
     if (gi < nseg && has) {
       const int c = e - elo[gi];
       if (elo[gi] != kNoBinade && (c == 0 || c == 1) && !F[2 * gi + c]) {
         simple = true;
-        q = (unsigned long long)Q[2 * gi + c];
+        q = Q[2 * gi + c];
       }
     }
-    const unsigned long long cum = block_scan_sat(q, wsum);  // inclusive
+    const Tx pre = block_scan_tx(q, wsum);  // inclusive
+    const unsigned long long cum = p0 ? pre.q1 : pre.q0;
     const bool stop = gi < nseg && (!simple || A + cum >= top);
     if (threadIdx.x == 0) stop_at = INT64_MAX;
     __syncthreads();
@@ -250,7 +309,7 @@ double sequential_sum_nonneg(const double* d_x, int64_t n, cudaStream_t s, int* 
     const int64_t nseg = (n - K + kSeg - 1) / kSeg;
     Scratch<double> T(nseg, s), P(nseg, s);
     Scratch<int32_t> elo(nseg, s), F(2 * nseg, s);
-    Scratch<long long> Q(2 * nseg, s);
+    Scratch<Tx> Q(2 * nseg, s);
     const unsigned grid = (unsigned)std::min<int64_t>(nseg, 148 * 32);
     k_seg_sums<<<grid, kSegThreads, 0, s>>>(d_x, K, n, nseg, T.p);
     size_t tmp_bytes = 0;

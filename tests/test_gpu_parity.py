@@ -329,7 +329,8 @@ def test_high_valence_hub_bitwise(gpu, port_oracle, n, source):
 
 
 @pytest.mark.parametrize("mode", ["auto", "col32", "win2", "win3", "win2_mixed", "win3_mixed", "morton",
-                                  "morton_win3_mixed", "morton_col32"])
+                                  "morton_win3_mixed", "morton_col32", "group1", "group7", "group16_normal",
+                                  "group3_period"])
 def test_diffusion_column_formats_bitwise(gpu, port_oracle, monkeypatch, mode):
     """The diffusion kernel streams 16-bit column offsets into 2 or 3 per-chunk
     windows (chunks whose windows do not fit keep 32-bit columns and take the
@@ -337,9 +338,19 @@ def test_diffusion_column_formats_bitwise(gpu, port_oracle, monkeypatch, mode):
     limit, give u bit-identical to the reference on every fixture and on
     reduced configs 2-5, single band and 3 bands. The "morton" modes lay each
     ring out in spatial order (the layout picked when vertex-id order leaves no
-    16-bit format usable), which moves rows between chunks but not their sums."""
+    16-bit format usable), which moves rows between chunks but not their sums.
+    The "group" modes run the sweeps in groups of K (one pipeline per group,
+    DESIGN.md §3.4): the same tasks in another order, so the same bits."""
     from paper_1812_06060_b200 import bands, meshgen
     gh = gpu
+    if mode.startswith("group"):  # sweep groups (GH_SWEEP_GROUP): same tasks, another step order
+        k = mode[5:].split("_")[0]
+        monkeypatch.setenv("GH_SWEEP_GROUP", k)
+        if mode.endswith("normal"):
+            monkeypatch.setenv("GH_STREAM_L2", "2")
+        if mode.endswith("period"):
+            monkeypatch.setenv("GH_SWEEP_PERIOD", "5000")
+        mode = "auto"
     if mode.startswith("morton"):
         monkeypatch.setenv("GH_LAYOUT", "morton")
         mode = mode[7:] or "auto"
