@@ -333,6 +333,26 @@ gh_status gh_band_prepare(gh_band* band, double t, const double* initial);
 /* u_out (host [V], may be NULL): this band's vertices hold the result. */
 gh_status gh_band_launch(gh_band* band, double t, int32_t sweeps, double* u_out, gh_solver_report* report);
 
+/* ---- Sector slices: every slice owns a contiguous 1/nslices
+ * of every BFS ring (in the diffusion layout's ring order), so every slice
+ * has work at every step of the sweep pipeline, however the level count
+ * compares with the sweep count. Foreign neighbours of a slice's rows are
+ * ghost rows the owners write (peer stores + per-(source, level) counters)
+ * from inside the one dataflow kernel. Results are bit-identical to
+ * gh_gs_diffuse. GH_PARTITION_BANDS selects the BFS bands above. */
+typedef enum { GH_PARTITION_BANDS = 0, GH_PARTITION_SLICES = 1 } gh_partition;
+/* All parts in one process on the current device (one launch), nparts <= 8. */
+gh_status gh_gs_diffuse_partitioned(gh_levels* levels, int32_t nparts, int32_t partition, double t, int32_t sweeps,
+                                    const double* initial, double* u_out, gh_solver_report* report);
+/* One part per process/GPU (bands: as gh_band_create). Slices connect to
+ * every other rank: blobs[nranks] from gh_band_export of each rank (its own
+ * entry is ignored). Prepare/launch and their barriers as for bands. */
+gh_status gh_band_create_partitioned(gh_levels* levels, int32_t rank, int32_t nranks, int32_t partition,
+                                     gh_band** out);
+gh_status gh_band_connect_all(gh_band* band, const void* const* blobs, int32_t nranks);
+/* mask_out[V] (host): 1 for the vertices whose u this part computes. */
+gh_status gh_band_own_mask(const gh_band* band, uint8_t* mask_out);
+
 /* deterministic_sum (parallel.hpp:50-54): the left-to-right sum of n host
  * doubles, bit-identical. Non-negative terms take the parallel exact path
  * (the library uses it for average_edge_length); any negative term falls

@@ -111,6 +111,10 @@ SIGNATURES = [
     ("gh_plan_bands", st, [vp, i32, i32, vp]),
     ("gh_gs_diffuse_bands", st, [vp, i32, f64, i32, vp, vp, C.POINTER(gh_solver_report)]),
     ("gh_band_create", st, [vp, i32, i32, C.POINTER(vp)]),
+    ("gh_gs_diffuse_partitioned", st, [vp, i32, i32, f64, i32, vp, vp, C.POINTER(gh_solver_report)]),
+    ("gh_band_create_partitioned", st, [vp, i32, i32, i32, C.POINTER(vp)]),
+    ("gh_band_connect_all", st, [vp, C.POINTER(C.c_char_p), i32]),
+    ("gh_band_own_mask", st, [vp, vp]),
     ("gh_band_destroy", st, [vp]),
     ("gh_band_info", st, [vp, C.POINTER(i32), C.POINTER(i32), C.POINTER(i32)]),
     ("gh_band_export", st, [vp, vp, i32, C.POINTER(i32)]),

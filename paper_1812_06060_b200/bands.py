@@ -20,6 +20,12 @@ Multi-process use (one process per GPU, torch.distributed for the plumbing):
 
 `gs_diffuse_bands` runs the same schedule with all bands on one GPU in one
 launch (the single-GPU emulation used by the tests).
+
+Sector slices (`partition="slices"`) cut every ring instead:
+slice r owns positions [ceil(r n / N), ceil((r + 1) n / N)) of each ring of n
+vertices, so every rank has work at every pipeline step; the foreign
+neighbours of its rows are ghost rows their owners write. Slices connect to
+every rank (`connect_all`), bands to their two neighbours.
 """
 from __future__ import annotations
 
@@ -64,27 +70,37 @@ def plan_bands_native(offsets: Sequence[int], nbands: int) -> list:
     return cut.tolist()
 
 
+PARTITIONS = {"bands": 0, "slices": 1}
+
+
 def gs_diffuse_bands(mesh: TriMesh, levels: BfsLevels, nbands: int, t: float, sweeps: int, initial=None,
-                     report: Optional[SolverReport] = None) -> np.ndarray:
-    """gs_diffuse split into nbands BFS bands, all on this GPU in one launch."""
+                     report: Optional[SolverReport] = None, partition: str = "bands") -> np.ndarray:
+    """gs_diffuse split into nbands BFS bands (or sector slices), all on this GPU in one launch."""
     init = None if initial is None else _f64(initial)
     u = np.empty(mesh.vertex_count(), np.float64)
     rep = gh_solver_report()
-    _check(mesh._lib.gh_gs_diffuse_bands(levels._h, int(nbands), float(t), int(sweeps), _ptr(init), _ptr(u),
-                                         C.byref(rep)))
+    _check(mesh._lib.gh_gs_diffuse_partitioned(levels._h, int(nbands), PARTITIONS[partition], float(t), int(sweeps),
+                                               _ptr(init), _ptr(u), C.byref(rep)))
     if report is not None:
         report.iterations, report.device_ms, report.kernel_launches = rep.iterations, rep.device_ms, rep.kernel_launches
     return u
 
 
+def gs_diffuse_slices(mesh: TriMesh, levels: BfsLevels, nslices: int, t: float, sweeps: int, initial=None,
+                      report: Optional[SolverReport] = None) -> np.ndarray:
+    """gs_diffuse split into nslices sector slices (every slice a 1/N of every ring), one launch."""
+    return gs_diffuse_bands(mesh, levels, nslices, t, sweeps, initial, report, partition="slices")
+
+
 class Band:
     """This process's band of a multi-GPU diffusion (one gh_band handle)."""
 
-    def __init__(self, levels: BfsLevels, rank: int, world: int):
-        self.levels, self.rank, self.world = levels, rank, world
+    def __init__(self, levels: BfsLevels, rank: int, world: int, partition: str = "bands"):
+        self.levels, self.rank, self.world, self.partition = levels, rank, world, partition
         self._lib = levels._lib
         self._h = C.c_void_p()
-        _check(self._lib.gh_band_create(levels._h, int(rank), int(world), C.byref(self._h)))
+        _check(self._lib.gh_band_create_partitioned(levels._h, int(rank), int(world), PARTITIONS[partition],
+                                                    C.byref(self._h)))
         lb, le, rows = C.c_int32(), C.c_int32(), C.c_int32()
         _check(self._lib.gh_band_info(self._h, C.byref(lb), C.byref(le), C.byref(rows)))
         self.lb, self.le, self.own_rows = lb.value, le.value, rows.value
@@ -105,12 +121,20 @@ class Band:
     def connect(self, lower: Optional[bytes], upper: Optional[bytes]) -> None:
         _check(self._lib.gh_band_connect(self._h, lower, upper))
 
+    def connect_all(self, blobs) -> None:
+        arr = (C.c_char_p * len(blobs))(*[bytes(x) for x in blobs])
+        _check(self._lib.gh_band_connect_all(self._h, arr, len(blobs)))
+
     def connect_via(self, dist) -> None:
-        """Exchange IPC blobs with every rank (all_gather_object) and map the two neighbours."""
+        """Exchange IPC blobs with every rank (all_gather_object) and map the two
+        neighbours (bands) or every other rank (slices)."""
         blobs = [None] * self.world
         dist.all_gather_object(blobs, self.export())
-        self.connect(blobs[self.rank - 1] if self.rank > 0 else None,
-                     blobs[self.rank + 1] if self.rank + 1 < self.world else None)
+        if self.partition == "slices":
+            self.connect_all(blobs)
+        else:
+            self.connect(blobs[self.rank - 1] if self.rank > 0 else None,
+                         blobs[self.rank + 1] if self.rank + 1 < self.world else None)
 
     def prepare(self, t: float, initial=None) -> None:
         init = None if initial is None else _f64(initial)
@@ -126,5 +150,7 @@ class Band:
         return u
 
     def own_mask(self) -> np.ndarray:
-        lv = self.levels.level_of_vertex
-        return (lv >= self.lb) & (lv < self.le)
+        """Vertices whose u this rank computes (its rows of the diffusion layout)."""
+        m = np.zeros(self.levels.mesh.vertex_count(), np.uint8)
+        _check(self._lib.gh_band_own_mask(self._h, _ptr(m)))
+        return m.astype(bool)

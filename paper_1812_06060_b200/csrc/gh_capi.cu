@@ -924,6 +924,8 @@ namespace {
 struct BandBlob {
   cudaIpcMemHandle_t ubuf;
   cudaIpcMemHandle_t done;
+  cudaIpcMemHandle_t gdone;  // slices: ghost counters per (source, level)
+  int32_t nslices, rank;
   int64_t nrows;
   int32_t lb, le;
   int32_t ghost_lo_row;  // row of level lb-1 inside this band, -1 without one
@@ -947,22 +949,40 @@ gh_status gh_plan_bands(const int32_t* offsets, int32_t nlev, int32_t nbands, in
 
 gh_status gh_gs_diffuse_bands(gh_levels* levels, int32_t nbands, double t, int32_t sweeps, const double* initial,
                               double* u_out, gh_solver_report* report) {
+  return gh_gs_diffuse_partitioned(levels, nbands, GH_PARTITION_BANDS, t, sweeps, initial, u_out, report);
+}
+
+gh_status gh_gs_diffuse_partitioned(gh_levels* levels, int32_t nbands, int32_t partition, double t, int32_t sweeps,
+                                    const double* initial, double* u_out, gh_solver_report* report) {
   return guarded([&] {
-    require(levels != nullptr, "gh_gs_diffuse_bands: null levels");
+    require(levels != nullptr, "gh_gs_diffuse_partitioned: null levels");
+    require(partition == GH_PARTITION_BANDS || partition == GH_PARTITION_SLICES,
+            "gh_gs_diffuse_partitioned: unknown partition");
     gh_mesh* m = levels->mesh;
     Use use_(m);
     cudaStream_t s = m->stream;
     const double w0 = now_s();
     take_launches(m);
-    const std::vector<int32_t> cut = gh::plan_bands(levels->h_offsets, nbands);
     std::vector<std::unique_ptr<gh::Band>> own;
     std::vector<gh::Band*> bands;
-    for (int32_t r = 0; r < nbands; ++r) {
-      own.emplace_back(new gh::Band());
-      gh::band_build(levels, own.back().get(), cut[r], cut[r + 1]);
-      bands.push_back(own.back().get());
+    if (partition == GH_PARTITION_SLICES) {
+      require(nbands >= 1 && nbands <= gh::Band::kMaxSlices, "gh_gs_diffuse_partitioned: 1 to 8 slices");
+      if (levels->nreach == 0) nbands = 1;
+      for (int32_t r = 0; r < nbands; ++r) {
+        own.emplace_back(new gh::Band());
+        gh::slice_build(levels, own.back().get(), r, nbands);
+        bands.push_back(own.back().get());
+      }
+      gh::slice_link(bands);
+    } else {
+      const std::vector<int32_t> cut = gh::plan_bands(levels->h_offsets, nbands);
+      for (int32_t r = 0; r < nbands; ++r) {
+        own.emplace_back(new gh::Band());
+        gh::band_build(levels, own.back().get(), cut[r], cut[r + 1]);
+        bands.push_back(own.back().get());
+      }
+      for (int32_t r = 0; r + 1 < nbands; ++r) gh::band_link(bands[r], bands[r + 1]);
     }
-    for (int32_t r = 0; r + 1 < nbands; ++r) gh::band_link(bands[r], bands[r + 1]);
     gh::Scratch<double> dinit(initial ? m->nv : 0, s);
     if (initial) GH_CUDA(cudaMemcpyAsync(dinit.p, initial, sizeof(double) * m->nv, cudaMemcpyHostToDevice, s));
     const double ms = gh::diffuse_bands_dev(levels, bands, t, sweeps, initial ? dinit.p : nullptr);
@@ -979,17 +999,28 @@ gh_status gh_gs_diffuse_bands(gh_levels* levels, int32_t nbands, double t, int32
 }
 
 gh_status gh_band_create(gh_levels* levels, int32_t rank, int32_t nranks, gh_band** out) {
+  return gh_band_create_partitioned(levels, rank, nranks, GH_PARTITION_BANDS, out);
+}
+
+gh_status gh_band_create_partitioned(gh_levels* levels, int32_t rank, int32_t nranks, int32_t partition,
+                                     gh_band** out) {
   return guarded([&] {
     require(levels && out, "gh_band_create: null argument");
     require(nranks >= 1 && rank >= 0 && rank < nranks, "gh_band_create: bad rank");
+    require(partition == GH_PARTITION_BANDS || partition == GH_PARTITION_SLICES, "gh_band_create: unknown partition");
     Use use_(levels->mesh);
-    const std::vector<int32_t> cut = gh::plan_bands(levels->h_offsets, nranks);
     std::unique_ptr<gh_band> b(new gh_band());
     b->levels = levels;
     b->rank = rank;
     b->nranks = nranks;
     b->band.ipc = true;  // its buffers are exported to the neighbour processes
-    gh::band_build(levels, &b->band, cut[rank], cut[rank + 1]);
+    if (partition == GH_PARTITION_SLICES) {
+      require(nranks <= gh::Band::kMaxSlices, "gh_band_create: 1 to 8 slices");
+      gh::slice_build(levels, &b->band, rank, nranks);
+    } else {
+      const std::vector<int32_t> cut = gh::plan_bands(levels->h_offsets, nranks);
+      gh::band_build(levels, &b->band, cut[rank], cut[rank + 1]);
+    }
     *out = b.release();
   });
 }
@@ -1024,6 +1055,9 @@ gh_status gh_band_export(const gh_band* band, void* blob, int32_t capacity, int3
     Use use_(band->levels->mesh);
     GH_CUDA(cudaIpcGetMemHandle(&x.ubuf, b.ubuf));
     GH_CUDA(cudaIpcGetMemHandle(&x.done, b.rows_done));
+    if (b.gdone) GH_CUDA(cudaIpcGetMemHandle(&x.gdone, b.gdone));
+    x.nslices = b.nslices;
+    x.rank = b.rank;
     x.nrows = b.nrows;
     x.lb = b.lb;
     x.le = b.le;
@@ -1039,6 +1073,7 @@ gh_status gh_band_connect(gh_band* band, const void* lower_blob, const void* upp
   return guarded([&] {
     require(band != nullptr, "gh_band_connect: null band");
     gh::Band& b = band->band;
+    require(b.nslices == 0, "gh_band_connect: slices connect to every rank (gh_band_connect_all)");
     Use use_(band->levels->mesh);
     auto open = [&](const cudaIpcMemHandle_t& h) {
       void* p = nullptr;
@@ -1064,6 +1099,47 @@ gh_status gh_band_connect(gh_band* band, const void* lower_blob, const void* upp
       b.hi_nrows = x.nrows;
       b.hi_ghost = x.ghost_lo_row;  // our last level is its lower ghost
     }
+  });
+}
+
+gh_status gh_band_connect_all(gh_band* band, const void* const* blobs, int32_t nranks) {
+  return guarded([&] {
+    require(band && blobs, "gh_band_connect_all: null argument");
+    gh::Band& b = band->band;
+    require(b.nslices > 0, "gh_band_connect_all: not a slice (level bands connect with gh_band_connect)");
+    require(nranks == b.nslices, "gh_band_connect_all: one blob per slice");
+    Use use_(band->levels->mesh);
+    for (int32_t d = 0; d < nranks; ++d) {
+      if (d == b.rank) {
+        b.peer_ubuf[d] = b.ubuf;
+        b.peer_gdone[d] = b.gdone;
+        continue;
+      }
+      require(blobs[d] != nullptr, "gh_band_connect_all: missing blob");
+      BandBlob x;
+      std::memcpy(&x, blobs[d], sizeof(x));
+      if (!(x.magic == kBlobMagic && x.nslices == b.nslices && x.rank == d))
+        gh::fail(GH_ERR_INVALID, "gh_band_connect_all: blob is not slice " + std::to_string(d) + " of this partition");
+      void* p = nullptr;
+      GH_CUDA(cudaIpcOpenMemHandle(&p, x.ubuf, cudaIpcMemLazyEnablePeerAccess));
+      band->opened.push_back(p);
+      b.peer_ubuf[d] = static_cast<double*>(p);
+      GH_CUDA(cudaIpcOpenMemHandle(&p, x.gdone, cudaIpcMemLazyEnablePeerAccess));
+      band->opened.push_back(p);
+      b.peer_gdone[d] = static_cast<unsigned long long*>(p);
+    }
+    b.peer_sys = true;  // the peers are other processes' GPUs
+  });
+}
+
+gh_status gh_band_own_mask(const gh_band* band, uint8_t* mask_out) {
+  return guarded([&] {
+    require(band && mask_out, "gh_band_own_mask: null argument");
+    gh_mesh* m = band->levels->mesh;
+    Use use_(m);
+    gh::Scratch<uint8_t> d(m->nv, m->stream);
+    gh::band_own_mask(&band->band, d.p, m->nv, m->stream);
+    to_host(mask_out, d.p, m->nv, m->stream);
   });
 }
 

@@ -104,6 +104,16 @@ struct BandArgs {
   int32_t lb, le;                 // own levels
   int32_t half2;                  // first row of the odd-level half
   int32_t gs_lo, gs_hi;           // first rows of the ghost levels lb-1, le (this band)
+  // sector slices (gh::Band, kSlice kernels only)
+  const uint32_t* src_mask;       // [nlev] slices this one reads ghost rows from
+  const uint32_t* dst_mask;       // [nlev] slices that read rows of this one
+  const int32_t* slice_cnt;       // [nslices][nlev] own rows per slice
+  const int32_t* xoff;            // [own chunks + 1] export entries per chunk
+  const int2* xent;               // (own row, dest << 28 | dest row)
+  unsigned long long* gdone;      // [nslices][nlev] this slice's ghost rows finished, per source
+  double* peer_ubuf[gh::Band::kMaxSlices];
+  unsigned long long* peer_gdone[gh::Band::kMaxSlices];
+  int32_t nslices, rank, peer_sys;
 };
 
 constexpr int kMaxBands = 8;  // bands per launch (one per GPU in production; more when emulated)
@@ -258,7 +268,9 @@ constexpr int kColOff16 = kDegOff + kTileChunks * 16;  // nibbles (16-bit-column
 // kWin: 0 = 32-bit columns; 2 or 3 = columns streamed as 16-bit offsets into
 // 2 or 3 per-chunk windows (gh::Band::col16), 12 B less per
 // row; chunks without 16-bit columns take the global-memory path.
-template <int kUnroll, bool kTable, int kWin>
+// kSlice: the band is a sector slice (gh::Band::nslices): ghost rows of every
+// level, counted per source slice; own rows exported to the readers' ghosts.
+template <int kUnroll, bool kTable, int kWin, bool kSlice>
 __global__ void __launch_bounds__(kTmaThreads, 2) k_diffuse_tma(const __grid_constant__ TmaArgs a) {
   extern __shared__ __align__(128) unsigned char smem[];
   // this block's band and its rank inside the band
@@ -376,11 +388,12 @@ __global__ void __launch_bounds__(kTmaThreads, 2) k_diffuse_tma(const __grid_con
         if (kCol16) {
           const int qs = (off + (lane & (kTileChunks - 1))) & 31;
           const int32_t bx = __shfl_sync(0xffffffffu, cb0.x, qs), by = __shfl_sync(0xffffffffu, cb0.y, qs);
-          const int32_t bz = __shfl_sync(0xffffffffu, cb0.z, qs);
+          const int32_t bz = __shfl_sync(0xffffffffu, cb0.z, qs), bw = __shfl_sync(0xffffffffu, cb0.w, qs);
           if (lane < kTileChunks) {
             hdr[kBaseHdr + 4 * lane] = bx;
             hdr[kBaseHdr + 4 * lane + 1] = by;
             hdr[kBaseHdr + 4 * lane + 2] = bz;
+            hdr[kBaseHdr + 4 * lane + 3] = bw;  // 3 windows: the ghost rows (window 3)
           }
         }
         const int64_t pend_tile = __shfl_sync(0xffffffffu, pi, nch);
@@ -470,20 +483,28 @@ __global__ void __launch_bounds__(kTmaThreads, 2) k_diffuse_tma(const __grid_con
           if (X >= 0 && X < a.nlev) {
             // level L-1 through sweep s, levels L and L+1 through sweep s-1
             const int32_t s = s_base - (Li >> 1);
-            const unsigned long long need =
-                (unsigned long long)(s + (X < Li ? 1 : 0)) * (unsigned long long)(pend[X] - pstart(X));
+            const unsigned long long sw = (unsigned long long)(s + (X < Li ? 1 : 0));
             const bool ghost = X < band_lb || X >= band_le;
-            if (ld_done(vba->rows_done + X, ghost) < need) {
+            auto wait_for = [&](const unsigned long long* ctr, unsigned long long need, bool sys) {
+              if (ld_done(ctr, sys) >= need) return;
               const long long t0 = clock64();
               unsigned ns = 64;
               for (unsigned it = 1;; ++it) {
                 __nanosleep(ns);
-                if (ld_done(vba->rows_done + X, ghost) >= need) break;
+                if (ld_done(ctr, sys) >= need) break;
                 if (ns < 512) ns <<= 1;
                 if ((it & 255) == 0 && clock64() - t0 > (1ll << 35)) {  // ~17 s: a neighbour is gone
                   atomicExch(vba->stalled, 1);
                   break;
                 }
+              }
+            };
+            wait_for(vba->rows_done + X, sw * (unsigned long long)(pend[X] - pstart(X)), ghost);
+            if (kSlice) {  // ghost rows of level X, per source slice
+              for (uint32_t msk = __ldg(vba->src_mask + X); msk; msk &= msk - 1) {
+                const int q = __ffs(msk) - 1;
+                wait_for(vba->gdone + (size_t)q * a.nlev + X,
+                         sw * (unsigned long long)__ldg(vba->slice_cnt + (size_t)q * a.nlev + X), sba.peer_sys != 0);
               }
             }
           }
@@ -596,6 +617,7 @@ __global__ void __launch_bounds__(kTmaThreads, 2) k_diffuse_tma(const __grid_con
             num[i] += w * __ldca(ub + (cc ^ px[i]));
           }
         }
+        double un = 0.0;
         if (on[i]) {
           const int32_t r = c * 32 + lane;
           const double u0 = Lq[i] == 0 ? 1.0 : 0.0;
@@ -604,7 +626,7 @@ __global__ void __launch_bounds__(kTmaThreads, 2) k_diffuse_tma(const __grid_con
           // quotient sends the IEEE division down its slow path; 0 / den with
           // den > 0 is that same zero, so skip the division there.
           const double nz = u0 + a.t * num[i];
-          double un = nz;
+          un = nz;
           if (!(nz == 0.0 && den[i] > 0.0))  // asm volatile: keeps the division under the branch
             asm volatile("div.rn.f64 %0, %1, %2;" : "=d"(un) : "d"(nz), "d"(den[i]));
           const uint32_t par = px[i] >> 5;
@@ -614,6 +636,19 @@ __global__ void __launch_bounds__(kTmaThreads, 2) k_diffuse_tma(const __grid_con
             __stcg(vba->lo_ubuf + gh::uidx((uint32_t)(vba->lo_ghost + (r - pstart(Lq[i]))), par), un);
           if (Lq[i] == band_le - 1 && vba->hi_ubuf)
             __stcg(vba->hi_ubuf + gh::uidx((uint32_t)(vba->hi_ghost + (r - pstart(Lq[i]))), par), un);
+        }
+        if (kSlice && live[i]) {
+          // rows other slices read: into their ghost rows (same sweep parity)
+          const int32_t x0 = __ldg(vba->xoff + c), x1 = __ldg(vba->xoff + c + 1);
+          for (int32_t e0 = x0; e0 < x1; e0 += 32) {
+            const bool ok = e0 + lane < x1;
+            const int2 en = ok ? __ldg(vba->xent + e0 + lane) : make_int2(0, 0);
+            const double val = __shfl_sync(0xffffffffu, un, en.x & 31);
+            if (ok) {
+              const uint32_t d = (uint32_t)en.y >> 28, row = (uint32_t)en.y & 0x0fffffffu;
+              __stcg(sba.peer_ubuf[d] + gh::uidx(row, px[i] >> 5), val);
+            }
+          }
         }
       }
       __syncwarp();
@@ -632,7 +667,21 @@ __global__ void __launch_bounds__(kTmaThreads, 2) k_diffuse_tma(const __grid_con
         const int32_t px0 = pstart(X);
         const int32_t lo = cb * 32 > px0 ? cb * 32 : px0;
         const int32_t hi = ce * 32 < pend[X] ? ce * 32 : pend[X];
-        if (hi > lo) publish_rows(vba, band_lb, band_le, X, (unsigned long long)(hi - lo));
+        if (hi > lo) {
+          if (kSlice) {  // own counter, then every reader slice's count of this source
+            const uint32_t dm = __ldg(vba->dst_mask + X);
+            if (sba.peer_sys && dm) asm volatile("fence.acq_rel.sys;" ::: "memory");
+            else asm volatile("fence.acq_rel.gpu;" ::: "memory");
+            atomicAdd(vba->rows_done + X, (unsigned long long)(hi - lo));
+            for (uint32_t msk = dm; msk; msk &= msk - 1) {
+              unsigned long long* ctr = sba.peer_gdone[__ffs(msk) - 1] + (size_t)sba.rank * a.nlev + X;
+              if (sba.peer_sys) atomicAdd_system(ctr, (unsigned long long)(hi - lo));
+              else atomicAdd(ctr, (unsigned long long)(hi - lo));
+            }
+          } else {
+            publish_rows(vba, band_lb, band_le, X, (unsigned long long)(hi - lo));
+          }
+        }
       }
     }
     // the block's own rows are published before any warp starts the next step:
@@ -699,6 +748,19 @@ BandArgs band_args(const Band& b) {
   x.hi_ghost = b.hi_ghost;
   x.lb = b.lb;
   x.le = b.le;
+  x.src_mask = b.src_mask.p;
+  x.dst_mask = b.dst_mask.p;
+  x.slice_cnt = b.slice_cnt.p;
+  x.xoff = b.xoff.p;
+  x.xent = b.xent.p;
+  x.gdone = b.gdone;
+  for (int d = 0; d < Band::kMaxSlices; ++d) {
+    x.peer_ubuf[d] = b.peer_ubuf[d];
+    x.peer_gdone[d] = b.peer_gdone[d];
+  }
+  x.nslices = b.nslices;
+  x.rank = b.rank;
+  x.peer_sys = b.peer_sys ? 1 : 0;
   return x;
 }
 
@@ -721,6 +783,7 @@ void bands_prepare(gh_levels* L, std::vector<Band*>& bands, double t, const doub
     GH_LAUNCH_CHECK();
     m->launches++;
     GH_CUDA(cudaMemsetAsync(b->rows_done, 0, sizeof(unsigned long long) * b->nlev, s));
+    if (b->gdone) GH_CUDA(cudaMemsetAsync(b->gdone, 0, sizeof(unsigned long long) * b->nslices * b->nlev, s));
     GH_CUDA(cudaMemsetAsync(b->stalled, 0, sizeof(int32_t), s));
   }
 }
@@ -733,7 +796,9 @@ double bands_launch(gh_levels* L, std::vector<Band*>& bands, double t, int32_t s
   int32_t wmax = 1;
   int64_t rows = 0;
   int32_t win = -1;  // the bands' common 16-bit column format (0: some band has none)
+  const bool slices = bands[0]->nslices > 0;
   for (Band* b : bands) {
+    if ((b->nslices > 0) != slices) fail(GH_ERR_INVALID, "diffusion: slices and level bands in one launch");
     wmax = std::max(wmax, b->max_chunk_width);
     rows += b->own_rows;
     if (!b->own_chunks) continue;
@@ -743,6 +808,7 @@ double bands_launch(gh_levels* L, std::vector<Band*>& bands, double t, int32_t s
   // picks one only if at most 1/64 of its chunks fall back to 32 bits);
   // GH_DIFFUSE_COL32 forces 32-bit columns (tests)
   if (win < 0 || getenv("GH_DIFFUSE_COL32")) win = 0;
+  if (slices && win == 2) win = 0;  // slices are laid out for 3 windows (ghost rows in window 3)
   const bool col16 = win != 0;
   // slot = 512 B header + per chunk (den 256 B + deg 64 B + wcap x 32 x (2 or 4 + 8) B of columns/weights)
   const int32_t wcap = std::min<int32_t>(wmax, 16);
@@ -758,10 +824,13 @@ double bands_launch(gh_levels* L, std::vector<Band*>& bands, double t, int32_t s
   }
   if (nslots < 2) nslots = 2;
   const size_t shmem = 16 * (size_t)nslots + table_bytes + 128 + (size_t)nslots * slot_bytes;
-#define GH_DIFFUSE_FN(W)                                                                                 \
-  (wmax <= 6 ? (table ? (void*)k_diffuse_tma<6, true, W> : (void*)k_diffuse_tma<6, false, W>)           \
-             : (table ? (void*)k_diffuse_tma<8, true, W> : (void*)k_diffuse_tma<8, false, W>))
-  void* fn = win == 2 ? GH_DIFFUSE_FN(2) : win == 3 ? GH_DIFFUSE_FN(3) : GH_DIFFUSE_FN(0);
+#define GH_DIFFUSE_FN(W, S)                                                                                    \
+  (wmax <= 6 ? (table ? (void*)k_diffuse_tma<6, true, W, S> : (void*)k_diffuse_tma<6, false, W, S>)           \
+             : (table ? (void*)k_diffuse_tma<8, true, W, S> : (void*)k_diffuse_tma<8, false, W, S>))
+  void* fn = slices     ? (win == 3 ? GH_DIFFUSE_FN(3, true) : GH_DIFFUSE_FN(0, true))
+             : win == 2 ? GH_DIFFUSE_FN(2, false)
+             : win == 3 ? GH_DIFFUSE_FN(3, false)
+                        : GH_DIFFUSE_FN(0, false);
 #undef GH_DIFFUSE_FN
   L->last_col16 = win;
   GH_CUDA(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)shmem));

@@ -251,6 +251,26 @@ struct Band {
   unsigned long long* hi_done = nullptr;
   int64_t hi_nrows = 0;
   int32_t hi_ghost = 0;  // row of level le-1 inside the upper neighbour
+  // Sector slices: nslices > 0 when this is slice `rank` of a
+  // partition that gives every slice a contiguous 1/nslices of every ring (so
+  // every slice has work at every pipeline step). Rows: own rows as above
+  // (lb = 0, le = nlev), then the ghost rows — every foreign neighbour of an
+  // own row, in ring order — from `own_rows` on. The owner of a ghosted row
+  // stores its new value into the reader's ghost row (export list) and counts
+  // its finished rows per level into the reader's gdone[source][level].
+  int32_t nslices = 0, rank = 0;
+  DevBuf<uint32_t> src_mask;    // [nlev] slices whose rows this slice ghosts, per level
+  DevBuf<uint32_t> dst_mask;    // [nlev] slices that ghost rows of this slice, per level
+  DevBuf<int32_t> slice_cnt;    // [nslices * nlev] own rows of every slice per level
+  DevBuf<int32_t> xoff;         // [own_chunks + 1] export entries of each own chunk
+  DevBuf<int2> xent;            // (own row, dest slice << 28 | dest ghost row), by own row
+  unsigned long long* gdone = nullptr;  // [nslices * nlev] ghost rows finished per (source, level)
+  static constexpr int kMaxSlices = 8;
+  double* peer_ubuf[kMaxSlices] = {};
+  unsigned long long* peer_gdone[kMaxSlices] = {};
+  bool peer_sys = false;        // peers on other devices: system-scope release and polls
+  int64_t ghost_rows = 0;       // rows [own_rows, own_rows + ghost_rows) are ghosts
+  int64_t exports = 0;          // export entries
   Band() = default;
   Band(const Band&) = delete;
   Band& operator=(const Band&) = delete;
@@ -293,6 +313,11 @@ void bfs_build(gh_levels* L, const int32_t* h_sources, int32_t ns);
 std::vector<int32_t> plan_bands(const std::vector<int32_t>& offsets, int32_t nbands);
 void band_build(gh_levels* L, Band* b, int32_t lb, int32_t le);
 void band_link(Band* lower, Band* upper);  // same-process neighbours (emulation)
+// slice `rank` of `nslices` (sector sharding); slice_link connects the slices of
+// one process (emulation) to each other
+void slice_build(gh_levels* L, Band* b, int32_t rank, int32_t nslices);
+void slice_link(std::vector<Band*>& slices);
+void band_own_mask(const Band* b, uint8_t* d_mask, int64_t nv, cudaStream_t s);  // 1 on the band's own vertices
 
 // diffusion (gh_diffuse.cu): result stays in L->u_orig (original order)
 double diffuse_dev(gh_levels* L, double t, int32_t sweeps, const double* d_initial);

@@ -257,6 +257,64 @@ def test_band_sharded_diffusion_bitwise(gpu, nbands):
     assert_same(bands.gs_diffuse_bands(mesh, lv, nbands, t, 200), one, f"config 3/8 with {nbands} bands")
 
 
+@pytest.mark.parametrize("nslices", [1, 2, 3, 5, 8])
+def test_slice_sharded_diffusion_bitwise(gpu, port_oracle, nslices):
+    """Sector slices (every slice owns 1/N of every ring; foreign neighbours are
+    ghost rows their owners store into, counted per source slice and level),
+    emulated with all slices in one launch on this GPU: bit-identical to the
+    reference on every fixture (cold and warm start), on configs 2-5 at reduced
+    size (config 4 in Morton ring order), and the ghost/export bookkeeping is
+    consistent (every reachable vertex owned by exactly one slice)."""
+    from paper_1812_06060_b200 import bands, meshgen
+    gh = gpu
+    for case in CASES:
+        g = np.load(os.path.join(GOLDEN, case + ".npz"))
+        if int(g["sweeps"]) == 0:
+            continue
+        mesh = gh.build_mesh(g["positions"], g["faces"])
+        lv = gh.bfs_levels(mesh, g["sources"])
+        u = bands.gs_diffuse_slices(mesh, lv, nslices, float(g["t"]), int(g["sweeps"]))
+        assert_same(u, g["u"], f"{case} with {nslices} slices")
+        if "u_warm3" in g.files:
+            uw = bands.gs_diffuse_slices(mesh, lv, nslices, float(g["t"]), 3, initial=g["u"])
+            assert_same(uw, g["u_warm3"], f"{case} warm start, {nslices} slices")
+    for config, scale, sweeps in ((2, 8, 150), (3, 8, 200), (4, 64, 120), (5, 128, 100)):
+        w = meshgen.config(config, scale=scale)
+        om = port_oracle.build_mesh(w.positions, w.faces)
+        ol = om.bfs(w.sources)
+        t = om.diffusion_time(1.0) if w.t is None else w.t
+        ref, _ = om.gs_diffuse(ol, t, sweeps)
+        mesh = gh.build_mesh(w.positions, w.faces)
+        lv = gh.bfs_levels(mesh, w.sources)
+        assert_same(bands.gs_diffuse_slices(mesh, lv, nslices, t, sweeps), ref, f"C{config} {nslices} slices")
+        if config == 3:
+            owned = np.zeros(mesh.vertex_count(), np.int64)
+            parts = [bands.Band(lv, r, nslices, partition="slices") for r in range(nslices)]
+            for p in parts:
+                owned += p.own_mask()
+            reach = lv.level_of_vertex >= 0
+            assert np.all(owned[reach] == 1) and np.all(owned[~reach] == 0)
+
+
+def test_slice_blobs_connect_all(gpu):
+    """Multi-process slice handles: every rank's IPC blob; connect_all refuses a
+    blob list in the wrong order or from another partition before mapping."""
+    from paper_1812_06060_b200 import bands
+    gh = gpu
+    g = np.load(os.path.join(GOLDEN, "icosphere3.npz"))
+    mesh = gh.build_mesh(g["positions"], g["faces"])
+    lv = gh.bfs_levels(mesh, g["sources"])
+    parts = [bands.Band(lv, r, 3, partition="slices") for r in range(3)]
+    blobs = [p.export() for p in parts]
+    with pytest.raises(ValueError, match="not slice"):
+        parts[0].connect_all([blobs[0], blobs[2], blobs[1]])
+    other = bands.Band(lv, 1, 2, partition="slices").export()
+    with pytest.raises(ValueError, match="not slice"):
+        parts[0].connect_all([blobs[0], other, blobs[2]])
+    with pytest.raises(ValueError, match="gh_band_connect_all"):
+        parts[0].connect(None, blobs[1])
+
+
 def test_band_export_and_neighbour_checks(gpu):
     """Multi-process band handles: the IPC blob round-trips and connect() refuses
     a blob that is not the adjacent band (before any peer mapping)."""
