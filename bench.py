@@ -18,11 +18,14 @@ config that fits one GPU with the CPU reference timed beside it: torus
   --impl reference  the reference's own CPU gs_diffuse (oracle/_ref, the
          unmodified reference headers, all host threads) on a bounded sample.
 
-Multi-GPU (torchrun, N > 1): the diffusion is sharded into BFS bands, one per
-rank; ranks exchange their boundary levels through CUDA IPC
-peer memory inside the one diffusion kernel. value = the whole solve's
-vertex-updates / the slowest rank's kernel time (strong scaling: the mesh is
-fixed); the roofline is rank 0's own band.
+Multi-GPU (torchrun, N > 1): the diffusion is partitioned over the ranks
+(DESIGN.md §7): sector slices by default (every rank owns 1/N
+of every BFS ring, so every rank works at every pipeline step), or BFS bands
+(--partition bands); ranks write the rows the others read into their ghost
+rows through CUDA IPC peer memory inside the one diffusion kernel. value =
+the whole solve's vertex-updates / the slowest rank's kernel time (strong
+scaling: the mesh is fixed); the roofline is rank 0's own part. The e2e
+merge of u is an NCCL all-reduce on the device.
 """
 from __future__ import annotations
 
@@ -55,6 +58,8 @@ def parse():
     ap.add_argument("--e2e-steps", type=int, default=3)
     ap.add_argument("--cpu-sample-sweeps", type=int, default=0, help="0 = auto (about 10-30 s of CPU work)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--partition", default="slices", choices=["slices", "bands"],
+                    help="N > 1: sector slices (every rank 1/N of every BFS ring) or BFS bands")
     return ap.parse_args()
 
 
@@ -261,7 +266,7 @@ def main():
     if world > 1:
         # BFS-band sharding: this rank computes its band of levels;
         # neighbours exchange boundary levels through peer memory inside the kernel
-        band = GB.Band(lv, rank, world)
+        band = GB.Band(lv, rank, world, partition=a.partition)
         band.connect_via(dist)
         mine = band.own_mask()
     else:
@@ -335,7 +340,8 @@ def main():
                       "d2h": rr.d2h_ms}
             e2e_extra = {"admm_iterations": rr.admm_iterations, "zero_count": rr.zero_count}
         else:
-            dt, stages, e2e_extra = sharded_e2e(G, GB, L, w, P, Fc, S, pp, pf, pd, rank, world, local, dist)
+            dt, stages, e2e_extra = sharded_e2e(G, GB, L, w, P, Fc, S, pp, pf, pd, rank, world, local, dist,
+                                                a.partition)
         if i > 1:  # two warm-up calls (module load, pool growth, first-touch of pinned pages)
             e2e_s.append(dt)
     e2e_sec = max_over_ranks(dist, float(np.mean(e2e_s)), local)
@@ -373,7 +379,7 @@ def main():
         "scaling": "weak" if world == 1 else "strong", "vs_baseline": None, "dtype": "f64",
         "data": "synthetic (seeded BASELINE config mesh, DESIGN.md §5)",
         "config": dict(base_cfg, t=t, levels=n_levels, max_level_width=max_width),
-        "parallelism": "single-gpu" if world == 1 else f"bfs-bands x{world}",
+        "parallelism": "single-gpu" if world == 1 else f"{'sector-slices' if a.partition == 'slices' else 'bfs-bands'} x{world}",
         **({} if band_info is None else {"band_levels_rank0": band_info[:2], "band_rows_rank0": rows_mine}),
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
                      "traffic": traffic, "peak_source": peak_src, "kernel": "k_diffuse_tma",
@@ -390,11 +396,14 @@ def main():
     print(json.dumps(line), flush=True)
 
 
-def sharded_e2e(G, GB, L, w, P, Fc, S, pp, pf, pd, rank, world, local, dist):
-    """One end-to-end solve with the diffusion sharded over the ranks: every rank
-    builds the mesh and BFS from the pinned host arrays, runs its band, the
-    band results are merged (NCCL all-reduce of the per-rank vertices), and
-    normalisation, ADMM and integration run through the C ABI on every rank."""
+def sharded_e2e(G, GB, L, w, P, Fc, S, pp, pf, pd, rank, world, local, dist, partition):
+    """One end-to-end solve with the diffusion partitioned over the ranks (sector
+    slices or BFS bands): every rank builds the mesh and BFS from the pinned host
+    arrays, runs its part (peer stores into the other ranks' ghost rows inside the
+    one diffusion kernel), the parts' u are merged on the device (each rank's own
+    vertices, NCCL all-reduce in place on the levels' u buffer — no host round
+    trip), and normalisation, ADMM and integration run on every rank from that u
+    (GH_PIPE_U_READY); rank 0's distances are copied to the pinned output."""
     import ctypes as C
 
     import torch
@@ -405,31 +414,29 @@ def sharded_e2e(G, GB, L, w, P, Fc, S, pp, pf, pd, rank, world, local, dist):
     t1 = time.perf_counter()
     lv = G.bfs_levels(mesh, S)
     t_ = w.t if w.t is not None else G.diffusion_time(mesh, w.m)
-    band = GB.Band(lv, rank, world)
+    band = GB.Band(lv, rank, world, partition=partition)
     band.connect_via(dist)
+    foreign = torch.from_numpy(~band.own_mask()).cuda(local)
     band.prepare(t_)
     t2 = time.perf_counter()
     barrier(dist)
     rep = G.SolverReport()
-    u = band.launch(t_, w.sweeps, rep)
+    band.launch(t_, w.sweeps, rep, copy_out=False)
+    barrier(dist)  # every part finished (its last ghost stores land in the others' rows)
     t3 = time.perf_counter()
-    mine = torch.from_numpy(np.where(band.own_mask(), u, 0.0)).cuda(local)
-    dist.all_reduce(mine)
-    u = mine.cpu().numpy()
-    u[lv.level_of_vertex < 0] = 0.0
+    u = lv.u_device()
+    u.masked_fill_(foreign, 0.0)  # this rank's vertices; the all-reduce adds the others' (x + 0 = x exactly)
+    dist.all_reduce(u)
+    torch.cuda.synchronize()
     t4 = time.perf_counter()
-    H = G.normalized_target_gradients(mesh, u)
-    if w.method == "face":
-        r = G.admm_face_optimize(mesh, H.field, G.AdmmConfig(max_iterations=w.admm_iters))
-        d = G.integrate_face_gradients(mesh, lv, r.gradients)
-    else:
-        r = G.admm_edge_optimize(mesh, H.field, G.AdmmConfig(max_iterations=w.admm_iters))
-        d = G.integrate_edge_differences(mesh, lv, r.differences)
+    d, r = G.distance(lv, w.method, w.sweeps, t_, admm=G.AdmmConfig(max_iterations=w.admm_iters), u_ready=True)
     C.memmove(pd, d.ctypes.data, d.nbytes)
     t5 = time.perf_counter()
-    stages = {"build": 1e3 * (t1 - t0), "bfs_band_setup": 1e3 * (t2 - t1), "diffusion": rep.device_ms,
-              "diffusion_wall": 1e3 * (t3 - t2), "merge_u": 1e3 * (t4 - t3), "normalize_admm_integrate": 1e3 * (t5 - t4)}
-    return t5 - t0, stages, {"admm_iterations": r.report.iterations, "zero_count": H.zero_count}
+    stages = {"build": 1e3 * (t1 - t0), "bfs_partition_setup": 1e3 * (t2 - t1), "diffusion": rep.device_ms,
+              "diffusion_wall": 1e3 * (t3 - t2), "merge_u_nccl": 1e3 * (t4 - t3),
+              "normalize_admm_integrate_d2h": 1e3 * (t5 - t4)}
+    band = None
+    return t5 - t0, stages, {"admm_iterations": r.admm_iterations, "zero_count": r.zero_count}
 
 if __name__ == "__main__":
     main()

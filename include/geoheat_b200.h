@@ -118,7 +118,11 @@ typedef struct {
 /* Pipeline selection (PipelineOptions, tools/geoheat.cpp:27-38). */
 typedef enum { GH_METHOD_FACE = 0, GH_METHOD_EDGE = 1, GH_METHOD_POISSON = 2 } gh_method;
 /* gh_pipeline_config.flags */
-enum { GH_PIPE_DIFFUSION_E1 = 1 /* also compute diffusion_residual of u (geoheat.cpp:117) */ };
+enum {
+  GH_PIPE_DIFFUSION_E1 = 1, /* also compute diffusion_residual of u (geoheat.cpp:117) */
+  GH_PIPE_U_READY = 2       /* u is already the levels' diffusion result (gh_levels_u_device, e.g. a
+                               partitioned solve merged across ranks on the device): skip the diffusion */
+};
 
 typedef struct {
   int32_t method;   /* gh_method */
@@ -350,6 +354,11 @@ gh_status gh_gs_diffuse_partitioned(gh_levels* levels, int32_t nparts, int32_t p
 gh_status gh_band_create_partitioned(gh_levels* levels, int32_t rank, int32_t nranks, int32_t partition,
                                      gh_band** out);
 gh_status gh_band_connect_all(gh_band* band, const void* const* blobs, int32_t nranks);
+/* The device buffer holding the levels' diffusion result u [V] (original
+ * vertex order): written by gh_gs_diffuse*, gh_band_launch (this part's
+ * vertices), read by gh_distance with GH_PIPE_U_READY. Valid while the
+ * levels live; for device-side merges (e.g. an NCCL all-reduce). */
+gh_status gh_levels_u_device(gh_levels* levels, double** u_dev, int64_t* n);
 /* mask_out[V] (host): 1 for the vertices whose u this part computes. */
 gh_status gh_band_own_mask(const gh_band* band, uint8_t* mask_out);
 

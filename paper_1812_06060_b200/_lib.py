@@ -115,6 +115,7 @@ SIGNATURES = [
     ("gh_band_create_partitioned", st, [vp, i32, i32, i32, C.POINTER(vp)]),
     ("gh_band_connect_all", st, [vp, C.POINTER(C.c_char_p), i32]),
     ("gh_band_own_mask", st, [vp, vp]),
+    ("gh_levels_u_device", st, [vp, C.POINTER(vp), C.POINTER(i64)]),
     ("gh_band_destroy", st, [vp]),
     ("gh_band_info", st, [vp, C.POINTER(i32), C.POINTER(i32), C.POINTER(i32)]),
     ("gh_band_export", st, [vp, vp, i32, C.POINTER(i32)]),

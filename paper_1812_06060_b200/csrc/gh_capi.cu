@@ -677,7 +677,7 @@ void distance_on_device(gh_levels* L, const gh_pipeline_config& c, double* d_dis
     return;
   }
   gh::EventTimer tn(s), ti(s);
-  const double diff_ms = gh::diffuse_dev(L, t, c.sweeps, nullptr);
+  const double diff_ms = (c.flags & GH_PIPE_U_READY) ? 0.0 : gh::diffuse_dev(L, t, c.sweeps, nullptr);
   if (rep && (c.flags & GH_PIPE_DIFFUSION_E1)) rep->diffusion_e1 = gh::diffusion_residual_dev(L, L->u_orig.p, t);
   gh::Scratch<double> H(3 * (size_t)m->nf, s);
   tn.start();
@@ -1129,6 +1129,14 @@ gh_status gh_band_connect_all(gh_band* band, const void* const* blobs, int32_t n
       b.peer_gdone[d] = static_cast<unsigned long long*>(p);
     }
     b.peer_sys = true;  // the peers are other processes' GPUs
+  });
+}
+
+gh_status gh_levels_u_device(gh_levels* levels, double** u_dev, int64_t* n) {
+  return guarded([&] {
+    require(levels && u_dev, "gh_levels_u_device: null argument");
+    *u_dev = levels->u_orig.p;
+    if (n) *n = (int64_t)levels->u_orig.n;
   });
 }
 

@@ -110,6 +110,7 @@ struct BandArgs {
   const int32_t* slice_cnt;       // [nslices][nlev] own rows per slice
   const int32_t* xoff;            // [own chunks + 1] export entries per chunk
   const int2* xent;               // (own row, dest << 28 | dest row)
+  int32_t xoff_src;               // this slice has ghost rows (from some source slice)
   unsigned long long* gdone;      // [nslices][nlev] this slice's ghost rows finished, per source
   double* peer_ubuf[gh::Band::kMaxSlices];
   unsigned long long* peer_gdone[gh::Band::kMaxSlices];
@@ -208,6 +209,24 @@ __device__ __forceinline__ unsigned long long ld_acquire_sys_u64(const unsigned 
 // neighbour band's GPU (system scope)
 __device__ __forceinline__ unsigned long long ld_done(const unsigned long long* p, bool ghost) {
   return ghost ? ld_acquire_sys_u64(p) : ld_acquire_gpu_u64(p);
+}
+
+// spin until *ctr >= need (acquire); a dependency that never arrives (a dead
+// peer) sets *stalled after ~17 s and gives up, so the launch can report it
+__device__ __forceinline__ void wait_counter(const unsigned long long* ctr, unsigned long long need, bool sys,
+                                             int32_t* stalled) {
+  if (ld_done(ctr, sys) >= need) return;
+  const long long t0 = clock64();
+  unsigned ns = 64;
+  for (unsigned it = 1;; ++it) {
+    __nanosleep(ns);
+    if (ld_done(ctr, sys) >= need) break;
+    if (ns < 512) ns <<= 1;
+    if ((it & 255) == 0 && clock64() - t0 > (1ll << 35)) {
+      atomicExch(stalled, 1);
+      break;
+    }
+  }
 }
 
 // rows [rb, re) of the band's own levels active at step tau: in group g
@@ -455,6 +474,34 @@ __global__ void __launch_bounds__(kTmaThreads, 2) k_diffuse_tma(const __grid_con
       lv_first = __ldg(vba->chunk_level + cb);
       lv_last = __ldg(vba->chunk_level + ce - 1);
     }
+    if (kSlice) {
+      // A slice's share of a step spans many levels (each slice holds 1/N of
+      // every ring), so its dependencies are checked once per step, for all of
+      // them, by warp 0 (own rows, and ghost rows per source slice): one round
+      // of acquires and one L1 invalidation instead of one per level change;
+      // the other warps start after the barrier, so their L1-cached gathers
+      // see only data published before warp 0's acquires (see below).
+      if (warp == 0) {
+        const int32_t l0 = __shfl_sync(0xffffffffu, lv_first, 0), l1 = __shfl_sync(0xffffffffu, lv_last, 0);
+        const int32_t npairs = ((l1 - l0) / 2 + 1) * 3;
+        for (int32_t p = lane; p < npairs; p += 32) {
+          const int32_t Lp = l0 + 2 * (p / 3), X = Lp - 1 + p % 3;
+          if (X < 0 || X >= a.nlev) continue;
+          // level L-1 through sweep s, levels L and L+1 through sweep s-1
+          const unsigned long long sw = (unsigned long long)(s_base - (Lp >> 1) + (X < Lp ? 1 : 0));
+          wait_counter(vba->rows_done + X, sw * (unsigned long long)(pend[X] - pstart(X)), false, vba->stalled);
+          if (vba->xoff_src)
+            for (uint32_t msk = __ldg(vba->src_mask + X); msk; msk &= msk - 1) {
+              const int q = __ffs(msk) - 1;
+              wait_counter(vba->gdone + (size_t)q * a.nlev + X,
+                           sw * (unsigned long long)__ldg(vba->slice_cnt + (size_t)q * a.nlev + X), sba.peer_sys != 0,
+                           vba->stalled);
+            }
+        }
+        __syncwarp();
+      }
+      asm volatile("bar.sync 1, %0;" ::"r"(32 * kConsumerWarps) : "memory");
+    }
     for (int32_t j = 0; j < ntile; ++j) {
       mbar_wait(full + slot, use);
       const unsigned char* sb = slots + (size_t)slot * a.slot_bytes;
@@ -474,7 +521,7 @@ __global__ void __launch_bounds__(kTmaThreads, 2) k_diffuse_tma(const __grid_con
       // drops the SM's whole L1: every value the step reads was published
       // before that acquire, so an L1 line is either refilled from L2 after it
       // or was filled after it — never older than the data the step needs.
-      if (Lq[0] != seen_L || Lq[kChunksPerWarp - 1] != seen_L2 || tau != seen_tau) {
+      if (!kSlice && (Lq[0] != seen_L || Lq[kChunksPerWarp - 1] != seen_L2 || tau != seen_tau)) {
         // operands: wait for levels L-1, L, L+1 of each chunk (lanes 3i..3i+2)
         const int i = lane / 3;
         const int32_t Li = i == 0 ? Lq[0] : Lq[kChunksPerWarp - 1];  // no dynamic register-array index
@@ -483,30 +530,9 @@ __global__ void __launch_bounds__(kTmaThreads, 2) k_diffuse_tma(const __grid_con
           if (X >= 0 && X < a.nlev) {
             // level L-1 through sweep s, levels L and L+1 through sweep s-1
             const int32_t s = s_base - (Li >> 1);
-            const unsigned long long sw = (unsigned long long)(s + (X < Li ? 1 : 0));
-            const bool ghost = X < band_lb || X >= band_le;
-            auto wait_for = [&](const unsigned long long* ctr, unsigned long long need, bool sys) {
-              if (ld_done(ctr, sys) >= need) return;
-              const long long t0 = clock64();
-              unsigned ns = 64;
-              for (unsigned it = 1;; ++it) {
-                __nanosleep(ns);
-                if (ld_done(ctr, sys) >= need) break;
-                if (ns < 512) ns <<= 1;
-                if ((it & 255) == 0 && clock64() - t0 > (1ll << 35)) {  // ~17 s: a neighbour is gone
-                  atomicExch(vba->stalled, 1);
-                  break;
-                }
-              }
-            };
-            wait_for(vba->rows_done + X, sw * (unsigned long long)(pend[X] - pstart(X)), ghost);
-            if (kSlice) {  // ghost rows of level X, per source slice
-              for (uint32_t msk = __ldg(vba->src_mask + X); msk; msk &= msk - 1) {
-                const int q = __ffs(msk) - 1;
-                wait_for(vba->gdone + (size_t)q * a.nlev + X,
-                         sw * (unsigned long long)__ldg(vba->slice_cnt + (size_t)q * a.nlev + X), sba.peer_sys != 0);
-              }
-            }
+            const unsigned long long need =
+                (unsigned long long)(s + (X < Li ? 1 : 0)) * (unsigned long long)(pend[X] - pstart(X));
+            wait_counter(vba->rows_done + X, need, X < band_lb || X >= band_le, vba->stalled);
           }
         }
         __syncwarp();
@@ -637,7 +663,7 @@ __global__ void __launch_bounds__(kTmaThreads, 2) k_diffuse_tma(const __grid_con
           if (Lq[i] == band_le - 1 && vba->hi_ubuf)
             __stcg(vba->hi_ubuf + gh::uidx((uint32_t)(vba->hi_ghost + (r - pstart(Lq[i]))), par), un);
         }
-        if (kSlice && live[i]) {
+        if (kSlice && live[i] && vba->xoff) {
           // rows other slices read: into their ghost rows (same sweep parity)
           const int32_t x0 = __ldg(vba->xoff + c), x1 = __ldg(vba->xoff + c + 1);
           for (int32_t e0 = x0; e0 < x1; e0 += 32) {
@@ -751,8 +777,9 @@ BandArgs band_args(const Band& b) {
   x.src_mask = b.src_mask.p;
   x.dst_mask = b.dst_mask.p;
   x.slice_cnt = b.slice_cnt.p;
-  x.xoff = b.xoff.p;
+  x.xoff = b.exports ? b.xoff.p : nullptr;  // no exports: no per-chunk lookups
   x.xent = b.xent.p;
+  x.xoff_src = b.ghost_rows > 0 ? 1 : 0;
   x.gdone = b.gdone;
   for (int d = 0; d < Band::kMaxSlices; ++d) {
     x.peer_ubuf[d] = b.peer_ubuf[d];

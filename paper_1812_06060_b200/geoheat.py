@@ -353,6 +353,17 @@ class BfsLevels:
     def level_count(self) -> int:
         return self._nlev
 
+    def u_device(self):
+        """The device buffer of the diffusion result u [V] as a torch tensor (no copy)."""
+        import torch
+        p, n = C.c_void_p(), C.c_int64()
+        _check(self._lib.gh_levels_u_device(self._h, C.byref(p), C.byref(n)))
+
+        class _View:
+            __cuda_array_interface__ = {"shape": (n.value,), "typestr": "<f8", "data": (p.value, False),
+                                        "version": 3}
+        return torch.as_tensor(_View(), device=f"cuda:{torch.cuda.current_device()}")
+
     def _arrays(self):
         if self._cache is None:
             nv = self.mesh.vertex_count()
@@ -563,10 +574,11 @@ _METHODS = {"face": 0, "edge": 1, "poisson": 2}
 
 
 def _pipeline_config(method, sweeps, t, m, admm: AdmmConfig, cg_tol: float = 1e-5,
-                     diffusion_e1: bool = False) -> gh_pipeline_config:
+                     diffusion_e1: bool = False, u_ready: bool = False) -> gh_pipeline_config:
     meth = _METHODS[method] if isinstance(method, str) else int(method)
+    flags = (1 if diffusion_e1 else 0) | (2 if u_ready else 0)
     return gh_pipeline_config(meth, int(sweeps), float(t if t is not None else 0.0), float(m), admm._c(),
-                              float(cg_tol), 1 if diffusion_e1 else 0, 0)
+                              float(cg_tol), flags, 0)
 
 
 def _run_report(r: gh_run_report) -> RunReport:
@@ -575,11 +587,14 @@ def _run_report(r: gh_run_report) -> RunReport:
 
 
 def distance(levels: BfsLevels, method: str = "face", sweeps: int = 1000, t: Optional[float] = None, m: float = 1.0,
-             admm: AdmmConfig = AdmmConfig(), cg_tol: float = 1e-5, diffusion_e1: bool = False):
+             admm: AdmmConfig = AdmmConfig(), cg_tol: float = 1e-5, diffusion_e1: bool = False,
+             u_ready: bool = False):
     """The solver chain of run_pipeline (tools/geoheat.cpp:96-143), device-resident between stages;
-    method "face" | "edge" | "poisson" (the CG heat method, cg_tol = the CLI's --eps)."""
+    method "face" | "edge" | "poisson" (the CG heat method, cg_tol = the CLI's --eps). u_ready: the
+    levels' device u (u_device()) already holds the diffusion result, e.g. a partitioned solve
+    merged across ranks on the device; the diffusion is skipped."""
     d = np.empty(levels.mesh.vertex_count(), np.float64)
-    cfg = _pipeline_config(method, sweeps, t, m, admm, cg_tol, diffusion_e1)
+    cfg = _pipeline_config(method, sweeps, t, m, admm, cg_tol, diffusion_e1, u_ready)
     rep = gh_run_report()
     _check(levels._lib.gh_distance(levels._h, C.byref(cfg), _ptr(d), C.byref(rep)))
     return d, _run_report(rep)

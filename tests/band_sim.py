@@ -74,3 +74,90 @@ def run_band(rank, world, mesh_arrays, levels, t, sweeps, plan):
     u = part.numpy()
     u[level_of < 0] = u0[level_of < 0]
     return u
+
+
+def slice_owner(levels, nslices):
+    """Slice of every vertex (-1 unreachable): position p of n in its ring -> p * N // n
+    (gh_band.cu k_slice_owner, with the BFS ring order as the layout order)."""
+    order, loff = levels["order"], levels["offsets"]
+    owner = np.full(len(levels["level_of_vertex"]), -1, np.int64)
+    for L in range(len(loff) - 1):
+        a, b = int(loff[L]), int(loff[L + 1])
+        owner[order[a:b]] = (np.arange(b - a, dtype=np.int64) * nslices) // (b - a)
+    return owner
+
+
+def run_slice(rank, world, mesh_arrays, levels, t, sweeps):
+    """One sector slice of the pipelined diffusion: this rank
+    updates its 1/N of every ring at every step; after every step it sends the
+    rows each other rank ghosts (foreign neighbours of that rank's rows) to it,
+    both parity buffers. The gathered own rows must equal gs_diffuse bit for bit."""
+    off = mesh_arrays["vv_offset"]
+    idx = mesh_arrays["vv_index"]
+    w = mesh_arrays["vv_weight"]
+    va = mesh_arrays["vertex_area"]
+    ws = mesh_arrays["vertex_weight_sum"]
+    level_of = levels["level_of_vertex"]
+    order, loff = levels["order"], levels["offsets"]
+    nlev = len(loff) - 1
+    owner = slice_owner(levels, world)
+    u0 = (level_of == 0).astype(np.float64)
+    buf = [u0.copy(), u0.copy()]
+    ring = [order[loff[L]:loff[L + 1]] for L in range(nlev)]
+    mine = [r[owner[r] == rank] for r in ring]
+    # ghosts of slice d: foreign neighbours of its rows; export[d] = this rank's rows d ghosts
+    reach = np.flatnonzero(level_of >= 0)
+    src = np.repeat(reach, off[reach + 1] - off[reach])
+    nbr = idx[np.concatenate([np.arange(off[v], off[v + 1]) for v in reach])] if reach.size else np.zeros(0, int)
+    export = {}
+    for d in range(world):
+        if d == rank:
+            continue
+        sel = (owner[src] == d) & (owner[nbr] == rank)
+        export[d] = np.unique(nbr[sel])
+    imports = {}
+    for q in range(world):
+        if q == rank:
+            continue
+        sel = (owner[src] == rank) & (owner[nbr] == q)
+        imports[q] = np.unique(nbr[sel])
+
+    def update(rows, L, s):
+        cur, prev = buf[s & 1], buf[(s & 1) ^ 1]
+        deg = off[rows + 1] - off[rows]
+        K = int(deg.max()) if rows.size else 0
+        num = np.zeros(rows.size)
+        for k in range(K):  # sequential row sums in the reference's neighbour order
+            has = k < deg
+            a = off[rows] + np.minimum(k, deg - 1)
+            nb = idx[a]
+            val = np.where(level_of[nb] == L - 1, cur[nb], prev[nb])
+            num = np.where(has, num + w[a] * val, num)
+        cur[rows] = ((L == 0) * 1.0 + t * num) / (va[rows] + t * ws[rows])
+
+    def exchange():
+        reqs, recvs = [], []
+        for d, rows in export.items():
+            reqs.append(dist.isend(torch.from_numpy(np.concatenate([buf[0][rows], buf[1][rows]])), d))
+        for q, rows in imports.items():
+            inc = torch.empty(2 * rows.size, dtype=torch.float64)
+            reqs.append(dist.irecv(inc, q))
+            recvs.append((rows, inc))
+        for r in reqs:
+            r.wait()
+        for rows, inc in recvs:
+            buf[0][rows] = inc[:rows.size].numpy()
+            buf[1][rows] = inc[rows.size:].numpy()
+
+    nsteps = (nlev - 1) + 2 * (sweeps - 1) + 1
+    for tau in range(nsteps):
+        for L in range(nlev):
+            if (tau - L) % 2 == 0 and 0 <= (tau - L) // 2 < sweeps and mine[L].size:
+                update(mine[L], L, (tau - L) // 2)
+        exchange()
+    result = buf[(sweeps - 1) & 1]
+    part = torch.from_numpy(np.where(owner == rank, result, 0.0))
+    dist.all_reduce(part)
+    u = part.numpy()
+    u[level_of < 0] = u0[level_of < 0]
+    return u
