@@ -523,25 +523,62 @@ gh_status gh_gs_diffuse_tol(gh_levels* levels, double t, int32_t sweeps, double 
     cudaStream_t s = m->stream;
     const double w0 = now_s();
     take_launches(m);
-    // E1 is checked after every sweep (diffusion.hpp:110-117), so sweeps run one
-    // launch at a time, each warm-started from the previous u (a sweep depends
-    // on u only, so this is bit-identical to running them back to back).
+    // E1 is checked after every sweep (diffusion.hpp:110-117). The sweeps run
+    // pipelined in groups of K per launch; the kernel also writes every
+    // update into a snapshot of its sweep, so after a group each sweep's u is
+    // scattered to vertex order, its E1 computed (the exact left-to-right sum)
+    // and the first sweep at or below the tolerance ends the solve with that
+    // sweep's u. The next group is warm-started from the group's last u (a
+    // sweep depends on u only, so this is bit-identical to one long run).
     gh::Scratch<double> cur(m->nv, s);
-    if (initial) GH_CUDA(cudaMemcpyAsync(cur.p, initial, sizeof(double) * m->nv, cudaMemcpyHostToDevice, s));
     double ms = 0.0;
     int done = 0;
     bool converged = false;
-    if (sweeps == 0) ms += gh::diffuse_dev(levels, t, 0, initial ? cur.p : nullptr);
-    for (int k = 0; k < sweeps; ++k) {
-      ms += gh::diffuse_dev(levels, t, 1, (k > 0 || initial) ? cur.p : nullptr);
-      ++done;
-      const double e1 = gh::diffusion_residual_dev(levels, levels->u_orig.p, t);
-      if (report && report->residual_history && k < report->history_capacity) report->residual_history[k] = e1;
-      if (e1 <= tolerance) {
-        converged = true;
-        break;
+    if (sweeps == 0 || levels->nreach == 0) {
+      if (initial) GH_CUDA(cudaMemcpyAsync(cur.p, initial, sizeof(double) * m->nv, cudaMemcpyHostToDevice, s));
+      ms += gh::diffuse_dev(levels, t, 0, initial ? cur.p : nullptr);
+      for (int k = 0; k < sweeps; ++k) {  // nothing reachable moves: every sweep leaves u as it is
+        const double e1 = gh::diffusion_residual_dev(levels, levels->u_orig.p, t);
+        ++done;
+        if (report && report->residual_history && k < report->history_capacity) report->residual_history[k] = e1;
+        if (e1 <= tolerance) {
+          converged = true;
+          break;
+        }
       }
-      GH_CUDA(cudaMemcpyAsync(cur.p, levels->u_orig.p, sizeof(double) * m->nv, cudaMemcpyDeviceToDevice, s));
+    } else {
+      if (!(t > 0.0)) gh::fail(GH_ERR_INVALID, "gs_diffuse: t must be positive");
+      // group size: up to 256 sweeps, within half the free device memory
+      size_t free_b = 0, total_b = 0;
+      GH_CUDA(cudaMemGetInfo(&free_b, &total_b));
+      const size_t per = sizeof(double) * (size_t)levels->main.nrows;
+      int32_t kmax = (int32_t)std::max<size_t>(1, std::min<size_t>(256, free_b / 2 / std::max<size_t>(per, 1)));
+      if (const char* e = getenv("GH_TOL_GROUP")) kmax = std::max(1, atoi(e));  // tests: small groups
+      kmax = std::min(kmax, sweeps);
+      gh::Scratch<double> snap((size_t)kmax * levels->main.nrows, s);
+      // unreachable vertices keep their start value through every sweep
+      gh::diffuse_dev(levels, t, 0, nullptr);  // u_orig = start state (u0 or the initial below)
+      if (initial) GH_CUDA(cudaMemcpyAsync(cur.p, initial, sizeof(double) * m->nv, cudaMemcpyHostToDevice, s));
+      else GH_CUDA(cudaMemcpyAsync(cur.p, levels->u_orig.p, sizeof(double) * m->nv, cudaMemcpyDeviceToDevice, s));
+      bool first = true;
+      while (done < sweeps && !converged) {
+        const int32_t k = std::min(kmax, sweeps - done);
+        ms += gh::diffuse_dev(levels, t, k, (first && !initial) ? nullptr : cur.p, snap.p);
+        first = false;
+        for (int32_t i = 0; i < k; ++i) {
+          gh::snapshot_to_orig(levels, snap.p + (size_t)i * levels->main.nrows, cur.p);
+          const double e1 = gh::diffusion_residual_dev(levels, cur.p, t);
+          if (report && report->residual_history && done < report->history_capacity)
+            report->residual_history[done] = e1;
+          ++done;
+          if (e1 <= tolerance) {
+            converged = true;
+            break;
+          }
+        }
+      }
+      GH_CUDA(cudaMemcpyAsync(levels->u_orig.p, cur.p, sizeof(double) * m->nv, cudaMemcpyDeviceToDevice, s));
+      levels->u_sweeps = done;
     }
     if (u_out) to_host(u_out, levels->u_orig.p, m->nv, s);
     else GH_CUDA(cudaStreamSynchronize(s));

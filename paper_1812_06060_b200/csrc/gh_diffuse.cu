@@ -133,6 +133,11 @@ struct TmaArgs {
   // over the levels, group g starting at step g * P. K = sweeps, P = huge is
   // the plain pipeline (step tau = L + 2s).
   int32_t group_sweeps, group_period;
+  // the E1 early stop (gh_gs_diffuse_tol): every update's value also lands in
+  // snap[s * snap_rows + row] (row order of the single band), so u of every
+  // sweep of the launch is available afterwards; null otherwise
+  double* snap;
+  int64_t snap_rows;
   double t;
 };
 
@@ -657,6 +662,7 @@ __global__ void __launch_bounds__(kTmaThreads, 2) k_diffuse_tma(const __grid_con
             asm volatile("div.rn.f64 %0, %1, %2;" : "=d"(un) : "d"(nz), "d"(den[i]));
           const uint32_t par = px[i] >> 5;
           __stcg(ub + gh::uidx((uint32_t)r, par), un);
+          if (a.snap) __stcs(a.snap + (int64_t)(s_base - (Lq[i] >> 1)) * a.snap_rows + r, un);
           // boundary levels also land in the neighbour band's ghost copy
           if (Lq[i] == band_lb && vba->lo_ubuf)
             __stcg(vba->lo_ubuf + gh::uidx((uint32_t)(vba->lo_ghost + (r - pstart(Lq[i]))), par), un);
@@ -722,6 +728,15 @@ T read_scalar(const T* d, cudaStream_t s) {
   GH_CUDA(cudaMemcpyAsync(&v, d, sizeof(T), cudaMemcpyDeviceToHost, s));
   GH_CUDA(cudaStreamSynchronize(s));
   return v;
+}
+
+// one sweep's snapshot (the single band's row order) -> original vertex order
+__global__ void k_scatter_rows(const int32_t* __restrict__ perm, const double* __restrict__ snap, int64_t nrows,
+                               double* __restrict__ u) {
+  for (int64_t r = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; r < nrows; r += (int64_t)gridDim.x * blockDim.x) {
+    const int32_t v = perm[r];
+    if (v >= 0) u[v] = snap[r];
+  }
 }
 
 // r_j = A_j u_j - t * sum theta (u_k - u_j) - u0_j (diffusion.hpp:41-47); sq_j = r_j^2
@@ -817,7 +832,7 @@ void bands_prepare(gh_levels* L, std::vector<Band*>& bands, double t, const doub
 
 // Run the bands in one cooperative launch on the current device, blocks split
 // in proportion to their rows, then scatter their own rows to u_orig.
-double bands_launch(gh_levels* L, std::vector<Band*>& bands, double t, int32_t sweeps) {
+double bands_launch(gh_levels* L, std::vector<Band*>& bands, double t, int32_t sweeps, double* d_snap) {
   gh_mesh* m = L->mesh;
   cudaStream_t s = m->stream;
   int32_t wmax = 1;
@@ -886,6 +901,9 @@ double bands_launch(gh_levels* L, std::vector<Band*>& bands, double t, int32_t s
   a.slot_bytes = slot_bytes;
   a.table_in_smem = table ? 1 : 0;
   a.t = t;
+  if (d_snap && nbands != 1) fail(GH_ERR_INTERNAL, "diffusion snapshots need the single band");
+  a.snap = d_snap;
+  a.snap_rows = bands[0]->nrows;
   // sweep groups: one pipeline of all sweeps unless GH_SWEEP_GROUP=K (then
   // groups of K sweeps, each starting GH_SWEEP_PERIOD steps after the last,
   // at least nlev + 2K - 1 so that the groups never share a step)
@@ -939,12 +957,13 @@ double bands_launch(gh_levels* L, std::vector<Band*>& bands, double t, int32_t s
 namespace {
 }  // namespace
 
-double diffuse_dev(gh_levels* L, double t, int32_t sweeps, const double* d_initial) {
+double diffuse_dev(gh_levels* L, double t, int32_t sweeps, const double* d_initial, double* d_snap) {
   std::vector<Band*> one{&L->main};
-  return diffuse_bands_dev(L, one, t, sweeps, d_initial);
+  return diffuse_bands_dev(L, one, t, sweeps, d_initial, d_snap);
 }
 
-double diffuse_bands_dev(gh_levels* L, std::vector<Band*>& bands, double t, int32_t sweeps, const double* d_initial) {
+double diffuse_bands_dev(gh_levels* L, std::vector<Band*>& bands, double t, int32_t sweeps, const double* d_initial,
+                         double* d_snap) {
   gh_mesh* m = L->mesh;
   cudaStream_t s = m->stream;
   if (sweeps < 0) fail(GH_ERR_INVALID, "DiffusionConfig: sweeps must be >= 0");
@@ -958,11 +977,20 @@ double diffuse_bands_dev(gh_levels* L, std::vector<Band*>& bands, double t, int3
   double ms = 0.0;
   if (sweeps > 0 && L->nreach > 0) {
     bands_prepare(L, bands, t, d_initial);
-    ms = bands_launch(L, bands, t, sweeps);
+    ms = bands_launch(L, bands, t, sweeps, d_snap);
   }
   L->u_valid = 1;
   L->u_sweeps = sweeps;
   return ms;
+}
+
+void snapshot_to_orig(gh_levels* L, const double* d_snap_sweep, double* d_u) {
+  gh_mesh* m = L->mesh;
+  const Band& b = L->main;
+  if (b.own_rows)
+    k_scatter_rows<<<grid_for(b.own_rows), B, 0, m->stream>>>(b.perm.p, d_snap_sweep, b.own_rows, d_u);
+  GH_LAUNCH_CHECK();
+  m->launches++;
 }
 
 double diffusion_residual_dev(gh_levels* L, const double* d_u, double t) {

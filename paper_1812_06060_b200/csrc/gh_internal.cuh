@@ -320,13 +320,17 @@ void slice_link(std::vector<Band*>& slices);
 void band_own_mask(const Band* b, uint8_t* d_mask, int64_t nv, cudaStream_t s);  // 1 on the band's own vertices
 
 // diffusion (gh_diffuse.cu): result stays in L->u_orig (original order)
-double diffuse_dev(gh_levels* L, double t, int32_t sweeps, const double* d_initial);
+// d_snap (optional, [sweeps][main.nrows]): every sweep's u in the band's row order
+double diffuse_dev(gh_levels* L, double t, int32_t sweeps, const double* d_initial, double* d_snap = nullptr);
 // the same solve split into bands that each compute their own levels and
 // exchange boundary levels; all bands on the current device in one launch
-double diffuse_bands_dev(gh_levels* L, std::vector<Band*>& bands, double t, int32_t sweeps, const double* d_initial);
+double diffuse_bands_dev(gh_levels* L, std::vector<Band*>& bands, double t, int32_t sweeps, const double* d_initial,
+                         double* d_snap = nullptr);
 // the two halves of diffuse_bands_dev, for bands that live in other processes
 void bands_prepare(gh_levels* L, std::vector<Band*>& bands, double t, const double* d_initial);
-double bands_launch(gh_levels* L, std::vector<Band*>& bands, double t, int32_t sweeps);
+double bands_launch(gh_levels* L, std::vector<Band*>& bands, double t, int32_t sweeps, double* d_snap = nullptr);
+// the single band's reachable rows of one snapshot sweep into d_u (original order; unreachable untouched)
+void snapshot_to_orig(gh_levels* L, const double* d_snap_sweep, double* d_u);
 double diffusion_residual_dev(gh_levels* L, const double* d_u, double t);
 
 // normalisation + optimisation (gh_grad.cu)

@@ -216,11 +216,16 @@ def test_cpp_wrapper_runs_reference_chain(gpu):
 TOL_CASES = sorted(os.path.basename(p)[:-4] for p in glob.glob(os.path.join(GOLDEN, "tol", "*.npz")))
 
 
+@pytest.mark.parametrize("group", [None, "1", "3", "7"])
 @pytest.mark.parametrize("case", TOL_CASES)
-def test_residual_tolerance_early_stop(gpu, case):
+def test_residual_tolerance_early_stop(gpu, case, group, monkeypatch):
     """gs_diffuse with residual_tolerance (diffusion.hpp:110-117): same stop sweep, bitwise u,
     and the E1 history bit-identical (the reference's left-to-right sum of r^2 is
-    reproduced exactly on the device)."""
+    reproduced exactly on the device). The sweeps run pipelined in groups whose
+    every sweep is snapshot; GH_TOL_GROUP forces small groups so the stop falls
+    inside, at the end of, and across groups."""
+    if group:
+        monkeypatch.setenv("GH_TOL_GROUP", group)
     gh = gpu
     g = np.load(os.path.join(GOLDEN, "tol", case + ".npz"))
     mesh = gh.build_mesh(g["positions"], g["faces"])
