@@ -41,3 +41,25 @@ def test_full_size_hash_equals_reference_chain(gpu, config, method):
         assert rep.converged == rec["converged"][1]
     if rec.get("zero_count") is not None:
         assert rep.zero_count == rec["zero_count"][1]
+
+
+TOL = json.load(open(os.path.join(ROOT, "profiles", "r2_tol_parity.json")))
+
+
+@pytest.mark.parametrize("rec", TOL, ids=lambda r: f"C{r['config']}")
+def test_full_size_residual_tolerance_stop(gpu, rec):
+    """The E1 early stop at full size (configs 2 and 3, 8.4 M vertices): with the
+    tolerance set to the reference's E1 at sweep 60, the device stops at the
+    reference's sweep with the reference's u (tools/tol_parity.py recorded both
+    sides bit-identical, E1 histories included)."""
+    from paper_1812_06060_b200 import meshgen
+    gh = gpu
+    w = meshgen.config(rec["config"])
+    mesh = gh.build_mesh(w.positions, w.faces)
+    lv = gh.bfs_levels(mesh, w.sources)
+    t = w.t if w.t is not None else gh.diffusion_time(mesh, w.m)
+    rep = gh.SolverReport()
+    u = gh.gs_diffuse(mesh, lv, t, gh.DiffusionConfig(sweeps=rec["sweeps"], residual_tolerance=rec["tolerance"]), rep)
+    assert [rep.iterations, rep.converged] == [rec["iterations"][1], rec["converged"][1]]
+    assert f"{gh.field_hash(u):016x}" == rec["u_hash"] and rec["u_bitwise"]
+    assert np.float64(rep.residual_history[-1]).view(np.uint64) == np.float64(rec["e1_final"][1]).view(np.uint64)
