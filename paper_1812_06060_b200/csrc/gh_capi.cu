@@ -1111,6 +1111,7 @@ gh_status gh_band_connect(gh_band* band, const void* lower_blob, const void* upp
     require(band != nullptr, "gh_band_connect: null band");
     gh::Band& b = band->band;
     require(b.nslices == 0, "gh_band_connect: slices connect to every rank (gh_band_connect_all)");
+    b.peer_sys = true;  // the neighbours are other processes' GPUs
     Use use_(band->levels->mesh);
     auto open = [&](const cudaIpcMemHandle_t& h) {
       void* p = nullptr;

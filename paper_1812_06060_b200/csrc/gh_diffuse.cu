@@ -260,16 +260,17 @@ __device__ __forceinline__ bool step_range(const TmaArgs& a, int32_t lb, int32_t
 // release fence, the band's own counter and, for a boundary level, the
 // neighbour band's copy of it (system scope: the neighbour is another GPU).
 __device__ __forceinline__ void publish_rows(const BandArgs* vba, int32_t band_lb, int32_t band_le, int32_t X,
-                                             unsigned long long n) {
+                                             unsigned long long n, bool sys) {
   unsigned long long* lo_done = vba->lo_done;
   unsigned long long* hi_done = vba->hi_done;
   const bool to_lo = X == band_lb && lo_done, to_hi = X == band_le - 1 && hi_done;
-  // release: acq_rel fences (not the sequentially consistent __threadfence)
-  if (to_lo || to_hi) asm volatile("fence.acq_rel.sys;" ::: "memory");
+  // release: acq_rel fences (not the sequentially consistent __threadfence);
+  // system scope only when the neighbour is another GPU
+  if ((to_lo || to_hi) && sys) asm volatile("fence.acq_rel.sys;" ::: "memory");
   else asm volatile("fence.acq_rel.gpu;" ::: "memory");
   atomicAdd(vba->rows_done + X, n);
-  if (to_lo) atomicAdd_system(lo_done + X, n);
-  if (to_hi) atomicAdd_system(hi_done + X, n);
+  if (to_lo) sys ? (void)atomicAdd_system(lo_done + X, n) : (void)atomicAdd(lo_done + X, n);
+  if (to_hi) sys ? (void)atomicAdd_system(hi_done + X, n) : (void)atomicAdd(hi_done + X, n);
 }
 
 // slot layout: header 512 B (int32: chunk offsets [0..kTileChunks], fits [31], chunk levels [32..],
@@ -537,7 +538,7 @@ __global__ void __launch_bounds__(kTmaThreads, 2) k_diffuse_tma(const __grid_con
             const int32_t s = s_base - (Li >> 1);
             const unsigned long long need =
                 (unsigned long long)(s + (X < Li ? 1 : 0)) * (unsigned long long)(pend[X] - pstart(X));
-            wait_counter(vba->rows_done + X, need, X < band_lb || X >= band_le, vba->stalled);
+            wait_counter(vba->rows_done + X, need, (X < band_lb || X >= band_le) && sba.peer_sys, vba->stalled);
           }
         }
         __syncwarp();
@@ -711,7 +712,7 @@ __global__ void __launch_bounds__(kTmaThreads, 2) k_diffuse_tma(const __grid_con
               else atomicAdd(ctr, (unsigned long long)(hi - lo));
             }
           } else {
-            publish_rows(vba, band_lb, band_le, X, (unsigned long long)(hi - lo));
+            publish_rows(vba, band_lb, band_le, X, (unsigned long long)(hi - lo), sba.peer_sys != 0);
           }
         }
       }
@@ -802,7 +803,10 @@ BandArgs band_args(const Band& b) {
   }
   x.nslices = b.nslices;
   x.rank = b.rank;
-  x.peer_sys = b.peer_sys ? 1 : 0;
+  // GH_PEER_SYS=1: system-scope release and polls between same-device parts
+  // too (the emulation then pays what links between GPUs cost)
+  const bool force_sys = getenv("GH_PEER_SYS") && atoi(getenv("GH_PEER_SYS")) != 0;
+  x.peer_sys = (b.peer_sys || force_sys) ? 1 : 0;
   return x;
 }
 
@@ -1002,7 +1006,14 @@ double diffusion_residual_dev(gh_levels* L, const double* d_u, double t) {
   GH_LAUNCH_CHECK();
   m->launches++;
   // sqrt(deterministic_sum(sq)) (diffusion.hpp:48): the left-to-right sum, bit for bit
-  return std::sqrt(sequential_sum_nonneg(sq.p, m->nv, m->stream, &m->launches));
+  static const bool prof = getenv("GH_E1_PROFILE") != nullptr;  // stage times on stderr (experiments)
+  if (!prof) return std::sqrt(sequential_sum_nonneg(sq.p, m->nv, m->stream, &m->launches));
+  EventTimer ts(m->stream);
+  ts.start();
+  const double sum = sequential_sum_nonneg(sq.p, m->nv, m->stream, &m->launches);
+  ts.stop();
+  fprintf(stderr, "e1_sum_ms %.4f\n", ts.ms());
+  return std::sqrt(sum);
 }
 
 }  // namespace gh

@@ -16,6 +16,7 @@
 // stop rule compares them against thresholds with the same formulas.
 
 #include <algorithm>
+#include <cstdlib>
 #include <cmath>
 
 #include "gh_internal.cuh"
@@ -74,18 +75,33 @@ __global__ void k_face_slots(const int32_t* __restrict__ he_edge, const int32_t*
 // Y-update for interior edge i (grad_face.hpp:126-137 + y_update_edge 31-36)
 // from the two side faces' g and lambda; d = lambda / (mu sqrt(A)) per side is
 // returned too (the G-update adds the same quotient, grad_face.hpp:150).
-__device__ __forceinline__ void face_y_update(int64_t i, v3 g1, v3 g2, double a1, double a2, double mu,
-                                              const double* __restrict__ edir, v3 l1, v3 l2, v3& y1, v3& y2, v3& d1,
-                                              v3& d2) {
-  d1 = divs(l1, mu * sqrt(a1));
-  d2 = divs(l2, mu * sqrt(a2));
+// msa = mu * sqrt(A) of each side face and w = (A2 / (A1 + A2), A1 / (A1 + A2))
+// of the edge are computed once per solve (k_face_consts, k_face_init_edges):
+// the same operations on the same operands as the reference's per-iteration
+// expressions, so the same bits, without 2 sqrt + 2 divisions per call.
+__device__ __forceinline__ void face_y_update(int64_t i, v3 g1, v3 g2, double msa1, double msa2, double w1,
+                                              double w2, const double* __restrict__ edir, v3 l1, v3 l2, v3& y1,
+                                              v3& y2, v3& d1, v3& d2) {
+  d1 = divs(l1, msa1);
+  d2 = divs(l2, msa2);
   const v3 q1 = sub(g1, d1);
   const v3 q2 = sub(g2, d2);
   const v3 ed = ld3(edir, i);
   const double mismatch = dot(ed, sub(q2, q1));
   const v3 shift = mk(ed.x * mismatch, ed.y * mismatch, ed.z * mismatch);
-  y1 = add(q1, scale(ddiv(a2, a1 + a2), shift));
-  y2 = sub(q2, scale(ddiv(a1, a1 + a2), shift));
+  y1 = add(q1, scale(w1, shift));
+  y2 = sub(q2, scale(w2, shift));
+}
+
+// per face: mu sqrt(A) (the dual offset's divisor, grad_face.hpp:130-131, 150)
+// and sqrt(A) (the primal rows' weight, grad_face.hpp:163-164)
+__global__ void k_face_consts(const double* __restrict__ area, int64_t nf, double mu, double* __restrict__ msa,
+                              double* __restrict__ sa) {
+  GRID_STRIDE(f, nf) {
+    const double r = sqrt(area[f]);
+    msa[f] = mu * r;
+    sa[f] = r;
+  }
 }
 
 // ctor (grad_face.hpp:76-85): edge_dir, incident faces, lambda = 0, scale
@@ -95,9 +111,9 @@ __device__ __forceinline__ void face_y_update(int64_t i, v3 g1, v3 g2, double a1
 __global__ void k_face_init_edges(const double* __restrict__ pos, const int32_t* __restrict__ interior_edges,
                                   const int32_t* __restrict__ edge_v, const int32_t* __restrict__ edge_he,
                                   const double* __restrict__ area, const double* __restrict__ h, int64_t ni,
-                                  double mu, double* __restrict__ edir, int32_t* __restrict__ ef,
-                                  double* __restrict__ lam, double* __restrict__ C, double* __restrict__ part,
-                                  double* __restrict__ term) {
+                                  double mu, const double* __restrict__ msa, double* __restrict__ edir,
+                                  int32_t* __restrict__ ef, double* __restrict__ wq, double* __restrict__ lam,
+                                  double* __restrict__ C, double* __restrict__ part, double* __restrict__ term) {
   double s = 0.0;
   GRID_STRIDE(i, ni) {
     const int32_t e = interior_edges[i];
@@ -112,9 +128,12 @@ __global__ void k_face_init_edges(const double* __restrict__ pos, const int32_t*
     const double tt = a1 + a2;  // scale2 += A1 + A2 (grad_face.hpp:83)
     term[i] = tt;
     s += tt;
+    const double w1 = ddiv(a2, a1 + a2), w2 = ddiv(a1, a1 + a2);  // y_update_edge (grad_face.hpp:35)
+    wq[2 * i] = w1;
+    wq[2 * i + 1] = w2;
     if (C) {
       v3 y1, y2, d1, d2;
-      face_y_update(i, ld3(h, f1), ld3(h, f2), a1, a2, mu, edir, zero, zero, y1, y2, d1, d2);
+      face_y_update(i, ld3(h, f1), ld3(h, f2), msa[f1], msa[f2], w1, w2, edir, zero, zero, y1, y2, d1, d2);
       st3(C, 2 * i, add(y1, d1));
       st3(C, 2 * i + 1, add(y2, d2));
     }
@@ -162,7 +181,9 @@ __global__ void k_face_g(const int32_t* __restrict__ slot, const double* __restr
 // lambda-update + primal rows per interior edge (grad_face.hpp:158-168) with
 // this iteration's Y recomputed from g_in (the previous g) and the old lambda,
 // then the next iteration's Y and c from the same registers.
-__global__ void __launch_bounds__(B, 4) k_face_lambda_c(const int32_t* __restrict__ ef, const double* __restrict__ area,
+template <int kMinBlocks>
+__global__ void __launch_bounds__(B, kMinBlocks) k_face_lambda_c(const int32_t* __restrict__ ef, const double* __restrict__ msa,
+                                const double* __restrict__ sa, const double* __restrict__ wq,
                                 const double* __restrict__ gin, const double* __restrict__ gout,
                                 const double* __restrict__ edir, int64_t ni, double mu, double* __restrict__ C,
                                 double* __restrict__ lam, double* __restrict__ part, double* __restrict__ term,
@@ -171,13 +192,13 @@ __global__ void __launch_bounds__(B, 4) k_face_lambda_c(const int32_t* __restric
   double s = 0.0;
   GRID_STRIDE(i, ni) {
     const int32_t f1 = ef[2 * i], f2 = ef[2 * i + 1];
-    const double a1 = area[f1], a2 = area[f2];
+    const double m1 = msa[f1], m2 = msa[f2], w1 = wq[2 * i], w2 = wq[2 * i + 1];
     v3 y1, y2, d1, d2;
-    face_y_update(i, ld3(gin, f1), ld3(gin, f2), a1, a2, mu, edir, ld3(lam, 2 * i), ld3(lam, 2 * i + 1), y1, y2, d1,
-                  d2);
+    face_y_update(i, ld3(gin, f1), ld3(gin, f2), m1, m2, w1, w2, edir, ld3(lam, 2 * i), ld3(lam, 2 * i + 1), y1, y2,
+                  d1, d2);
     const v3 g1 = ld3(gout, f1), g2 = ld3(gout, f2);
-    const v3 r1 = scale(sqrt(a1), sub(y1, g1));
-    const v3 r2 = scale(sqrt(a2), sub(y2, g2));
+    const v3 r1 = scale(sa[f1], sub(y1, g1));
+    const v3 r2 = scale(sa[f2], sub(y2, g2));
     const v3 l1 = add(ld3(lam, 2 * i), scale(mu, r1));
     const v3 l2 = add(ld3(lam, 2 * i + 1), scale(mu, r2));
     st3(lam, 2 * i, l1);
@@ -185,7 +206,7 @@ __global__ void __launch_bounds__(B, 4) k_face_lambda_c(const int32_t* __restric
     const double tt = sqnorm(r1) + sqnorm(r2);
     term[i] = tt;
     s += tt;
-    face_y_update(i, g1, g2, a1, a2, mu, edir, l1, l2, y1, y2, d1, d2);
+    face_y_update(i, g1, g2, m1, m2, w1, w2, edir, l1, l2, y1, y2, d1, d2);
     st3(C, 2 * i, add(y1, d1));
     st3(C, 2 * i + 1, add(y2, d2));
   }
@@ -495,7 +516,8 @@ AdmmResult admm_face_dev(gh_mesh* m, const double* d_h, const gh_admm_config& cf
   AdmmResult res;
   Scratch<double> Cs(6 * NI + 6, s), lam(6 * NI + 6, s), edir(3 * NI + 3, s), gtmp(3 * F + 3, s);
   Scratch<int32_t> ef(2 * NI + 2, s), slot(3 * F + 3, s);
-  res.state_bytes = sizeof(double) * (3 * F /*g*/ + 3 * F /*targets*/ + 15 * NI) + sizeof(int32_t) * (2 * NI + 3 * F);
+  res.state_bytes = sizeof(double) * (3 * F /*g*/ + 3 * F /*targets*/ + 15 * NI + 2 * F + 2 * NI) +
+                    sizeof(int32_t) * (2 * NI + 3 * F);
   double* part_dual = m->partials.p;  // admm_loop's k_admm_stop reads both halves
   double* part_primal = m->partials.p + G;
   EventTimer timer(s);
@@ -507,20 +529,28 @@ AdmmResult admm_face_dev(gh_mesh* m, const double* d_h, const gh_admm_config& cf
   GH_CUDA(cudaMemcpyAsync(gtmp.p, d_h, sizeof(double) * 3 * F, cudaMemcpyDeviceToDevice, s));
   if (F) k_face_slots<<<G, B, 0, s>>>(m->he_edge.p, m->interior_edge_index.p, m->edge_he.p, F, slot.p);
   Scratch<double> term_p(NI + 1, s), term_d(F + 1, s);  // per-element residual terms
+  Scratch<double> msa(F + 1, s), sa(F + 1, s), wq(2 * NI + 2, s);  // per-solve constants (face_y_update)
+  if (F) k_face_consts<<<G, B, 0, s>>>(m->face_area.p, F, mu, msa.p, sa.p);
   k_face_init_edges<<<G, B, 0, s>>>(m->pos.p, m->interior_edges.p, m->edge_v.p, m->edge_he.p, m->face_area.p, d_h,
-                                    NI, mu, edir.p, ef.p, lam.p, cfg.max_iterations > 0 ? Cs.p : nullptr,
-                                    part_primal, term_p.p);
+                                    NI, mu, msa.p, edir.p, ef.p, wq.p, lam.p,
+                                    cfg.max_iterations > 0 ? Cs.p : nullptr, part_primal, term_p.p);
   GH_LAUNCH_CHECK();
-  m->launches += 2;
+  m->launches += 3;
   // ||M||_F (grad_face.hpp:85): the reference's left-to-right sum, exactly
   const double scale = std::sqrt(sequential_sum_nonneg(term_p.p, NI, s, &m->launches));
+  // k_face_lambda_c: 4 blocks per SM (64 registers, some spills) or 3 (no spills); GH_FACE_LC_BLOCKS picks
+  const int lc_blocks = getenv("GH_FACE_LC_BLOCKS") ? atoi(getenv("GH_FACE_LC_BLOCKS")) : 4;
   // grad_face.hpp:175-177
   admm_loop(m, res, cfg, scale, mu, term_p.p, NI, term_d.p, F, [&](int32_t it, const int32_t* halt) {
     const double* gin = gbuf[(it + 1) & 1];
     double* gout = gbuf[it & 1];
     k_face_g<<<G, B, 0, s>>>(slot.p, m->face_area.p, d_h, Cs.p, F, mu, gin, gout, part_dual, term_d.p, halt);
-    k_face_lambda_c<<<G, B, 0, s>>>(ef.p, m->face_area.p, gin, gout, edir.p, NI, mu, Cs.p, lam.p, part_primal,
-                                    term_p.p, halt);
+    if (lc_blocks == 3)
+      k_face_lambda_c<3><<<G, B, 0, s>>>(ef.p, msa.p, sa.p, wq.p, gin, gout, edir.p, NI, mu, Cs.p, lam.p, part_primal,
+                                         term_p.p, halt);
+    else
+      k_face_lambda_c<4><<<G, B, 0, s>>>(ef.p, msa.p, sa.p, wq.p, gin, gout, edir.p, NI, mu, Cs.p, lam.p, part_primal,
+                                         term_p.p, halt);
   });
   // the last iteration's g: odd iterations wrote gtmp
   if (res.iterations > 0 && ((res.iterations - 1) & 1))
