@@ -405,7 +405,14 @@ static void build_rows(gh_levels* L, Band* b, const int32_t* local_p) {
     // window is the ghost area) expresses them
     const int forced = b->nslices ? 3 : force ? atoi(force) : 0;
     Scratch<unsigned long long> nwide(1, s);
-    for (int windows : {2, 3}) {
+    // A band with ghost rows (a neighbour's boundary level, or a slice's
+    // foreign neighbours) tries 3 windows first: only their 4th window reaches
+    // the ghost rows, and chunks that fit no window take the global-memory
+    // path — a few of them per step are stragglers the whole pipeline waits
+    // for (2 BFS bands at config 3: 1.78x one band in 2-window format, 1.20x
+    // with 3 windows; profiles/r2_partitions_emulated_*.json)
+    const bool ghosts = b->nrows > b->own_rows;
+    for (int windows : {ghosts ? 3 : 2, ghosts ? 2 : 3}) {
       if (forced && windows != forced) continue;
       GH_CUDA(cudaMemsetAsync(nwide.p, 0, sizeof(unsigned long long), s));
       k_col16<<<grid_for((int64_t)b->own_chunks * 32), B, 0, s>>>(

@@ -538,8 +538,9 @@ AdmmResult admm_face_dev(gh_mesh* m, const double* d_h, const gh_admm_config& cf
   m->launches += 3;
   // ||M||_F (grad_face.hpp:85): the reference's left-to-right sum, exactly
   const double scale = std::sqrt(sequential_sum_nonneg(term_p.p, NI, s, &m->launches));
-  // k_face_lambda_c: 4 blocks per SM (64 registers, some spills) or 3 (no spills); GH_FACE_LC_BLOCKS picks
-  const int lc_blocks = getenv("GH_FACE_LC_BLOCKS") ? atoi(getenv("GH_FACE_LC_BLOCKS")) : 4;
+  // k_face_lambda_c: 3 blocks per SM (80 registers) or 4 (64, more spills); GH_FACE_LC_BLOCKS picks.
+  // Measured per iteration: config 3 1.87 vs 1.90 ms, config 4 11.2 vs 11.9 ms.
+  const int lc_blocks = getenv("GH_FACE_LC_BLOCKS") ? atoi(getenv("GH_FACE_LC_BLOCKS")) : 3;
   // grad_face.hpp:175-177
   admm_loop(m, res, cfg, scale, mu, term_p.p, NI, term_d.p, F, [&](int32_t it, const int32_t* halt) {
     const double* gin = gbuf[(it + 1) & 1];
