@@ -169,6 +169,11 @@ gh_status gh_device_count(int32_t* count);
 /* Pinned host memory for staging (cudaMallocHost / cudaFreeHost). */
 gh_status gh_host_alloc(size_t bytes, void** out);
 gh_status gh_host_free(void* p);
+/* Return the device memory this library keeps cached for reuse (its exact-size
+   block cache and the stream-ordered pool's free blocks) to the driver, on every
+   device it has used. Handles stay valid. Call it before other processes need
+   the memory (the pool otherwise keeps what a large solve grew to). */
+gh_status gh_release_cached_memory(void);
 
 /* ---- mesh: build_mesh (mesh.hpp:113-286), device preprocessing */
 gh_status gh_mesh_create(const double* positions, int32_t nv, const int32_t* faces, int32_t nf, gh_mesh** out);

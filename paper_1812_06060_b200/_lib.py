@@ -76,6 +76,7 @@ SIGNATURES = [
     ("gh_device_count", st, [C.POINTER(i32)]),
     ("gh_host_alloc", st, [C.c_size_t, C.POINTER(vp)]),
     ("gh_host_free", st, [vp]),
+    ("gh_release_cached_memory", st, []),
     ("gh_mesh_create", st, [vp, i32, vp, i32, C.POINTER(vp)]),
     ("gh_mesh_destroy", st, [vp]),
     ("gh_mesh_get_info", st, [vp, C.POINTER(gh_mesh_info)]),

@@ -90,8 +90,10 @@ uint64_t state_formula(const gh_mesh* m, int method) {
 // Handle memory comes from the device's default stream-ordered pool. Keeping
 // freed blocks cached (release threshold = max) makes repeated solves reuse
 // them instead of paying cudaMalloc/cudaFree on every call.
+bool pool_done[64] = {false};
+bool pool_touched(int device) { return device >= 0 && device < 64 && pool_done[device]; }
 void keep_pool_memory(int device) {
-  static bool done[64] = {false};
+  bool* done = pool_done;
   if (device < 0 || device >= 64 || done[device]) return;
   cudaMemPool_t pool;
   GH_CUDA(cudaDeviceGetDefaultMemPool(&pool, device));
@@ -158,6 +160,24 @@ gh_status gh_host_alloc(size_t bytes, void** out) {
 gh_status gh_host_free(void* p) {
   return guarded([&] {
     if (p) GH_CUDA(cudaFreeHost(p));
+  });
+}
+
+gh_status gh_release_cached_memory(void) {
+  return guarded([&] {
+    int cur = 0, ndev = 0;
+    GH_CUDA(cudaGetDevice(&cur));
+    GH_CUDA(cudaGetDeviceCount(&ndev));
+    gh::dev_cache_flush();
+    for (int d = 0; d < ndev && d < 64; ++d) {
+      if (!pool_touched(d)) continue;
+      GH_CUDA(cudaSetDevice(d));
+      GH_CUDA(cudaDeviceSynchronize());
+      cudaMemPool_t pool;
+      GH_CUDA(cudaDeviceGetDefaultMemPool(&pool, d));
+      GH_CUDA(cudaMemPoolTrimTo(pool, 0));
+    }
+    GH_CUDA(cudaSetDevice(cur));
   });
 }
 

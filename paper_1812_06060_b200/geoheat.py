@@ -703,3 +703,8 @@ def device_count() -> int:
     n = C.c_int32()
     _check(_lib.load().gh_device_count(C.byref(n)))
     return n.value
+
+
+def release_cached_memory() -> None:
+    """Hand the library's cached device memory (block cache + pool free blocks) back to the driver."""
+    _check(_lib.load().gh_release_cached_memory())

@@ -31,6 +31,8 @@ def ref():
 
 
 def run(cli, args, env=None, **kw):
+    import paper_1812_06060_b200 as gh
+    gh.geoheat.release_cached_memory()  # the child process needs device memory this one may cache
     e = dict(os.environ)
     e.pop("GEOHEAT_THREADS", None)
     if env:

@@ -25,6 +25,16 @@ RECORDS = json.load(open(os.path.join(ROOT, "profiles", "reference_hashes.json")
 CASES = sorted({(r["config"], r["method"]) for r in RECORDS})
 
 
+@pytest.fixture(autouse=True)
+def _release_device_memory(gpu):
+    """A full-size solve grows the memory pool to tens of GB; hand it back after
+    each test so later tests' child processes (CLI, C++ drop-in) can allocate."""
+    yield
+    import gc
+    gc.collect()
+    gpu.geoheat.release_cached_memory()
+
+
 @pytest.mark.parametrize("config,method", CASES)
 def test_full_size_hash_equals_reference_chain(gpu, config, method):
     from paper_1812_06060_b200 import meshgen

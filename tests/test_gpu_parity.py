@@ -208,6 +208,7 @@ def test_cpp_wrapper_runs_reference_chain(gpu):
         subprocess.run(["g++", "-std=c++20", "-O2", "-I", os.path.join(ROOT, "include"), src, "-o", exe, "-L",
                         _build.LIBDIR, "-lgeoheat_b200", "-lgh_meshgen", f"-Wl,-rpath,{_build.LIBDIR}"], check=True)
     t = float(np.load(os.path.join(GOLDEN, "icosphere5_config1.npz"))["t"])
+    gpu.geoheat.release_cached_memory()
     r = subprocess.run([exe, t.hex()], capture_output=True, text=True, timeout=300)
     assert r.returncode == 0, r.stdout + r.stderr
     assert "PASS" in r.stdout
@@ -347,6 +348,7 @@ def test_dropin_reference_program_bitwise(gpu):
     exe = os.path.join(_build.LIBDIR, "dropin_run_pipeline")
     if not os.path.exists(exe):
         pytest.skip("drop-in program not prebuilt (built by tests/test_abi.py in the build container)")
+    gpu.geoheat.release_cached_memory()
     r = subprocess.run([exe], capture_output=True, text=True, timeout=600)
     assert r.returncode == 0, r.stdout + r.stderr
     assert r.stdout.count("identical") == 6, r.stdout
