@@ -372,6 +372,10 @@ gh_status gh_band_own_mask(const gh_band* band, uint8_t* mask_out);
  * (the library uses it for average_edge_length); any negative term falls
  * back to one device thread adding in order. */
 gh_status gh_deterministic_sum(const double* terms, int64_t n, double* sum_out);
+/* count independent deterministic_sums at once: sums_out[i] = the left-to-right
+ * sum of terms[i*n .. i*n+n), bit-identical, one device block per sum (the
+ * engine behind the E1 history of gh_gs_diffuse_tol). Any signs. */
+gh_status gh_deterministic_sums(const double* terms, int64_t n, int32_t count, double* sums_out);
 
 /* field_hash (report.hpp:145-153): FNV-1a over the bytes of n doubles. */
 uint64_t gh_field_hash(const double* values, int64_t n);

@@ -130,6 +130,7 @@ SIGNATURES = [
     ("gh_dijkstra_distance", st, [vp, vp, i32, vp]),
     ("gh_error_metrics", st, [vp, vp, i64, vp, i32, C.POINTER(f64), C.POINTER(i32), C.POINTER(f64)]),
     ("gh_deterministic_sum", st, [vp, i64, C.POINTER(f64)]),
+    ("gh_deterministic_sums", st, [vp, i64, i32, vp]),
     ("gh_field_hash", C.c_uint64, [vp, i64]),
 ]
 

@@ -568,36 +568,77 @@ gh_status gh_gs_diffuse_tol(gh_levels* levels, double t, int32_t sweeps, double 
       }
     } else {
       if (!(t > 0.0)) gh::fail(GH_ERR_INVALID, "gs_diffuse: t must be positive");
-      // group size: up to 256 sweeps, within half the free device memory
+      // per sweep of a group: its snapshot (row order) and its r^2 terms
+      // (vertex order); groups of up to 256 sweeps within half the free memory
       size_t free_b = 0, total_b = 0;
       GH_CUDA(cudaMemGetInfo(&free_b, &total_b));
-      const size_t per = sizeof(double) * (size_t)levels->main.nrows;
+      const size_t nv = (size_t)m->nv, nrows = (size_t)levels->main.nrows;
+      const size_t own = (size_t)levels->main.own_rows;
+      const size_t per = sizeof(double) * (nrows + own + nv);
       int32_t kmax = (int32_t)std::max<size_t>(1, std::min<size_t>(256, free_b / 2 / std::max<size_t>(per, 1)));
       if (const char* e = getenv("GH_TOL_GROUP")) kmax = std::max(1, atoi(e));  // tests: small groups
       kmax = std::min(kmax, sweeps);
-      gh::Scratch<double> snap((size_t)kmax * levels->main.nrows, s);
-      // unreachable vertices keep their start value through every sweep
-      gh::diffuse_dev(levels, t, 0, nullptr);  // u_orig = start state (u0 or the initial below)
-      if (initial) GH_CUDA(cudaMemcpyAsync(cur.p, initial, sizeof(double) * m->nv, cudaMemcpyHostToDevice, s));
-      else GH_CUDA(cudaMemcpyAsync(cur.p, levels->u_orig.p, sizeof(double) * m->nv, cudaMemcpyDeviceToDevice, s));
-      bool first = true;
+      gh::Scratch<double> snap((size_t)kmax * nrows, s), sqr((size_t)kmax * own, s), sq((size_t)kmax * nv, s);
+      gh::Scratch<double> sums((size_t)kmax, s);
+      gh::Scratch<int32_t> rowof(nv, s), vv_row(m->vv_index.n, s);
+      std::vector<double> h_sums((size_t)kmax);
+      // cur = the start state (u0, or the initial field) = u_orig; unreachable
+      // vertices keep it through every sweep, so cur also serves as their values
+      if (initial) GH_CUDA(cudaMemcpyAsync(cur.p, initial, sizeof(double) * nv, cudaMemcpyHostToDevice, s));
+      gh::diffuse_dev(levels, t, 0, initial ? cur.p : nullptr);
+      if (!initial)
+        GH_CUDA(cudaMemcpyAsync(cur.p, levels->u_orig.p, sizeof(double) * nv, cudaMemcpyDeviceToDevice, s));
+      gh::e1_setup_dev(levels, rowof.p, vv_row.p, cur.p, t, kmax, sq.p);
+      const double* start = initial ? cur.p : nullptr;  // the next group's start state (nullptr: u0)
+      std::vector<double> hist;
       while (done < sweeps && !converged) {
-        const int32_t k = std::min(kmax, sweeps - done);
-        ms += gh::diffuse_dev(levels, t, k, (first && !initial) ? nullptr : cur.p, snap.p);
-        first = false;
+        // group size: the first sweeps, then what the E1 decay so far predicts
+        // is left to the tolerance (sweeps past the stop are wasted), at most kmax
+        int32_t k = std::min(kmax, 128);
+        if (hist.size() >= 8) {
+          const size_t n = hist.size();
+          const double a = std::log(hist[n - 8]), b = std::log(hist[n - 1]);
+          const double rate = (b - a) / 7.0;
+          if (rate < 0.0 && std::isfinite(rate) && hist[n - 1] > 0.0) {
+            const double left = (std::log(tolerance) - b) / rate;
+            k = left < (double)kmax ? std::max(8, (int32_t)std::ceil(left * 1.05) + 2) : kmax;
+          } else {
+            k = kmax;
+          }
+        }
+        k = std::min(std::min(k, kmax), sweeps - done);
+        ms += gh::diffuse_dev(levels, t, k, start, snap.p);
+        static const bool prof = getenv("GH_E1_PROFILE") != nullptr;  // stage times on stderr (experiments)
+        if (prof) {
+          gh::EventTimer te(s);
+          te.start();
+          gh::e1_group_dev(levels, snap.p, k, t, rowof.p, vv_row.p, sqr.p, sq.p, sums.p);
+          te.stop();
+          fprintf(stderr, "e1_group k=%d e1_ms %.3f per_sweep_us %.1f\n", k, te.ms(), 1e3 * te.ms() / k);
+        } else {
+          gh::e1_group_dev(levels, snap.p, k, t, rowof.p, vv_row.p, sqr.p, sq.p, sums.p);
+        }
+        GH_CUDA(cudaMemcpyAsync(h_sums.data(), sums.p, sizeof(double) * k, cudaMemcpyDeviceToHost, s));
+        GH_CUDA(cudaStreamSynchronize(s));
+        int32_t at = k - 1;
         for (int32_t i = 0; i < k; ++i) {
-          gh::snapshot_to_orig(levels, snap.p + (size_t)i * levels->main.nrows, cur.p);
-          const double e1 = gh::diffusion_residual_dev(levels, cur.p, t);
+          const double e1 = std::sqrt(h_sums[i]);  // diffusion.hpp:48
+          hist.push_back(e1);
           if (report && report->residual_history && done < report->history_capacity)
             report->residual_history[done] = e1;
           ++done;
           if (e1 <= tolerance) {
             converged = true;
+            at = i;
             break;
           }
         }
+        // cur = u after the last sweep kept (a sweep depends on u only: the next
+        // group continues from it bit for bit)
+        gh::snapshot_to_orig(levels, snap.p + (size_t)at * nrows, cur.p);
+        start = cur.p;
       }
-      GH_CUDA(cudaMemcpyAsync(levels->u_orig.p, cur.p, sizeof(double) * m->nv, cudaMemcpyDeviceToDevice, s));
+      GH_CUDA(cudaMemcpyAsync(levels->u_orig.p, cur.p, sizeof(double) * nv, cudaMemcpyDeviceToDevice, s));
       levels->u_sweeps = done;
     }
     if (u_out) to_host(u_out, levels->u_orig.p, m->nv, s);
@@ -952,6 +993,29 @@ gh_status gh_deterministic_sum(const double* terms, int64_t n, double* sum_out) 
     gh::Scratch<double> x(n, s);
     if (n) GH_CUDA(cudaMemcpyAsync(x.p, terms, sizeof(double) * n, cudaMemcpyHostToDevice, s));
     *sum_out = gh::deterministic_sum_dev(x.p, n, s);
+  });
+}
+
+gh_status gh_deterministic_sums(const double* terms, int64_t n, int32_t count, double* sums_out) {
+  return guarded([&] {
+    require(sums_out && n >= 0 && count >= 0 && (n == 0 || count == 0 || terms), "gh_deterministic_sums: bad argument");
+    int ndev = 0;
+    if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev == 0) {
+      (void)cudaGetLastError();
+      gh::fail(GH_ERR_CUDA, "no CUDA device available (the geoheat_b200 path has no CPU fallback)");
+    }
+    if (count == 0) return;
+    if (g_device >= 0) GH_CUDA(cudaSetDevice(g_device));
+    int dev = 0;
+    GH_CUDA(cudaGetDevice(&dev));
+    keep_pool_memory(dev);
+    cudaStream_t s;
+    thread_context(dev, &s, nullptr);
+    gh::Scratch<double> x((size_t)n * count, s), out((size_t)count, s);
+    if (n) GH_CUDA(cudaMemcpyAsync(x.p, terms, sizeof(double) * n * count, cudaMemcpyHostToDevice, s));
+    gh::sequential_sums_group(x.p, n, n, count, out.p, s);
+    GH_CUDA(cudaMemcpyAsync(sums_out, out.p, sizeof(double) * count, cudaMemcpyDeviceToHost, s));
+    GH_CUDA(cudaStreamSynchronize(s));
   });
 }
 

@@ -32,6 +32,7 @@
 
 #include <algorithm>
 #include <cstdlib>
+#include <cstring>
 
 #include "gh_internal.cuh"
 
@@ -754,6 +755,134 @@ __global__ void k_residual(const int32_t* __restrict__ vv_off, const int32_t* __
   }
 }
 
+// vertex -> row of the single band (-1: unreachable), and the CSR's columns as rows
+__global__ void k_rowof(const int32_t* __restrict__ perm, int64_t own_rows, int32_t* __restrict__ rowof) {
+  for (int64_t r = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; r < own_rows; r += (int64_t)gridDim.x * blockDim.x) {
+    const int32_t v = perm[r];
+    if (v >= 0) rowof[v] = (int32_t)r;
+  }
+}
+__global__ void k_vv_row(const int32_t* __restrict__ vv_idx, const int32_t* __restrict__ rowof, int64_t nnz,
+                         int32_t* __restrict__ vv_row) {
+  for (int64_t c = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; c < nnz; c += (int64_t)gridDim.x * blockDim.x)
+    vv_row[c] = rowof[vv_idx[c]];
+}
+
+// k_residual for the k sweeps of a group at once, in the band's row order
+// straight from the sweeps' snapshots (snap_rows apart): thread = row, its
+// vertex's CSR row (columns as rows) kept in registers (valence <= 8; larger
+// rows loop over it) while it loops over the sweeps, so the CSR is read once
+// per group, and per sweep only the gathers of neighbouring rows (levels L-1,
+// L, L+1 near the same ring position: the diffusion kernel's own locality)
+// and one coalesced store remain. The arithmetic and its order are
+// k_residual's (diffusion.hpp:41-47), hence the same bits. r^2 goes to sqr
+// (k x own_rows, row order); k_scatter_sq puts it in vertex order.
+constexpr int kResRow = 8;
+__global__ void __launch_bounds__(256) k_residual_rows(const int32_t* __restrict__ perm, int64_t own_rows,
+                                                       const int32_t* __restrict__ vv_off,
+                                                       const int32_t* __restrict__ vv_row,
+                                                       const double* __restrict__ vv_w, const double* __restrict__ va,
+                                                       const int32_t* __restrict__ level,
+                                                       const double* __restrict__ snap, int64_t snap_rows, double t,
+                                                       int32_t k, double* __restrict__ sqr) {
+  for (int64_t r = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; r < own_rows; r += (int64_t)gridDim.x * blockDim.x) {
+    const int32_t v = perm[r];
+    if (v < 0) continue;  // padding row
+    const int32_t b = vv_off[v], e = vv_off[v + 1], n = e - b;
+    const double a = va[v];
+    const double u0 = level[v] == 0 ? 1.0 : 0.0;
+    if (n <= kResRow) {
+      int32_t rr[kResRow];
+      double w[kResRow];
+#pragma unroll
+      for (int c = 0; c < kResRow; ++c) {
+        rr[c] = c < n ? vv_row[b + c] : (int32_t)r;
+        w[c] = c < n ? vv_w[b + c] : 0.0;
+      }
+      for (int32_t i = 0; i < k; ++i) {
+        const double* __restrict__ sp = snap + (int64_t)i * snap_rows;
+        const double uj = sp[r];
+        double x[kResRow];
+#pragma unroll
+        for (int c = 0; c < kResRow; ++c) x[c] = c < n ? sp[rr[c]] : 0.0;
+        double lap = 0.0;
+#pragma unroll
+        for (int c = 0; c < kResRow; ++c)
+          if (c < n) lap += w[c] * (x[c] - uj);
+        const double res = a * uj - t * lap - u0;
+        __stcs(sqr + (int64_t)i * own_rows + r, res * res);
+      }
+    } else {
+      for (int32_t i = 0; i < k; ++i) {
+        const double* __restrict__ sp = snap + (int64_t)i * snap_rows;
+        const double uj = sp[r];
+        double lap = 0.0;
+        for (int32_t c = b; c < e; ++c) lap += vv_w[c] * (sp[vv_row[c]] - uj);
+        const double res = a * uj - t * lap - u0;
+        __stcs(sqr + (int64_t)i * own_rows + r, res * res);
+      }
+    }
+  }
+}
+
+// warp sum of r^2 (32 consecutive vertices, inside one 1024-vertex segment)
+// into that segment's bound T (fp64 atomics: the order does not matter, T only
+// chooses which binades the exact sum prepares)
+__device__ __forceinline__ void seg_add(double val, int64_t jw, int64_t i, int64_t nseg, double* __restrict__ T) {
+  for (int o = 16; o > 0; o >>= 1) val += __shfl_down_sync(0xffffffffu, val, o);
+  if ((threadIdx.x & 31) == 0 && val != 0.0) atomicAdd(T + i * nseg + jw / gh::kSeqsumSegment, val);
+}
+
+// r^2 of the k sweeps, row order -> vertex order, as a gather: coalesced
+// stores, and reads through vertex -> row (rows of one ring sit together, so
+// the other rows of a sector are read a few thousand vertices later: L2
+// hits). A scatter (8-byte stores to scattered vertices) made HBM fill and
+// write back a 32-byte sector per store: 3x the bytes.
+__global__ void k_gather_sq(const int32_t* __restrict__ rowof, const double* __restrict__ sqr, int64_t own_rows,
+                            int32_t k, int64_t nv, int64_t nseg, double* __restrict__ sq, double* __restrict__ T) {
+  const int lane = threadIdx.x & 31;
+  constexpr int U = 4;  // grid-stride iterations in flight per thread
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  for (int32_t i = 0; i < k; ++i) {
+    const double* __restrict__ src = sqr + (int64_t)i * own_rows;
+    double* __restrict__ dst = sq + (int64_t)i * nv;
+    for (int64_t jw0 = blockIdx.x * (int64_t)blockDim.x + threadIdx.x - lane; jw0 < nv; jw0 += U * stride) {
+      double val[U];
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        const int64_t v = jw0 + u * stride + lane;
+        val[u] = 0.0;
+        if (v < nv) {
+          const int32_t r = rowof[v];
+          val[u] = r >= 0 ? src[r] : dst[v];  // unreachable: the fixed value
+        }
+      }
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        const int64_t jw = jw0 + u * stride;
+        if (jw + lane < nv) __stcs(dst + jw + lane, val[u]);
+        if (jw < nv) seg_add(val[u], jw, i, nseg, T);
+      }
+    }
+  }
+}
+
+// r^2 of the unreachable vertices: they and all their neighbours keep the
+// start state, so the value is the same every sweep (k_residual's arithmetic)
+__global__ void k_residual_fixed(const int32_t* __restrict__ vv_off, const int32_t* __restrict__ vv_idx,
+                                 const double* __restrict__ vv_w, const double* __restrict__ va,
+                                 const int32_t* __restrict__ level, const double* __restrict__ base, double t,
+                                 int64_t nv, int32_t k, double* __restrict__ sq) {
+  for (int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; j < nv; j += (int64_t)gridDim.x * blockDim.x) {
+    if (level[j] >= 0) continue;
+    const double uj = base[j];
+    double lap = 0.0;
+    for (int32_t c = vv_off[j]; c < vv_off[j + 1]; ++c) lap += vv_w[c] * (base[vv_idx[c]] - uj);
+    const double res = va[j] * uj - t * lap - 0.0;
+    for (int32_t i = 0; i < k; ++i) sq[(int64_t)i * nv + j] = res * res;
+  }
+}
+
 }  // namespace
 
 namespace gh {
@@ -995,6 +1124,56 @@ void snapshot_to_orig(gh_levels* L, const double* d_snap_sweep, double* d_u) {
     k_scatter_rows<<<grid_for(b.own_rows), B, 0, m->stream>>>(b.perm.p, d_snap_sweep, b.own_rows, d_u);
   GH_LAUNCH_CHECK();
   m->launches++;
+}
+
+void e1_setup_dev(gh_levels* L, int32_t* d_rowof, int32_t* d_vv_row, const double* d_base, double t, int32_t kmax,
+                  double* d_sq) {
+  gh_mesh* m = L->mesh;
+  const Band& b = L->main;
+  GH_CUDA(cudaMemsetAsync(d_rowof, 0xff, sizeof(int32_t) * m->nv, m->stream));
+  if (b.own_rows) k_rowof<<<grid_for(b.own_rows), B, 0, m->stream>>>(b.perm.p, b.own_rows, d_rowof);
+  const int64_t nnz = (int64_t)m->vv_index.n;
+  if (nnz) k_vv_row<<<grid_for(nnz), B, 0, m->stream>>>(m->vv_index.p, d_rowof, nnz, d_vv_row);
+  GH_LAUNCH_CHECK();
+  m->launches += 2;
+  if (L->nreach < m->nv) {
+    k_residual_fixed<<<grid_for(m->nv), B, 0, m->stream>>>(m->vv_offset.p, m->vv_index.p, m->vv_weight.p,
+                                                           m->vertex_area.p, L->level.p, d_base, t, m->nv, kmax, d_sq);
+    GH_LAUNCH_CHECK();
+    m->launches++;
+  }
+}
+
+int resident_grid(const void* kernel, int block, int device) {
+  int nsm = 0, per_sm = 0;
+  GH_CUDA(cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, device));
+  GH_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kernel, block, 0));
+  return std::max(1, nsm * std::max(1, per_sm));
+}
+
+void e1_group_dev(gh_levels* L, const double* d_snap, int32_t k, double t, const int32_t* d_rowof,
+                  const int32_t* d_vv_row, double* d_sqr, double* d_sq, double* d_sums) {
+  gh_mesh* m = L->mesh;
+  const Band& b = L->main;
+  if (k <= 0) return;
+  const int64_t nseg = seqsum_segments(m->nv);
+  Scratch<double> T((size_t)nseg * k, m->stream);
+  GH_CUDA(cudaMemsetAsync(T.p, 0, sizeof(double) * nseg * k, m->stream));
+  // r^2 in row order: one resident wave grid-striding over the rows, so the
+  // rows of neighbouring levels are worked on together, sweep by sweep, and
+  // their snapshot values are L2 hits; then gathered into vertex order
+  if (b.own_rows) {
+    static const int rg_max = resident_grid((const void*)k_residual_rows, 256, m->device);
+    const unsigned rg = (unsigned)std::min<int64_t>(rg_max, (b.own_rows + 255) / 256);
+    k_residual_rows<<<rg, 256, 0, m->stream>>>(b.perm.p, b.own_rows, m->vv_offset.p, d_vv_row, m->vv_weight.p,
+                                               m->vertex_area.p, L->level.p, d_snap, b.nrows, t, k, d_sqr);
+    m->launches++;
+  }
+  k_gather_sq<<<grid_for(m->nv), B, 0, m->stream>>>(d_rowof, d_sqr, b.own_rows, k, m->nv, nseg, d_sq, T.p);
+  GH_LAUNCH_CHECK();
+  m->launches++;
+  sequential_sums_from_T(d_sq, m->nv, m->nv, k, T.p, d_sums, m->stream);
+  m->launches += 3;
 }
 
 double diffusion_residual_dev(gh_levels* L, const double* d_u, double t) {

@@ -332,6 +332,16 @@ double bands_launch(gh_levels* L, std::vector<Band*>& bands, double t, int32_t s
 // the single band's reachable rows of one snapshot sweep into d_u (original order; unreachable untouched)
 void snapshot_to_orig(gh_levels* L, const double* d_snap_sweep, double* d_u);
 double diffusion_residual_dev(gh_levels* L, const double* d_u, double t);
+// E1 of a group of k sweeps from their snapshots (k x main.nrows, row order):
+// e1_setup_dev once per solve (vertex -> row and the CSR's columns as rows,
+// nv and nnz int32; the fixed r^2 of unreachable vertices into every one of
+// the kmax vertex-order arrays of d_sq, from the start state d_base), then per
+// group r^2 in row order into d_sqr (k x own_rows), in vertex order into d_sq
+// (k x nv) and the k left-to-right sums into d_sums (device; E1 = sqrt).
+void e1_setup_dev(gh_levels* L, int32_t* d_rowof, int32_t* d_vv_row, const double* d_base, double t, int32_t kmax,
+                  double* d_sq);
+void e1_group_dev(gh_levels* L, const double* d_snap, int32_t k, double t, const int32_t* d_rowof,
+                  const int32_t* d_vv_row, double* d_sqr, double* d_sq, double* d_sums);
 
 // normalisation + optimisation (gh_grad.cu)
 int32_t normalize_dev(gh_mesh* m, const double* d_u, double* d_h);
@@ -356,6 +366,15 @@ void reduce_partials(gh_mesh* m, double* d_result_slot);
 double sequential_sum_nonneg(const double* d_x, int64_t n, cudaStream_t s, int* launches);
 // any signs: the exact path when every term is >= 0, else one thread in order
 double deterministic_sum_dev(const double* d_x, int64_t n, cudaStream_t s);
+// count independent left-to-right sums (any sign), sum i over d_x[i * stride + 0 .. n), into d_out[i]
+void sequential_sums_group(const double* d_x, int64_t n, int64_t stride, int32_t count, double* d_out,
+                           cudaStream_t s);
+// the same with the per-segment sums T (count x seqsum_segments(n); any
+// summation order, only a bound) already computed by the caller
+int64_t seqsum_segments(int64_t n);
+constexpr int kSeqsumSegment = 1024;  // terms per segment of T
+void sequential_sums_from_T(const double* d_x, int64_t n, int64_t stride, int32_t count, const double* d_T,
+                            double* d_out, cudaStream_t s);
 
 // classic heat method on CG (gh_poisson.cu)
 struct PoissonOut {

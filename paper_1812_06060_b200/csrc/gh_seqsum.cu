@@ -1,52 +1,57 @@
-// Bit-exact left-to-right sums of non-negative doubles on the device.
+// Bit-exact left-to-right sums on the device, one or many at a time.
 //
 // The reference accumulates global sums sequentially (`double s = 0.0;
-// for (x : terms) s += x;`, e.g. average_edge_length, mesh.hpp:289-293, and
-// deterministic_sum, parallel.hpp:50-54). A tree sum is reproducible but
-// rounds differently. For non-negative terms the sequential result can be
-// reproduced exactly in parallel: while the running sum s stays inside one
-// binade [2^e, 2^(e+1)) every partial sum is a multiple of u = 2^(e-52), and
+// for (x : terms) s += x;`, e.g. average_edge_length, mesh.hpp:289-293,
+// deterministic_sum, parallel.hpp:50-54, and E1 after every sweep,
+// diffusion.hpp:48, 110-117). A tree sum is reproducible but rounds
+// differently. For non-negative terms the sequential result can be reproduced
+// exactly in parallel: while the running sum s stays inside one binade
+// [2^e, 2^(e+1)) every partial sum is a multiple of u = 2^(e-52), and
 // fl(s + x) = s + rint(x / u) * u unless x / u has fractional part exactly
 // 1/2 (a tie, whose rounding depends on the parity of s / u) or the addition
-// leaves the binade. So, with 1024-term segments:
-//   1. the first K terms are summed sequentially (one block);
-//   2. a tree prefix over the segment sums bounds the running sum at the
-//      start of every segment (relative error <= (n + 2^11) 2^-52), giving at
-//      most two candidate binades per segment; for each, the segment's
-//      sum(rint(x / u)) and a flag (a tie, or a term >= 2^e) are recorded;
-//   3. one block walks the segments 1024 at a time: every thread takes a
-//      segment's integer sum for the current binade, a block scan finds the
-//      first segment that is flagged, has no candidate for that binade, or
-//      would carry s out of it; the segments before it are added exactly as
-//      integers, that segment is added term by term in double (exactly the
-//      reference's operations), and the walk goes on from the next one.
-// Ties do not stop the walk: their rounding depends only on the parity of
-// the running count, so every term, segment and run of segments is a 2-state
-// transducer (quanta added and outgoing parity per incoming parity), and the
-// sums are scans of those (see Tx below). The walk stops once per binade
-// change; everything else is a parallel pass over the terms plus one scan per
-// 1024 segments.
+// leaves the binade. Ties do not break this: a term's effect on the integer
+// count s / u is a function of the incoming parity only, so every term,
+// segment and run of segments is a 2-state transducer (quanta added and
+// outgoing parity per incoming parity; Tx below) and sums of them are scans.
+//
+// Several sums (count, stride apart) run at once, one block per sum in the
+// walk, everything else as fully parallel passes; with 1024-term segments:
+//   1. T = each segment's tree sum (any order: only a bound). The E1 path
+//      gets T from its residual kernel, for free;
+//   2. P = exclusive prefix of T per sum: about the running sum at the start of
+//      every segment, so almost always in the binade there (P only chooses the
+//      binade to prepare; results never depend on it);
+//   3. per segment, its transducer in that binade and a flag (a term >= 2^e,
+//      negative or NaN);
+//   4. the walk: one block per sum takes 1024 segments per step, each thread
+//      one segment's transducer, and a block scan finds the first segment
+//      that was prepared for another binade, is flagged,
+//      or would carry s out of it; the segments before it are added exactly as
+//      integers, that one term by term (a block scan per binade the sum
+//      climbs through, the leaving term itself added in double as the
+//      reference adds it), and the walk goes on after it.
+// A negative or non-finite running sum (terms of any sign are accepted) makes
+// thread 0 add the rest of that segment one term at a time, as the reference.
 
+#include <climits>
 #include <cmath>
-
-#include <cub/device/device_scan.cuh>
 
 #include "gh_internal.cuh"
 
 namespace {
 
-constexpr int kSeg = 1024;         // terms per segment
-constexpr int kSeqPrefix = 4096;   // leading terms summed sequentially
-constexpr int kWalkThreads = 1024;
+constexpr int kSeg = 1024;          // terms per segment
+constexpr int kWalkThreads = 1024;  // = kSeg: one term per thread when a segment is walked term by term
 constexpr int kSegThreads = 256;
 constexpr int kPerThread = kSeg / kSegThreads;
 constexpr int kNoBinade = -100000;
+constexpr int kSeqRun = 64;  // terms thread 0 adds in order before each block scan of a walked segment
 
-// s += x[b..e) in order: the block stages 1024 terms at a time in shared
-// memory (coalesced) and thread 0 adds them one by one.
+// s += x[b..e) in order: the block stages terms in shared memory (coalesced)
+// and thread 0 adds them one by one.
 __device__ double block_ordered_add(double s, const double* __restrict__ x, int64_t b, int64_t e, double* sh) {
-  for (int64_t c = b; c < e; c += kWalkThreads) {
-    const int64_t m = e - c < kWalkThreads ? e - c : kWalkThreads;
+  for (int64_t c = b; c < e; c += blockDim.x) {
+    const int64_t m = e - c < (int64_t)blockDim.x ? e - c : (int64_t)blockDim.x;
     __syncthreads();
     if (threadIdx.x < m) sh[threadIdx.x] = x[c + threadIdx.x];
     __syncthreads();
@@ -75,32 +80,18 @@ __device__ __forceinline__ double scale2(double x, int k) {
   const int k1 = k > 1000 ? 1000 : k;
   return x * ldexp(1.0, k1) * ldexp(1.0, k - k1);
 }
-
-// step 2a: per-segment tree sums (any order: they only bound the running sum)
-__global__ void __launch_bounds__(kSegThreads) k_seg_sums(const double* __restrict__ x, int64_t b, int64_t n,
-                                                          int64_t nseg, double* __restrict__ T) {
-  for (int64_t g = blockIdx.x; g < nseg; g += gridDim.x) {
-    double v = 0.0;
-#pragma unroll
-    for (int i = 0; i < kPerThread; ++i) {
-      const int64_t k = b + g * kSeg + i * kSegThreads + threadIdx.x;
-      if (k < n) v += x[k];
-    }
-    v = ghd::block_sum<kSegThreads>(v);
-    if (threadIdx.x == 0) T[g] = v;
-    __syncthreads();
-  }
+// the two factors of 2^(52-e) that scale2 uses
+__device__ __forceinline__ void quantum_factors(int e, double& f1, double& f2) {
+  const int k = 52 - e, k1 = k > 1000 ? 1000 : k;
+  f1 = ldexp(1.0, k1);
+  f2 = ldexp(1.0, k - k1);
 }
 
 // Ties: fl(s + x) with x / u = m + 1/2 rounds to the even multiple of u, so
-// it adds m + ((A + m) & 1) quanta (A = s / u) and leaves an even count. A
-// term's effect on the integer running count is therefore a function of the
-// incoming parity only: (q(p), out(p)) for p in {0, 1}, with q the quanta
-// added and out the parity after (a tie: q(p) = m + ((p + m) & 1), out = 0;
-// else q = rint(x / u), out = p ^ (q & 1)). These 2-state transducers compose
-// associatively, so a segment (and a run of segments) reduces to one, and the
-// walk scans them in parallel: ties never stop it, only a change of binade.
-// saturating non-negative int64 sums (cap 2^62: a saturated count is past any binade)
+// it adds m + ((A + m) & 1) quanta (A = s / u) and leaves an even count: a
+// tie's transducer is q(p) = m + ((p + m) & 1), out = 0; any other term's is
+// q = rint(x / u), out = p ^ (q & 1). Counts saturate at 2^62 (a saturated
+// count is past any binade).
 constexpr unsigned long long kCap = 1ull << 62;
 __device__ __forceinline__ unsigned long long sat_add(unsigned long long a, unsigned long long b) {
   const unsigned long long c = a + b;  // both <= 2^62: no wrap
@@ -129,13 +120,15 @@ __device__ __forceinline__ Tx tx_shfl_up(const Tx& t, int d) {
   return Tx{__shfl_up_sync(0xffffffffu, t.q0, d), __shfl_up_sync(0xffffffffu, t.q1, d),
             __shfl_up_sync(0xffffffffu, t.o, d)};
 }
-// the transducer of term x in binade e; *flag when x >= 2^e (leaves the binade)
-__device__ __forceinline__ Tx tx_term(double x, int e, double lim, bool& flag) {
-  if (x >= lim) {
+// the transducer of term x in binade e; *flag when x >= lim = 2^e (it leaves
+// the binade) or x is negative or NaN
+// (f1 * f2 = 2^(52-e), split so that both factors are finite: see scale2)
+__device__ __forceinline__ Tx tx_term(double x, double f1, double f2, double lim, bool& flag) {
+  if (!(x >= 0.0) || x >= lim) {
     flag = true;
     return tx_identity();
   }
-  const double y = scale2(x, 52 - e);  // exact
+  const double y = x * f1 * f2;  // x / u, exact
   const double m = floor(y);
   const unsigned long long mi = (unsigned long long)m;
   if (y - m == 0.5) {
@@ -147,146 +140,325 @@ __device__ __forceinline__ Tx tx_term(double x, int e, double lim, bool& flag) {
   return Tx{q, q, b | ((1u ^ b) << 1)};
 }
 
-// step 2b: candidate binades from the bounded prefix, then per candidate the
-// segment's transducer and a flag (a term that leaves the binade). Thread t
-// takes the 4 consecutive terms 4t .. 4t+3 of the segment.
-__global__ void __launch_bounds__(kSegThreads) k_seg_q(const double* __restrict__ x, int64_t b, int64_t n, int64_t nseg,
-                                                       const double* __restrict__ P, const double* __restrict__ acc,
-                                                       double rel, int32_t* __restrict__ elo,
-                                                       Tx* __restrict__ Q, int32_t* __restrict__ F) {
-  __shared__ Tx sq[kSegThreads / 32][2];
-  __shared__ int32_t sf[kSegThreads / 32][2];
+// exclusive block scan of transducers in thread order (NT threads); *total = all of them
+template <int NT>
+__device__ Tx block_exscan_tx(Tx v, Tx* wsum, Tx* total) {
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
-  for (int64_t g = blockIdx.x; g < nseg; g += gridDim.x) {
-    const double pre = acc[0] + P[g];  // ~ running sum before segment g
-    const double lo = pre * (1.0 - rel);  // at most the running sum (terms >= 0)
-    const int e0 = isfinite(pre) ? binade_of(lo > 0.0 ? lo : 0.0) : kNoBinade;
-    const bool ok = e0 != kNoBinade && e0 + 2 < 1023;
-    double xv[kPerThread];
-    bool in[kPerThread];
-#pragma unroll
-    for (int i = 0; i < kPerThread; ++i) {
-      const int64_t k = b + g * kSeg + kPerThread * threadIdx.x + i;
-      in[i] = k < n;
-      xv[i] = in[i] ? x[k] : 0.0;
-    }
-    for (int c = 0; c < 2; ++c) {
-      const int e = e0 + c;
-      const double lim = ok ? ldexp(1.0, e + (e == -1022 ? 1 : 0)) : 0.0;  // the lowest "binade" ends at 2^-1021
-      Tx t = tx_identity();
-      bool flag = !ok;
-      if (ok) {
-#pragma unroll
-        for (int i = 0; i < kPerThread; ++i)
-          if (in[i]) t = tx_then(t, tx_term(xv[i], e, lim, flag));
-      }
-      // ordered warp reduction: lane l composes with lanes above it
-      for (int o = 1; o < 32; o <<= 1) {
-        const Tx up = tx_shfl_down(t, o);
-        if ((lane & (2 * o - 1)) == 0) t = tx_then(t, up);
-      }
-      const unsigned any = __ballot_sync(0xffffffffu, flag);
-      if (lane == 0) {
-        sq[w][c] = t;
-        sf[w][c] = any ? 1 : 0;
-      }
-    }
-    __syncthreads();
-    if (threadIdx.x < 2) {
-      Tx tq = tx_identity();
-      int32_t tf = 0;
-      for (int v = 0; v < kSegThreads / 32; ++v) {
-        tq = tx_then(tq, sq[v][threadIdx.x]);
-        tf |= sf[v][threadIdx.x];
-      }
-      Q[2 * g + threadIdx.x] = tq;
-      F[2 * g + threadIdx.x] = tf;
-      if (threadIdx.x == 0) elo[g] = ok ? e0 : kNoBinade;
-    }
-    __syncthreads();
-  }
-}
-
-// block-wide inclusive scan of transducers in thread order
-__device__ Tx block_scan_tx(Tx v, Tx* wsum) {
-  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  Tx inc = v;
   for (int o = 1; o < 32; o <<= 1) {
-    const Tx t = tx_shfl_up(v, o);
-    if (lane >= o) v = tx_then(t, v);
+    const Tx t = tx_shfl_up(inc, o);
+    if (lane >= o) inc = tx_then(t, inc);
   }
+  Tx ex = tx_shfl_up(inc, 1);
+  if (lane == 0) ex = tx_identity();
   __syncthreads();
-  if (lane == 31) wsum[w] = v;
+  if (lane == 31) wsum[w] = inc;
   __syncthreads();
   if (w == 0) {
-    Tx a = wsum[lane];
+    constexpr int nw = NT / 32;
+    Tx a = lane < nw ? wsum[lane] : tx_identity();
     for (int o = 1; o < 32; o <<= 1) {
       const Tx t = tx_shfl_up(a, o);
       if (lane >= o) a = tx_then(t, a);
     }
-    wsum[lane] = a;
+    if (lane < nw) wsum[lane] = a;  // inclusive over warps
   }
   __syncthreads();
-  return w ? tx_then(wsum[w - 1], v) : v;
+  *total = wsum[NT / 32 - 1];
+  return w ? tx_then(wsum[w - 1], ex) : ex;
 }
 
-// step 3: one block of 1024 threads
-__global__ void __launch_bounds__(kWalkThreads) k_walk(const double* __restrict__ x, int64_t b, int64_t n,
-                                                       int64_t nseg, const int32_t* __restrict__ elo,
-                                                       const Tx* __restrict__ Q, const int32_t* __restrict__ F,
-                                                       double* __restrict__ acc) {
-  __shared__ double sh[kWalkThreads];
-  __shared__ Tx wsum[32];
-  __shared__ double s_sh;
-  __shared__ int64_t stop_at;
-  __shared__ unsigned long long cum_before;
-  double s = acc[0];
-  int64_t g = 0;
+struct WalkShared {
+  Tx wsum[32];
+  double sh[kWalkThreads];
+  int brk;
+  unsigned long long cum;
+  double x;
+  long long stop;
+};
+
+// s += the tile's terms in order, exactly as the reference's additions: thread
+// t holds terms t*TPT .. t*TPT+TPT-1 of the tile in v (zeros past its end).
+// xt / len: the tile in memory (the ordered path re-reads it). s is the same in
+// every thread on entry and on return.
+template <int NT, int TPT>
+__device__ double walk_terms(double s, const double (&v)[TPT], const double* __restrict__ xt, int len,
+                             WalkShared& W) {
   const unsigned long long top = 1ull << 53;
-  while (g < nseg) {
-    if (threadIdx.x == 0) s_sh = s;
+  int cursor = 0;  // tile index of the first term not yet added
+  if (TPT == 1) {
+    W.sh[threadIdx.x] = v[0];
     __syncthreads();
-    const double sc = s_sh;
-    if (sc == INFINITY) break;  // inf + (x >= 0) stays inf
-    // the current binade (none if s is not finite: term by term)
-    const bool has = isfinite(sc);
-    const int e = has ? binade_of(sc) : kNoBinade;
-    const double u = has ? ldexp(1.0, e - 52) : 0.0;
-    const unsigned long long A = has ? (unsigned long long)scale2(sc, 52 - e) : 0;  // s / u, exact
+  }
+  while (cursor < len) {
+    if (TPT == 1) {
+      // a short run of the reference's own additions by thread 0 first: where
+      // the running sum climbs a binade every few terms (small sums, rising
+      // terms) that is far cheaper than a block scan per binade
+      const int run_end = cursor + kSeqRun < len ? cursor + kSeqRun : len;
+      if (threadIdx.x == 0) {
+        double r = s;
+        for (int k = cursor; k < run_end; ++k) r += W.sh[k];
+        W.x = r;
+      }
+      __syncthreads();
+      s = W.x;
+      cursor = run_end;
+      __syncthreads();
+      if (cursor >= len) break;
+    }
+    if (!(s >= 0.0) || s == INFINITY) {
+      // negative or non-finite running sum: the reference's additions, one by one
+      s = block_ordered_add(s, xt, cursor, len, W.sh);
+      __syncthreads();
+      if (threadIdx.x == 0) W.x = s;
+      __syncthreads();
+      return W.x;
+    }
+    const int e = binade_of(s);
+    const double halfu = e > -1022 ? ldexp(1.0, e - 53) : 0.0;
+    bool work = false;
+#pragma unroll
+    for (int q = 0; q < TPT; ++q)
+      if ((int)threadIdx.x * TPT + q >= cursor)  // a no-op term: 0 <= x < u/2 (x == 0 in the lowest binade)
+        work |= e > -1022 ? !(v[q] >= 0.0 && v[q] < halfu) : !(v[q] == 0.0);
+    if (!__syncthreads_or(work)) break;  // nothing left in this tile moves s
+    const unsigned long long A = (unsigned long long)scale2(s, 52 - e);  // s / u, exact
+    const uint32_t p0 = (uint32_t)(A & 1ull);
+    const double lim = ldexp(1.0, e + (e == -1022 ? 1 : 0));
+    double f1, f2;
+    quantum_factors(e, f1, f2);
+    Tx mine = tx_identity();
+    int firstflag = TPT;
+#pragma unroll
+    for (int q = 0; q < TPT; ++q) {
+      if ((int)threadIdx.x * TPT + q < cursor || firstflag < TPT) continue;
+      bool f = false;
+      const Tx t = tx_term(v[q], f1, f2, lim, f);
+      if (f) firstflag = q;
+      else mine = tx_then(mine, t);
+    }
+    Tx total;
+    const Tx pre = block_exscan_tx<NT>(mine, W.wsum, &total);
+    unsigned long long cum = p0 ? pre.q1 : pre.q0;
+    uint32_t p = (pre.o >> p0) & 1u;
+    int brk = INT_MAX;
+    unsigned long long cum_brk = 0;
+    double x_brk = 0.0;
+#pragma unroll
+    for (int q = 0; q < TPT; ++q) {
+      const int ti = (int)threadIdx.x * TPT + q;
+      if (ti < cursor || brk != INT_MAX) continue;
+      bool f = q == firstflag;
+      const Tx t = f ? tx_identity() : tx_term(v[q], f1, f2, lim, f);
+      const unsigned long long dq = p ? t.q1 : t.q0;
+      if (f || A + cum + dq >= top) {
+        brk = ti;
+        cum_brk = cum;
+        x_brk = v[q];
+        continue;
+      }
+      cum += dq;
+      p = (t.o >> p) & 1u;
+    }
+    if (threadIdx.x == 0) W.brk = INT_MAX;
+    __syncthreads();
+    if (brk != INT_MAX) atomicMin(&W.brk, brk);
+    __syncthreads();
+    const int b = W.brk;
+    if (b == INT_MAX) {
+      const unsigned long long all = p0 ? total.q1 : total.q0;
+      s = (double)(A + all) * ldexp(1.0, e - 52);  // a multiple of u below 2^(e+1): exact
+      break;
+    }
+    if (brk == b) {
+      W.cum = cum_brk;
+      W.x = x_brk;
+    }
+    __syncthreads();
+    s = (double)(A + W.cum) * ldexp(1.0, e - 52);
+    s = s + W.x;  // the term that leaves the binade (or is flagged), added as the reference adds it
+    cursor = b + 1;
+    __syncthreads();  // W is rewritten next round
+  }
+  return s;
+}
+
+// 1. per-segment tree sums T[y * nseg + g] of sum y = blockIdx.y
+__global__ void __launch_bounds__(kSegThreads) k_seg_sums(const double* __restrict__ X, int64_t n, int64_t stride,
+                                                          int64_t nseg, double* __restrict__ T) {
+  const double* __restrict__ x = X + (int64_t)blockIdx.y * stride;
+  for (int64_t g = blockIdx.x; g < nseg; g += gridDim.x) {
+    double v = 0.0;
+#pragma unroll
+    for (int i = 0; i < kPerThread; ++i) {
+      const int64_t k = g * kSeg + i * kSegThreads + threadIdx.x;
+      if (k < n) v += x[k];
+    }
+    v = ghd::block_sum<kSegThreads>(v);
+    if (threadIdx.x == 0) T[(int64_t)blockIdx.y * nseg + g] = v;
+    __syncthreads();
+  }
+}
+
+// 2. P = exclusive prefix of T, per sum (one block each)
+__global__ void __launch_bounds__(1024) k_seg_scan(const double* __restrict__ T, int64_t nseg, double* __restrict__ P) {
+  __shared__ double ws[32];
+  __shared__ double carry_sh;
+  const double* __restrict__ t = T + (int64_t)blockIdx.x * nseg;
+  double* __restrict__ p = P + (int64_t)blockIdx.x * nseg;
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  double carry = 0.0;
+  for (int64_t b = 0; b < nseg; b += 1024) {
+    const int64_t g = b + threadIdx.x;
+    const double v = g < nseg ? t[g] : 0.0;
+    double inc = v;
+    for (int o = 1; o < 32; o <<= 1) {
+      const double y = __shfl_up_sync(0xffffffffu, inc, o);
+      if (lane >= o) inc += y;
+    }
+    if (lane == 31) ws[w] = inc;
+    __syncthreads();
+    if (w == 0) {
+      double a = ws[lane];
+      for (int o = 1; o < 32; o <<= 1) {
+        const double y = __shfl_up_sync(0xffffffffu, a, o);
+        if (lane >= o) a += y;
+      }
+      ws[lane] = a;
+      if (lane == 31) carry_sh = a;
+    }
+    __syncthreads();
+    if (g < nseg) p[g] = carry + (w ? ws[w - 1] : 0.0) + (inc - v);
+    carry += carry_sh;
+    __syncthreads();
+  }
+}
+
+// 3. the binade of P (the running sum at the segment's start is within ~n 2^-53
+// of P: another binade only for P within that of a power of two, and then the
+// walk just takes the segment term by term), the segment's transducer in it
+// and a flag. Thread t takes the 4 consecutive terms 4t .. 4t+3; terms below
+// half a quantum (E1's far field: zeros and terms far below the running sum)
+// are the identity and skipped.
+__global__ void __launch_bounds__(kSegThreads) k_seg_q(const double* __restrict__ X, int64_t n, int64_t stride,
+                                                       int64_t nseg, const double* __restrict__ P,
+                                                       int32_t* __restrict__ elo, Tx* __restrict__ Q,
+                                                       int32_t* __restrict__ F) {
+  __shared__ Tx sq[kSegThreads / 32];
+  __shared__ int32_t sf[kSegThreads / 32];
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  const int64_t y = blockIdx.y;
+  const double* __restrict__ x = X + y * stride;
+  for (int64_t g = blockIdx.x; g < nseg; g += gridDim.x) {
+    const int64_t gy = y * nseg + g;
+    const double pre = P[gy];  // ~ the running sum before segment g
+    const int e = isfinite(pre) ? binade_of(pre > 0.0 ? pre : 0.0) : kNoBinade;
+    const bool ok = e != kNoBinade && e + 1 < 1023;
+    double xv[kPerThread];
+#pragma unroll
+    for (int i = 0; i < kPerThread; ++i) {
+      const int64_t k = g * kSeg + kPerThread * threadIdx.x + i;
+      xv[i] = k < n ? x[k] : 0.0;
+    }
+    Tx t = tx_identity();
+    bool flag = !ok;
+    if (ok) {
+      const double lim = ldexp(1.0, e + (e == -1022 ? 1 : 0));  // the lowest "binade" ends at 2^-1021
+      const double halfu = e > -1022 ? ldexp(1.0, e - 53) : 0.0;
+      double f1, f2;
+      quantum_factors(e, f1, f2);
+#pragma unroll
+      for (int i = 0; i < kPerThread; ++i) {
+        if (xv[i] >= 0.0 && (e > -1022 ? xv[i] < halfu : xv[i] == 0.0)) continue;  // a no-op term
+        t = tx_then(t, tx_term(xv[i], f1, f2, lim, flag));
+      }
+    }
+    // ordered warp reduction: lane l composes with lanes above it
+    if (__any_sync(0xffffffffu, t.o != 2u || t.q0 || t.q1)) {
+      for (int o = 1; o < 32; o <<= 1) {
+        const Tx up = tx_shfl_down(t, o);
+        if ((lane & (2 * o - 1)) == 0) t = tx_then(t, up);
+      }
+    }
+    const unsigned any = __ballot_sync(0xffffffffu, flag);
+    if (lane == 0) {
+      sq[w] = t;
+      sf[w] = any ? 1 : 0;
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      Tx tq = tx_identity();
+      int32_t tf = 0;
+      for (int v = 0; v < kSegThreads / 32; ++v) {
+        tq = tx_then(tq, sq[v]);
+        tf |= sf[v];
+      }
+      Q[gy] = tq;
+      F[gy] = tf;
+      elo[gy] = ok ? e : kNoBinade;
+    }
+    __syncthreads();
+  }
+}
+
+// 4. the walk: one block of kWalkThreads per sum (sum y = blockIdx.x)
+__global__ void __launch_bounds__(kWalkThreads) k_walk(const double* __restrict__ X, int64_t n, int64_t stride,
+                                                       int64_t nseg, const int32_t* __restrict__ elo_all,
+                                                       const Tx* __restrict__ Q_all, const int32_t* __restrict__ F_all,
+                                                       double* __restrict__ out) {
+  __shared__ WalkShared W;
+  const int64_t y = blockIdx.x;
+  const double* __restrict__ x = X + y * stride;
+  const int32_t* __restrict__ elo = elo_all + y * nseg;
+  const Tx* __restrict__ Q = Q_all + y * nseg;
+  const int32_t* __restrict__ F = F_all + y * nseg;
+  const unsigned long long top = 1ull << 53;
+  double s = 0.0;  // the running sum, the same in every thread
+  int64_t g = 0;
+  while (g < nseg) {
+    if (s != s) break;  // NaN + anything = NaN
+    const bool has = s >= 0.0 && s < INFINITY;
+    const int e = has ? binade_of(s) : kNoBinade;
+    const unsigned long long A = has ? (unsigned long long)scale2(s, 52 - e) : 0;  // s / u, exact
     const uint32_t p0 = (uint32_t)(A & 1ull);
     const int64_t gi = g + threadIdx.x;
     bool simple = false;
     Tx q = tx_identity();
-    if (gi < nseg && has) {
-      const int c = e - elo[gi];
-      if (elo[gi] != kNoBinade && (c == 0 || c == 1) && !F[2 * gi + c]) {
-        simple = true;
-        q = Q[2 * gi + c];
-      }
+    if (gi < nseg && has && elo[gi] == e && !F[gi]) {
+      simple = true;
+      q = Q[gi];
     }
-    const Tx pre = block_scan_tx(q, wsum);  // inclusive
+    Tx total;
+    const Tx ex = block_exscan_tx<kWalkThreads>(q, W.wsum, &total);
+    const Tx pre = tx_then(ex, q);  // inclusive
     const unsigned long long cum = p0 ? pre.q1 : pre.q0;
     const bool stop = gi < nseg && (!simple || A + cum >= top);
-    if (threadIdx.x == 0) stop_at = INT64_MAX;
+    if (threadIdx.x == 0) W.stop = LLONG_MAX;
     __syncthreads();
-    if (stop) atomicMin(reinterpret_cast<unsigned long long*>(&stop_at), (unsigned long long)gi);
+    if (stop) atomicMin(&W.stop, (long long)gi);
     __syncthreads();
-    const int64_t sa = stop_at;
+    const int64_t sa = W.stop;
     // exact integer sum of the simple segments before the stop (or the whole batch)
-    const int64_t last = sa == INT64_MAX ? (nseg < g + kWalkThreads ? nseg : g + kWalkThreads) - 1 : sa - 1;
-    if (threadIdx.x == 0) cum_before = 0;
+    const int64_t last = sa == LLONG_MAX ? (nseg < g + kWalkThreads ? nseg : g + kWalkThreads) - 1 : sa - 1;
+    if (last >= g && gi == last) W.cum = cum;
     __syncthreads();
-    if (last >= g && gi == last) cum_before = cum;
+    if (has && last >= g) s = (double)(A + W.cum) * ldexp(1.0, e - 52);  // a multiple of u below 2^(e+1): exact
     __syncthreads();
-    if (threadIdx.x == 0 && has) s = (double)(A + cum_before) * u;  // a multiple of u below 2^(e+1): exact
-    if (sa == INT64_MAX) {
+    if (sa == LLONG_MAX) {
       g = last + 1;
       continue;
     }
-    const int64_t kb = b + sa * kSeg;
-    s = block_ordered_add(s, x, kb, kb + kSeg < n ? kb + kSeg : n, sh);  // the reference's own additions
+    // segment sa term by term
+    const int64_t kb = sa * kSeg;
+    const int len = (int)(n - kb < kSeg ? n - kb : kSeg);
+    double v[1];
+    v[0] = (int)threadIdx.x < len ? x[kb + threadIdx.x] : 0.0;
+    s = walk_terms<kWalkThreads, 1>(s, v, x + kb, len, W);
+    __syncthreads();
     g = sa + 1;
   }
-  if (threadIdx.x == 0) acc[0] = s;
+  if (threadIdx.x == 0) out[y] = s;
 }
 
 __global__ void k_any_negative(const double* __restrict__ x, int64_t n, int32_t* __restrict__ flag) {
@@ -298,37 +470,47 @@ __global__ void k_any_negative(const double* __restrict__ x, int64_t n, int32_t*
 
 namespace gh {
 
+int64_t seqsum_segments(int64_t n) { return (n + kSeg - 1) / kSeg; }
+
+void sequential_sums_from_T(const double* d_x, int64_t n, int64_t stride, int32_t count, const double* d_T,
+                            double* d_out, cudaStream_t s) {
+  if (count <= 0) return;
+  if (n == 0) {
+    GH_CUDA(cudaMemsetAsync(d_out, 0, sizeof(double) * count, s));
+    return;
+  }
+  const int64_t nseg = seqsum_segments(n);
+  Scratch<double> P((size_t)nseg * count, s);
+  Scratch<int32_t> elo((size_t)nseg * count, s), F((size_t)nseg * count, s);
+  Scratch<Tx> Q((size_t)nseg * count, s);
+  k_seg_scan<<<count, 1024, 0, s>>>(d_T, nseg, P.p);
+  const unsigned gx = (unsigned)std::max<int64_t>(1, std::min<int64_t>(nseg, (148LL * 16 + count - 1) / count));
+  k_seg_q<<<dim3(gx, (unsigned)count), kSegThreads, 0, s>>>(d_x, n, stride, nseg, P.p, elo.p, Q.p, F.p);
+  k_walk<<<count, kWalkThreads, 0, s>>>(d_x, n, stride, nseg, elo.p, Q.p, F.p, d_out);
+  GH_LAUNCH_CHECK();
+}
+
+void sequential_sums_group(const double* d_x, int64_t n, int64_t stride, int32_t count, double* d_out,
+                           cudaStream_t s) {
+  if (count <= 0) return;
+  const int64_t nseg = seqsum_segments(n);
+  Scratch<double> T((size_t)std::max<int64_t>(1, nseg) * count, s);
+  if (nseg) {
+    const unsigned gx = (unsigned)std::max<int64_t>(1, std::min<int64_t>(nseg, (148LL * 16 + count - 1) / count));
+    k_seg_sums<<<dim3(gx, (unsigned)count), kSegThreads, 0, s>>>(d_x, n, stride, nseg, T.p);
+    GH_LAUNCH_CHECK();
+  }
+  sequential_sums_from_T(d_x, n, stride, count, T.p, d_out, s);
+}
+
 double sequential_sum_nonneg(const double* d_x, int64_t n, cudaStream_t s, int* launches) {
   if (n == 0) return 0.0;
-  Scratch<double> acc(1, s);
-  GH_CUDA(cudaMemsetAsync(acc.p, 0, sizeof(double), s));
-  const int64_t K = n < kSeqPrefix ? n : kSeqPrefix;
-  k_seq_block<<<1, kWalkThreads, 0, s>>>(d_x, 0, K, acc.p);
-  int nl = 1;
-  if (n > K) {
-    const int64_t nseg = (n - K + kSeg - 1) / kSeg;
-    Scratch<double> T(nseg, s), P(nseg, s);
-    Scratch<int32_t> elo(nseg, s), F(2 * nseg, s);
-    Scratch<Tx> Q(2 * nseg, s);
-    const unsigned grid = (unsigned)std::min<int64_t>(nseg, 148 * 32);
-    k_seg_sums<<<grid, kSegThreads, 0, s>>>(d_x, K, n, nseg, T.p);
-    size_t tmp_bytes = 0;
-    GH_CUDA(cub::DeviceScan::ExclusiveSum(nullptr, tmp_bytes, T.p, P.p, (int)nseg, s));
-    {
-      Scratch<unsigned char> tmp(tmp_bytes, s);
-      GH_CUDA(cub::DeviceScan::ExclusiveSum(tmp.p, tmp_bytes, T.p, P.p, (int)nseg, s));
-    }
-    // |sequential - exact| and |scan - exact| are both <= (n + 2^11) 2^-53 of the sum
-    const double rel = (double)(n + 4096) * 2.3e-16;
-    k_seg_q<<<grid, kSegThreads, 0, s>>>(d_x, K, n, nseg, P.p, acc.p, rel, elo.p, Q.p, F.p);
-    k_walk<<<1, kWalkThreads, 0, s>>>(d_x, K, n, nseg, elo.p, Q.p, F.p, acc.p);
-    GH_LAUNCH_CHECK();
-    nl += 4;
-  }
+  Scratch<double> out(1, s);
+  sequential_sums_group(d_x, n, n, 1, out.p, s);
   double h = 0.0;
-  GH_CUDA(cudaMemcpyAsync(&h, acc.p, sizeof(double), cudaMemcpyDeviceToHost, s));
+  GH_CUDA(cudaMemcpyAsync(&h, out.p, sizeof(double), cudaMemcpyDeviceToHost, s));
   GH_CUDA(cudaStreamSynchronize(s));
-  if (launches) *launches += nl;
+  if (launches) *launches += 4;
   return h;
 }
 

@@ -693,6 +693,16 @@ def deterministic_sum(terms) -> float:
     return out.value
 
 
+def deterministic_sums(terms) -> np.ndarray:
+    """One deterministic_sum per row of a 2-D array (parallel.hpp:50-54), bit for bit, one device block per row."""
+    v = np.ascontiguousarray(terms, dtype=np.float64)
+    if v.ndim != 2:
+        raise ValueError("deterministic_sums: terms must be a 2-D array (one sum per row)")
+    out = np.empty(v.shape[0], dtype=np.float64)
+    _check(_lib.load().gh_deterministic_sums(_ptr(v), v.shape[1], v.shape[0], _ptr(out)))
+    return out
+
+
 def field_hash(values) -> int:
     """field_hash (report.hpp:145-153)."""
     v = _f64(values)

@@ -81,3 +81,56 @@ def test_average_edge_length_bitwise(gpu, port_oracle, config, scale):
     om = port_oracle.build_mesh(w.positions, w.faces)
     assert g.average_edge_length(mesh) == om.average_edge_length()
     assert g.diffusion_time(mesh, 1.0) == om.diffusion_time(1.0)
+
+
+def _same(a, b):
+    return np.float64(a).view(np.uint64) == np.float64(b).view(np.uint64) or (np.isnan(a) and np.isnan(b))
+
+
+def test_batched_sums_every_family(gpu):
+    """deterministic_sums (one device block per sum, the E1-group engine):
+    every family above as rows of one batch — ties, binade jumps, denormals,
+    saturating prefixes, hundreds of binades, zeros, negatives, inf and NaN."""
+    g = gpu.geoheat
+    rng = np.random.RandomState(21)
+    n = 300_001
+    rows = [
+        rng.uniform(0, 1, n),
+        np.exp(rng.normal(0, 6, n)),
+        rng.uniform(0, 1e-3, n) * (rng.uniform(size=n) > 0.3),
+        rng.choice([0.5, 1.5, 0.25, 2.5, 1.0, 3.0], size=n),
+        np.concatenate([[2.0 ** 52], rng.choice([0.5, 1.0, 1.5], size=n - 1)]),
+        np.concatenate([np.zeros(5000), rng.uniform(0, 1, 5000) * 5e-324 * 1e3, rng.uniform(0, 1e-300, n - 10000)]),
+        np.concatenate([np.ones(4096), np.full(n - 4096, 4095.9)]),
+        rng.uniform(0, 1, n) * 10.0 ** rng.randint(-8, 8, n),
+        10.0 ** rng.uniform(-300, 0, n),
+        np.concatenate([np.full(100_000, 1e-310), 10.0 ** np.linspace(-300, 300, n - 100_000)]),
+        np.sort(10.0 ** rng.uniform(-250, 250, n)),
+        rng.normal(0, 1, n),
+        np.zeros(n),
+        np.full(n, 5e-324),
+        np.concatenate([rng.uniform(0, 1, 1000), [np.inf], rng.uniform(0, 1, n - 1001)]),
+        np.concatenate([rng.uniform(0, 1, 1000), [np.nan], rng.uniform(0, 1, n - 1001)]),
+        np.concatenate([rng.uniform(0, 1, 1000), [np.inf], rng.uniform(0, 1, 1000), [np.nan], np.ones(n - 2002)]),
+        np.concatenate([[1e300] * 10, [1.7e308] * 3, rng.uniform(0, 1, n - 13)]),  # overflow to inf
+        np.concatenate([rng.uniform(0, 1, n // 2), -rng.uniform(0, 1, n - n // 2)]),  # goes negative
+    ]
+    x = np.stack(rows)
+    x[3, 5000] = 2.0 ** 53
+    x[3, 100_000] = 2.0 ** 60
+    got = g.deterministic_sums(x)
+    for i, r in enumerate(x):
+        assert _same(got[i], seq(r)), (i, got[i], seq(r))
+
+
+@pytest.mark.parametrize("n", [1, 2, 4095, 4096, 4097, 8191, 12_289])
+def test_batched_sums_ragged_tiles(gpu, n):
+    """Lengths around the 4096-term tile, many rows of adversarial halves."""
+    g = gpu.geoheat
+    rng = np.random.RandomState(n)
+    x = rng.choice([0.5, 1.5, 2.0 ** -53, 2.0 ** -54, 3.0 * 2.0 ** -54, 1.0], size=(37, n))
+    x[:, 0] = 2.0 ** rng.randint(-60, 60, 37)
+    got = g.deterministic_sums(x)
+    for i, r in enumerate(x):
+        assert _same(got[i], seq(r)), (i, got[i], seq(r))
+    assert g.deterministic_sums(np.zeros((3, 0))).tolist() == [0.0, 0.0, 0.0]
