@@ -342,6 +342,21 @@ gh_status gh_band_prepare(gh_band* band, double t, const double* initial);
 /* u_out (host [V], may be NULL): this band's vertices hold the result. */
 gh_status gh_band_launch(gh_band* band, double t, int32_t sweeps, double* u_out, gh_solver_report* report);
 
+/* One process driving parts whose buffers live in other processes (more
+ * parts than GPUs, or tests on one GPU): gh_band_adopt maps the mutable
+ * buffers (u, per-level counters, per-source ghost counters) of the same part
+ * exported by another process (its gh_band_export blob) through CUDA IPC and
+ * uses them in place of the band's own; gh_band_launch_group runs parts
+ * 0..n-1 of one partition (in order) in ONE cooperative launch on this device,
+ * linked to each other through their current buffers (system-scope releases
+ * and polls when any is adopted), and returns u; gh_band_download writes this
+ * part's own rows of u after `sweeps` sweeps into u_out (vertex order; other
+ * entries kept). */
+gh_status gh_band_adopt(gh_band* band, const void* blob);
+gh_status gh_band_launch_group(gh_band* const* bands, int32_t n, double t, int32_t sweeps, const double* initial,
+                               double* u_out, gh_solver_report* report);
+gh_status gh_band_download(const gh_band* band, int32_t sweeps, double* u_out);
+
 /* ---- Sector slices: every slice owns a contiguous 1/nslices
  * of every BFS ring (in the diffusion layout's ring order), so every slice
  * has work at every step of the sweep pipeline, however the level count

@@ -115,6 +115,9 @@ SIGNATURES = [
     ("gh_gs_diffuse_partitioned", st, [vp, i32, i32, f64, i32, vp, vp, C.POINTER(gh_solver_report)]),
     ("gh_band_create_partitioned", st, [vp, i32, i32, i32, C.POINTER(vp)]),
     ("gh_band_connect_all", st, [vp, C.POINTER(C.c_char_p), i32]),
+    ("gh_band_adopt", st, [vp, vp]),
+    ("gh_band_launch_group", st, [vp, i32, f64, i32, vp, vp, vp]),
+    ("gh_band_download", st, [vp, i32, vp]),
     ("gh_band_own_mask", st, [vp, vp]),
     ("gh_levels_u_device", st, [vp, C.POINTER(vp), C.POINTER(i64)]),
     ("gh_band_destroy", st, [vp]),

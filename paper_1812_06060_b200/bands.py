@@ -149,8 +149,32 @@ class Band:
                 rep.kernel_launches
         return u
 
+    def adopt(self, blob: bytes) -> None:
+        """Drive another process's copy of this part: map its buffers (its export()) in place of ours."""
+        _check(self._lib.gh_band_adopt(self._h, bytes(blob)))
+
+    def download(self, sweeps: int, u: Optional[np.ndarray] = None) -> np.ndarray:
+        """This part's own rows of u after `sweeps` sweeps, in vertex order (other entries of u kept, else NaN)."""
+        out = np.full(self.levels.mesh.vertex_count(), np.nan) if u is None else np.ascontiguousarray(u, np.float64)
+        _check(self._lib.gh_band_download(self._h, int(sweeps), _ptr(out)))
+        return out
+
     def own_mask(self) -> np.ndarray:
         """Vertices whose u this rank computes (its rows of the diffusion layout)."""
         m = np.zeros(self.levels.mesh.vertex_count(), np.uint8)
         _check(self._lib.gh_band_own_mask(self._h, _ptr(m)))
         return m.astype(bool)
+
+
+def launch_group(parts: Sequence[Band], t: float, sweeps: int, initial=None,
+                 report: Optional[SolverReport] = None) -> np.ndarray:
+    """Parts 0..n-1 of one partition (some possibly adopted from other processes) in one launch on this GPU."""
+    lib = parts[0]._lib
+    arr = (C.c_void_p * len(parts))(*[p._h.value for p in parts])
+    init = None if initial is None else _f64(initial)
+    u = np.empty(parts[0].levels.mesh.vertex_count(), np.float64)
+    rep = gh_solver_report()
+    _check(lib.gh_band_launch_group(arr, len(parts), float(t), int(sweeps), _ptr(init), _ptr(u), C.byref(rep)))
+    if report is not None:
+        report.iterations, report.device_ms, report.kernel_launches = rep.iterations, rep.device_ms, rep.kernel_launches
+    return u

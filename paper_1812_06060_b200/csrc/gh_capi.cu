@@ -1038,6 +1038,12 @@ struct gh_band {
   gh::Band band;
   int32_t rank = 0, nranks = 1;
   std::vector<void*> opened;  // peer allocations mapped with cudaIpcOpenMemHandle
+  // gh_band_adopt: the band's own buffers, set aside while it drives another
+  // process's copies of them (restored before the band is freed)
+  bool adopted = false;
+  double* own_ubuf = nullptr;
+  unsigned long long* own_done = nullptr;
+  unsigned long long* own_gdone = nullptr;
 };
 
 namespace {
@@ -1152,6 +1158,11 @@ gh_status gh_band_destroy(gh_band* band) {
     Use use_(band->levels->mesh);
     cudaStreamSynchronize(band->levels->mesh->stream);
     for (void* p : band->opened) cudaIpcCloseMemHandle(p);
+    if (band->adopted) {  // ~Band frees the band's own buffers, never the mapped ones
+      band->band.ubuf = band->own_ubuf;
+      band->band.rows_done = band->own_done;
+      band->band.gdone = band->own_gdone;
+    }
     delete band;
   });
 }
@@ -1251,6 +1262,92 @@ gh_status gh_band_connect_all(gh_band* band, const void* const* blobs, int32_t n
       b.peer_gdone[d] = static_cast<unsigned long long*>(p);
     }
     b.peer_sys = true;  // the peers are other processes' GPUs
+  });
+}
+
+gh_status gh_band_adopt(gh_band* band, const void* blob) {
+  return guarded([&] {
+    require(band && blob, "gh_band_adopt: null argument");
+    require(!band->adopted, "gh_band_adopt: band already drives another process's buffers");
+    gh::Band& b = band->band;
+    BandBlob x;
+    std::memcpy(&x, blob, sizeof(x));
+    require(x.magic == kBlobMagic, "gh_band_adopt: not a band blob");
+    if (!(x.nslices == b.nslices && (b.nslices == 0 || x.rank == b.rank) && x.nrows == b.nrows && x.lb == b.lb &&
+          x.le == b.le && x.device == b.device))
+      gh::fail(GH_ERR_INVALID, "gh_band_adopt: the blob is not this part of this partition on this device");
+    Use use_(band->levels->mesh);
+    auto open = [&](const cudaIpcMemHandle_t& h) {
+      void* p = nullptr;
+      GH_CUDA(cudaIpcOpenMemHandle(&p, h, cudaIpcMemLazyEnablePeerAccess));
+      band->opened.push_back(p);
+      return p;
+    };
+    band->own_ubuf = b.ubuf;
+    band->own_done = b.rows_done;
+    band->own_gdone = b.gdone;
+    b.ubuf = static_cast<double*>(open(x.ubuf));
+    b.rows_done = static_cast<unsigned long long*>(open(x.done));
+    if (b.gdone) b.gdone = static_cast<unsigned long long*>(open(x.gdone));
+    band->adopted = true;
+  });
+}
+
+gh_status gh_band_launch_group(gh_band* const* bands, int32_t n, double t, int32_t sweeps, const double* initial,
+                               double* u_out, gh_solver_report* report) {
+  return guarded([&] {
+    require(bands && n >= 1, "gh_band_launch_group: no bands");
+    gh_levels* L = bands[0] ? bands[0]->levels : nullptr;
+    require(L != nullptr, "gh_band_launch_group: null band");
+    std::vector<gh::Band*> v;
+    bool any_adopted = false;
+    for (int32_t r = 0; r < n; ++r) {
+      require(bands[r] && bands[r]->levels == L, "gh_band_launch_group: bands of different BFS levels");
+      require(bands[r]->rank == r && bands[r]->nranks == n,
+              "gh_band_launch_group: the group must be parts 0..n-1 of one partition, in order");
+      v.push_back(&bands[r]->band);
+      any_adopted |= bands[r]->adopted;
+    }
+    const bool slices = v[0]->nslices > 0;
+    for (gh::Band* b : v)
+      require((b->nslices > 0) == slices, "gh_band_launch_group: slices and level bands in one group");
+    gh_mesh* m = L->mesh;
+    Use use_(m);
+    cudaStream_t s = m->stream;
+    const double w0 = now_s();
+    take_launches(m);
+    if (slices) {
+      gh::slice_link(v);
+    } else {
+      for (int32_t r = 0; r + 1 < n; ++r) gh::band_link(v[r], v[r + 1]);
+    }
+    // buffers of other processes: system-scope releases and polls, as between GPUs
+    for (gh::Band* b : v) b->peer_sys = any_adopted;
+    gh::Scratch<double> dinit(initial ? m->nv : 0, s);
+    if (initial) GH_CUDA(cudaMemcpyAsync(dinit.p, initial, sizeof(double) * m->nv, cudaMemcpyHostToDevice, s));
+    const double ms = gh::diffuse_bands_dev(L, v, t, sweeps, initial ? dinit.p : nullptr);
+    if (u_out) to_host(u_out, L->u_orig.p, m->nv, s);
+    else GH_CUDA(cudaStreamSynchronize(s));
+    if (report) {
+      report->iterations = sweeps;
+      report->converged = 0;
+      report->wall_seconds = now_s() - w0;
+      report->device_ms = ms;
+      report->kernel_launches = take_launches(m);
+    }
+  });
+}
+
+gh_status gh_band_download(const gh_band* band, int32_t sweeps, double* u_out) {
+  return guarded([&] {
+    require(band && u_out && sweeps >= 1, "gh_band_download: bad argument");
+    gh_mesh* m = band->levels->mesh;
+    Use use_(m);
+    cudaStream_t s = m->stream;
+    gh::Scratch<double> du(m->nv, s);
+    GH_CUDA(cudaMemcpyAsync(du.p, u_out, sizeof(double) * m->nv, cudaMemcpyHostToDevice, s));
+    gh::band_own_u(&band->band, sweeps, du.p, s);
+    to_host(u_out, du.p, m->nv, s);
   });
 }
 

@@ -1117,6 +1117,12 @@ double diffuse_bands_dev(gh_levels* L, std::vector<Band*>& bands, double t, int3
   return ms;
 }
 
+void band_own_u(const Band* b, int32_t sweeps, double* d_u, cudaStream_t s) {
+  if (!b->own_rows) return;
+  k_scatter<<<grid_for(b->own_rows), B, 0, s>>>(b->perm.p, b->ubuf, (uint32_t)((sweeps - 1) & 1), b->own_rows, d_u);
+  GH_LAUNCH_CHECK();
+}
+
 void snapshot_to_orig(gh_levels* L, const double* d_snap_sweep, double* d_u) {
   gh_mesh* m = L->mesh;
   const Band& b = L->main;

@@ -93,15 +93,11 @@ __device__ __forceinline__ void face_y_update(int64_t i, v3 g1, v3 g2, double ms
   y2 = sub(q2, scale(w2, shift));
 }
 
-// per face: mu sqrt(A) (the dual offset's divisor, grad_face.hpp:130-131, 150)
-// and sqrt(A) (the primal rows' weight, grad_face.hpp:163-164)
-__global__ void k_face_consts(const double* __restrict__ area, int64_t nf, double mu, double* __restrict__ msa,
-                              double* __restrict__ sa) {
-  GRID_STRIDE(f, nf) {
-    const double r = sqrt(area[f]);
-    msa[f] = mu * r;
-    sa[f] = r;
-  }
+// per face: sqrt(A) (the primal rows' weight, grad_face.hpp:163-164); the dual
+// offset's divisor mu sqrt(A) (grad_face.hpp:130-131, 150) is mu * sa[f], the
+// same operation on the same operands, formed where it is used
+__global__ void k_face_consts(const double* __restrict__ area, int64_t nf, double* __restrict__ sa) {
+  GRID_STRIDE(f, nf) sa[f] = sqrt(area[f]);
 }
 
 // ctor (grad_face.hpp:76-85): edge_dir, incident faces, lambda = 0, scale
@@ -111,7 +107,7 @@ __global__ void k_face_consts(const double* __restrict__ area, int64_t nf, doubl
 __global__ void k_face_init_edges(const double* __restrict__ pos, const int32_t* __restrict__ interior_edges,
                                   const int32_t* __restrict__ edge_v, const int32_t* __restrict__ edge_he,
                                   const double* __restrict__ area, const double* __restrict__ h, int64_t ni,
-                                  double mu, const double* __restrict__ msa, double* __restrict__ edir,
+                                  double mu, const double* __restrict__ sa, double* __restrict__ edir,
                                   int32_t* __restrict__ ef, double* __restrict__ wq, double* __restrict__ lam,
                                   double* __restrict__ C, double* __restrict__ part, double* __restrict__ term) {
   double s = 0.0;
@@ -133,7 +129,7 @@ __global__ void k_face_init_edges(const double* __restrict__ pos, const int32_t*
     wq[2 * i + 1] = w2;
     if (C) {
       v3 y1, y2, d1, d2;
-      face_y_update(i, ld3(h, f1), ld3(h, f2), msa[f1], msa[f2], w1, w2, edir, zero, zero, y1, y2, d1, d2);
+      face_y_update(i, ld3(h, f1), ld3(h, f2), mu * sa[f1], mu * sa[f2], w1, w2, edir, zero, zero, y1, y2, d1, d2);
       st3(C, 2 * i, add(y1, d1));
       st3(C, 2 * i + 1, add(y2, d2));
     }
@@ -182,8 +178,7 @@ __global__ void k_face_g(const int32_t* __restrict__ slot, const double* __restr
 // this iteration's Y recomputed from g_in (the previous g) and the old lambda,
 // then the next iteration's Y and c from the same registers.
 template <int kMinBlocks>
-__global__ void __launch_bounds__(B, kMinBlocks) k_face_lambda_c(const int32_t* __restrict__ ef, const double* __restrict__ msa,
-                                const double* __restrict__ sa, const double* __restrict__ wq,
+__global__ void __launch_bounds__(B, kMinBlocks) k_face_lambda_c(const int32_t* __restrict__ ef, const double* __restrict__ sa, const double* __restrict__ wq,
                                 const double* __restrict__ gin, const double* __restrict__ gout,
                                 const double* __restrict__ edir, int64_t ni, double mu, double* __restrict__ C,
                                 double* __restrict__ lam, double* __restrict__ part, double* __restrict__ term,
@@ -192,13 +187,14 @@ __global__ void __launch_bounds__(B, kMinBlocks) k_face_lambda_c(const int32_t* 
   double s = 0.0;
   GRID_STRIDE(i, ni) {
     const int32_t f1 = ef[2 * i], f2 = ef[2 * i + 1];
-    const double m1 = msa[f1], m2 = msa[f2], w1 = wq[2 * i], w2 = wq[2 * i + 1];
+    const double s1 = sa[f1], s2 = sa[f2];
+    const double m1 = mu * s1, m2 = mu * s2, w1 = wq[2 * i], w2 = wq[2 * i + 1];
     v3 y1, y2, d1, d2;
     face_y_update(i, ld3(gin, f1), ld3(gin, f2), m1, m2, w1, w2, edir, ld3(lam, 2 * i), ld3(lam, 2 * i + 1), y1, y2,
                   d1, d2);
     const v3 g1 = ld3(gout, f1), g2 = ld3(gout, f2);
-    const v3 r1 = scale(sa[f1], sub(y1, g1));
-    const v3 r2 = scale(sa[f2], sub(y2, g2));
+    const v3 r1 = scale(s1, sub(y1, g1));
+    const v3 r2 = scale(s2, sub(y2, g2));
     const v3 l1 = add(ld3(lam, 2 * i), scale(mu, r1));
     const v3 l2 = add(ld3(lam, 2 * i + 1), scale(mu, r2));
     st3(lam, 2 * i, l1);
@@ -516,7 +512,7 @@ AdmmResult admm_face_dev(gh_mesh* m, const double* d_h, const gh_admm_config& cf
   AdmmResult res;
   Scratch<double> Cs(6 * NI + 6, s), lam(6 * NI + 6, s), edir(3 * NI + 3, s), gtmp(3 * F + 3, s);
   Scratch<int32_t> ef(2 * NI + 2, s), slot(3 * F + 3, s);
-  res.state_bytes = sizeof(double) * (3 * F /*g*/ + 3 * F /*targets*/ + 15 * NI + 2 * F + 2 * NI) +
+  res.state_bytes = sizeof(double) * (3 * F /*g*/ + 3 * F /*targets*/ + 15 * NI + F /*sqrt A*/ + 2 * NI /*w*/) +
                     sizeof(int32_t) * (2 * NI + 3 * F);
   double* part_dual = m->partials.p;  // admm_loop's k_admm_stop reads both halves
   double* part_primal = m->partials.p + G;
@@ -529,10 +525,10 @@ AdmmResult admm_face_dev(gh_mesh* m, const double* d_h, const gh_admm_config& cf
   GH_CUDA(cudaMemcpyAsync(gtmp.p, d_h, sizeof(double) * 3 * F, cudaMemcpyDeviceToDevice, s));
   if (F) k_face_slots<<<G, B, 0, s>>>(m->he_edge.p, m->interior_edge_index.p, m->edge_he.p, F, slot.p);
   Scratch<double> term_p(NI + 1, s), term_d(F + 1, s);  // per-element residual terms
-  Scratch<double> msa(F + 1, s), sa(F + 1, s), wq(2 * NI + 2, s);  // per-solve constants (face_y_update)
-  if (F) k_face_consts<<<G, B, 0, s>>>(m->face_area.p, F, mu, msa.p, sa.p);
+  Scratch<double> sa(F + 1, s), wq(2 * NI + 2, s);  // per-solve constants (face_y_update)
+  if (F) k_face_consts<<<G, B, 0, s>>>(m->face_area.p, F, sa.p);
   k_face_init_edges<<<G, B, 0, s>>>(m->pos.p, m->interior_edges.p, m->edge_v.p, m->edge_he.p, m->face_area.p, d_h,
-                                    NI, mu, msa.p, edir.p, ef.p, wq.p, lam.p,
+                                    NI, mu, sa.p, edir.p, ef.p, wq.p, lam.p,
                                     cfg.max_iterations > 0 ? Cs.p : nullptr, part_primal, term_p.p);
   GH_LAUNCH_CHECK();
   m->launches += 3;
@@ -547,10 +543,10 @@ AdmmResult admm_face_dev(gh_mesh* m, const double* d_h, const gh_admm_config& cf
     double* gout = gbuf[it & 1];
     k_face_g<<<G, B, 0, s>>>(slot.p, m->face_area.p, d_h, Cs.p, F, mu, gin, gout, part_dual, term_d.p, halt);
     if (lc_blocks == 3)
-      k_face_lambda_c<3><<<G, B, 0, s>>>(ef.p, msa.p, sa.p, wq.p, gin, gout, edir.p, NI, mu, Cs.p, lam.p, part_primal,
+      k_face_lambda_c<3><<<G, B, 0, s>>>(ef.p, sa.p, wq.p, gin, gout, edir.p, NI, mu, Cs.p, lam.p, part_primal,
                                          term_p.p, halt);
     else
-      k_face_lambda_c<4><<<G, B, 0, s>>>(ef.p, msa.p, sa.p, wq.p, gin, gout, edir.p, NI, mu, Cs.p, lam.p, part_primal,
+      k_face_lambda_c<4><<<G, B, 0, s>>>(ef.p, sa.p, wq.p, gin, gout, edir.p, NI, mu, Cs.p, lam.p, part_primal,
                                          term_p.p, halt);
   });
   // the last iteration's g: odd iterations wrote gtmp

@@ -331,6 +331,8 @@ void bands_prepare(gh_levels* L, std::vector<Band*>& bands, double t, const doub
 double bands_launch(gh_levels* L, std::vector<Band*>& bands, double t, int32_t sweeps, double* d_snap = nullptr);
 // the single band's reachable rows of one snapshot sweep into d_u (original order; unreachable untouched)
 void snapshot_to_orig(gh_levels* L, const double* d_snap_sweep, double* d_u);
+// a band's own rows of u after `sweeps` sweeps -> vertex order
+void band_own_u(const Band* b, int32_t sweeps, double* d_u, cudaStream_t s);
 double diffusion_residual_dev(gh_levels* L, const double* d_u, double t);
 // E1 of a group of k sweeps from their snapshots (k x main.nrows, row order):
 // e1_setup_dev once per solve (vertex -> row and the CSR's columns as rows,
