@@ -346,6 +346,20 @@ def main():
             e2e_s.append(dt)
     e2e_sec = max_over_ranks(dist, float(np.mean(e2e_s)), local)
     e2e_value = reach * w.sweeps / e2e_sec
+    # the same call from pageable (numpy) arrays, as the C++ drop-in's
+    # geoheat::b200::build_mesh(std::vector...) passes them: H2D from pageable
+    # memory inside the timed call
+    pageable_s = []
+    if world == 1:
+        d_page = np.empty(P.shape[0], np.float64)
+        for i in range(1 + a.e2e_steps):
+            rr = G.gh_run_report()
+            t0 = time.perf_counter()
+            G._check(L.gh_distance_host(P.ctypes.data_as(C.c_void_p), P.shape[0], Fc.ctypes.data_as(C.c_void_p),
+                                        Fc.shape[0], S.ctypes.data_as(C.c_void_p), S.size, C.byref(pcfg),
+                                        d_page.ctypes.data_as(C.c_void_p), C.byref(rr)))
+            if i > 0:
+                pageable_s.append(time.perf_counter() - t0)
     # the distances of the last timed call vs the reference chain's field_hash
     # recorded for this config (tools/e2e_parity.py -> profiles/reference_hashes.json)
     d_out = np.ctypeslib.as_array(C.cast(pd, C.POINTER(C.c_double)), shape=(P.shape[0],))
@@ -388,7 +402,10 @@ def main():
                      "scope": "per GPU (rank 0)" if world > 1 else "whole launch"},
         "e2e": {"value": e2e_value, "unit": "vertex-updates/s", "seconds": e2e_sec,
                 "h2d_bytes_per_step": nbytes_p + nbytes_f + S.nbytes, "d2h_bytes_per_step": nbytes_d,
-                "stages_ms": stages, "parity": parity, "samples_s": [round(x, 6) for x in e2e_s], **e2e_extra},
+                "stages_ms": stages, "parity": parity, "samples_s": [round(x, 6) for x in e2e_s], **e2e_extra,
+                **({"pageable_seconds": float(np.mean(pageable_s)),
+                    "pageable_value": reach * w.sweeps / float(np.mean(pageable_s)),
+                    "pageable_samples_s": [round(x, 6) for x in pageable_s]} if pageable_s else {})},
         "gpu_launches": launches,
         "clocks": clk.summary(),
         "cpu_baseline": cpu,
