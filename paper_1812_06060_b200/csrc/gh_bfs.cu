@@ -41,7 +41,7 @@ __global__ void k_bfs_seed(const int32_t* __restrict__ vv_off, int32_t* __restri
 // One ring per iteration; level_size[d] counts ring d. Returns nlev in *out.
 // Frontier entries carry their row bounds (read by the claiming thread while
 // its append slot is reserved), so expanding a ring starts at vv_idx.
-constexpr int kBfsBlock = 1024;  // one block per SM; more threads = fewer rounds per wide ring
+constexpr int kBfsBlock = 512;
 __global__ void __launch_bounds__(kBfsBlock) k_bfs(const int32_t* __restrict__ vv_off, const int32_t* __restrict__ vv_idx,
                                                    int32_t* __restrict__ level, int4* __restrict__ fa,
                                                    int4* __restrict__ fb, int32_t* __restrict__ level_size,

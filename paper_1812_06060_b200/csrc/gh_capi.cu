@@ -59,7 +59,15 @@ struct Use {
 
 template <class T>
 void to_host(T* dst, const T* src, size_t n, cudaStream_t s) {
-  if (n) GH_CUDA(cudaMemcpyAsync(dst, src, sizeof(T) * n, cudaMemcpyDeviceToHost, s));
+  const uint64_t bytes = sizeof(T) * (uint64_t)n;
+  if (bytes >= (32ull << 20) && gh::host_pageable(dst)) {  // large pageable results: staged by host threads
+    int dev = 0;
+    GH_CUDA(cudaGetDevice(&dev));
+    GH_CUDA(cudaStreamSynchronize(s));
+    gh::device_to_host_staged(src, bytes, dst, dev);
+    return;
+  }
+  if (n) GH_CUDA(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyDeviceToHost, s));
   GH_CUDA(cudaStreamSynchronize(s));
 }
 

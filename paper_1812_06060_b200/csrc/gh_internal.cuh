@@ -298,6 +298,12 @@ struct gh_levels {
 namespace gh {
 
 // mesh build / queries (gh_mesh.cu)
+// host -> device copies from pageable memory: up to 16 host threads copy
+// through pinned 16 MiB slots, each overlapping its memcpy with the H2D of
+// the previous slot (gh_load.cu); returns when the data is on the device
+bool host_pageable(const void* p);
+void host_to_device_staged(const void* src, uint64_t n, void* dst, int device);
+void device_to_host_staged(const void* src, uint64_t n, void* dst, int device);
 void mesh_build(gh_mesh* m, const double* h_pos, const int32_t* h_faces);
 // gh_load.cu: load_mesh into an initialised handle (device, stream set).
 void load_mesh_bytes(gh_mesh* m, const unsigned char* bytes, uint64_t n, int format, int threads, gh_load_report* rep);

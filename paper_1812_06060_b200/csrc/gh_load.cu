@@ -141,6 +141,62 @@ void stage_to_device(const unsigned char* src, uint64_t n, unsigned char* dst, i
     if (!e.empty()) fail(GH_ERR_CUDA, e);
 }
 
+// The reverse: device [src, src+n) to pageable host dst, each worker taking
+// chunks through two pinned slots (H2D of one while the other is copied out).
+void stage_from_device(const unsigned char* src, uint64_t n, unsigned char* dst, int threads, int device) {
+  if (!n) return;
+  const uint64_t chunks = (n + kSlot - 1) / kSlot;
+  const int nt = (int)std::max<uint64_t>(1, std::min<uint64_t>((uint64_t)std::max(threads, 1), chunks));
+  std::vector<void*> slots = take_slots(2 * (size_t)nt);
+  std::vector<std::string> errors(nt);
+  auto worker = [&](int j) {
+    cudaStream_t s = nullptr;
+    cudaEvent_t ev[2] = {nullptr, nullptr};
+    try {
+      GH_CUDA(cudaSetDevice(device));
+      GH_CUDA(cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking));
+      GH_CUDA(cudaEventCreateWithFlags(&ev[0], cudaEventDisableTiming));
+      GH_CUDA(cudaEventCreateWithFlags(&ev[1], cudaEventDisableTiming));
+      uint64_t pend_off[2] = {0, 0}, pend_len[2] = {0, 0};
+      int k = 0;
+      for (uint64_t c = (uint64_t)j;; c += (uint64_t)nt, ++k) {
+        const int b = k & 1;
+        if (c < chunks) {  // start chunk c into slot b
+          const uint64_t off = c * kSlot, len = std::min(kSlot, n - off);
+          GH_CUDA(cudaMemcpyAsync(slots[2 * j + b], src + off, len, cudaMemcpyDeviceToHost, s));
+          GH_CUDA(cudaEventRecord(ev[b], s));
+          pend_off[b] = off;
+          pend_len[b] = len;
+        }
+        const int o = b ^ 1;  // finish the other slot's chunk (started last round)
+        if (pend_len[o]) {
+          GH_CUDA(cudaEventSynchronize(ev[o]));
+          std::memcpy(dst + pend_off[o], slots[2 * j + o], pend_len[o]);
+          pend_len[o] = 0;
+        }
+        if (c >= chunks && !pend_len[b]) break;
+      }
+    } catch (const gh::Error& e) {
+      errors[j] = e.msg;
+    } catch (...) {
+      errors[j] = "device->host staging failed";
+    }
+    if (s) {
+      cudaStreamSynchronize(s);
+      cudaStreamDestroy(s);
+    }
+    for (cudaEvent_t e : ev)
+      if (e) cudaEventDestroy(e);
+  };
+  std::vector<std::thread> pool;
+  for (int j = 1; j < nt; ++j) pool.emplace_back(worker, j);
+  worker(0);
+  for (auto& t : pool) t.join();
+  give_slots(slots);
+  for (const std::string& e : errors)
+    if (!e.empty()) fail(GH_ERR_CUDA, e);
+}
+
 // ------------------------------------------------------- device decode
 __device__ __forceinline__ double load_scalar(const unsigned char* p, int type) {
   uint64_t bits = 0;
@@ -297,6 +353,30 @@ void load_binary_ply(gh_mesh* m, const ghio::PlyHeader& h, const unsigned char* 
 }  // namespace
 
 namespace gh {
+
+bool host_pageable(const void* p) {
+  cudaPointerAttributes a{};
+  if (cudaPointerGetAttributes(&a, p) != cudaSuccess) {
+    (void)cudaGetLastError();
+    return true;
+  }
+  return a.type == cudaMemoryTypeUnregistered;
+}
+
+int staging_threads() {
+  const unsigned hw = std::thread::hardware_concurrency();
+  return (int)std::max(1u, std::min(16u, hw ? hw : 1u));
+}
+
+void host_to_device_staged(const void* src, uint64_t n, void* dst, int device) {
+  stage_to_device(static_cast<const unsigned char*>(src), n, static_cast<unsigned char*>(dst), staging_threads(),
+                  device);
+}
+
+void device_to_host_staged(const void* src, uint64_t n, void* dst, int device) {
+  stage_from_device(static_cast<const unsigned char*>(src), n, static_cast<unsigned char*>(dst), staging_threads(),
+                    device);
+}
 
 void load_mesh_bytes(gh_mesh* m, const unsigned char* bytes, uint64_t n, int format, int threads,
                      gh_load_report* rep) {

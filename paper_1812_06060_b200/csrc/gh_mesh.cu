@@ -508,8 +508,19 @@ void mesh_build(gh_mesh* m, const double* h_pos, const int32_t* h_faces) {
   if (h_pos || h_faces || m->pos.n != (size_t)(3 * V) || m->faces.n != (size_t)(3 * F)) {
     m->pos.alloc(3 * V, s);
     m->faces.alloc(3 * F, s);
-    if (F) GH_CUDA(cudaMemcpyAsync(m->faces.p, h_faces, sizeof(int32_t) * 3 * F, cudaMemcpyHostToDevice, s));
-    if (V) {
+    // large pageable arrays (std::vector / numpy, as the reference's callers
+    // hold them): staged through pinned slots by host threads (~4x the
+    // driver's own pageable copy); pinned or device arrays: async copies
+    const uint64_t fbytes = sizeof(int32_t) * 3 * (uint64_t)F, pbytes = sizeof(double) * 3 * (uint64_t)V;
+    constexpr uint64_t kStageMin = 32ull << 20;
+    const bool stage_f = F && fbytes >= kStageMin && host_pageable(h_faces);
+    const bool stage_p = V && pbytes >= kStageMin && host_pageable(h_pos);
+    if (stage_f || stage_p) GH_CUDA(cudaStreamSynchronize(s));  // the pool allocations above, before other streams write
+    if (stage_f) host_to_device_staged(h_faces, fbytes, m->faces.p, m->device);
+    else if (F) GH_CUDA(cudaMemcpyAsync(m->faces.p, h_faces, fbytes, cudaMemcpyHostToDevice, s));
+    if (stage_p) {
+      host_to_device_staged(h_pos, pbytes, m->pos.p, m->device);
+    } else if (V) {
       Event faces_done;
       faces_done.record(s);  // also orders the pos allocation before the copy stream uses it
       GH_CUDA(cudaStreamWaitEvent(m->copy_stream, faces_done.e, 0));
