@@ -103,7 +103,7 @@ __global__ void k_face_consts(const double* __restrict__ area, int64_t nf, doubl
 // ctor (grad_face.hpp:76-85): edge_dir, incident faces, lambda = 0, scale
 // partials; with C set, also the first iteration's c per slot: y1, y2 start
 // at h of the side faces (grad_face.hpp:82-83), which is the Y-update from
-// g = h, lambda = 0 (computed exactly like later ones, see k_face_lambda_c)
+// g = h, lambda = 0 (computed exactly like later ones, see k_face_lambda_pair)
 __global__ void k_face_init_edges(const double* __restrict__ pos, const int32_t* __restrict__ interior_edges,
                                   const int32_t* __restrict__ edge_v, const int32_t* __restrict__ edge_he,
                                   const double* __restrict__ area, const double* __restrict__ h, int64_t ni,
@@ -176,35 +176,74 @@ __global__ void k_face_g(const int32_t* __restrict__ slot, const double* __restr
 
 // lambda-update + primal rows per interior edge (grad_face.hpp:158-168) with
 // this iteration's Y recomputed from g_in (the previous g) and the old lambda,
-// then the next iteration's Y and c from the same registers.
-template <int kMinBlocks>
-__global__ void __launch_bounds__(B, kMinBlocks) k_face_lambda_c(const int32_t* __restrict__ ef, const double* __restrict__ sa, const double* __restrict__ wq,
-                                const double* __restrict__ gin, const double* __restrict__ gout,
-                                const double* __restrict__ edir, int64_t ni, double mu, double* __restrict__ C,
-                                double* __restrict__ lam, double* __restrict__ part, double* __restrict__ term,
-                                const int32_t* __restrict__ halt) {
+// then the next iteration's Y and c from the same registers; two lanes per
+// edge (lane 2k + side handles side
+// `side` of edge i = k >> 1: face ef[2i + side], its lambda / c slots), so each
+// thread holds one side's state (half the registers, twice the resident warps)
+// and the per-side streams (ef, wq, lambda, c) are contiguous across lanes.
+// The two sides meet only in the mismatch dot(e, q2 - q1) and in the primal
+// term |r1|^2 + |r2|^2: their q and |r|^2 cross the pair with one shuffle, and
+// both lanes evaluate the reference's expressions on the same operands in the
+// same order (grad_face.hpp:31-36, 126-168), so every value keeps its bits.
+// Only side-0 lanes add the primal term into the block's tree sum.
+__device__ __forceinline__ v3 shfl_pair(const v3& a) {
+  return mk(__shfl_xor_sync(0xffffffffu, a.x, 1), __shfl_xor_sync(0xffffffffu, a.y, 1),
+            __shfl_xor_sync(0xffffffffu, a.z, 1));
+}
+// y for this side from both sides' q (y_update_edge, grad_face.hpp:31-36)
+__device__ __forceinline__ v3 pair_y(int side, const v3& q, const v3& ed, double w) {
+  const v3 qo = shfl_pair(q);
+  const v3 q1 = side ? qo : q, q2 = side ? q : qo;
+  const double mismatch = dot(ed, sub(q2, q1));
+  const v3 shift = mk(ed.x * mismatch, ed.y * mismatch, ed.z * mismatch);
+  return side ? sub(q, scale(w, shift)) : add(q, scale(w, shift));
+}
+// 4 blocks per SM (64 registers; g_out is loaded after the first y so that
+// fits): config 3 18.3 vs 19.0 ms, config 4 103 vs 107.5 ms per 10 iterations
+// against one thread per edge at 3 blocks per SM (same box, interleaved runs).
+__global__ void __launch_bounds__(B, 4) k_face_lambda_pair(const int32_t* __restrict__ ef, const double* __restrict__ sa,
+                                                        const double* __restrict__ wq, const double* __restrict__ gin,
+                                                        const double* __restrict__ gout,
+                                                        const double* __restrict__ edir, int64_t ni, double mu,
+                                                        double* __restrict__ C, double* __restrict__ lam,
+                                                        double* __restrict__ part, double* __restrict__ term,
+                                                        const int32_t* __restrict__ halt) {
   if (*halt) return;
   double s = 0.0;
-  GRID_STRIDE(i, ni) {
-    const int32_t f1 = ef[2 * i], f2 = ef[2 * i + 1];
-    const double s1 = sa[f1], s2 = sa[f2];
-    const double m1 = mu * s1, m2 = mu * s2, w1 = wq[2 * i], w2 = wq[2 * i + 1];
-    v3 y1, y2, d1, d2;
-    face_y_update(i, ld3(gin, f1), ld3(gin, f2), m1, m2, w1, w2, edir, ld3(lam, 2 * i), ld3(lam, 2 * i + 1), y1, y2,
-                  d1, d2);
-    const v3 g1 = ld3(gout, f1), g2 = ld3(gout, f2);
-    const v3 r1 = scale(s1, sub(y1, g1));
-    const v3 r2 = scale(s2, sub(y2, g2));
-    const v3 l1 = add(ld3(lam, 2 * i), scale(mu, r1));
-    const v3 l2 = add(ld3(lam, 2 * i + 1), scale(mu, r2));
-    st3(lam, 2 * i, l1);
-    st3(lam, 2 * i + 1, l2);
-    const double tt = sqnorm(r1) + sqnorm(r2);
-    term[i] = tt;
-    s += tt;
-    face_y_update(i, g1, g2, m1, m2, w1, w2, edir, l1, l2, y1, y2, d1, d2);
-    st3(C, 2 * i, add(y1, d1));
-    st3(C, 2 * i + 1, add(y2, d2));
+  const int side = threadIdx.x & 1;
+  const int64_t n = 2 * ni, stride = (int64_t)gridDim.x * blockDim.x;
+  // the whole warp steps together (the pair shuffles need every lane)
+  for (int64_t k0 = blockIdx.x * (int64_t)blockDim.x + (threadIdx.x & ~31); k0 < n; k0 += stride) {
+    const int64_t k = k0 + (threadIdx.x & 31);
+    const bool valid = k < n;  // n even: both lanes of a pair agree
+    const int64_t i = k >> 1;
+    const int32_t f = valid ? ef[k] : 0;
+    const double sf = valid ? sa[f] : 1.0;
+    const double m = mu * sf, w = valid ? wq[k] : 0.0;
+    const v3 ed = valid ? ld3(edir, i) : mk(0.0, 0.0, 0.0);
+    const v3 lold = valid ? ld3(lam, k) : mk(0.0, 0.0, 0.0);
+    const v3 gi = valid ? ld3(gin, f) : mk(0.0, 0.0, 0.0);
+    // this iteration's y from g_in and the old lambda (grad_face.hpp:126-137)
+    const v3 d = divs(lold, m);
+    const v3 y = pair_y(side, sub(gi, d), ed, w);
+    asm volatile("" ::: "memory");  // g_out's load after y: fewer live registers
+    const v3 go = valid ? ld3(gout, f) : mk(0.0, 0.0, 0.0);
+    // lambda += mu r, r = sqrt(A) (y - g) (grad_face.hpp:158-168)
+    const v3 r = scale(sf, sub(y, go));
+    const v3 l = add(lold, scale(mu, r));
+    const double sq = sqnorm(r), sqo = __shfl_xor_sync(0xffffffffu, sq, 1);
+    if (valid) {
+      st3(lam, k, l);
+      if (!side) {
+        const double tt = sq + sqo;
+        term[i] = tt;
+        s += tt;
+      }
+    }
+    // the next iteration's y and c = y + lambda / (mu sqrt(A)) from the same registers
+    const v3 d2 = divs(l, m);
+    const v3 y2 = pair_y(side, sub(go, d2), ed, w);
+    if (valid) st3(C, k, add(y2, d2));
   }
   s = block_sum<B>(s);
   if (threadIdx.x == 0) part[blockIdx.x] = s;
@@ -534,20 +573,13 @@ AdmmResult admm_face_dev(gh_mesh* m, const double* d_h, const gh_admm_config& cf
   m->launches += 3;
   // ||M||_F (grad_face.hpp:85): the reference's left-to-right sum, exactly
   const double scale = std::sqrt(sequential_sum_nonneg(term_p.p, NI, s, &m->launches));
-  // k_face_lambda_c: 3 blocks per SM (80 registers) or 4 (64, more spills); GH_FACE_LC_BLOCKS picks.
-  // Measured per iteration: config 3 1.87 vs 1.90 ms, config 4 11.2 vs 11.9 ms.
-  const int lc_blocks = getenv("GH_FACE_LC_BLOCKS") ? atoi(getenv("GH_FACE_LC_BLOCKS")) : 3;
   // grad_face.hpp:175-177
   admm_loop(m, res, cfg, scale, mu, term_p.p, NI, term_d.p, F, [&](int32_t it, const int32_t* halt) {
     const double* gin = gbuf[(it + 1) & 1];
     double* gout = gbuf[it & 1];
     k_face_g<<<G, B, 0, s>>>(slot.p, m->face_area.p, d_h, Cs.p, F, mu, gin, gout, part_dual, term_d.p, halt);
-    if (lc_blocks == 3)
-      k_face_lambda_c<3><<<G, B, 0, s>>>(ef.p, sa.p, wq.p, gin, gout, edir.p, NI, mu, Cs.p, lam.p, part_primal,
-                                         term_p.p, halt);
-    else
-      k_face_lambda_c<4><<<G, B, 0, s>>>(ef.p, sa.p, wq.p, gin, gout, edir.p, NI, mu, Cs.p, lam.p, part_primal,
-                                         term_p.p, halt);
+    k_face_lambda_pair<<<G, B, 0, s>>>(ef.p, sa.p, wq.p, gin, gout, edir.p, NI, mu, Cs.p, lam.p, part_primal,
+                                       term_p.p, halt);
   });
   // the last iteration's g: odd iterations wrote gtmp
   if (res.iterations > 0 && ((res.iterations - 1) & 1))

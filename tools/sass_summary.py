@@ -30,7 +30,7 @@ def demangle(names):
 
 def main():
     ap = argparse.ArgumentParser()
-    ap.add_argument("--kernels", default="k_diffuse_tma|k_face_g|k_face_lambda_c|k_edge_x|k_edge_lambda_w|k_bfs|k_chain")
+    ap.add_argument("--kernels", default="k_diffuse_tma|k_face_g|k_face_lambda_pair|k_edge_x|k_edge_lambda_w|k_bfs|k_chain")
     ap.add_argument("--out", default="")
     a = ap.parse_args()
     sass = subprocess.run(["cuobjdump", "-sass", LIB], capture_output=True, text=True, check=True).stdout
