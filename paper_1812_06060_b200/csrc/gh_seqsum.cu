@@ -27,11 +27,10 @@
 //      one segment's transducer, and a block scan finds the first segment
 //      that was prepared for another binade, is flagged,
 //      or would carry s out of it; the segments before it are added exactly as
-//      integers, that one term by term (a block scan per binade the sum
-//      climbs through, the leaving term itself added in double as the
-//      reference adds it), and the walk goes on after it.
-// A negative or non-finite running sum (terms of any sign are accepted) makes
-// thread 0 add the rest of that segment one term at a time, as the reference.
+//      integers, that one term by term in double (its nonzero terms, in
+//      order: zeros are exact no-ops), and the walk goes on after it. A
+//      negative or non-finite running sum (terms of any sign are accepted)
+//      stops the walk at every segment, which is then added the same way.
 
 #include <climits>
 #include <cmath>
@@ -45,7 +44,6 @@ constexpr int kWalkThreads = 1024;  // = kSeg: one term per thread when a segmen
 constexpr int kSegThreads = 256;
 constexpr int kPerThread = kSeg / kSegThreads;
 constexpr int kNoBinade = -100000;
-constexpr int kSeqRun = 64;  // terms thread 0 adds in order before each block scan of a walked segment
 
 // s += x[b..e) in order: the block stages terms in shared memory (coalesced)
 // and thread 0 adds them one by one.
@@ -171,116 +169,48 @@ __device__ Tx block_exscan_tx(Tx v, Tx* wsum, Tx* total) {
 struct WalkShared {
   Tx wsum[32];
   double sh[kWalkThreads];
-  int brk;
+  int cnt[kWalkThreads / 32];
+  int total;
   unsigned long long cum;
   double x;
   long long stop;
 };
 
-// s += the tile's terms in order, exactly as the reference's additions: thread
-// t holds terms t*TPT .. t*TPT+TPT-1 of the tile in v (zeros past its end).
-// xt / len: the tile in memory (the ordered path re-reads it). s is the same in
-// every thread on entry and on return.
-template <int NT, int TPT>
-__device__ double walk_terms(double s, const double (&v)[TPT], const double* __restrict__ xt, int len,
-                             WalkShared& W) {
-  const unsigned long long top = 1ull << 53;
-  int cursor = 0;  // tile index of the first term not yet added
-  if (TPT == 1) {
-    W.sh[threadIdx.x] = v[0];
-    __syncthreads();
+// s += one segment's terms in order, exactly as the reference's additions
+// (one term per thread, v; zeros past the end). Zero terms are exact no-ops
+// (s + 0 = s for every s, signed zeros and NaN included), so the block keeps
+// the nonzero terms in order (warp ballots, a prefix over the warps) and
+// thread 0 adds just those, one by one: a walked segment is where the running
+// sum leaves its binade, often several times in a few terms (E1: ~1000 binade
+// changes in ~300 of 8192 segments at config 3), where a block scan per change
+// costs more than the additions. s is the same in every thread on return.
+__device__ double walk_segment(double s, double v, WalkShared& W) {
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  const bool nz = !(v == 0.0);
+  const unsigned m = __ballot_sync(0xffffffffu, nz);
+  if (lane == 0) W.cnt[w] = __popc(m);
+  __syncthreads();
+  if (w == 0) {  // exclusive prefix over the warps
+    const int c = lane < kWalkThreads / 32 ? W.cnt[lane] : 0;
+    int inc = c;
+    for (int o = 1; o < 32; o <<= 1) {
+      const int y = __shfl_up_sync(0xffffffffu, inc, o);
+      if (lane >= o) inc += y;
+    }
+    if (lane < kWalkThreads / 32) W.cnt[lane] = inc - c;
+    if (lane == 31) W.total = inc;
   }
-  while (cursor < len) {
-    if (TPT == 1) {
-      // a short run of the reference's own additions by thread 0 first: where
-      // the running sum climbs a binade every few terms (small sums, rising
-      // terms) that is far cheaper than a block scan per binade
-      const int run_end = cursor + kSeqRun < len ? cursor + kSeqRun : len;
-      if (threadIdx.x == 0) {
-        double r = s;
-        for (int k = cursor; k < run_end; ++k) r += W.sh[k];
-        W.x = r;
-      }
-      __syncthreads();
-      s = W.x;
-      cursor = run_end;
-      __syncthreads();
-      if (cursor >= len) break;
-    }
-    if (!(s >= 0.0) || s == INFINITY) {
-      // negative or non-finite running sum: the reference's additions, one by one
-      s = block_ordered_add(s, xt, cursor, len, W.sh);
-      __syncthreads();
-      if (threadIdx.x == 0) W.x = s;
-      __syncthreads();
-      return W.x;
-    }
-    const int e = binade_of(s);
-    const double halfu = e > -1022 ? ldexp(1.0, e - 53) : 0.0;
-    bool work = false;
-#pragma unroll
-    for (int q = 0; q < TPT; ++q)
-      if ((int)threadIdx.x * TPT + q >= cursor)  // a no-op term: 0 <= x < u/2 (x == 0 in the lowest binade)
-        work |= e > -1022 ? !(v[q] >= 0.0 && v[q] < halfu) : !(v[q] == 0.0);
-    if (!__syncthreads_or(work)) break;  // nothing left in this tile moves s
-    const unsigned long long A = (unsigned long long)scale2(s, 52 - e);  // s / u, exact
-    const uint32_t p0 = (uint32_t)(A & 1ull);
-    const double lim = ldexp(1.0, e + (e == -1022 ? 1 : 0));
-    double f1, f2;
-    quantum_factors(e, f1, f2);
-    Tx mine = tx_identity();
-    int firstflag = TPT;
-#pragma unroll
-    for (int q = 0; q < TPT; ++q) {
-      if ((int)threadIdx.x * TPT + q < cursor || firstflag < TPT) continue;
-      bool f = false;
-      const Tx t = tx_term(v[q], f1, f2, lim, f);
-      if (f) firstflag = q;
-      else mine = tx_then(mine, t);
-    }
-    Tx total;
-    const Tx pre = block_exscan_tx<NT>(mine, W.wsum, &total);
-    unsigned long long cum = p0 ? pre.q1 : pre.q0;
-    uint32_t p = (pre.o >> p0) & 1u;
-    int brk = INT_MAX;
-    unsigned long long cum_brk = 0;
-    double x_brk = 0.0;
-#pragma unroll
-    for (int q = 0; q < TPT; ++q) {
-      const int ti = (int)threadIdx.x * TPT + q;
-      if (ti < cursor || brk != INT_MAX) continue;
-      bool f = q == firstflag;
-      const Tx t = f ? tx_identity() : tx_term(v[q], f1, f2, lim, f);
-      const unsigned long long dq = p ? t.q1 : t.q0;
-      if (f || A + cum + dq >= top) {
-        brk = ti;
-        cum_brk = cum;
-        x_brk = v[q];
-        continue;
-      }
-      cum += dq;
-      p = (t.o >> p) & 1u;
-    }
-    if (threadIdx.x == 0) W.brk = INT_MAX;
-    __syncthreads();
-    if (brk != INT_MAX) atomicMin(&W.brk, brk);
-    __syncthreads();
-    const int b = W.brk;
-    if (b == INT_MAX) {
-      const unsigned long long all = p0 ? total.q1 : total.q0;
-      s = (double)(A + all) * ldexp(1.0, e - 52);  // a multiple of u below 2^(e+1): exact
-      break;
-    }
-    if (brk == b) {
-      W.cum = cum_brk;
-      W.x = x_brk;
-    }
-    __syncthreads();
-    s = (double)(A + W.cum) * ldexp(1.0, e - 52);
-    s = s + W.x;  // the term that leaves the binade (or is flagged), added as the reference adds it
-    cursor = b + 1;
-    __syncthreads();  // W is rewritten next round
+  __syncthreads();
+  if (nz) W.sh[W.cnt[w] + __popc(m & ((1u << lane) - 1u))] = v;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    const int n = W.total;
+    for (int k = 0; k < n; ++k) s += W.sh[k];
+    W.x = s;
   }
+  __syncthreads();
+  s = W.x;
+  __syncthreads();  // W is reused by the next segment
   return s;
 }
 
@@ -452,10 +382,7 @@ __global__ void __launch_bounds__(kWalkThreads) k_walk(const double* __restrict_
     // segment sa term by term
     const int64_t kb = sa * kSeg;
     const int len = (int)(n - kb < kSeg ? n - kb : kSeg);
-    double v[1];
-    v[0] = (int)threadIdx.x < len ? x[kb + threadIdx.x] : 0.0;
-    s = walk_terms<kWalkThreads, 1>(s, v, x + kb, len, W);
-    __syncthreads();
+    s = walk_segment(s, (int)threadIdx.x < len ? x[kb + threadIdx.x] : 0.0, W);
     g = sa + 1;
   }
   if (threadIdx.x == 0) out[y] = s;
