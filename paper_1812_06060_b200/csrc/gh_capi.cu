@@ -1285,18 +1285,29 @@ gh_status gh_band_adopt(gh_band* band, const void* blob) {
           x.le == b.le && x.device == b.device))
       gh::fail(GH_ERR_INVALID, "gh_band_adopt: the blob is not this part of this partition on this device");
     Use use_(band->levels->mesh);
+    // map every buffer first: on a failure the band keeps its own buffers
+    std::vector<void*> mapped;
     auto open = [&](const cudaIpcMemHandle_t& h) {
       void* p = nullptr;
-      GH_CUDA(cudaIpcOpenMemHandle(&p, h, cudaIpcMemLazyEnablePeerAccess));
-      band->opened.push_back(p);
+      const cudaError_t e = cudaIpcOpenMemHandle(&p, h, cudaIpcMemLazyEnablePeerAccess);
+      if (e != cudaSuccess) {
+        (void)cudaGetLastError();
+        for (void* q : mapped) cudaIpcCloseMemHandle(q);
+        gh::fail(GH_ERR_CUDA, std::string("gh_band_adopt: cudaIpcOpenMemHandle failed: ") + cudaGetErrorString(e));
+      }
+      mapped.push_back(p);
       return p;
     };
+    double* ubuf = static_cast<double*>(open(x.ubuf));
+    unsigned long long* done = static_cast<unsigned long long*>(open(x.done));
+    unsigned long long* gdone = b.gdone ? static_cast<unsigned long long*>(open(x.gdone)) : nullptr;
+    band->opened.insert(band->opened.end(), mapped.begin(), mapped.end());
     band->own_ubuf = b.ubuf;
     band->own_done = b.rows_done;
     band->own_gdone = b.gdone;
-    b.ubuf = static_cast<double*>(open(x.ubuf));
-    b.rows_done = static_cast<unsigned long long*>(open(x.done));
-    if (b.gdone) b.gdone = static_cast<unsigned long long*>(open(x.gdone));
+    b.ubuf = ubuf;
+    b.rows_done = done;
+    b.gdone = gdone;
     band->adopted = true;
   });
 }
