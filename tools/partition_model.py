@@ -47,7 +47,7 @@ def model(sizes, S=1000, a=3e-6, c=2e-6, b=1 / 70e9):
         emu = float(np.sum(a + np.max([p * b / f for p, f in zip(parts, frac)], axis=0)))
         real_b = float(np.sum(a + c + np.max([p * b for p in parts], axis=0)))
         real_s = float(np.sum(a + c + tot * b / N))
-        res[N] = {"bands_speedup": single / real_b, "slices_speedup": single / real_s,
+        res[str(N)] = {"bands_speedup": single / real_b, "slices_speedup": single / real_s,
                   "bands_emulated_over_one": emu / single}
     return res
 
