@@ -467,6 +467,25 @@ def test_repeated_solves_reuse_cached_blocks(gpu):
                 assert_same(d, first[k], f"round {rnd}, mesh {k}")
 
 
+def test_release_cached_memory_keeps_handles(gpu):
+    """gh_release_cached_memory hands cached blocks back to the driver between
+    solves: live handles keep working and results keep their bits."""
+    from paper_1812_06060_b200 import meshgen
+    gh = gpu
+    w = meshgen.config(3, scale=16)
+    mesh = gh.build_mesh(w.positions, w.faces)
+    lv = gh.bfs_levels(mesh, w.sources)
+    t = w.t if w.t is not None else gh.diffusion_time(mesh, w.m)
+    u1 = gh.gs_diffuse(mesh, lv, t, gh.DiffusionConfig(sweeps=50))
+    d1, _ = gh.distance(lv, "face", 50, t)
+    gh.geoheat.release_cached_memory()
+    u2 = gh.gs_diffuse(mesh, lv, t, gh.DiffusionConfig(sweeps=50))
+    gh.geoheat.release_cached_memory()
+    d2, _ = gh.distance(lv, "face", 50, t)
+    assert_same(u2, u1, "u after a release")
+    assert_same(d2, d1, "distances after a release")
+
+
 def _strip(nx: int, wobble: float = 0.013):
     """A 2 x nx triangle strip (a ladder): a source at one end gives ~nx BFS rings."""
     i = np.arange(nx, dtype=np.float64)
