@@ -386,21 +386,51 @@ __global__ void k_bucket_scatter(const uint64_t* __restrict__ key, const int32_t
   }
 }
 
-__global__ void k_bucket_sort(const int32_t* __restrict__ off, int64_t nb, uint64_t* __restrict__ key,
-                              int32_t* __restrict__ val) {
-  for (int64_t b = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; b < nb; b += (int64_t)gridDim.x * blockDim.x) {
-    const int32_t s = off[b], e = off[b + 1];
-    for (int32_t i = s + 1; i < e; ++i) {  // insertion sort by (key, value)
-      const uint64_t k = key[i];
-      const int32_t v = val[i];
-      int32_t j = i - 1;
-      while (j >= s && (key[j] > k || (key[j] == k && val[j] > v))) {
-        key[j + 1] = key[j];
-        val[j + 1] = val[j];
-        --j;
+// insertion sort of one bucket [s, e) by (key, value)
+template <class K, class V>
+__device__ __forceinline__ void insertion_sort(K* key, V* val, int32_t s, int32_t e) {
+  for (int32_t i = s + 1; i < e; ++i) {
+    const uint64_t k = key[i];
+    const int32_t v = val[i];
+    int32_t j = i - 1;
+    while (j >= s && (key[j] > k || (key[j] == k && val[j] > v))) {
+      key[j + 1] = key[j];
+      val[j + 1] = val[j];
+      --j;
+    }
+    key[j + 1] = k;
+    val[j + 1] = v;
+  }
+}
+
+// A block takes B consecutive buckets: their entries are one contiguous range,
+// staged in shared memory with coalesced loads, each thread insertion-sorts
+// its bucket there, and the range goes back coalesced (a range too large for
+// the stage is sorted in place in global memory).
+constexpr int kStageEntries = 3072;
+__global__ void __launch_bounds__(B) k_bucket_sort(const int32_t* __restrict__ off, int64_t nb,
+                                                   uint64_t* __restrict__ key, int32_t* __restrict__ val) {
+  __shared__ uint64_t sk[kStageEntries];
+  __shared__ int32_t sv[kStageEntries];
+  for (int64_t b0 = (int64_t)blockIdx.x * B; b0 < nb; b0 += (int64_t)gridDim.x * B) {
+    const int64_t b1 = b0 + B < nb ? b0 + B : nb;
+    const int32_t lo = off[b0], hi = off[b1];
+    const int64_t b = b0 + threadIdx.x;
+    if (hi - lo <= kStageEntries) {
+      for (int32_t i = lo + threadIdx.x; i < hi; i += B) {
+        sk[i - lo] = key[i];
+        sv[i - lo] = val[i];
       }
-      key[j + 1] = k;
-      val[j + 1] = v;
+      __syncthreads();
+      if (b < b1) insertion_sort(sk - lo, sv - lo, off[b], off[b + 1]);
+      __syncthreads();
+      for (int32_t i = lo + threadIdx.x; i < hi; i += B) {
+        key[i] = sk[i - lo];
+        val[i] = sv[i - lo];
+      }
+      __syncthreads();
+    } else if (b < b1) {
+      insertion_sort(key, val, off[b], off[b + 1]);
     }
   }
 }
@@ -422,7 +452,7 @@ bool bucket_sort_pairs(const uint64_t* keys, const int32_t* vals, int64_t n, uin
   if (mb > kMaxBucket) return false;
   exclusive_scan(cnt.p, off.p, nb + 1, s);
   k_bucket_scatter<<<gh::grid_for(n), B, 0, s>>>(keys, vals, n, div, off.p, cur.p, keys_out, vals_out);
-  k_bucket_sort<<<gh::grid_for(nb), B, 0, s>>>(off.p, nb, keys_out, vals_out);
+  k_bucket_sort<<<gh::grid_for(nb, B, 148 * 8), B, 0, s>>>(off.p, nb, keys_out, vals_out);
   GH_LAUNCH_CHECK();
   if (offsets_out) GH_CUDA(cudaMemcpyAsync(offsets_out, off.p, sizeof(int32_t) * (nb + 1), cudaMemcpyDeviceToDevice, s));
   return true;
