@@ -149,6 +149,20 @@ __global__ void k_morton_keys(const double* __restrict__ pos, const int32_t* __r
   }
 }
 
+// mean |v - w| over the CSR's (v, w) pairs, scaled down by 2^10 per term to
+// stay within int64 (a locality test of the vertex numbering)
+__global__ void k_index_spread(const int32_t* __restrict__ vv_off, const int32_t* __restrict__ vv_idx, int64_t nv,
+                               unsigned long long* __restrict__ acc) {
+  unsigned long long sum = 0;
+  for (int64_t v = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; v < nv; v += (int64_t)gridDim.x * blockDim.x)
+    for (int32_t i = vv_off[v]; i < vv_off[v + 1]; ++i) {
+      const int64_t d = (int64_t)vv_idx[i] - v;
+      sum += (unsigned long long)((d < 0 ? -d : d) >> 10);
+    }
+  for (int o = 16; o > 0; o >>= 1) sum += __shfl_down_sync(0xffffffffu, sum, o);
+  if ((threadIdx.x & 31) == 0 && sum) atomicAdd(acc, sum);
+}
+
 template <class T>
 T read_scalar(const T* d, cudaStream_t s) {
   T v;
@@ -248,18 +262,31 @@ void bfs_build(gh_levels* L, const int32_t* h_sources, int32_t ns) {
   L->u_orig.alloc(V, s);
   L->u_valid = 0;
   m->launches += 4;
-  // diffusion layout of the whole level range (one band, no ghosts)
-  band_build(L, &L->main, 0, nlev);
   // Rings in vertex-id order are spatially coherent on grid-like numberings;
   // when they are not (ring neighbours scattered over the ring, as with the
   // icosphere's subdivision numbering) no 16-bit column format fits, and the
-  // layout is rebuilt with each ring in Morton order (GH_LAYOUT=id|morton
-  // forces one, for tests).
+  // layout is built with each ring in Morton order (GH_LAYOUT=id|morton
+  // forces one, for tests). A numbering whose neighbours lie on average more
+  // than V/64 apart goes to Morton order directly (config 4: saves building
+  // the id-order layout first); otherwise the id-order layout is tried and
+  // rebuilt in Morton order when no 16-bit format fits.
   const char* lay = getenv("GH_LAYOUT");
   const bool force_morton = lay && std::strcmp(lay, "morton") == 0;
   const bool force_id = lay && std::strcmp(lay, "id") == 0;
+  bool scattered = false;
+  if (!force_id && !force_morton && L->nreach > 0 && m->vv_index.n > 0) {
+    Scratch<unsigned long long> acc(1, s);
+    GH_CUDA(cudaMemsetAsync(acc.p, 0, sizeof(unsigned long long), s));
+    k_index_spread<<<grid_for(V), B, 0, s>>>(m->vv_offset.p, m->vv_index.p, V, acc.p);
+    GH_LAUNCH_CHECK();
+    m->launches++;
+    const double mean = 1024.0 * (double)read_scalar(acc.p, s) / (double)m->vv_index.n;
+    scattered = mean > (double)V / 64.0;
+  }
   L->layout_order.release();
-  if (L->nreach > 0 && (force_morton || (!force_id && L->main.col16_windows == 0))) {
+  // diffusion layout of the whole level range (one band, no ghosts)
+  if (!(scattered || force_morton)) band_build(L, &L->main, 0, nlev);
+  if (L->nreach > 0 && (force_morton || scattered || (!force_id && L->main.col16_windows == 0))) {
     L->layout_order.alloc(V, s);
     {
       Scratch<uint64_t> k0(V, s), k1(V, s);
