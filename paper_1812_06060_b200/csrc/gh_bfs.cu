@@ -96,21 +96,26 @@ __global__ void __launch_bounds__(kBfsBlock) k_bfs(const int32_t* __restrict__ v
 }
 
 // parent(v) = smallest-index neighbour at depth - 1 (bfs.hpp:57-65)
+// (and the edge (parent, v): the CSR entry that found the parent carries it,
+// so integration needs no edge_between search)
 __global__ void k_parent(const int32_t* __restrict__ vv_off, const int32_t* __restrict__ vv_idx,
-                         const int32_t* __restrict__ level, int64_t nv, int32_t* __restrict__ parent,
+                         const int32_t* __restrict__ vv_edge, const int32_t* __restrict__ level, int64_t nv,
+                         int32_t* __restrict__ parent, int32_t* __restrict__ parent_edge,
                          uint32_t* __restrict__ key, int32_t* __restrict__ val, uint32_t unreach_key) {
   for (int64_t v = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; v < nv; v += (int64_t)gridDim.x * blockDim.x) {
     const int32_t L = level[v];
-    int32_t p = -1;
+    int32_t p = -1, pe = -1;
     if (L > 0)
       for (int32_t a = vv_off[v]; a < vv_off[v + 1]; ++a) {
         const int32_t w = vv_idx[a];
         if (level[w] == L - 1) {
           p = w;
+          pe = vv_edge[a];
           break;
         }
       }
     parent[v] = p;
+    parent_edge[v] = pe;
     key[v] = L >= 0 ? (uint32_t)L : unreach_key;
     val[v] = (int32_t)v;
   }
@@ -174,7 +179,8 @@ T read_scalar(const T* d, cudaStream_t s) {
 }  // namespace
 
 uint64_t gh_levels::device_bytes() const {
-  return level.bytes() + parent.bytes() + order.bytes() + offsets.bytes() + u_orig.bytes() + main.device_bytes();
+  return level.bytes() + parent.bytes() + parent_edge.bytes() + order.bytes() + offsets.bytes() + u_orig.bytes() +
+         main.device_bytes();
 }
 
 namespace gh {
@@ -242,7 +248,9 @@ void bfs_build(gh_levels* L, const int32_t* h_sources, int32_t ns) {
   {
     Scratch<uint32_t> k0(V, s), k1(V, s);
     Scratch<int32_t> v1(V, s);
-    k_parent<<<grid_for(V), B, 0, s>>>(m->vv_offset.p, m->vv_index.p, L->level.p, V, L->parent.p, k0.p, L->order.p,
+    L->parent_edge.alloc(V, s);
+    k_parent<<<grid_for(V), B, 0, s>>>(m->vv_offset.p, m->vv_index.p, m->vv_edge.p, L->level.p, V, L->parent.p,
+                                       L->parent_edge.p, k0.p, L->order.p,
                                        (uint32_t)nlev);
     GH_LAUNCH_CHECK();
     int end_bit = 1;

@@ -19,27 +19,16 @@ namespace {
 
 constexpr int B = gh::kBlock;
 
-// edge_between (mesh.hpp:87-93): lower_bound in a's ascending row
-__device__ __forceinline__ int32_t edge_between(const int32_t* __restrict__ off, const int32_t* __restrict__ idx,
-                                                const int32_t* __restrict__ eid, int32_t a, int32_t b) {
-  int32_t lo = off[a], hi = off[a + 1];
-  const int32_t end = hi;
-  while (lo < hi) {
-    const int32_t mid = lo + ((hi - lo) >> 1);
-    if (idx[mid] < b) lo = mid + 1;
-    else hi = mid;
-  }
-  return (lo == end || idx[lo] != b) ? -1 : eid[lo];
-}
-
-// inc(v) for the face method (integrate.hpp:45-56), indexed by BFS position
-__global__ void k_inc_face(const int32_t* __restrict__ order, const int32_t* __restrict__ parent, int64_t b,
-                           int64_t e, const int32_t* __restrict__ off, const int32_t* __restrict__ idx,
-                           const int32_t* __restrict__ eid, const int32_t* __restrict__ edge_he,
-                           const double* __restrict__ pos, const double* __restrict__ g, double* __restrict__ inc) {
+// inc(v) for the face method (integrate.hpp:45-56), indexed by BFS position;
+// e = edge_between(parent, v) (mesh.hpp:87-93) is the edge the BFS recorded
+// with the parent
+__global__ void k_inc_face(const int32_t* __restrict__ order, const int32_t* __restrict__ parent,
+                           const int32_t* __restrict__ parent_edge, int64_t b, int64_t e,
+                           const int32_t* __restrict__ edge_he, const double* __restrict__ pos,
+                           const double* __restrict__ g, double* __restrict__ inc) {
   for (int64_t i = b + blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < e; i += (int64_t)gridDim.x * blockDim.x) {
     const int32_t v = order[i], p = parent[v];
-    const int32_t ed = edge_between(off, idx, eid, p, v);
+    const int32_t ed = parent_edge[v];
     const v3 step = sub(ld3(pos, v), ld3(pos, p));
     double sum = 0.0;
     int count = 0;
@@ -54,13 +43,13 @@ __global__ void k_inc_face(const int32_t* __restrict__ order, const int32_t* __r
 }
 
 // inc(v) for the edge method (integrate.hpp:67-72)
-__global__ void k_inc_edge(const int32_t* __restrict__ order, const int32_t* __restrict__ parent, int64_t b,
-                           int64_t e, const int32_t* __restrict__ off, const int32_t* __restrict__ idx,
-                           const int32_t* __restrict__ eid, const int32_t* __restrict__ edge_v,
-                           const double* __restrict__ x, double* __restrict__ inc) {
+__global__ void k_inc_edge(const int32_t* __restrict__ order, const int32_t* __restrict__ parent,
+                           const int32_t* __restrict__ parent_edge, int64_t b, int64_t e,
+                           const int32_t* __restrict__ edge_v, const double* __restrict__ x,
+                           double* __restrict__ inc) {
   for (int64_t i = b + blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < e; i += (int64_t)gridDim.x * blockDim.x) {
     const int32_t v = order[i], p = parent[v];
-    const int32_t ed = edge_between(off, idx, eid, p, v);
+    const int32_t ed = parent_edge[v];
     const double sigma = edge_v[2 * ed] == p ? 1.0 : -1.0;
     inc[i] = sigma * x[ed];
   }
@@ -132,8 +121,8 @@ void integrate_face_dev(gh_levels* L, const double* d_g, double* d_d) {
   Scratch<double> inc(L->nreach + 1, m->stream);
   const int64_t b = L->h_offsets.size() > 1 ? L->h_offsets[1] : 0, e = L->nreach;
   if (e > b) {
-    k_inc_face<<<grid_for(e - b), B, 0, m->stream>>>(L->order.p, L->parent.p, b, e, m->vv_offset.p, m->vv_index.p,
-                                                     m->vv_edge.p, m->edge_he.p, m->pos.p, d_g, inc.p);
+    k_inc_face<<<grid_for(e - b), B, 0, m->stream>>>(L->order.p, L->parent.p, L->parent_edge.p, b, e, m->edge_he.p,
+                                                     m->pos.p, d_g, inc.p);
     GH_LAUNCH_CHECK();
     m->launches++;
   }
@@ -145,8 +134,8 @@ void integrate_edge_dev(gh_levels* L, const double* d_x, double* d_d) {
   Scratch<double> inc(L->nreach + 1, m->stream);
   const int64_t b = L->h_offsets.size() > 1 ? L->h_offsets[1] : 0, e = L->nreach;
   if (e > b) {
-    k_inc_edge<<<grid_for(e - b), B, 0, m->stream>>>(L->order.p, L->parent.p, b, e, m->vv_offset.p, m->vv_index.p,
-                                                     m->vv_edge.p, m->edge_v.p, d_x, inc.p);
+    k_inc_edge<<<grid_for(e - b), B, 0, m->stream>>>(L->order.p, L->parent.p, L->parent_edge.p, b, e, m->edge_v.p,
+                                                     d_x, inc.p);
     GH_LAUNCH_CHECK();
     m->launches++;
   }

@@ -286,6 +286,7 @@ struct gh_levels {
   int32_t nlev = 0, unreachable = 0, nreach = 0, max_width = 0;
   std::vector<int32_t> h_offsets;  // BFS order ring boundaries (nlev + 1)
   gh::DevBuf<int32_t> level, parent, order, offsets;  // level/parent [V], order [nreach], offsets [nlev+1]
+  gh::DevBuf<int32_t> parent_edge;  // [V] edge id of (parent(v), v), -1 for sources / unreachable
   gh::DevBuf<int32_t> layout_order;  // rings in the diffusion layout's order when not `order` (spatial, see gh_bfs.cu)
   gh::Band main;                                       // the whole level range
   int32_t u_valid = 0;
