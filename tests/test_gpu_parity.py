@@ -528,3 +528,43 @@ def test_more_levels_than_the_shared_table(gpu, port_oracle, nbands):
         X, _ = om.admm_edge(H, 10)
         d, _ = gh.distance(lv, "edge", 37, t)
         assert_same(d, om.integrate_edge(ol, X), "edge-method distances")
+
+
+def test_pageable_and_pinned_uploads_agree(gpu):
+    """Large pageable host arrays go through pinned staging slots filled by host
+    threads (both ways: mesh upload, result download); sizes past the staging
+    threshold and not a multiple of the 16 MiB slot must give the same bits as
+    the pinned path (the driver's async copies)."""
+    import ctypes as C
+    from paper_1812_06060_b200 import geoheat as G, meshgen
+    gh = gpu
+    P, F, S = meshgen.torus(2900, 1500, 1.0, 0.3, 3e-4, 4, 2)  # 104 MB positions and faces, 35 MB distances
+    Fi = np.ascontiguousarray(F, np.int32)
+    n = P.shape[0]
+    assert P.nbytes % (16 << 20) and 8 * n > (32 << 20)
+    L = G._lib.load()
+    mesh_a = gh.build_mesh(P, Fi)  # pageable -> staged
+    pp, pf, pd = C.c_void_p(), C.c_void_p(), C.c_void_p()
+    for ptr, nb in ((pp, P.nbytes), (pf, Fi.nbytes), (pd, 8 * n)):
+        G._check(L.gh_host_alloc(nb, C.byref(ptr)))
+    try:
+        C.memmove(pp, P.ctypes.data, P.nbytes)
+        C.memmove(pf, Fi.ctypes.data, Fi.nbytes)
+        h = C.c_void_p()
+        G._check(L.gh_mesh_create(pp, n, pf, Fi.shape[0], C.byref(h)))
+        mesh_b = G.TriMesh(h)  # pinned -> async copies
+        for name in ("positions", "faces", "vv_weight", "vertex_area", "face_area", "vv_index"):
+            assert np.array_equal(mesh_a.download(name).view(np.uint8), mesh_b.download(name).view(np.uint8)), name
+        del mesh_b
+        # the result into pageable memory (staged) and into pinned memory (async copy)
+        d_page, _ = gh.distance_host(P, Fi, S, "face", 20, None, 1.0)
+        Sa = np.ascontiguousarray(S, np.int32)
+        pcfg = G._pipeline_config("face", 20, None, 1.0, G.AdmmConfig())
+        rr = G.gh_run_report()
+        G._check(L.gh_distance_host(pp, n, pf, Fi.shape[0], Sa.ctypes.data_as(C.c_void_p), Sa.size, C.byref(pcfg), pd,
+                                    C.byref(rr)))
+        d_pin = np.ctypeslib.as_array(C.cast(pd, C.POINTER(C.c_double)), shape=(n,)).copy()
+        assert np.array_equal(d_page.view(np.uint64), d_pin.view(np.uint64))
+    finally:
+        for ptr in (pp, pf, pd):
+            L.gh_host_free(ptr)
