@@ -600,9 +600,9 @@ gh_status gh_gs_diffuse_tol(gh_levels* levels, double t, int32_t sweeps, double 
       const double* start = initial ? cur.p : nullptr;  // the next group's start state (nullptr: u0)
       std::vector<double> hist;
       while (done < sweeps && !converged) {
-        // group size: the first sweeps, then what the E1 decay so far predicts
+        // group size: 32 sweeps first (a stop there wastes little), then what the E1 decay predicts
         // is left to the tolerance (sweeps past the stop are wasted), at most kmax
-        int32_t k = std::min(kmax, 128);
+        int32_t k = std::min(kmax, 32);
         if (hist.size() >= 8) {
           const size_t n = hist.size();
           const double a = std::log(hist[n - 8]), b = std::log(hist[n - 1]);
