@@ -42,12 +42,19 @@ __global__ void k_bfs_seed(const int32_t* __restrict__ vv_off, int32_t* __restri
 // Frontier entries carry their row bounds (read by the claiming thread while
 // its append slot is reserved), so expanding a ring starts at vv_idx.
 constexpr int kBfsBlock = 512;
+constexpr int kBfsStage = 2048;       // claims a block stages per ring before one global append
+constexpr int kBfsStageRing = 12288;  // rings wider than this stage their appends
 __global__ void __launch_bounds__(kBfsBlock) k_bfs(const int32_t* __restrict__ vv_off, const int32_t* __restrict__ vv_idx,
                                                    int32_t* __restrict__ level, int4* __restrict__ fa,
                                                    int4* __restrict__ fb, int32_t* __restrict__ level_size,
                                                    int32_t* __restrict__ out, unsigned* __restrict__ bar) {
   // 8 lanes per frontier vertex, one neighbour each, so a ring costs a few
-  // dependent memory round trips instead of one per neighbour
+  // dependent memory round trips instead of one per neighbour. A block's new
+  // frontier entries are staged in shared memory and appended with one global
+  // atomic per block and ring (a per-warp atomic on the one ring counter
+  // serialised thousands of atomics per ring on wide rings).
+  __shared__ int4 stage[kBfsStage];
+  __shared__ int32_t s_cnt, s_base;
   const int64_t tid = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   const int64_t groups = ((int64_t)gridDim.x * blockDim.x) >> 3;
   const int sub = threadIdx.x & 7, lane = threadIdx.x & 31;
@@ -56,6 +63,13 @@ __global__ void __launch_bounds__(kBfsBlock) k_bfs(const int32_t* __restrict__ v
   int32_t ncur = __ldcg(level_size);
   int32_t depth = 1;
   for (;;) {
+    // wide rings stage (the ring counter's contention dominates there); narrow
+    // ones append per warp (two block barriers per ring cost more than they save)
+    const bool staged = ncur > kBfsStageRing;
+    if (staged) {
+      if (threadIdx.x == 0) s_cnt = 0;
+      __syncthreads();
+    }
     const int64_t rounds = (ncur + groups - 1) / groups;
     for (int64_t k = 0; k < rounds; ++k) {
       const int64_t i = (tid >> 3) + k * groups;
@@ -77,11 +91,36 @@ __global__ void __launch_bounds__(kBfsBlock) k_bfs(const int32_t* __restrict__ v
           w1 = vv_off[w + 1];
         }
         const unsigned mask = __ballot_sync(0xffffffffu, claimed);
-        int32_t base = 0;
-        if (lane == 0 && mask) base = atomicAdd(level_size + depth, __popc(mask));
-        base = __shfl_sync(0xffffffffu, base, 0);
-        if (claimed) nxt[base + __popc(mask & ((1u << lane) - 1u))] = make_int4(w, w0, w1, 0);
+        if (!mask) continue;
+        if (!staged) {
+          int32_t base = 0;
+          if (lane == 0) base = atomicAdd(level_size + depth, __popc(mask));
+          base = __shfl_sync(0xffffffffu, base, 0);
+          if (claimed) nxt[base + __popc(mask & ((1u << lane) - 1u))] = make_int4(w, w0, w1, 0);
+          continue;
+        }
+        int32_t off = 0;
+        if (lane == 0) off = atomicAdd(&s_cnt, __popc(mask));
+        off = __shfl_sync(0xffffffffu, off, 0);
+        const int32_t p = off + __popc(mask & ((1u << lane) - 1u));
+        // past the stage: straight to the global frontier
+        const unsigned spill = __ballot_sync(0xffffffffu, claimed && p >= kBfsStage);
+        int32_t gbase = 0;
+        if (lane == 0 && spill) gbase = atomicAdd(level_size + depth, __popc(spill));
+        gbase = __shfl_sync(0xffffffffu, gbase, 0);
+        if (claimed) {
+          const int4 ent = make_int4(w, w0, w1, 0);
+          if (p < kBfsStage) stage[p] = ent;
+          else nxt[gbase + __popc(spill & ((1u << lane) - 1u))] = ent;
+        }
       }
+    }
+    if (staged) {
+      __syncthreads();
+      const int32_t n = s_cnt < kBfsStage ? s_cnt : kBfsStage;
+      if (threadIdx.x == 0 && n) s_base = atomicAdd(level_size + depth, n);
+      __syncthreads();
+      for (int32_t j = threadIdx.x; j < n; j += blockDim.x) nxt[s_base + j] = stage[j];
     }
     ghd::grid_barrier(bar, (unsigned)(depth - 1));
     const int32_t nn = __ldcg(level_size + depth);
