@@ -135,7 +135,8 @@ def recorded_traffic(workload: str, sweeps: int):
     try:
         with open(path) as f:
             rec = json.load(f)
-        if rec.get("workload") == workload:
+        # the capture is one launch of the same mesh and method ("C3 torus4096x2048 face, ...")
+        if rec.get("workload", "").split(",")[0] == workload.split(",")[0]:
             return float(rec["dram_bytes_per_sweep"]) * sweeps, rec.get("source")
     except (OSError, KeyError, ValueError):
         pass

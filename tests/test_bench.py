@@ -49,3 +49,16 @@ def test_our_arm_line():
     assert e["value"] > 0 and e["h2d_bytes_per_step"] > 0 and e["d2h_bytes_per_step"] > 0
     assert d["gpu_launches"] > 0
     assert {"sm_mhz", "sm_max_mhz", "reasons"} <= set(d["clocks"])
+
+
+def test_recorded_traffic_matches_default_workload():
+    """roofline.traffic: the committed ncu capture (profiles/diffusion_traffic.json) is found
+    for the default bench workload (config 3, face) whatever the sweep / ADMM counts in its label."""
+    import importlib.util
+    spec = importlib.util.spec_from_file_location("bench_mod", os.path.join(ROOT, "bench.py"))
+    b = importlib.util.module_from_spec(spec)
+    spec.loader.exec_module(b)
+    t, src = b.recorded_traffic("C3 torus4096x2048 face, 1000 sweeps, 10 ADMM iters", 1000)
+    assert t is not None and src
+    assert 0.5 * 838860800000 < t < 1.2 * 838860800000  # DRAM bytes per 1000-sweep launch vs algorithmic
+    assert b.recorded_traffic("C2 grid1025 face, 1000 sweeps, 10 ADMM iters", 1000) == (None, None)
