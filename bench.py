@@ -287,6 +287,10 @@ def main():
             # prepares the next solve until every rank's kernel has returned
             barrier(dist)
 
+    # `value` and the roofline are the diffusion kernel's: every vertex update
+    # the metric counts is executed (zero-level truncation, DESIGN.md §3.7,
+    # applies to meshes like configs 4 and 5 and is measured in the e2e leg)
+    gh.set_zero_level_truncation(False)
     launches = 0
     for _ in range(a.warmup):
         one_solve(G.SolverReport())
@@ -305,6 +309,7 @@ def main():
     step_ms_max = max_over_ranks(dist, step_ms, local)
     value = reach * w.sweeps / (step_ms_max * 1e-3)  # total work over all ranks / slowest rank
 
+    gh.set_zero_level_truncation(True)
     peak, peak_src = load_peaks()
     achieved = bytes_per_sweep * w.sweeps / (step_ms * 1e-3) / 1e9
     traffic, traffic_src = recorded_traffic(workload, w.sweeps) if world == 1 else (None, None)
@@ -339,7 +344,11 @@ def main():
             stages = {"build": rr.build_ms, "bfs_layout": rr.bfs_ms, "diffusion": rr.diffusion_ms,
                       "normalize": rr.normalize_ms, "admm": rr.optimization_ms, "integrate": rr.integration_ms,
                       "d2h": rr.d2h_ms}
-            e2e_extra = {"admm_iterations": rr.admm_iterations, "zero_count": rr.zero_count}
+            e2e_extra = {"admm_iterations": rr.admm_iterations, "zero_count": rr.zero_count,
+                         "diffusion": {"row_updates_executed": int(rr.diffusion_row_updates),
+                                       "row_updates_nominal": int(reach) * w.sweeps,
+                                       "active_levels": int(rr.diffusion_active_levels),
+                                       "launches": int(rr.diffusion_launches)}}
         else:
             dt, stages, e2e_extra = sharded_e2e(G, GB, L, w, P, Fc, S, pp, pf, pd, rank, world, local, dist,
                                                 a.partition)
@@ -347,6 +356,23 @@ def main():
             e2e_s.append(dt)
     e2e_sec = max_over_ranks(dist, float(np.mean(e2e_s)), local)
     e2e_value = reach * w.sweeps / e2e_sec
+    # when the diffusion was truncated to the levels the heat reaches (same
+    # bits), also time the call with every level updated
+    full_s = []
+    if world == 1 and e2e_extra.get("diffusion", {}).get("launches", 1) > 1:
+        gh.set_zero_level_truncation(False)
+        for i in range(2):
+            rr = G.gh_run_report()
+            t0 = time.perf_counter()
+            G._check(L.gh_distance_host(pp, P.shape[0], pf, Fc.shape[0], S.ctypes.data_as(C.c_void_p), S.size,
+                                        C.byref(pcfg), pd, C.byref(rr)))
+            full_s.append(time.perf_counter() - t0)
+        gh.set_zero_level_truncation(True)
+        e2e_extra["every_level_seconds"] = min(full_s)
+        e2e_extra["every_level_diffusion_ms"] = rr.diffusion_ms
+        # leave the truncated call's result in pd for the parity hash below
+        G._check(L.gh_distance_host(pp, P.shape[0], pf, Fc.shape[0], S.ctypes.data_as(C.c_void_p), S.size,
+                                    C.byref(pcfg), pd, None))
     # the same call from pageable (numpy) arrays, as the C++ drop-in's
     # geoheat::b200::build_mesh(std::vector...) passes them: H2D from pageable
     # memory inside the timed call

@@ -87,6 +87,12 @@ typedef struct {
   int32_t unreachable_count; /* BfsLevels::unreachable_count    */
   int32_t max_level_width;   /* widest ring                     */
   int32_t column_bits;       /* columns the last gs_diffuse streamed: 16 or 32 (0 before the first) */
+  /* zero-level truncation of the last gs_diffuse (gh_set_zero_level_truncation): */
+  int32_t active_levels;      /* levels its last launch updated; level_count when nothing was truncated */
+  int32_t diffusion_launches; /* pipelined launches it ran (1 without truncation) */
+  int32_t diffusion_retries;  /* launches redone with a larger cap */
+  int32_t reserved_;
+  uint64_t row_updates;       /* vertex updates executed (reachable x sweeps without truncation) */
 } gh_levels_info;
 
 /* AdmmConfig (grad_face.hpp:15-26). */
@@ -159,6 +165,10 @@ typedef struct {
   double diffusion_e1;    /* GH_PIPE_DIFFUSION_E1, else -1 */
   double poisson_residual;/* GH_METHOD_POISSON: final relative residual (reported as final_primal) */
   uint64_t state_bytes_allocated; /* device bytes of the optimiser state (SolverReport field) */
+  /* zero-level truncation of the diffusion (gh_set_zero_level_truncation; gh_levels_info has the same): */
+  uint64_t diffusion_row_updates;   /* vertex updates executed (reachable x sweeps without truncation) */
+  int32_t diffusion_active_levels;  /* levels the last diffusion launch updated */
+  int32_t diffusion_launches;       /* pipelined launches (1 without truncation) */
 } gh_run_report;
 
 /* ---- runtime */
@@ -174,6 +184,14 @@ gh_status gh_host_free(void* p);
    device it has used. Handles stay valid. Call it before other processes need
    the memory (the pool otherwise keeps what a large solve grew to). */
 gh_status gh_release_cached_memory(void);
+/* Zero-level truncation of gs_diffuse (on by default; GH_ZERO_LEVELS=0 in the
+   environment also turns it off). With t ~ h^2 the heat underflows to exactly
+   +0 a few hundred rings from the sources; levels beyond that front provably
+   stay +0, and the solve updates only the levels below a cap that the kernel
+   verifies (a nonzero bit at the cap's top level redoes the launch with a
+   larger cap). The result is the reference's u bit for bit (diffusion.hpp:
+   73-108 evaluated on the levels that can differ from zero); process-wide. */
+gh_status gh_set_zero_level_truncation(int32_t on);
 
 /* ---- mesh: build_mesh (mesh.hpp:113-286), device preprocessing */
 gh_status gh_mesh_create(const double* positions, int32_t nv, const int32_t* faces, int32_t nf, gh_mesh** out);

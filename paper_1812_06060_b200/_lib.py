@@ -21,7 +21,8 @@ class gh_mesh_info(C.Structure):
 
 class gh_levels_info(C.Structure):
     _fields_ = [("level_count", C.c_int32), ("unreachable_count", C.c_int32), ("max_level_width", C.c_int32),
-                ("column_bits", C.c_int32)]
+                ("column_bits", C.c_int32), ("active_levels", C.c_int32), ("diffusion_launches", C.c_int32),
+                ("diffusion_retries", C.c_int32), ("reserved_", C.c_int32), ("row_updates", C.c_uint64)]
 
 
 class gh_admm_config(C.Structure):
@@ -51,7 +52,8 @@ class gh_run_report(C.Structure):
                 ("total_ms", C.c_double), ("h2d_bytes", C.c_uint64), ("d2h_bytes", C.c_uint64),
                 ("solver_state_bytes", C.c_uint64), ("kernel_launches", C.c_int32), ("cg_iterations", C.c_int32),
                 ("diffusion_e1", C.c_double), ("poisson_residual", C.c_double),
-                ("state_bytes_allocated", C.c_uint64)]
+                ("state_bytes_allocated", C.c_uint64), ("diffusion_row_updates", C.c_uint64),
+                ("diffusion_active_levels", C.c_int32), ("diffusion_launches", C.c_int32)]
 
 
 class gh_poisson_report(C.Structure):
@@ -77,6 +79,7 @@ SIGNATURES = [
     ("gh_host_alloc", st, [C.c_size_t, C.POINTER(vp)]),
     ("gh_host_free", st, [vp]),
     ("gh_release_cached_memory", st, []),
+    ("gh_set_zero_level_truncation", st, [C.c_int32]),
     ("gh_mesh_create", st, [vp, i32, vp, i32, C.POINTER(vp)]),
     ("gh_mesh_destroy", st, [vp]),
     ("gh_mesh_get_info", st, [vp, C.POINTER(gh_mesh_info)]),

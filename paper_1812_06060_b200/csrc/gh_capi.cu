@@ -171,6 +171,10 @@ gh_status gh_host_free(void* p) {
   });
 }
 
+gh_status gh_set_zero_level_truncation(int32_t on) {
+  return guarded([&] { gh::set_zero_level_truncation(on != 0); });
+}
+
 gh_status gh_release_cached_memory(void) {
   return guarded([&] {
     int cur = 0, ndev = 0;
@@ -500,6 +504,11 @@ gh_status gh_bfs_get_info(const gh_levels* levels, gh_levels_info* info) {
     info->unreachable_count = levels->unreachable;
     info->max_level_width = levels->max_width;
     info->column_bits = levels->last_col16 ? 16 : levels->u_valid ? 32 : 0;
+    info->active_levels = levels->last_active_levels;
+    info->diffusion_launches = levels->last_launches;
+    info->diffusion_retries = levels->last_retries;
+    info->reserved_ = 0;
+    info->row_updates = levels->last_row_updates;
   });
 }
 
@@ -812,6 +821,9 @@ void distance_on_device(gh_levels* L, const gh_pipeline_config& c, double* d_dis
     rep->final_primal = r.final_primal;
     rep->final_dual = r.final_dual;
     rep->diffusion_ms = diff_ms;
+    rep->diffusion_row_updates = L->last_row_updates;
+    rep->diffusion_active_levels = L->last_active_levels;
+    rep->diffusion_launches = L->last_launches;
     rep->normalize_ms = tn.ms();
     rep->optimization_ms = r.device_ms;
     rep->integration_ms = ti.ms();

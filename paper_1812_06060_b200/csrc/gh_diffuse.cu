@@ -31,6 +31,7 @@
 //    steps and all blocks are co-resident, so the schedule cannot deadlock.
 
 #include <algorithm>
+#include <atomic>
 #include <cstdlib>
 #include <cstring>
 
@@ -139,6 +140,9 @@ struct TmaArgs {
   // sweep of the launch is available afterwards; null otherwise
   double* snap;
   int64_t snap_rows;
+  // zero-level truncation (diffuse_truncated_dev): set to 1 when a row of the
+  // band's top own level (le - 1) gets a value with any bit set; null otherwise
+  int32_t* top_nonzero;
   double t;
 };
 
@@ -670,6 +674,7 @@ __global__ void __launch_bounds__(kTmaThreads, 2) k_diffuse_tma(const __grid_con
             __stcg(vba->lo_ubuf + gh::uidx((uint32_t)(vba->lo_ghost + (r - pstart(Lq[i]))), par), un);
           if (Lq[i] == band_le - 1 && vba->hi_ubuf)
             __stcg(vba->hi_ubuf + gh::uidx((uint32_t)(vba->hi_ghost + (r - pstart(Lq[i]))), par), un);
+          if (Lq[i] == band_le - 1 && a.top_nonzero && __double_as_longlong(un) != 0) *a.top_nonzero = 1;
         }
         if (kSlice && live[i] && vba->xoff) {
           // rows other slices read: into their ghost rows (same sweep parity)
@@ -965,7 +970,8 @@ void bands_prepare(gh_levels* L, std::vector<Band*>& bands, double t, const doub
 
 // Run the bands in one cooperative launch on the current device, blocks split
 // in proportion to their rows, then scatter their own rows to u_orig.
-double bands_launch(gh_levels* L, std::vector<Band*>& bands, double t, int32_t sweeps, double* d_snap) {
+double bands_launch(gh_levels* L, std::vector<Band*>& bands, double t, int32_t sweeps, double* d_snap,
+                    int32_t level_cap, int32_t* d_top_nonzero, bool scatter) {
   gh_mesh* m = L->mesh;
   cudaStream_t s = m->stream;
   int32_t wmax = 1;
@@ -1037,6 +1043,14 @@ double bands_launch(gh_levels* L, std::vector<Band*>& bands, double t, int32_t s
   if (d_snap && nbands != 1) fail(GH_ERR_INTERNAL, "diffusion snapshots need the single band");
   a.snap = d_snap;
   a.snap_rows = bands[0]->nrows;
+  a.top_nonzero = d_top_nonzero;
+  if (level_cap > 0 && level_cap < L->nlev) {
+    // the single band stops below level_cap: that level keeps its (zero) rows
+    // and counts as finished for every sweep (its counter was set to ~0)
+    if (nbands != 1 || slices || bands[0] != &L->main) fail(GH_ERR_INTERNAL, "diffusion: level cap needs the single band");
+    a.bands[0].le = level_cap;
+    a.bands[0].gs_hi = bands[0]->h_pstart[level_cap];
+  }
   // sweep groups: one pipeline of all sweeps unless GH_SWEEP_GROUP=K (then
   // groups of K sweeps, each starting GH_SWEEP_PERIOD steps after the last,
   // at least nlev + 2K - 1 so that the groups never share a step)
@@ -1078,6 +1092,7 @@ double bands_launch(gh_levels* L, std::vector<Band*>& bands, double t, int32_t s
     GH_CUDA(cudaMemcpyAsync(&stalled, b->stalled, sizeof(int32_t), cudaMemcpyDeviceToHost, s));
     GH_CUDA(cudaStreamSynchronize(s));
     if (stalled) fail(GH_ERR_INTERNAL, "diffusion: a band dependency never arrived (neighbour band not running?)");
+    if (!scatter) continue;
     k_scatter<<<grid_for(b->own_rows), B, 0, s>>>(b->perm.p, b->ubuf, (uint32_t)((sweeps - 1) & 1), b->own_rows,
                                                   L->u_orig.p);
     GH_LAUNCH_CHECK();
@@ -1090,9 +1105,244 @@ double bands_launch(gh_levels* L, std::vector<Band*>& bands, double t, int32_t s
 namespace {
 }  // namespace
 
+// ---------------------------------------------------------------- zero-level truncation
+// Far from the sources the heat underflows to exactly +0 and stays there: the
+// update of a row whose neighbours are all +0 is (0 + t * 0) / den = +0 for
+// den > 0, whatever the weights. So if level C - 1 holds only +0 after every
+// sweep, every level >= C stays +0 for all sweeps (induction over levels and
+// sweeps, diffusion.hpp:73-82), and running the pipeline on levels [0, C)
+// alone — level C read as the zeros it holds — gives the reference's u bit for
+// bit. The solve runs in a few launches of an even number of sweeps (so the
+// state is back in the parity buffer a launch starts from): each launch covers
+// the levels below a cap beyond the nonzero front seen so far, the kernel
+// flags any nonzero bit written to the cap's top level, and a flagged launch
+// is undone (saved rows restored) and redone with a larger cap. Only meshes
+// whose first 1024 rings hold less than half the vertices try it (a single
+// source on a large mesh: configs 4 and 5); the others take the plain launch.
+namespace {
+
+std::atomic<int> g_zero_levels{-1};  // -1: from GH_ZERO_LEVELS on first use
+
+__global__ void k_den_nonpositive(const double* __restrict__ den, const int32_t* __restrict__ perm, int64_t nrows,
+                                  int32_t* __restrict__ flag) {
+  for (int64_t r = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; r < nrows; r += (int64_t)gridDim.x * blockDim.x)
+    if (perm[r] >= 0 && !(den[r] > 0.0)) *flag = 1;
+}
+
+// largest level below `cap` with a nonzero value in sweep buffer `parity` (warp per chunk)
+__global__ void k_nonzero_front(const double* __restrict__ ubuf, const int32_t* __restrict__ chunk_level,
+                                int64_t nchunks, int32_t cap, uint32_t parity, int32_t* __restrict__ front) {
+  const int lane = threadIdx.x & 31;
+  const int64_t w0 = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+  const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  int32_t best = -1;
+  for (int64_t c = w0; c < nchunks; c += nw) {
+    const int32_t lv = chunk_level[c];
+    if (lv >= cap || lv <= best) continue;
+    const bool nz = __double_as_longlong(ubuf[gh::uidx((uint32_t)(c * 32 + lane), parity)]) != 0;
+    if (__any_sync(0xffffffffu, nz)) best = lv;
+  }
+  if (lane == 0 && best >= 0) atomicMax(front, best);
+}
+
+// uidx ranges (in doubles) holding both parities of the rows of levels [0, cap): the even and the odd half
+void capped_ranges(const Band& b, int32_t cap, int64_t off[2], int64_t len[2]) {
+  for (int h = 0; h < 2; ++h) {
+    off[h] = len[h] = 0;
+    int32_t top = cap - 1;
+    if ((top & 1) != h) --top;
+    if (top < h) continue;
+    const int64_t r0 = b.h_pstart[h], r1 = ((int64_t)b.h_pend[top] + 31) & ~int64_t(31);
+    off[h] = 2 * r0;
+    len[h] = 2 * (r1 - r0);
+  }
+}
+
+}  // namespace
+
+void set_zero_level_truncation(bool on) { g_zero_levels.store(on ? 1 : 0); }
+bool zero_level_truncation() {
+  int v = g_zero_levels.load();
+  if (v < 0) {
+    const char* e = getenv("GH_ZERO_LEVELS");
+    v = (e && atoi(e) == 0) ? 0 : 1;
+    g_zero_levels.store(v);
+  }
+  return v != 0;
+}
+
+namespace {
+
+// first cap tried (one sweep carries the heat ~500-900 rings before it
+// underflows) and the least margin between the front and the next cap;
+// GH_ZERO_LEVELS_FIRST / GH_ZERO_LEVELS_MARGIN shrink them so tests reach the redo paths
+int32_t cap_first() {
+  const char* e = getenv("GH_ZERO_LEVELS_FIRST");
+  return e && atoi(e) > 1 ? atoi(e) : 1024;
+}
+int32_t margin_min() {
+  const char* e = getenv("GH_ZERO_LEVELS_MARGIN");
+  return e && atoi(e) > 0 ? atoi(e) : 160;
+}
+
+// sweeps in the next launch: short launches first (the front moves fastest
+// early: it advances like sqrt(sweeps)), then half of what is done so far, at
+// least 256; always even unless it is the last one
+int32_t next_group(int32_t done, int32_t sweeps) {
+  static const int32_t plan[] = {2, 14, 48, 192};
+  int32_t acc = 0, k = std::max(256, done / 2);
+  for (int32_t p : plan) {
+    if (done == acc) {
+      k = p;
+      break;
+    }
+    acc += p;
+  }
+  k = std::min(k, sweeps - done);
+  if (k < sweeps - done && (k & 1)) ++k;
+  // a short tail joins this launch
+  if (sweeps - done - k < k / 2) k = sweeps - done;
+  return k;
+}
+
+double diffuse_truncated_dev(gh_levels* L, double t, int32_t sweeps) {
+  gh_mesh* m = L->mesh;
+  cudaStream_t s = m->stream;
+  Band& b = L->main;
+  std::vector<Band*> one{&b};
+  bands_prepare(L, one, t, nullptr);
+  Scratch<int32_t> flags(2, s);  // [0] top level nonzero, [1] front
+  const auto rows_below = [&](int32_t cap) { return (int64_t)L->h_offsets[std::min(cap, L->nlev)]; };
+  const auto dense_enough = [&](int32_t cap) { return cap >= L->nlev || 2 * rows_below(cap) > (int64_t)L->nreach; };
+  EventTimer span(s);
+  span.start();
+  const int32_t mmin = margin_min();
+  const bool trace = getenv("GH_ZERO_LEVELS_TRACE") != nullptr;  // per-launch lines on stderr (tuning)
+  int32_t done = 0, cap = cap_first(), front = -1, margin = mmin, last_k = 0;
+  L->last_launches = L->last_retries = 0;
+  L->last_row_updates = 0;
+  while (done < sweeps) {
+    if (dense_enough(cap)) {
+      // the rest in one plain launch over every level (it continues from the
+      // state in parity buffer 1; the levels never run so far hold zeros)
+      const int32_t k = sweeps - done;
+      if (done) {
+        GH_CUDA(cudaMemsetAsync(b.rows_done, 0, sizeof(unsigned long long) * b.nlev, s));
+        GH_CUDA(cudaMemsetAsync(b.stalled, 0, sizeof(int32_t), s));
+      }
+      bands_launch(L, one, t, k, nullptr, 0, nullptr, false);
+      L->last_launches++;
+      L->last_row_updates += (uint64_t)L->nreach * (uint64_t)k;
+      L->last_active_levels = L->nlev;
+      last_k = k;
+      done = sweeps;
+      break;
+    }
+    const int32_t k = next_group(done, sweeps);
+    // the rows this launch may write, saved for a redo
+    int64_t off[2], len[2];
+    capped_ranges(b, cap, off, len);
+    Scratch<double> saved((size_t)(len[0] + len[1]), s);
+    GH_CUDA(cudaMemcpyAsync(saved.p, b.ubuf + off[0], sizeof(double) * len[0], cudaMemcpyDeviceToDevice, s));
+    GH_CUDA(cudaMemcpyAsync(saved.p + len[0], b.ubuf + off[1], sizeof(double) * len[1], cudaMemcpyDeviceToDevice, s));
+    GH_CUDA(cudaMemsetAsync(b.rows_done, 0, sizeof(unsigned long long) * b.nlev, s));
+    GH_CUDA(cudaMemsetAsync(b.rows_done + cap, 0xff, sizeof(unsigned long long), s));  // level `cap`: done for every sweep
+    GH_CUDA(cudaMemsetAsync(b.stalled, 0, sizeof(int32_t), s));
+    GH_CUDA(cudaMemsetAsync(flags.p, 0, sizeof(int32_t), s));
+    GH_CUDA(cudaMemsetAsync(flags.p + 1, 0xff, sizeof(int32_t), s));
+    const double launch_ms = bands_launch(L, one, t, k, nullptr, cap, flags.p, false);
+    L->last_launches++;
+    L->last_row_updates += (uint64_t)rows_below(cap) * (uint64_t)k;
+    k_nonzero_front<<<grid_for(std::min<int64_t>((int64_t)b.own_chunks * 32, 1 << 22)), B, 0, s>>>(
+        b.ubuf, b.chunk_level.p, b.own_chunks, cap, (uint32_t)((k - 1) & 1), flags.p + 1);
+    GH_LAUNCH_CHECK();
+    m->launches++;
+    int32_t h[2];
+    GH_CUDA(cudaMemcpyAsync(h, flags.p, sizeof(h), cudaMemcpyDeviceToHost, s));
+    GH_CUDA(cudaStreamSynchronize(s));
+    if (trace)
+      fprintf(stderr, "zero_levels: sweeps [%d, %d) cap %d rows %lld front %d flagged %d %.3f ms\n", done, done + k, cap,
+              (long long)rows_below(cap), h[1], h[0], launch_ms);
+    if (h[0]) {
+      // the top level saw a nonzero value: level `cap` would have too. Undo, widen, redo.
+      GH_CUDA(cudaMemcpyAsync(b.ubuf + off[0], saved.p, sizeof(double) * len[0], cudaMemcpyDeviceToDevice, s));
+      GH_CUDA(cudaMemcpyAsync(b.ubuf + off[1], saved.p + len[0], sizeof(double) * len[1], cudaMemcpyDeviceToDevice, s));
+      L->last_retries++;
+      margin *= 2;
+      cap = done == 0 ? (cap > L->nlev / 2 ? L->nlev : 2 * cap) : std::min<int64_t>(L->nlev, (int64_t)cap + margin);
+      continue;
+    }
+    L->last_active_levels = cap;
+    const int32_t grown = front >= 0 ? std::max(0, h[1] - front) : 0;
+    front = h[1];
+    done += k;
+    if (done < sweeps) {
+      // margin for the next launch: the front advances like sqrt(sweeps)
+      // (diffusively), so this launch's growth scaled by the ratio of the
+      // launches' sqrt-spans predicts the next one's; 1.5 x that + 32, at
+      // least margin_min() levels
+      const int32_t kn = next_group(done, sweeps);
+      const double span = std::sqrt((double)done) - std::sqrt((double)(done - k));
+      const double next_span = std::sqrt((double)(done + kn)) - std::sqrt((double)done);
+      const double scaled = 1.5 * (double)grown * next_span / span + 32.0;
+      margin = std::max<int32_t>(mmin, (int32_t)std::min<double>(scaled, 1e9));
+      cap = (int32_t)std::min<int64_t>(L->nlev, std::max<int64_t>(cap, (int64_t)front + 1 + margin));
+    }
+    last_k = k;
+  }
+  span.stop();
+  const double ms = span.ms();
+  k_scatter<<<grid_for(b.own_rows), B, 0, s>>>(b.perm.p, b.ubuf, (uint32_t)((last_k - 1) & 1), b.own_rows, L->u_orig.p);
+  GH_LAUNCH_CHECK();
+  m->launches++;
+  return ms;
+}
+
+}  // namespace
+
 double diffuse_dev(gh_levels* L, double t, int32_t sweeps, const double* d_initial, double* d_snap) {
   std::vector<Band*> one{&L->main};
-  return diffuse_bands_dev(L, one, t, sweeps, d_initial, d_snap);
+  gh_mesh* m = L->mesh;
+  // zero-level truncation: from u0 only (a warm start may be nonzero anywhere),
+  // no snapshots, a mesh whose first rings hold a minority of the vertices,
+  // and every den > 0 (0 / den must be +0)
+  bool truncate = zero_level_truncation() && !d_initial && !d_snap && sweeps >= 2 && t > 0.0 && L->nreach > 0 &&
+                  L->nlev > cap_first() && 2 * (int64_t)L->h_offsets[cap_first()] <= (int64_t)L->nreach &&
+                  !getenv("GH_SWEEP_GROUP") && (int64_t)L->nlev + 2 * (int64_t)sweeps < 0x7fffffffLL;
+  if (truncate) {
+    Band& b = L->main;
+    if (b.den_t != t) {
+      k_den<<<grid_for(b.nrows), B, 0, m->stream>>>(b.area_r.p, b.wsum_r.p, t, b.nrows, b.den.p);
+      GH_LAUNCH_CHECK();
+      m->launches++;
+      b.den_t = t;
+    }
+    if (L->den_positive < 0 || L->den_positive_t != t) {
+      Scratch<int32_t> flag(1, m->stream);
+      GH_CUDA(cudaMemsetAsync(flag.p, 0, sizeof(int32_t), m->stream));
+      k_den_nonpositive<<<grid_for(b.nrows), B, 0, m->stream>>>(b.den.p, b.perm.p, b.nrows, flag.p);
+      GH_LAUNCH_CHECK();
+      m->launches++;
+      L->den_positive = read_scalar(flag.p, m->stream) ? 0 : 1;
+      L->den_positive_t = t;
+    }
+    truncate = L->den_positive == 1;
+  }
+  if (!truncate) {
+    const double ms = diffuse_bands_dev(L, one, t, sweeps, d_initial, d_snap);
+    L->last_active_levels = L->nlev;
+    L->last_launches = sweeps > 0 && L->nreach > 0 ? 1 : 0;
+    L->last_retries = 0;
+    L->last_row_updates = (uint64_t)L->nreach * (uint64_t)std::max(sweeps, 0);
+    return ms;
+  }
+  k_init_orig<<<grid_for(m->nv), B, 0, m->stream>>>(L->level.p, nullptr, m->nv, L->u_orig.p);
+  GH_LAUNCH_CHECK();
+  m->launches++;
+  const double ms = diffuse_truncated_dev(L, t, sweeps);
+  L->u_valid = 1;
+  L->u_sweeps = sweeps;
+  return ms;
 }
 
 double diffuse_bands_dev(gh_levels* L, std::vector<Band*>& bands, double t, int32_t sweeps, const double* d_initial,

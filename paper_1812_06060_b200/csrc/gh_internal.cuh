@@ -292,6 +292,13 @@ struct gh_levels {
   int32_t u_valid = 0;
   int32_t u_sweeps = 0;
   int32_t last_col16 = 0;  // the last diffusion launch streamed 16-bit columns
+  // the last gs_diffuse: levels its last launch updated (nlev when nothing was
+  // truncated), pipelined launches, launches redone after a truncation proved
+  // too tight, and row updates executed (reachable x sweeps without truncation)
+  int32_t last_active_levels = 0, last_launches = 0, last_retries = 0;
+  uint64_t last_row_updates = 0;
+  int32_t den_positive = -1;  // every den of the main band is > 0 for den_positive_t (-1: not checked)
+  double den_positive_t = 0.0;
   gh::DevBuf<double> u_orig;  // last diffusion result, original order [V]
   uint64_t device_bytes() const;
 };
@@ -335,7 +342,13 @@ double diffuse_bands_dev(gh_levels* L, std::vector<Band*>& bands, double t, int3
                          double* d_snap = nullptr);
 // the two halves of diffuse_bands_dev, for bands that live in other processes
 void bands_prepare(gh_levels* L, std::vector<Band*>& bands, double t, const double* d_initial);
-double bands_launch(gh_levels* L, std::vector<Band*>& bands, double t, int32_t sweeps, double* d_snap = nullptr);
+// level_cap in (0, nlev): the single band runs levels [0, level_cap) only;
+// d_top_nonzero is set when a row of its top level gets a nonzero value
+double bands_launch(gh_levels* L, std::vector<Band*>& bands, double t, int32_t sweeps, double* d_snap = nullptr,
+                    int32_t level_cap = 0, int32_t* d_top_nonzero = nullptr, bool scatter = true);
+// zero-level truncation: on by default, GH_ZERO_LEVELS=0 or this switch turn it off
+void set_zero_level_truncation(bool on);
+bool zero_level_truncation();
 // the single band's reachable rows of one snapshot sweep into d_u (original order; unreachable untouched)
 void snapshot_to_orig(gh_levels* L, const double* d_snap_sweep, double* d_u);
 // a band's own rows of u after `sweeps` sweeps -> vertex order

@@ -344,6 +344,15 @@ class BfsLevels:
         _check(self._lib.gh_bfs_get_info(self._h, C.byref(info)))
         return info.column_bits
 
+    @property
+    def diffusion_stats(self) -> dict:
+        """The last gs_diffuse on these levels: levels its last launch updated, launches, launches
+        redone after a too-tight truncation, vertex updates executed."""
+        info = gh_levels_info()
+        _check(self._lib.gh_bfs_get_info(self._h, C.byref(info)))
+        return {"active_levels": info.active_levels, "launches": info.diffusion_launches,
+                "retries": info.diffusion_retries, "row_updates": info.row_updates}
+
     def __del__(self):
         h = getattr(self, "_h", None)
         if h and not _SHUTTING_DOWN[0]:
@@ -568,6 +577,9 @@ class RunReport:
     diffusion_e1: float = -1.0
     poisson_residual: float = 0.0
     state_bytes_allocated: int = 0
+    diffusion_row_updates: int = 0
+    diffusion_active_levels: int = 0
+    diffusion_launches: int = 0
 
 
 _METHODS = {"face": 0, "edge": 1, "poisson": 2}
@@ -713,6 +725,12 @@ def device_count() -> int:
     n = C.c_int32()
     _check(_lib.load().gh_device_count(C.byref(n)))
     return n.value
+
+
+def set_zero_level_truncation(on: bool) -> None:
+    """gs_diffuse updates only the BFS levels the heat can reach before it underflows to +0
+    (bit-identical, verified in the kernel; include/geoheat_b200.h). On by default."""
+    _check(_lib.load().gh_set_zero_level_truncation(1 if on else 0))
 
 
 def release_cached_memory() -> None:

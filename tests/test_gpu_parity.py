@@ -568,3 +568,80 @@ def test_pageable_and_pinned_uploads_agree(gpu):
     finally:
         for ptr in (pp, pf, pd):
             L.gh_host_free(ptr)
+
+
+def _ribbon(nx: int, ny: int, seed: int = 5):
+    """A jittered ny-wide, nx-long triangulated ribbon: a corner source gives ~nx + ny BFS rings of <= ny + 1 vertices."""
+    rng = np.random.default_rng(seed)
+    x, y = np.meshgrid(np.arange(nx, dtype=np.float64), np.arange(ny, dtype=np.float64), indexing="ij")
+    P = np.stack([x, y, 0.05 * np.sin(0.3 * x) * np.cos(0.4 * y)], -1).reshape(-1, 3)
+    P[:, :2] += rng.uniform(-0.2, 0.2, (nx * ny, 2))
+    i, j = np.meshgrid(np.arange(nx - 1), np.arange(ny - 1), indexing="ij")
+    a = (i * ny + j).ravel()
+    b, c, d = a + ny, a + ny + 1, a + 1
+    flip = ((i + j) & 1).ravel().astype(bool)
+    F = np.where(flip[:, None, None], np.stack([np.stack([a, b, d], 1), np.stack([b, c, d], 1)], 1),
+                 np.stack([np.stack([a, b, c], 1), np.stack([a, c, d], 1)], 1)).reshape(-1, 3).astype(np.int32)
+    return P, F
+
+
+@pytest.mark.parametrize("m,expect", [(1.0, "truncated"), (40.0, "widened")])
+def test_zero_level_truncation_bitwise(gpu, port_oracle, m, expect, monkeypatch):
+    """gs_diffuse on a mesh with far more rings than the heat reaches: only the
+    levels below a verified cap are updated, in several launches. u is the oracle's bit for
+    bit, equal to the plain launch's (truncation off), for sweep counts that end inside the
+    first, a middle and the last launch. "widened": a first cap of 128 levels and a margin of
+    8 (the heat reaches ~500 rings in one sweep and ~640 by sweep 71), so the first launch and
+    later ones are undone and redone with larger caps."""
+    gh = gpu
+    if expect == "widened":
+        monkeypatch.setenv("GH_ZERO_LEVELS_FIRST", "128")
+        monkeypatch.setenv("GH_ZERO_LEVELS_MARGIN", "8")
+    P, F = _ribbon(3000, 12)
+    src = np.array([0], np.int32)
+    mesh = gh.build_mesh(P, F)
+    lv = gh.bfs_levels(mesh, src)
+    reach = P.shape[0]
+    assert lv.level_count() > 2500
+    om = port_oracle.build_mesh(P, F)
+    ol = om.bfs(src)
+    t = om.diffusion_time(m)
+    seen_retry = False
+    for sweeps in (2, 3, 16, 71):
+        want, _ = om.gs_diffuse(ol, t, sweeps)
+        got = gh.gs_diffuse(mesh, lv, t, gh.DiffusionConfig(sweeps=sweeps))
+        st = lv.diffusion_stats
+        assert_same(got, want, f"u after {sweeps} sweeps (m = {m}), {st}")
+        gh.set_zero_level_truncation(False)
+        try:
+            plain = gh.gs_diffuse(mesh, lv, t, gh.DiffusionConfig(sweeps=sweeps))
+            sp = lv.diffusion_stats
+        finally:
+            gh.set_zero_level_truncation(True)
+        assert_same(plain, want, f"plain launch, {sweeps} sweeps")
+        assert sp == {"active_levels": lv.level_count(), "launches": 1, "retries": 0, "row_updates": reach * sweeps}
+        seen_retry |= st["retries"] > 0
+        if expect == "truncated":
+            assert st["retries"] == 0 and st["active_levels"] < lv.level_count(), st
+            assert st["row_updates"] < reach * sweeps // 2, st
+            assert st["launches"] == {2: 1, 3: 2, 16: 2, 71: 3}[sweeps], st
+            # every value past the last launch's cap is +0
+            far = lv.level_of_vertex >= st["active_levels"]
+            assert far.any() and not got.view(np.uint64)[far].any()
+        else:
+            assert st["retries"] >= 2, st  # 128 -> 256 -> 512 in the first launch alone
+    if expect == "widened":
+        assert seen_retry
+    # the chain behind it: same distances with and without truncation
+    d1, _ = gh.distance(lv, "face", 16, t)
+    gh.set_zero_level_truncation(False)
+    try:
+        d0, _ = gh.distance(lv, "face", 16, t)
+    finally:
+        gh.set_zero_level_truncation(True)
+    assert_same(d1, d0, "distances with and without truncation")
+    # a warm start may be nonzero anywhere: the plain launch
+    u1 = gh.gs_diffuse(mesh, lv, t, gh.DiffusionConfig(sweeps=4), initial=want)
+    assert lv.diffusion_stats["launches"] == 1 and lv.diffusion_stats["active_levels"] == lv.level_count()
+    w1, _ = om.gs_diffuse(ol, t, 4, initial=want)
+    assert_same(u1, w1, "warm start")

@@ -41,7 +41,9 @@ for it in range(repeats):
                iteration=it, wall_s=wall, t=rr.t, build_ms=rr.build_ms, bfs_ms=rr.bfs_ms, diffusion_ms=rr.diffusion_ms,
                normalize_ms=rr.normalize_ms, admm_ms=rr.optimization_ms, integrate_ms=rr.integration_ms,
                admm_iterations=rr.admm_iterations, converged=bool(rr.converged), zero_count=rr.zero_count,
-               vertex_updates_per_s=P.shape[0] * sweeps / (rr.diffusion_ms * 1e-3),
+               vertex_updates_per_s=int(rr.diffusion_row_updates) / (rr.diffusion_ms * 1e-3),  # executed
+               row_updates_executed=int(rr.diffusion_row_updates), row_updates_nominal=int(P.shape[0]) * sweeps,
+               diffusion_active_levels=int(rr.diffusion_active_levels), diffusion_launches=int(rr.diffusion_launches),
                finite=int(fin.sum()), d_max=float(d[fin].max()), hash=f"{hashes[-1]:016x}", meshgen_s=gen_s)
     print(json.dumps(out), flush=True)
 print(json.dumps({"deterministic": len(set(hashes)) == 1}))
