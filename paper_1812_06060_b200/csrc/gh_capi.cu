@@ -799,15 +799,21 @@ void distance_on_device(gh_levels* L, const gh_pipeline_config& c, double* d_dis
   const int32_t zc = gh::normalize_dev(m, L->u_orig.p, H.p);
   tn.stop();
   gh::AdmmResult r;
+  // elements that provably stay +0 through the optimisation are skipped (gh_grad.cu)
+  const int32_t bound = gh::admm_active_level(L, H.p, c.admm.max_iterations);
+  const bool skip = bound >= 0;
+  gh::Scratch<uint8_t> act_f(skip ? (size_t)m->nf : 0, s);
+  gh::Scratch<uint8_t> act_e(skip ? (size_t)(c.method == GH_METHOD_FACE ? m->ni : m->ne) : 0, s);
+  if (skip) gh::admm_active_flags(L, bound, c.method == GH_METHOD_FACE, act_f.p, act_e.p);
   if (c.method == GH_METHOD_FACE) {
     gh::Scratch<double> G(3 * (size_t)m->nf, s);
-    r = gh::admm_face_dev(m, H.p, c.admm, G.p);
+    r = gh::admm_face_dev(m, H.p, c.admm, G.p, act_f.p, act_e.p);
     ti.start();
     gh::integrate_face_dev(L, G.p, d_dist);
     ti.stop();
   } else {
     gh::Scratch<double> X(m->ne, s);
-    r = gh::admm_edge_dev(m, H.p, c.admm, X.p);
+    r = gh::admm_edge_dev(m, H.p, c.admm, X.p, act_f.p, act_e.p);
     ti.start();
     gh::integrate_edge_dev(L, X.p, d_dist);
     ti.stop();

@@ -1126,7 +1126,8 @@ std::atomic<int> g_zero_levels{-1};  // -1: from GH_ZERO_LEVELS on first use
 __global__ void k_den_nonpositive(const double* __restrict__ den, const int32_t* __restrict__ perm, int64_t nrows,
                                   int32_t* __restrict__ flag) {
   for (int64_t r = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; r < nrows; r += (int64_t)gridDim.x * blockDim.x)
-    if (perm[r] >= 0 && !(den[r] > 0.0)) *flag = 1;
+    // finite and positive: then every weight of the row is finite too (den = A + t * their sum)
+    if (perm[r] >= 0 && !(den[r] > 0.0 && den[r] < INFINITY)) *flag = 1;
 }
 
 // largest level below `cap` with a nonzero value in sweep buffer `parity` (warp per chunk)
@@ -1226,10 +1227,9 @@ double diffuse_truncated_dev(gh_levels* L, double t, int32_t sweeps) {
       // the rest in one plain launch over every level (it continues from the
       // state in parity buffer 1; the levels never run so far hold zeros)
       const int32_t k = sweeps - done;
-      if (done) {
-        GH_CUDA(cudaMemsetAsync(b.rows_done, 0, sizeof(unsigned long long) * b.nlev, s));
-        GH_CUDA(cudaMemsetAsync(b.stalled, 0, sizeof(int32_t), s));
-      }
+      // (counters: earlier launches, also undone ones, left theirs)
+      GH_CUDA(cudaMemsetAsync(b.rows_done, 0, sizeof(unsigned long long) * b.nlev, s));
+      GH_CUDA(cudaMemsetAsync(b.stalled, 0, sizeof(int32_t), s));
       bands_launch(L, one, t, k, nullptr, 0, nullptr, false);
       L->last_launches++;
       L->last_row_updates += (uint64_t)L->nreach * (uint64_t)k;
@@ -1305,7 +1305,7 @@ double diffuse_dev(gh_levels* L, double t, int32_t sweeps, const double* d_initi
   gh_mesh* m = L->mesh;
   // zero-level truncation: from u0 only (a warm start may be nonzero anywhere),
   // no snapshots, a mesh whose first rings hold a minority of the vertices,
-  // and every den > 0 (0 / den must be +0)
+  // and every den finite and > 0 (w * 0 must be a zero and 0 / den must be +0)
   bool truncate = zero_level_truncation() && !d_initial && !d_snap && sweeps >= 2 && t > 0.0 && L->nreach > 0 &&
                   L->nlev > cap_first() && 2 * (int64_t)L->h_offsets[cap_first()] <= (int64_t)L->nreach &&
                   !getenv("GH_SWEEP_GROUP") && (int64_t)L->nlev + 2 * (int64_t)sweeps < 0x7fffffffLL;

@@ -109,21 +109,23 @@ __global__ void k_face_init_edges(const double* __restrict__ pos, const int32_t*
                                   const double* __restrict__ area, const double* __restrict__ h, int64_t ni,
                                   double mu, const double* __restrict__ sa, double* __restrict__ edir,
                                   int32_t* __restrict__ ef, double* __restrict__ wq, double* __restrict__ lam,
-                                  double* __restrict__ C, double* __restrict__ part, double* __restrict__ term) {
+                                  double* __restrict__ C, double* __restrict__ part, double* __restrict__ term,
+                                  const uint8_t* __restrict__ act) {
   double s = 0.0;
   GRID_STRIDE(i, ni) {
     const int32_t e = interior_edges[i];
-    st3(edir, i, normalized(sub(ld3(pos, edge_v[2 * e + 1]), ld3(pos, edge_v[2 * e]))));
     const int32_t f1 = edge_he[2 * e] / 3, f2 = edge_he[2 * e + 1] / 3;
+    const double a1 = area[f1], a2 = area[f2];
+    const double tt = a1 + a2;  // scale2 += A1 + A2 (grad_face.hpp:83)
+    term[i] = tt;
+    s += tt;
+    if (act && !act[i]) continue;  // an edge that stays zero: only its scale term (lambda, c were zeroed)
+    st3(edir, i, normalized(sub(ld3(pos, edge_v[2 * e + 1]), ld3(pos, edge_v[2 * e]))));
     ef[2 * i] = f1;
     ef[2 * i + 1] = f2;
     const v3 zero = mk(0.0, 0.0, 0.0);
     st3(lam, 2 * i, zero);
     st3(lam, 2 * i + 1, zero);
-    const double a1 = area[f1], a2 = area[f2];
-    const double tt = a1 + a2;  // scale2 += A1 + A2 (grad_face.hpp:83)
-    term[i] = tt;
-    s += tt;
     const double w1 = ddiv(a2, a1 + a2), w2 = ddiv(a1, a1 + a2);  // y_update_edge (grad_face.hpp:35)
     wq[2 * i] = w1;
     wq[2 * i + 1] = w2;
@@ -149,10 +151,12 @@ __global__ void k_face_init_edges(const double* __restrict__ pos, const int32_t*
 __global__ void k_face_g(const int32_t* __restrict__ slot, const double* __restrict__ area,
                          const double* __restrict__ h, const double* __restrict__ C, int64_t nf, double mu,
                          const double* __restrict__ gin, double* __restrict__ gout, double* __restrict__ part,
-                         double* __restrict__ term, const int32_t* __restrict__ halt) {
+                         double* __restrict__ term, const int32_t* __restrict__ halt,
+                         const uint8_t* __restrict__ act) {
   if (*halt) return;  // the device stop rule ended the loop (see admm_loop)
   double s = 0.0;
   GRID_STRIDE(f, nf) {
+    if (act && !act[f]) continue;  // g stays +0 here (both buffers hold it), its dual term 0
     const double A = area[f];
     v3 sum = mk(0.0, 0.0, 0.0);
     int count = 0;
@@ -207,7 +211,8 @@ __global__ void __launch_bounds__(B, 4) k_face_lambda_pair(const int32_t* __rest
                                                         const double* __restrict__ edir, int64_t ni, double mu,
                                                         double* __restrict__ C, double* __restrict__ lam,
                                                         double* __restrict__ part, double* __restrict__ term,
-                                                        const int32_t* __restrict__ halt) {
+                                                        const int32_t* __restrict__ halt,
+                                                        const uint8_t* __restrict__ act) {
   if (*halt) return;
   double s = 0.0;
   const int side = threadIdx.x & 1;
@@ -215,8 +220,9 @@ __global__ void __launch_bounds__(B, 4) k_face_lambda_pair(const int32_t* __rest
   // the whole warp steps together (the pair shuffles need every lane)
   for (int64_t k0 = blockIdx.x * (int64_t)blockDim.x + (threadIdx.x & ~31); k0 < n; k0 += stride) {
     const int64_t k = k0 + (threadIdx.x & 31);
-    const bool valid = k < n;  // n even: both lanes of a pair agree
     const int64_t i = k >> 1;
+    // n even: both lanes of a pair agree; an edge that stays zero is skipped (lambda, c, term keep their 0)
+    const bool valid = k < n && (!act || act[i]);
     const int32_t f = valid ? ef[k] : 0;
     const double sf = valid ? sa[f] : 1.0;
     const double m = mu * sf, w = valid ? wq[k] : 0.0;
@@ -254,8 +260,10 @@ __global__ void __launch_bounds__(B, 4) k_face_lambda_pair(const int32_t* __rest
 __global__ void k_edge_init_faces(const double* __restrict__ pos, const int32_t* __restrict__ faces,
                                   const int32_t* __restrict__ he_edge, const int32_t* __restrict__ edge_v,
                                   const double* __restrict__ h, int64_t nf, double* __restrict__ w,
-                                  double* __restrict__ lam, int8_t* __restrict__ sgn) {
+                                  double* __restrict__ lam, int8_t* __restrict__ sgn,
+                                  const uint8_t* __restrict__ act) {
   GRID_STRIDE(f, nf) {
+    if (act && !act[f]) continue;  // w, lambda were zeroed
     const v3 hf = ld3(h, f);
     for (int k = 0; k < 3; ++k) {
       const int64_t hh = 3 * f + k;
@@ -270,8 +278,10 @@ __global__ void k_edge_init_faces(const double* __restrict__ pos, const int32_t*
 
 // target_sum in ascending halfedge order from 0.0; x = target_sum / deg (85-93)
 __global__ void k_edge_init_edges(const int32_t* __restrict__ edge_he, const double* __restrict__ z, int64_t ne,
-                                  double* __restrict__ tsum, double* __restrict__ x) {
+                                  double* __restrict__ tsum, double* __restrict__ x,
+                                  const uint8_t* __restrict__ act) {
   GRID_STRIDE(e, ne) {
+    if (act && !act[e]) continue;  // x was zeroed
     int32_t h0 = edge_he[2 * e], h1 = edge_he[2 * e + 1];
     if (h0 >= 0 && h1 >= 0 && h1 < h0) {
       const int32_t t = h0;
@@ -308,8 +318,9 @@ __device__ __forceinline__ void edge_w_update(int64_t f, const int32_t* __restri
 
 __global__ void k_edge_first_w(const int32_t* __restrict__ he_edge, const double* __restrict__ x,
                                const double* __restrict__ lam, const int8_t* __restrict__ sgn, int64_t nf, double mu,
-                               double* __restrict__ w) {
+                               double* __restrict__ w, const uint8_t* __restrict__ act) {
   GRID_STRIDE(f, nf) {
+    if (act && !act[f]) continue;
     const double l[3] = {lam[3 * f], lam[3 * f + 1], lam[3 * f + 2]};
     edge_w_update(f, he_edge, x, l, sgn, mu, w);
   }
@@ -319,10 +330,11 @@ __global__ void k_edge_first_w(const int32_t* __restrict__ he_edge, const double
 __global__ void k_edge_x(const int32_t* __restrict__ edge_he, const double* __restrict__ tsum,
                          const double* __restrict__ lam, const double* __restrict__ w, int64_t ne, double mu,
                          double* __restrict__ x, double* __restrict__ part, double* __restrict__ term,
-                         const int32_t* __restrict__ halt) {
+                         const int32_t* __restrict__ halt, const uint8_t* __restrict__ act) {
   if (*halt) return;
   double s = 0.0;
   GRID_STRIDE(e, ne) {
+    if (act && !act[e]) continue;
     const double xold = x[e];
     double sum = tsum[e];
     const int32_t h0 = edge_he[2 * e], h1 = edge_he[2 * e + 1];
@@ -344,10 +356,11 @@ __global__ void k_edge_x(const int32_t* __restrict__ edge_he, const double* __re
 __global__ void k_edge_lambda_w(const int32_t* __restrict__ he_edge, const double* __restrict__ x,
                                 const int8_t* __restrict__ sgn, int64_t nf, double mu, double* __restrict__ w,
                                 double* __restrict__ lam, double* __restrict__ part, double* __restrict__ term,
-                                const int32_t* __restrict__ halt) {
+                                const int32_t* __restrict__ halt, const uint8_t* __restrict__ act) {
   if (*halt) return;
   double s = 0.0;
   GRID_STRIDE(f, nf) {
+    if (act && !act[f]) continue;
     double l[3], rs = 0.0;
     for (int k = 0; k < 3; ++k) {
       const int64_t hh = 3 * f + k;
@@ -543,7 +556,99 @@ void admm_loop(gh_mesh* m, AdmmResult& res, const gh_admm_config& cfg, double sc
 
 }  // namespace
 
-AdmmResult admm_face_dev(gh_mesh* m, const double* d_h, const gh_admm_config& cfg, double* d_g) {
+// ---------------------------------------------------------------- zero skipping
+// The targets H are exactly +0 on every face whose heat gradient is below
+// 1e-20 (diffusion.hpp:138-143) — all but the faces within ~100-150 rings of
+// the sources at t = h^2. Both optimisers keep +0 where everything around is
+// +0 (every update is a sum/difference/product/quotient of +0 operands with
+// positive divisors: grad_face.hpp:31-36, 126-168; grad_edge.hpp:131-158), and a
+// nonzero value moves by one face per iteration. With D(f) = the least BFS
+// level of f's vertices (neighbouring faces differ by at most 1 in D), a face
+// can differ from +0 after k iterations only if D(f) <= D_H + k, D_H = the
+// largest D of a face with a nonzero target; an edge only if the lower level
+// of its end points is <= D_H + k + 1. Elements past those bounds (+1 to
+// spare) are skipped: their state is zero-filled once and their residual terms
+// are 0, which a sum does not see.
+namespace {
+
+__global__ void k_target_front(const double* __restrict__ h, const int32_t* __restrict__ faces,
+                               const int32_t* __restrict__ level, int64_t nf, int32_t* __restrict__ front) {
+  int32_t best = -1;
+  GRID_STRIDE(f, nf) {
+    const v3 hf = ld3(h, f);
+    if ((__double_as_longlong(hf.x) | __double_as_longlong(hf.y) | __double_as_longlong(hf.z)) == 0) continue;
+    int32_t d = 0x7fffffff;
+    for (int k = 0; k < 3; ++k) {
+      const int32_t l = level[faces[3 * f + k]];
+      d = l >= 0 && l < d ? l : d;
+    }
+    // a nonzero target on an unreachable face cannot happen (u = 0 there); if it did, every level is active
+    best = d == 0x7fffffff ? 0x7ffffff0 : (d > best ? d : best);
+  }
+  for (int o = 16; o > 0; o >>= 1) {
+    const int32_t other = __shfl_down_sync(0xffffffffu, best, o);
+    best = other > best ? other : best;
+  }
+  if ((threadIdx.x & 31) == 0 && best >= 0) atomicMax(front, best);
+}
+
+__global__ void k_active_faces(const int32_t* __restrict__ faces, const int32_t* __restrict__ level, int64_t nf,
+                               int32_t bound, uint8_t* __restrict__ act) {
+  GRID_STRIDE(f, nf) {
+    bool on = false;
+    for (int k = 0; k < 3; ++k) {
+      const int32_t l = level[faces[3 * f + k]];
+      on = on || (l >= 0 && l <= bound);
+    }
+    act[f] = on ? 1 : 0;
+  }
+}
+
+// list == null: act[e] for every edge e; else act[i] for interior edge i = list[i]
+__global__ void k_active_edges(const int32_t* __restrict__ list, const int32_t* __restrict__ edge_v,
+                               const int32_t* __restrict__ level, int64_t n, int32_t bound, uint8_t* __restrict__ act) {
+  GRID_STRIDE(i, n) {
+    const int64_t e = list ? list[i] : i;
+    const int32_t la = level[edge_v[2 * e]], lb = level[edge_v[2 * e + 1]];
+    act[i] = ((la >= 0 && la <= bound) || (lb >= 0 && lb <= bound)) ? 1 : 0;
+  }
+}
+
+}  // namespace
+
+int32_t admm_active_level(gh_levels* L, const double* d_h, int32_t iterations) {
+  gh_mesh* m = L->mesh;
+  if (!zero_level_truncation() || iterations <= 0 || !m->nf || L->nreach <= 0) return -1;
+  cudaStream_t s = m->stream;
+  Scratch<int32_t> front(1, s);
+  GH_CUDA(cudaMemsetAsync(front.p, 0xff, sizeof(int32_t), s));
+  k_target_front<<<G, B, 0, s>>>(d_h, m->faces.p, L->level.p, m->nf, front.p);
+  GH_LAUNCH_CHECK();
+  m->launches++;
+  int32_t dh = -1;
+  GH_CUDA(cudaMemcpyAsync(&dh, front.p, sizeof(int32_t), cudaMemcpyDeviceToHost, s));
+  GH_CUDA(cudaStreamSynchronize(s));
+  const int64_t bound = (int64_t)dh + iterations + 1;
+  // worth it when the levels past the edges' bound hold at least 30 % of the vertices
+  const int64_t lim = bound + 2;
+  if (lim >= L->nlev || 10 * (int64_t)L->h_offsets[lim] > 7 * (int64_t)L->nreach) return -1;
+  return (int32_t)bound;
+}
+
+void admm_active_flags(gh_levels* L, int32_t level_bound, bool interior_edges, uint8_t* act_f, uint8_t* act_e) {
+  gh_mesh* m = L->mesh;
+  cudaStream_t s = m->stream;
+  k_active_faces<<<G, B, 0, s>>>(m->faces.p, L->level.p, m->nf, level_bound, act_f);
+  const int64_t n = interior_edges ? m->ni : m->ne;
+  if (n)
+    k_active_edges<<<G, B, 0, s>>>(interior_edges ? m->interior_edges.p : nullptr, m->edge_v.p, L->level.p, n,
+                                   level_bound + 1, act_e);
+  GH_LAUNCH_CHECK();
+  m->launches += 2;
+}
+
+AdmmResult admm_face_dev(gh_mesh* m, const double* d_h, const gh_admm_config& cfg, double* d_g, const uint8_t* act_f,
+                         const uint8_t* act_e) {
   validate(cfg);
   cudaStream_t s = m->stream;
   const int64_t F = m->nf, NI = m->ni;
@@ -566,20 +671,28 @@ AdmmResult admm_face_dev(gh_mesh* m, const double* d_h, const gh_admm_config& cf
   Scratch<double> term_p(NI + 1, s), term_d(F + 1, s);  // per-element residual terms
   Scratch<double> sa(F + 1, s), wq(2 * NI + 2, s);  // per-solve constants (face_y_update)
   if (F) k_face_consts<<<G, B, 0, s>>>(m->face_area.p, F, sa.p);
+  if (act_e) {
+    // edges outside the active set (admm_active_level) keep lambda = c = +0 for
+    // the whole solve, as in the reference; their terms stay 0 in both sums
+    GH_CUDA(cudaMemsetAsync(lam.p, 0, sizeof(double) * 6 * NI, s));
+    GH_CUDA(cudaMemsetAsync(Cs.p, 0, sizeof(double) * 6 * NI, s));
+    GH_CUDA(cudaMemsetAsync(term_d.p, 0, sizeof(double) * F, s));
+  }
   k_face_init_edges<<<G, B, 0, s>>>(m->pos.p, m->interior_edges.p, m->edge_v.p, m->edge_he.p, m->face_area.p, d_h,
                                     NI, mu, sa.p, edir.p, ef.p, wq.p, lam.p,
-                                    cfg.max_iterations > 0 ? Cs.p : nullptr, part_primal, term_p.p);
+                                    cfg.max_iterations > 0 ? Cs.p : nullptr, part_primal, term_p.p, act_e);
   GH_LAUNCH_CHECK();
   m->launches += 3;
   // ||M||_F (grad_face.hpp:85): the reference's left-to-right sum, exactly
   const double scale = std::sqrt(sequential_sum_nonneg(term_p.p, NI, s, &m->launches));
+  if (act_e) GH_CUDA(cudaMemsetAsync(term_p.p, 0, sizeof(double) * NI, s));  // from here on: primal terms
   // grad_face.hpp:175-177
   admm_loop(m, res, cfg, scale, mu, term_p.p, NI, term_d.p, F, [&](int32_t it, const int32_t* halt) {
     const double* gin = gbuf[(it + 1) & 1];
     double* gout = gbuf[it & 1];
-    k_face_g<<<G, B, 0, s>>>(slot.p, m->face_area.p, d_h, Cs.p, F, mu, gin, gout, part_dual, term_d.p, halt);
+    k_face_g<<<G, B, 0, s>>>(slot.p, m->face_area.p, d_h, Cs.p, F, mu, gin, gout, part_dual, term_d.p, halt, act_f);
     k_face_lambda_pair<<<G, B, 0, s>>>(ef.p, sa.p, wq.p, gin, gout, edir.p, NI, mu, Cs.p, lam.p, part_primal,
-                                       term_p.p, halt);
+                                       term_p.p, halt, act_e);
   });
   // the last iteration's g: odd iterations wrote gtmp
   if (res.iterations > 0 && ((res.iterations - 1) & 1))
@@ -589,7 +702,8 @@ AdmmResult admm_face_dev(gh_mesh* m, const double* d_h, const gh_admm_config& cf
   return res;
 }
 
-AdmmResult admm_edge_dev(gh_mesh* m, const double* d_h, const gh_admm_config& cfg, double* d_x) {
+AdmmResult admm_edge_dev(gh_mesh* m, const double* d_h, const gh_admm_config& cfg, double* d_x, const uint8_t* act_f,
+                         const uint8_t* act_e) {
   validate(cfg);
   cudaStream_t s = m->stream;
   const int64_t F = m->nf, E = m->ne;
@@ -603,20 +717,31 @@ AdmmResult admm_edge_dev(gh_mesh* m, const double* d_h, const gh_admm_config& cf
   const double scale = std::sqrt(3.0 * (double)F);  // ||R||_F (grad_edge.hpp:79)
   EventTimer timer(s);
   timer.start();
-  if (F) k_edge_init_faces<<<G, B, 0, s>>>(m->pos.p, m->faces.p, m->he_edge.p, m->edge_v.p, d_h, F, w.p, lam.p, sgn.p);
-  if (E) k_edge_init_edges<<<G, B, 0, s>>>(m->edge_he.p, w.p, E, tsum.p, d_x);
+  Scratch<double> term_p(F + 1, s), term_d(E + 1, s);  // per-element residual terms
+  if (act_f) {
+    // faces and edges outside the active set (admm_active_level) keep w = lambda
+    // = x = +0 for the whole solve, as in the reference (an active edge next to
+    // such a face reads those zeros), and their terms stay 0 in both sums
+    GH_CUDA(cudaMemsetAsync(w.p, 0, sizeof(double) * 3 * F, s));
+    GH_CUDA(cudaMemsetAsync(lam.p, 0, sizeof(double) * 3 * F, s));
+    GH_CUDA(cudaMemsetAsync(d_x, 0, sizeof(double) * E, s));
+    GH_CUDA(cudaMemsetAsync(term_p.p, 0, sizeof(double) * F, s));
+    GH_CUDA(cudaMemsetAsync(term_d.p, 0, sizeof(double) * E, s));
+  }
+  if (F)
+    k_edge_init_faces<<<G, B, 0, s>>>(m->pos.p, m->faces.p, m->he_edge.p, m->edge_v.p, d_h, F, w.p, lam.p, sgn.p, act_f);
+  if (E) k_edge_init_edges<<<G, B, 0, s>>>(m->edge_he.p, w.p, E, tsum.p, d_x, act_e);
   GH_LAUNCH_CHECK();
   m->launches += 2;
   if (cfg.max_iterations > 0 && F) {
-    k_edge_first_w<<<G, B, 0, s>>>(m->he_edge.p, d_x, lam.p, sgn.p, F, mu, w.p);
+    k_edge_first_w<<<G, B, 0, s>>>(m->he_edge.p, d_x, lam.p, sgn.p, F, mu, w.p, act_f);
     GH_LAUNCH_CHECK();
     m->launches++;
   }
-  Scratch<double> term_p(F + 1, s), term_d(E + 1, s);  // per-element residual terms
   // grad_edge.hpp:168-170
   admm_loop(m, res, cfg, scale, mu, term_p.p, F, term_d.p, E, [&](int32_t, const int32_t* halt) {
-    k_edge_x<<<G, B, 0, s>>>(m->edge_he.p, tsum.p, lam.p, w.p, E, mu, d_x, part_dual, term_d.p, halt);
-    k_edge_lambda_w<<<G, B, 0, s>>>(m->he_edge.p, d_x, sgn.p, F, mu, w.p, lam.p, part_primal, term_p.p, halt);
+    k_edge_x<<<G, B, 0, s>>>(m->edge_he.p, tsum.p, lam.p, w.p, E, mu, d_x, part_dual, term_d.p, halt, act_e);
+    k_edge_lambda_w<<<G, B, 0, s>>>(m->he_edge.p, d_x, sgn.p, F, mu, w.p, lam.p, part_primal, term_p.p, halt, act_f);
   });
   timer.stop();
   res.device_ms = timer.ms();

@@ -375,8 +375,19 @@ struct AdmmResult {
   uint64_t state_bytes = 0;
   double device_ms = 0;
 };
-AdmmResult admm_face_dev(gh_mesh* m, const double* d_h, const gh_admm_config& cfg, double* d_g);
-AdmmResult admm_edge_dev(gh_mesh* m, const double* d_h, const gh_admm_config& cfg, double* d_x);
+// act_f [F] / act_e (face method: [interior edges], edge method: [E]): optional
+// activity flags from admm_active_flags; elements flagged 0 provably stay +0
+// through every iteration and are skipped
+AdmmResult admm_face_dev(gh_mesh* m, const double* d_h, const gh_admm_config& cfg, double* d_g,
+                         const uint8_t* act_f = nullptr, const uint8_t* act_e = nullptr);
+AdmmResult admm_edge_dev(gh_mesh* m, const double* d_h, const gh_admm_config& cfg, double* d_x,
+                         const uint8_t* act_f = nullptr, const uint8_t* act_e = nullptr);
+// Zero skipping in the ADMM: the level bound below which a
+// face can differ from +0 within `iterations` iterations (from the targets H:
+// the largest min-vertex-level of a face with a nonzero target, + iterations
+// + 1), or -1 when skipping would not pay / is switched off; and the flags.
+int32_t admm_active_level(gh_levels* L, const double* d_h, int32_t iterations);
+void admm_active_flags(gh_levels* L, int32_t level_bound, bool interior_edges, uint8_t* act_f, uint8_t* act_e);
 
 // integration (gh_integrate.cu)
 void integrate_face_dev(gh_levels* L, const double* d_g, double* d_d);

@@ -632,14 +632,42 @@ def test_zero_level_truncation_bitwise(gpu, port_oracle, m, expect, monkeypatch)
             assert st["retries"] >= 2, st  # 128 -> 256 -> 512 in the first launch alone
     if expect == "widened":
         assert seen_retry
-    # the chain behind it: same distances with and without truncation
-    d1, _ = gh.distance(lv, "face", 16, t)
-    gh.set_zero_level_truncation(False)
-    try:
-        d0, _ = gh.distance(lv, "face", 16, t)
-    finally:
-        gh.set_zero_level_truncation(True)
-    assert_same(d1, d0, "distances with and without truncation")
+    if expect == "widened":
+        # caps that keep failing until most of the mesh is inside: the solve goes back to every level
+        # (900 rings, first cap 128: 128 and 256 are flagged, 512 holds more than half the vertices)
+        P2, F2 = _ribbon(900, 12)
+        mesh2 = gh.build_mesh(P2, F2)
+        lv2 = gh.bfs_levels(mesh2, src)
+        om2 = port_oracle.build_mesh(P2, F2)
+        ol2 = om2.bfs(src)
+        t2 = om2.diffusion_time(m)
+        for sweeps in (2, 9):
+            want2, _ = om2.gs_diffuse(ol2, t2, sweeps)
+            assert_same(gh.gs_diffuse(mesh2, lv2, t2, gh.DiffusionConfig(sweeps=sweeps)), want2, "back to every level")
+            st = lv2.diffusion_stats
+            assert st["retries"] == 2 and st["active_levels"] == lv2.level_count() and st["launches"] == 3, st
+    # the chain behind it (the ADMM skips the faces and edges that stay +0, gh_grad.cu): the
+    # oracle's distances bit for bit, with and without the zero skipping, both methods
+    u16, _ = om.gs_diffuse(ol, t, 16)
+    H16, _ = om.normalized_target_gradients(u16)
+    for method in ("face", "edge"):
+        if method == "face":
+            Gf, orep = om.admm_face(H16, 10)
+            want_d = om.integrate_face(ol, Gf)
+        else:
+            Xe, orep = om.admm_edge(H16, 10)
+            want_d = om.integrate_edge(ol, Xe)
+        d1, r1 = gh.distance(lv, method, 16, t)
+        gh.set_zero_level_truncation(False)
+        try:
+            d0, r0 = gh.distance(lv, method, 16, t)
+        finally:
+            gh.set_zero_level_truncation(True)
+        assert_same(d1, want_d, f"{method} distances with zero skipping")
+        assert_same(d0, want_d, f"{method} distances without zero skipping")
+        assert r1.admm_iterations == r0.admm_iterations == orep.iterations and r1.converged == r0.converged
+        assert np.float64(r1.final_primal).view(np.uint64) == np.float64(r0.final_primal).view(np.uint64)
+        assert np.float64(r1.final_dual).view(np.uint64) == np.float64(r0.final_dual).view(np.uint64)
     # a warm start may be nonzero anywhere: the plain launch
     u1 = gh.gs_diffuse(mesh, lv, t, gh.DiffusionConfig(sweeps=4), initial=want)
     assert lv.diffusion_stats["launches"] == 1 and lv.diffusion_stats["active_levels"] == lv.level_count()
