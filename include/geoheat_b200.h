@@ -91,7 +91,7 @@ typedef struct {
   int32_t active_levels;      /* levels its last launch updated; level_count when nothing was truncated */
   int32_t diffusion_launches; /* pipelined launches it ran (1 without truncation) */
   int32_t diffusion_retries;  /* launches redone with a larger cap */
-  int32_t reserved_;
+  int32_t layout_levels;      /* levels the diffusion layout covers (the first rings only on meshes the heat cannot cross; grows on demand) */
   uint64_t row_updates;       /* vertex updates executed (reachable x sweeps without truncation) */
 } gh_levels_info;
 

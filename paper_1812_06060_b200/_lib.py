@@ -22,7 +22,7 @@ class gh_mesh_info(C.Structure):
 class gh_levels_info(C.Structure):
     _fields_ = [("level_count", C.c_int32), ("unreachable_count", C.c_int32), ("max_level_width", C.c_int32),
                 ("column_bits", C.c_int32), ("active_levels", C.c_int32), ("diffusion_launches", C.c_int32),
-                ("diffusion_retries", C.c_int32), ("reserved_", C.c_int32), ("row_updates", C.c_uint64)]
+                ("diffusion_retries", C.c_int32), ("layout_levels", C.c_int32), ("row_updates", C.c_uint64)]
 
 
 class gh_admm_config(C.Structure):

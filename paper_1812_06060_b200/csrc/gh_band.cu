@@ -296,7 +296,9 @@ T read_scalar(const T* d, cudaStream_t s) {
 
 namespace gh {
 
-Band::~Band() {
+Band::~Band() { release_state(); }
+
+void Band::release_state() {
   if (!ubuf && !rows_done && !stalled && !gdone) return;
   int prev = -1;
   if (cudaGetDevice(&prev) != cudaSuccess) prev = -1;
@@ -306,6 +308,10 @@ Band::~Band() {
     if (ipc) cudaFree(p);
     else cudaFreeAsync(p, astream);
   }
+  ubuf = nullptr;
+  rows_done = nullptr;
+  stalled = nullptr;
+  gdone = nullptr;
   if (prev >= 0 && prev != device) cudaSetDevice(prev);  // the caller's current device stays
 }
 

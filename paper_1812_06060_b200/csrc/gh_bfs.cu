@@ -22,6 +22,7 @@
 namespace {
 
 constexpr int B = gh::kBlock;
+constexpr int32_t kPartialLevels = 2048;  // levels of a partial main band (bfs_build)
 
 __global__ void k_bfs_init(int32_t* __restrict__ level, int64_t nv) {
   for (int64_t v = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; v < nv; v += (int64_t)gridDim.x * blockDim.x)
@@ -331,8 +332,14 @@ void bfs_build(gh_levels* L, const int32_t* h_sources, int32_t ns) {
     scattered = mean > (double)V / 64.0;
   }
   L->layout_order.release();
-  // diffusion layout of the whole level range (one band, no ghosts)
-  if (!(scattered || force_morton)) band_build(L, &L->main, 0, nlev);
+  // diffusion layout: one band, no ghosts. A mesh whose first 2048 rings hold
+  // less than half the vertices gets those rings only (the heat underflows to
+  // +0 long before the rest: config 5 builds 13 of 201 M rows);
+  // main_layout_ensure extends the band when a solve needs more levels.
+  int32_t main_le = nlev, part = kPartialLevels;
+  if (const char* e = getenv("GH_PARTIAL_LEVELS")) part = std::max(2, atoi(e));  // tests: small partial bands
+  if (zero_level_truncation() && nlev > part && 2 * (int64_t)L->h_offsets[part] <= (int64_t)L->nreach) main_le = part;
+  if (!(scattered || force_morton)) band_build(L, &L->main, 0, main_le);
   if (L->nreach > 0 && (force_morton || scattered || (!force_id && L->main.col16_windows == 0))) {
     L->layout_order.alloc(V, s);
     {
@@ -352,8 +359,16 @@ void bfs_build(gh_levels* L, const int32_t* h_sources, int32_t ns) {
         GH_CUDA(cudaMemcpyAsync(L->layout_order.p, vb.Current(), sizeof(int32_t) * V, cudaMemcpyDeviceToDevice, s));
     }
     m->launches += 2;
-    band_build(L, &L->main, 0, nlev);
+    band_build(L, &L->main, 0, main_le);
   }
+}
+
+void main_layout_ensure(gh_levels* L, int32_t le) {
+  le = std::min(le, L->nlev);
+  if (L->main.le >= le || L->nreach <= 0) return;
+  L->main.release_state();
+  band_build(L, &L->main, 0, le);  // in the ring order bfs_build chose (order or layout_order)
+  L->u_valid = 0;
 }
 
 }  // namespace gh

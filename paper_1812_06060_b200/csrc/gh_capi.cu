@@ -507,7 +507,7 @@ gh_status gh_bfs_get_info(const gh_levels* levels, gh_levels_info* info) {
     info->active_levels = levels->last_active_levels;
     info->diffusion_launches = levels->last_launches;
     info->diffusion_retries = levels->last_retries;
-    info->reserved_ = 0;
+    info->layout_levels = levels->main.le;
     info->row_updates = levels->last_row_updates;
   });
 }
@@ -585,6 +585,7 @@ gh_status gh_gs_diffuse_tol(gh_levels* levels, double t, int32_t sweeps, double 
       }
     } else {
       if (!(t > 0.0)) gh::fail(GH_ERR_INVALID, "gs_diffuse: t must be positive");
+      gh::main_layout_ensure(levels, levels->nlev);  // the snapshots hold every level's rows
       // per sweep of a group: its snapshot (row order) and its r^2 terms
       // (vertex order); groups of up to 256 sweeps within half the free memory
       size_t free_b = 0, total_b = 0;

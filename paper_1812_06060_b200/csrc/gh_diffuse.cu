@@ -1123,11 +1123,15 @@ namespace {
 
 std::atomic<int> g_zero_levels{-1};  // -1: from GH_ZERO_LEVELS on first use
 
-__global__ void k_den_nonpositive(const double* __restrict__ den, const int32_t* __restrict__ perm, int64_t nrows,
-                                  int32_t* __restrict__ flag) {
-  for (int64_t r = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; r < nrows; r += (int64_t)gridDim.x * blockDim.x)
+// den of every reachable vertex (k_den's expression on the mesh's arrays: the
+// rows a truncated launch skips are the ones that must give +0)
+__global__ void k_den_nonpositive(const double* __restrict__ area, const double* __restrict__ wsum,
+                                  const int32_t* __restrict__ level, double t, int64_t nv, int32_t* __restrict__ flag) {
+  for (int64_t v = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; v < nv; v += (int64_t)gridDim.x * blockDim.x) {
+    const double den = area[v] + t * wsum[v];
     // finite and positive: then every weight of the row is finite too (den = A + t * their sum)
-    if (perm[r] >= 0 && !(den[r] > 0.0 && den[r] < INFINITY)) *flag = 1;
+    if (level[v] >= 0 && !(den > 0.0 && den < INFINITY)) *flag = 1;
+  }
 }
 
 // largest level below `cap` with a nonzero value in sweep buffer `parity` (warp per chunk)
@@ -1222,8 +1226,23 @@ double diffuse_truncated_dev(gh_levels* L, double t, int32_t sweeps) {
   int32_t done = 0, cap = cap_first(), front = -1, margin = mmin, last_k = 0;
   L->last_launches = L->last_retries = 0;
   L->last_row_updates = 0;
+  // the band covers levels [0, b.le) (bfs_build lays out the first rings only
+  // on meshes like this one); a cap past it rebuilds the band with more levels
+  // and carries the state over through u_orig
+  const auto extend = [&](int32_t le) {
+    if (b.le >= std::min(le, L->nlev)) return;
+    const bool carry = done > 0;
+    if (carry) {
+      k_scatter<<<grid_for(b.own_rows), B, 0, s>>>(b.perm.p, b.ubuf, 1u, b.own_rows, L->u_orig.p);
+      GH_LAUNCH_CHECK();
+      m->launches++;
+    }
+    main_layout_ensure(L, le);
+    bands_prepare(L, one, t, carry ? L->u_orig.p : nullptr);
+  };
   while (done < sweeps) {
     if (dense_enough(cap)) {
+      extend(L->nlev);
       // the rest in one plain launch over every level (it continues from the
       // state in parity buffer 1; the levels never run so far hold zeros)
       const int32_t k = sweeps - done;
@@ -1239,6 +1258,7 @@ double diffuse_truncated_dev(gh_levels* L, double t, int32_t sweeps) {
       break;
     }
     const int32_t k = next_group(done, sweeps);
+    if (cap > b.le) extend((int32_t)std::min<int64_t>(L->nlev, std::max<int64_t>(2 * (int64_t)b.le, (int64_t)cap + cap / 2)));
     // the rows this launch may write, saved for a redo
     int64_t off[2], len[2];
     capped_ranges(b, cap, off, len);
@@ -1310,17 +1330,11 @@ double diffuse_dev(gh_levels* L, double t, int32_t sweeps, const double* d_initi
                   L->nlev > cap_first() && 2 * (int64_t)L->h_offsets[cap_first()] <= (int64_t)L->nreach &&
                   !getenv("GH_SWEEP_GROUP") && (int64_t)L->nlev + 2 * (int64_t)sweeps < 0x7fffffffLL;
   if (truncate) {
-    Band& b = L->main;
-    if (b.den_t != t) {
-      k_den<<<grid_for(b.nrows), B, 0, m->stream>>>(b.area_r.p, b.wsum_r.p, t, b.nrows, b.den.p);
-      GH_LAUNCH_CHECK();
-      m->launches++;
-      b.den_t = t;
-    }
     if (L->den_positive < 0 || L->den_positive_t != t) {
       Scratch<int32_t> flag(1, m->stream);
       GH_CUDA(cudaMemsetAsync(flag.p, 0, sizeof(int32_t), m->stream));
-      k_den_nonpositive<<<grid_for(b.nrows), B, 0, m->stream>>>(b.den.p, b.perm.p, b.nrows, flag.p);
+      k_den_nonpositive<<<grid_for(m->nv), B, 0, m->stream>>>(m->vertex_area.p, m->vertex_weight_sum.p, L->level.p, t,
+                                                              m->nv, flag.p);
       GH_LAUNCH_CHECK();
       m->launches++;
       L->den_positive = read_scalar(flag.p, m->stream) ? 0 : 1;
@@ -1329,6 +1343,7 @@ double diffuse_dev(gh_levels* L, double t, int32_t sweeps, const double* d_initi
     truncate = L->den_positive == 1;
   }
   if (!truncate) {
+    main_layout_ensure(L, L->nlev);  // the plain launch runs every level
     const double ms = diffuse_bands_dev(L, one, t, sweeps, d_initial, d_snap);
     L->last_active_levels = L->nlev;
     L->last_launches = sweeps > 0 && L->nreach > 0 ? 1 : 0;

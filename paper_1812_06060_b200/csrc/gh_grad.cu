@@ -223,6 +223,7 @@ __global__ void __launch_bounds__(B, 4) k_face_lambda_pair(const int32_t* __rest
     const int64_t i = k >> 1;
     // n even: both lanes of a pair agree; an edge that stays zero is skipped (lambda, c, term keep their 0)
     const bool valid = k < n && (!act || act[i]);
+    if (!__any_sync(0xffffffffu, valid)) continue;  // a warp of skipped edges: nothing to load or shuffle
     const int32_t f = valid ? ef[k] : 0;
     const double sf = valid ? sa[f] : 1.0;
     const double m = mu * sf, w = valid ? wq[k] : 0.0;

@@ -275,6 +275,7 @@ struct Band {
   Band(const Band&) = delete;
   Band& operator=(const Band&) = delete;
   ~Band();
+  void release_state();  // frees ubuf / rows_done / stalled / gdone (a rebuild with another size)
   uint64_t device_bytes() const;
   int32_t ghost_row(int32_t level) const { return h_pstart[level]; }
 };
@@ -347,6 +348,10 @@ void bands_prepare(gh_levels* L, std::vector<Band*>& bands, double t, const doub
 double bands_launch(gh_levels* L, std::vector<Band*>& bands, double t, int32_t sweeps, double* d_snap = nullptr,
                     int32_t level_cap = 0, int32_t* d_top_nonzero = nullptr, bool scatter = true);
 // zero-level truncation: on by default, GH_ZERO_LEVELS=0 or this switch turn it off
+// The single band L->main may cover only the first levels of a mesh whose
+// heat cannot reach the rest (bfs_build); this rebuilds it to
+// cover levels [0, le) when it does not yet (its u state is lost).
+void main_layout_ensure(gh_levels* L, int32_t le);
 void set_zero_level_truncation(bool on);
 bool zero_level_truncation();
 // the single band's reachable rows of one snapshot sweep into d_u (original order; unreachable untouched)

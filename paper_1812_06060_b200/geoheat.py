@@ -353,6 +353,13 @@ class BfsLevels:
         return {"active_levels": info.active_levels, "launches": info.diffusion_launches,
                 "retries": info.diffusion_retries, "row_updates": info.row_updates}
 
+    @property
+    def layout_levels(self) -> int:
+        """Levels the diffusion layout covers (all of them, or the first rings of a mesh the heat cannot cross)."""
+        info = gh_levels_info()
+        _check(self._lib.gh_bfs_get_info(self._h, C.byref(info)))
+        return info.layout_levels
+
     def __del__(self):
         h = getattr(self, "_h", None)
         if h and not _SHUTTING_DOWN[0]:

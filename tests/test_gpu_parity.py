@@ -585,7 +585,7 @@ def _ribbon(nx: int, ny: int, seed: int = 5):
     return P, F
 
 
-@pytest.mark.parametrize("m,expect", [(1.0, "truncated"), (40.0, "widened")])
+@pytest.mark.parametrize("m,expect", [(1.0, "truncated"), (40.0, "widened"), (1.0, "partial")])
 def test_zero_level_truncation_bitwise(gpu, port_oracle, m, expect, monkeypatch):
     """gs_diffuse on a mesh with far more rings than the heat reaches: only the
     levels below a verified cap are updated, in several launches. u is the oracle's bit for
@@ -597,6 +597,12 @@ def test_zero_level_truncation_bitwise(gpu, port_oracle, m, expect, monkeypatch)
     if expect == "widened":
         monkeypatch.setenv("GH_ZERO_LEVELS_FIRST", "128")
         monkeypatch.setenv("GH_ZERO_LEVELS_MARGIN", "8")
+    if expect == "partial":
+        # the diffusion layout covers the first 600 rings only (bfs_build lays out 2048 on large
+        # meshes); the second launch's cap (front ~476 + 161) passes it, so the band is rebuilt with
+        # more levels and the state carried over; the plain launches rebuild it over every level
+        monkeypatch.setenv("GH_PARTIAL_LEVELS", "600")
+        monkeypatch.setenv("GH_ZERO_LEVELS_FIRST", "512")
     P, F = _ribbon(3000, 12)
     src = np.array([0], np.int32)
     mesh = gh.build_mesh(P, F)
@@ -607,10 +613,15 @@ def test_zero_level_truncation_bitwise(gpu, port_oracle, m, expect, monkeypatch)
     ol = om.bfs(src)
     t = om.diffusion_time(m)
     seen_retry = False
+    assert lv.layout_levels == (600 if expect == "partial" else lv.level_count())
     for sweeps in (2, 3, 16, 71):
         want, _ = om.gs_diffuse(ol, t, sweeps)
+        if expect == "partial":
+            lv = gh.bfs_levels(mesh, src)  # a fresh partial layout (the plain launch below completes it)
         got = gh.gs_diffuse(mesh, lv, t, gh.DiffusionConfig(sweeps=sweeps))
         st = lv.diffusion_stats
+        if expect == "partial":
+            assert lv.layout_levels == (600 if sweeps == 2 else 1200), (sweeps, lv.layout_levels)
         assert_same(got, want, f"u after {sweeps} sweeps (m = {m}), {st}")
         gh.set_zero_level_truncation(False)
         try:
@@ -619,9 +630,10 @@ def test_zero_level_truncation_bitwise(gpu, port_oracle, m, expect, monkeypatch)
         finally:
             gh.set_zero_level_truncation(True)
         assert_same(plain, want, f"plain launch, {sweeps} sweeps")
+        assert lv.layout_levels == lv.level_count()
         assert sp == {"active_levels": lv.level_count(), "launches": 1, "retries": 0, "row_updates": reach * sweeps}
         seen_retry |= st["retries"] > 0
-        if expect == "truncated":
+        if expect in ("truncated", "partial"):
             assert st["retries"] == 0 and st["active_levels"] < lv.level_count(), st
             assert st["row_updates"] < reach * sweeps // 2, st
             assert st["launches"] == {2: 1, 3: 2, 16: 2, 71: 3}[sweeps], st
