@@ -804,8 +804,13 @@ void distance_on_device(gh_levels* L, const gh_pipeline_config& c, double* d_dis
   const int32_t bound = gh::admm_active_level(L, H.p, c.admm.max_iterations);
   const bool skip = bound >= 0;
   gh::Scratch<uint8_t> act_f(skip ? (size_t)m->nf : 0, s);
-  gh::Scratch<uint8_t> act_e(skip ? (size_t)(c.method == GH_METHOD_FACE ? m->ni : m->ne) : 0, s);
-  if (skip) gh::admm_active_flags(L, bound, c.method == GH_METHOD_FACE, act_f.p, act_e.p);
+  // (+32: k_face_lambda_pair reads the edge flags 16 bytes at a time; the pad is zero)
+  const size_t n_act_e = (size_t)(c.method == GH_METHOD_FACE ? m->ni : m->ne);
+  gh::Scratch<uint8_t> act_e(skip ? n_act_e + 32 : 0, s);
+  if (skip) {
+    GH_CUDA(cudaMemsetAsync(act_e.p + n_act_e, 0, 32, s));
+    gh::admm_active_flags(L, bound, c.method == GH_METHOD_FACE, act_f.p, act_e.p);
+  }
   if (c.method == GH_METHOD_FACE) {
     gh::Scratch<double> G(3 * (size_t)m->nf, s);
     r = gh::admm_face_dev(m, H.p, c.admm, G.p, act_f.p, act_e.p);

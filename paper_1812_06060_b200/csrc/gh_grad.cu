@@ -205,6 +205,13 @@ __device__ __forceinline__ v3 pair_y(int side, const v3& q, const v3& ed, double
 // 4 blocks per SM (64 registers; g_out is loaded after the first y so that
 // fits): config 3 18.3 vs 19.0 ms, config 4 103 vs 107.5 ms per 10 iterations
 // against one thread per edge at 3 blocks per SM (same box, interleaved runs).
+// kAct: activity flags per interior edge (admm_active_flags, padded to a
+// multiple of 16 bytes): a warp iteration covers 16 consecutive edges, and lane
+// j of a warp looks at the 16 flags of the warp's j-th next iteration in one
+// 16-byte load, so 32 iterations are screened per round trip and only the
+// active ones run (in the same ascending order: the partial sums keep their
+// bits).
+template <bool kAct>
 __global__ void __launch_bounds__(B, 4) k_face_lambda_pair(const int32_t* __restrict__ ef, const double* __restrict__ sa,
                                                         const double* __restrict__ wq, const double* __restrict__ gin,
                                                         const double* __restrict__ gout,
@@ -217,13 +224,13 @@ __global__ void __launch_bounds__(B, 4) k_face_lambda_pair(const int32_t* __rest
   double s = 0.0;
   const int side = threadIdx.x & 1;
   const int64_t n = 2 * ni, stride = (int64_t)gridDim.x * blockDim.x;
+  const int lane = threadIdx.x & 31;
   // the whole warp steps together (the pair shuffles need every lane)
-  for (int64_t k0 = blockIdx.x * (int64_t)blockDim.x + (threadIdx.x & ~31); k0 < n; k0 += stride) {
-    const int64_t k = k0 + (threadIdx.x & 31);
+  const auto body = [&](int64_t k0) {
+    const int64_t k = k0 + lane;
     const int64_t i = k >> 1;
     // n even: both lanes of a pair agree; an edge that stays zero is skipped (lambda, c, term keep their 0)
-    const bool valid = k < n && (!act || act[i]);
-    if (!__any_sync(0xffffffffu, valid)) continue;  // a warp of skipped edges: nothing to load or shuffle
+    const bool valid = k < n && (!kAct || act[i]);
     const int32_t f = valid ? ef[k] : 0;
     const double sf = valid ? sa[f] : 1.0;
     const double m = mu * sf, w = valid ? wq[k] : 0.0;
@@ -251,6 +258,21 @@ __global__ void __launch_bounds__(B, 4) k_face_lambda_pair(const int32_t* __rest
     const v3 d2 = divs(l, m);
     const v3 y2 = pair_y(side, sub(go, d2), ed, w);
     if (valid) st3(C, k, add(y2, d2));
+  };
+  const int64_t first = blockIdx.x * (int64_t)blockDim.x + (threadIdx.x & ~31);
+  if (!kAct) {
+    for (int64_t k0 = first; k0 < n; k0 += stride) body(k0);
+  } else {
+    for (int64_t base = first; base < n; base += 32 * stride) {
+      const int64_t kk = base + lane * stride;  // the warp's k0 `lane` iterations from now
+      bool any = false;
+      if (kk < n) {
+        const uint4 a = __ldg(reinterpret_cast<const uint4*>(act + (kk >> 1)));
+        any = (a.x | a.y | a.z | a.w) != 0;
+      }
+      for (unsigned msk = __ballot_sync(0xffffffffu, any); msk; msk &= msk - 1)
+        body(base + (int64_t)(__ffs(msk) - 1) * stride);
+    }
   }
   s = block_sum<B>(s);
   if (threadIdx.x == 0) part[blockIdx.x] = s;
@@ -692,8 +714,12 @@ AdmmResult admm_face_dev(gh_mesh* m, const double* d_h, const gh_admm_config& cf
     const double* gin = gbuf[(it + 1) & 1];
     double* gout = gbuf[it & 1];
     k_face_g<<<G, B, 0, s>>>(slot.p, m->face_area.p, d_h, Cs.p, F, mu, gin, gout, part_dual, term_d.p, halt, act_f);
-    k_face_lambda_pair<<<G, B, 0, s>>>(ef.p, sa.p, wq.p, gin, gout, edir.p, NI, mu, Cs.p, lam.p, part_primal,
-                                       term_p.p, halt, act_e);
+    if (act_e)
+      k_face_lambda_pair<true><<<G, B, 0, s>>>(ef.p, sa.p, wq.p, gin, gout, edir.p, NI, mu, Cs.p, lam.p, part_primal,
+                                               term_p.p, halt, act_e);
+    else
+      k_face_lambda_pair<false><<<G, B, 0, s>>>(ef.p, sa.p, wq.p, gin, gout, edir.p, NI, mu, Cs.p, lam.p, part_primal,
+                                                term_p.p, halt, nullptr);
   });
   // the last iteration's g: odd iterations wrote gtmp
   if (res.iterations > 0 && ((res.iterations - 1) & 1))

@@ -685,3 +685,37 @@ def test_zero_level_truncation_bitwise(gpu, port_oracle, m, expect, monkeypatch)
     assert lv.diffusion_stats["launches"] == 1 and lv.diffusion_stats["active_levels"] == lv.level_count()
     w1, _ = om.gs_diffuse(ol, t, 4, initial=want)
     assert_same(u1, w1, "warm start")
+
+
+def test_zero_skipping_with_several_sources_and_an_unreachable_part(gpu, port_oracle):
+    """The exact-zero skipping (truncated diffusion, ADMM active sets, partial layout) on a long
+    ribbon with sources at both ends and in the middle plus a second, unreachable ribbon: u and the
+    distances of both methods are the oracle's bit for bit (unreachable vertices: u = 0, d = inf)."""
+    gh = gpu
+    P1, F1 = _ribbon(9000, 10, seed=11)
+    P2, F2 = _ribbon(300, 10, seed=12)
+    P2 = P2 + np.array([0.0, 50.0, 0.0])
+    P = np.concatenate([P1, P2])
+    F = np.concatenate([F1, F2 + P1.shape[0]]).astype(np.int32)
+    n1 = P1.shape[0]
+    src = np.array([0, n1 - 1, (4500 * 10) + 5], np.int32)
+    mesh = gh.build_mesh(P, F)
+    lv = gh.bfs_levels(mesh, src)
+    assert lv.unreachable_count == P2.shape[0] and lv.level_count() > 1024
+    assert lv.layout_levels == lv.level_count()  # ~2250 rings from three sources, most vertices within 2048: every level laid out
+    om = port_oracle.build_mesh(P, F)
+    ol = om.bfs(src)
+    t = om.diffusion_time(1.0)
+    want, _ = om.gs_diffuse(ol, t, 40)
+    got = gh.gs_diffuse(mesh, lv, t, gh.DiffusionConfig(sweeps=40))
+    st = lv.diffusion_stats
+    assert_same(got, want, f"u, {st}")
+    assert st["launches"] == 3 and st["active_levels"] < lv.level_count() and st["retries"] == 0, st
+    H, _ = om.normalized_target_gradients(want)
+    Gf, _ = om.admm_face(H, 10)
+    Xe, _ = om.admm_edge(H, 10)
+    d_face, _ = gh.distance(lv, "face", 40, t)
+    d_edge, _ = gh.distance(lv, "edge", 40, t)
+    assert_same(d_face, om.integrate_face(ol, Gf), "face distances")
+    assert_same(d_edge, om.integrate_edge(ol, Xe), "edge distances")
+    assert np.isinf(d_face[n1:]).all() and np.isfinite(d_face[:n1]).all()
