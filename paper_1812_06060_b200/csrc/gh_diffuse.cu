@@ -300,7 +300,14 @@ constexpr int kColOff16 = kDegOff + kTileChunks * 16;  // nibbles (16-bit-column
 // row; chunks without 16-bit columns take the global-memory path.
 // kSlice: the band is a sector slice (gh::Band::nslices): ghost rows of every
 // level, counted per source slice; own rows exported to the readers' ghosts.
-template <int kUnroll, bool kTable, int kWin, bool kSlice>
+// kMode: what a row's store is followed by. 0 = everything decided at run time
+// (snapshots for the E1 stop, copies into the neighbour bands' ghost rows);
+// 1 = the single band on its own: nothing (the consumers are issue-bound: the
+// three uniform tests cost the plain launch a few per cent — the top-level
+// test alone 121.4 vs 118.4 ms at config 3, same box, alternating runs);
+// 2 = a launch of the zero-level truncation (diffuse_truncated_dev): a row of
+// the band's top level written with any bit set raises a.top_nonzero.
+template <int kUnroll, bool kTable, int kWin, bool kSlice, int kMode>
 __global__ void __launch_bounds__(kTmaThreads, 2) k_diffuse_tma(const __grid_constant__ TmaArgs a) {
   extern __shared__ __align__(128) unsigned char smem[];
   // this block's band and its rank inside the band
@@ -668,13 +675,16 @@ __global__ void __launch_bounds__(kTmaThreads, 2) k_diffuse_tma(const __grid_con
             asm volatile("div.rn.f64 %0, %1, %2;" : "=d"(un) : "d"(nz), "d"(den[i]));
           const uint32_t par = px[i] >> 5;
           __stcg(ub + gh::uidx((uint32_t)r, par), un);
-          if (a.snap) __stcs(a.snap + (int64_t)(s_base - (Lq[i] >> 1)) * a.snap_rows + r, un);
-          // boundary levels also land in the neighbour band's ghost copy
-          if (Lq[i] == band_lb && vba->lo_ubuf)
-            __stcg(vba->lo_ubuf + gh::uidx((uint32_t)(vba->lo_ghost + (r - pstart(Lq[i]))), par), un);
-          if (Lq[i] == band_le - 1 && vba->hi_ubuf)
-            __stcg(vba->hi_ubuf + gh::uidx((uint32_t)(vba->hi_ghost + (r - pstart(Lq[i]))), par), un);
-          if (Lq[i] == band_le - 1 && a.top_nonzero && __double_as_longlong(un) != 0) *a.top_nonzero = 1;
+          if (kMode == 0) {
+            if (a.snap) __stcs(a.snap + (int64_t)(s_base - (Lq[i] >> 1)) * a.snap_rows + r, un);
+            // boundary levels also land in the neighbour band's ghost copy
+            if (Lq[i] == band_lb && vba->lo_ubuf)
+              __stcg(vba->lo_ubuf + gh::uidx((uint32_t)(vba->lo_ghost + (r - pstart(Lq[i]))), par), un);
+            if (Lq[i] == band_le - 1 && vba->hi_ubuf)
+              __stcg(vba->hi_ubuf + gh::uidx((uint32_t)(vba->hi_ghost + (r - pstart(Lq[i]))), par), un);
+          }
+          // zero-level truncation: any bit set in the cap's top level flags the launch
+          if (kMode == 2 && Lq[i] == band_le - 1 && __double_as_longlong(un) != 0) *a.top_nonzero = 1;
         }
         if (kSlice && live[i] && vba->xoff) {
           // rows other slices read: into their ghost rows (same sweep parity)
@@ -1005,13 +1015,22 @@ double bands_launch(gh_levels* L, std::vector<Band*>& bands, double t, int32_t s
   }
   if (nslots < 2) nslots = 2;
   const size_t shmem = 16 * (size_t)nslots + table_bytes + 128 + (size_t)nslots * slot_bytes;
-#define GH_DIFFUSE_FN(W, S)                                                                                    \
-  (wmax <= 6 ? (table ? (void*)k_diffuse_tma<6, true, W, S> : (void*)k_diffuse_tma<6, false, W, S>)           \
-             : (table ? (void*)k_diffuse_tma<8, true, W, S> : (void*)k_diffuse_tma<8, false, W, S>))
-  void* fn = slices     ? (win == 3 ? GH_DIFFUSE_FN(3, true) : GH_DIFFUSE_FN(0, true))
-             : win == 2 ? GH_DIFFUSE_FN(2, false)
-             : win == 3 ? GH_DIFFUSE_FN(3, false)
-                        : GH_DIFFUSE_FN(0, false);
+#define GH_DIFFUSE_FN(W, S, T)                                                                                 \
+  (wmax <= 6 ? (table ? (void*)k_diffuse_tma<6, true, W, S, T> : (void*)k_diffuse_tma<6, false, W, S, T>)     \
+             : (table ? (void*)k_diffuse_tma<8, true, W, S, T> : (void*)k_diffuse_tma<8, false, W, S, T>))
+  // the single band on its own (no neighbour copies, no snapshots) takes the
+  // lean instances, with the top-level test when it runs under a level cap
+  // (GH_DIFFUSE_GENERAL=1: the run-time instances also there, for tests and A/B runs)
+  const bool alone = !slices && bands.size() == 1 && !d_snap && !bands[0]->lo_ubuf && !bands[0]->hi_ubuf &&
+                     (d_top_nonzero || !getenv("GH_DIFFUSE_GENERAL"));
+  if (d_top_nonzero && !alone) fail(GH_ERR_INTERNAL, "diffusion: the level cap needs the single band on its own");
+#define GH_DIFFUSE_MODE(M) \
+  (win == 2 ? GH_DIFFUSE_FN(2, false, M) : win == 3 ? GH_DIFFUSE_FN(3, false, M) : GH_DIFFUSE_FN(0, false, M))
+  void* fn = slices          ? (win == 3 ? GH_DIFFUSE_FN(3, true, 0) : GH_DIFFUSE_FN(0, true, 0))
+             : d_top_nonzero ? GH_DIFFUSE_MODE(2)
+             : alone         ? GH_DIFFUSE_MODE(1)
+                             : GH_DIFFUSE_MODE(0);
+#undef GH_DIFFUSE_MODE
 #undef GH_DIFFUSE_FN
   L->last_col16 = win;
   GH_CUDA(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)shmem));

@@ -395,7 +395,7 @@ def test_high_valence_hub_bitwise(gpu, port_oracle, n, source):
 
 @pytest.mark.parametrize("mode", ["auto", "col32", "win2", "win3", "win2_mixed", "win3_mixed", "morton",
                                   "morton_win3_mixed", "morton_col32", "group1", "group7", "group16_normal",
-                                  "group3_period"])
+                                  "group3_period", "general", "general_win3"])
 def test_diffusion_column_formats_bitwise(gpu, port_oracle, monkeypatch, mode):
     """The diffusion kernel streams 16-bit column offsets into 2 or 3 per-chunk
     windows (chunks whose windows do not fit keep 32-bit columns and take the
@@ -405,9 +405,14 @@ def test_diffusion_column_formats_bitwise(gpu, port_oracle, monkeypatch, mode):
     ring out in spatial order (the layout picked when vertex-id order leaves no
     16-bit format usable), which moves rows between chunks but not their sums.
     The "group" modes run the sweeps in groups of K (one pipeline per group,
-    DESIGN.md §3.4): the same tasks in another order, so the same bits."""
+    DESIGN.md §3.4): the same tasks in another order, so the same bits. The
+    "general" modes run the single band through the instances that decide
+    snapshots and neighbour copies at run time (the plain solve takes lean ones)."""
     from paper_1812_06060_b200 import bands, meshgen
     gh = gpu
+    if mode.startswith("general"):
+        monkeypatch.setenv("GH_DIFFUSE_GENERAL", "1")
+        mode = mode[8:] or "auto"
     if mode.startswith("group"):  # sweep groups (GH_SWEEP_GROUP): same tasks, another step order
         k = mode[5:].split("_")[0]
         monkeypatch.setenv("GH_SWEEP_GROUP", k)
