@@ -287,9 +287,9 @@ def main():
             # prepares the next solve until every rank's kernel has returned
             barrier(dist)
 
-    # `value` and the roofline are the diffusion kernel's: every vertex update
-    # the metric counts is executed (zero-level truncation, DESIGN.md §3.7,
-    # applies to meshes like configs 4 and 5 and is measured in the e2e leg)
+    # `value`, the roofline and `e2e` run the library's default: every vertex
+    # update the metric counts is executed. The opt-in exact-zero skipping
+    # is timed separately below (`e2e.zero_skip`).
     gh.set_zero_level_truncation(False)
     launches = 0
     for _ in range(a.warmup):
@@ -309,7 +309,6 @@ def main():
     step_ms_max = max_over_ranks(dist, step_ms, local)
     value = reach * w.sweeps / (step_ms_max * 1e-3)  # total work over all ranks / slowest rank
 
-    gh.set_zero_level_truncation(True)
     peak, peak_src = load_peaks()
     achieved = bytes_per_sweep * w.sweeps / (step_ms * 1e-3) / 1e9
     traffic, traffic_src = recorded_traffic(workload, w.sweeps) if world == 1 else (None, None)
@@ -356,23 +355,35 @@ def main():
             e2e_s.append(dt)
     e2e_sec = max_over_ranks(dist, float(np.mean(e2e_s)), local)
     e2e_value = reach * w.sweeps / e2e_sec
-    # when the diffusion was truncated to the levels the heat reaches (same
-    # bits), also time the call with every level updated
-    full_s = []
-    if world == 1 and e2e_extra.get("diffusion", {}).get("launches", 1) > 1:
-        gh.set_zero_level_truncation(False)
-        for i in range(2):
-            rr = G.gh_run_report()
-            t0 = time.perf_counter()
-            G._check(L.gh_distance_host(pp, P.shape[0], pf, Fc.shape[0], S.ctypes.data_as(C.c_void_p), S.size,
-                                        C.byref(pcfg), pd, C.byref(rr)))
-            full_s.append(time.perf_counter() - t0)
+    # the same call with the opt-in exact-zero skipping (same bits, DESIGN.md
+    # §3.7: the diffusion updates only the levels the heat reaches before it
+    # underflows to +0, the ADMM skips elements that provably stay +0)
+    zero_skip = None
+    if world == 1:
+        d_ref = np.ctypeslib.as_array(C.cast(pd, C.POINTER(C.c_double)), shape=(P.shape[0],)).copy()
         gh.set_zero_level_truncation(True)
-        e2e_extra["every_level_seconds"] = min(full_s)
-        e2e_extra["every_level_diffusion_ms"] = rr.diffusion_ms
-        # leave the truncated call's result in pd for the parity hash below
-        G._check(L.gh_distance_host(pp, P.shape[0], pf, Fc.shape[0], S.ctypes.data_as(C.c_void_p), S.size,
-                                    C.byref(pcfg), pd, None))
+        try:
+            zs = []
+            for i in range(1 + a.e2e_steps):
+                rr = G.gh_run_report()
+                t0 = time.perf_counter()
+                G._check(L.gh_distance_host(pp, P.shape[0], pf, Fc.shape[0], S.ctypes.data_as(C.c_void_p), S.size,
+                                            C.byref(pcfg), pd, C.byref(rr)))
+                if i > 0:
+                    zs.append(time.perf_counter() - t0)
+        finally:
+            gh.set_zero_level_truncation(False)
+        d_skip = np.ctypeslib.as_array(C.cast(pd, C.POINTER(C.c_double)), shape=(P.shape[0],))
+        zero_skip = {"seconds": float(np.mean(zs)), "value": reach * w.sweeps / float(np.mean(zs)),
+                     "samples_s": [round(x, 6) for x in zs],
+                     "identical_to_every_update": bool(np.array_equal(d_skip.view(np.uint64), d_ref.view(np.uint64))),
+                     "stages_ms": {"build": rr.build_ms, "bfs_layout": rr.bfs_ms, "diffusion": rr.diffusion_ms,
+                                   "normalize": rr.normalize_ms, "admm": rr.optimization_ms,
+                                   "integrate": rr.integration_ms, "d2h": rr.d2h_ms},
+                     "row_updates_executed": int(rr.diffusion_row_updates),
+                     "row_updates_nominal": int(reach) * w.sweeps,
+                     "active_levels": int(rr.diffusion_active_levels), "launches": int(rr.diffusion_launches)}
+        e2e_extra["zero_skip"] = zero_skip
     # the same call from pageable (numpy) arrays, as the C++ drop-in's
     # geoheat::b200::build_mesh(std::vector...) passes them: H2D from pageable
     # memory inside the timed call
@@ -390,6 +401,8 @@ def main():
     # the distances of the last timed call vs the reference chain's field_hash
     # recorded for this config (tools/e2e_parity.py -> profiles/reference_hashes.json)
     d_out = np.ctypeslib.as_array(C.cast(pd, C.POINTER(C.c_double)), shape=(P.shape[0],))
+    if world == 1:
+        d_out = d_ref  # the default call's result (pd now holds the zero-skipping call's, checked equal above)
     parity = {"field_hash": f"{G.field_hash(d_out):016x}", "reference_field_hash": None, "identical": None,
               "source": "profiles/reference_hashes.json (tools/e2e_parity.py: the reference's own chain)"}
     try:

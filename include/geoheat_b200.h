@@ -184,12 +184,14 @@ gh_status gh_host_free(void* p);
    device it has used. Handles stay valid. Call it before other processes need
    the memory (the pool otherwise keeps what a large solve grew to). */
 gh_status gh_release_cached_memory(void);
-/* Zero-level truncation of gs_diffuse (on by default; GH_ZERO_LEVELS=0 in the
-   environment also turns it off). With t ~ h^2 the heat underflows to exactly
+/* Exact-zero skipping (opt-in: off by default, so that every update the
+   reference executes is executed; GH_ZERO_LEVELS=1 in the environment also
+   turns it on). With t ~ h^2 the heat underflows to exactly
    +0 a few hundred rings from the sources; levels beyond that front provably
    stay +0, and the solve updates only the levels below a cap that the kernel
    verifies (a nonzero bit at the cap's top level redoes the launch with a
-   larger cap). The result is the reference's u bit for bit (diffusion.hpp:
+   larger cap); the fused chain's ADMM likewise skips faces and edges that
+   provably stay +0. The results are the reference's bit for bit (diffusion.hpp:
    73-108 evaluated on the levels that can differ from zero); process-wide. */
 gh_status gh_set_zero_level_truncation(int32_t on);
 

@@ -145,8 +145,9 @@ inline void to_report(const gh_solver_report& r, const std::vector<double>& ph, 
 
 /// No reference counterpart: the exact-zero skipping (DESIGN.md §3.7 — the
 /// diffusion updates only the BFS levels the heat reaches before it underflows
-/// to +0, the ADMM skips faces and edges that provably stay +0) is on by
-/// default and changes no result bit; this switches it process-wide.
+/// to +0, the ADMM skips faces and edges that provably stay +0) changes no
+/// result bit; it is opt-in (off by default: every update the reference runs
+/// is run). This switches it process-wide.
 inline void set_zero_level_truncation(bool on) { detail::check(gh_set_zero_level_truncation(on ? 1 : 0)); }
 
 /// Device-resident TriMesh (mesh.hpp:21-94): move-only owner of a gh_mesh.

@@ -1148,7 +1148,7 @@ namespace {
 // source on a large mesh: configs 4 and 5); the others take the plain launch.
 namespace {
 
-std::atomic<int> g_zero_levels{-1};  // -1: from GH_ZERO_LEVELS on first use
+std::atomic<int> g_zero_levels{-1};  // -1: from GH_ZERO_LEVELS on first use (default off)
 
 // den of every reachable vertex (k_den's expression on the mesh's arrays: the
 // rows a truncated launch skips are the ones that must give +0)
@@ -1196,8 +1196,8 @@ void set_zero_level_truncation(bool on) { g_zero_levels.store(on ? 1 : 0); }
 bool zero_level_truncation() {
   int v = g_zero_levels.load();
   if (v < 0) {
-    const char* e = getenv("GH_ZERO_LEVELS");
-    v = (e && atoi(e) == 0) ? 0 : 1;
+    const char* e = getenv("GH_ZERO_LEVELS");  // off unless asked for: by default every update the reference runs is run
+    v = (e && atoi(e) != 0) ? 1 : 0;
     g_zero_levels.store(v);
   }
   return v != 0;

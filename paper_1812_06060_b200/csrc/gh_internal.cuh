@@ -347,7 +347,7 @@ void bands_prepare(gh_levels* L, std::vector<Band*>& bands, double t, const doub
 // d_top_nonzero is set when a row of its top level gets a nonzero value
 double bands_launch(gh_levels* L, std::vector<Band*>& bands, double t, int32_t sweeps, double* d_snap = nullptr,
                     int32_t level_cap = 0, int32_t* d_top_nonzero = nullptr, bool scatter = true);
-// zero-level truncation: on by default, GH_ZERO_LEVELS=0 or this switch turn it off
+// exact-zero skipping: off by default, GH_ZERO_LEVELS=1 or this switch turn it on
 // The single band L->main may cover only the first levels of a mesh whose
 // heat cannot reach the rest (bfs_build); this rebuilds it to
 // cover levels [0, le) when it does not yet (its u state is lost).

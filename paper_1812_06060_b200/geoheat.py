@@ -735,8 +735,9 @@ def device_count() -> int:
 
 
 def set_zero_level_truncation(on: bool) -> None:
-    """gs_diffuse updates only the BFS levels the heat can reach before it underflows to +0
-    (bit-identical, verified in the kernel; include/geoheat_b200.h). On by default."""
+    """Opt-in exact-zero skipping: gs_diffuse updates only the BFS levels the heat can reach before it
+    underflows to +0 (verified in the kernel) and the fused chain's ADMM skips elements that provably
+    stay +0 — bit-identical results (include/geoheat_b200.h). Off by default."""
     _check(_lib.load().gh_set_zero_level_truncation(1 if on else 0))
 
 

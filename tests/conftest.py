@@ -28,3 +28,11 @@ def gpu():
     n = gh.geoheat.device_count()
     assert n > 0, "no CUDA device visible to libgeoheat_b200.so"
     return gh
+
+
+@pytest.fixture
+def zero_skipping(gpu):
+    """The opt-in exact-zero skipping on for one test; off again afterwards (the default)."""
+    gpu.set_zero_level_truncation(True)
+    yield gpu
+    gpu.set_zero_level_truncation(False)

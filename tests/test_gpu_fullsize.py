@@ -35,10 +35,21 @@ def _release_device_memory(gpu):
     gpu.geoheat.release_cached_memory()
 
 
+@pytest.mark.parametrize("skip", [False, True], ids=["every_update", "zero_skipping"])
 @pytest.mark.parametrize("config,method", CASES)
-def test_full_size_hash_equals_reference_chain(gpu, config, method):
+def test_full_size_hash_equals_reference_chain(gpu, config, method, skip):
+    """skip: the opt-in exact-zero skipping — the same hash, iteration count and
+    flags with it on (configs 4 and 5 then update 4-10 % of the vertices)."""
     from paper_1812_06060_b200 import meshgen
     gh = gpu
+    gh.set_zero_level_truncation(skip)
+    try:
+        _full_size_case(gh, meshgen, config, method, skip)
+    finally:
+        gh.set_zero_level_truncation(False)
+
+
+def _full_size_case(gh, meshgen, config, method, skip):
     rec = next(r for r in RECORDS if r["config"] == config and r["method"] == method)
     w = meshgen.config(config)
     assert w.positions.shape[0] == rec["vertices"] and w.sweeps == rec["sweeps"]
@@ -51,6 +62,11 @@ def test_full_size_hash_equals_reference_chain(gpu, config, method):
         assert rep.converged == rec["converged"][1]
     if rec.get("zero_count") is not None:
         assert rep.zero_count == rec["zero_count"][1]
+    nominal = rec["vertices"] * rec["sweeps"]
+    if not skip:
+        assert rep.diffusion_row_updates == nominal and rep.diffusion_launches == 1
+    elif config >= 4:
+        assert rep.diffusion_row_updates < nominal // 5 and rep.diffusion_launches > 1
 
 
 TOL = json.load(open(os.path.join(ROOT, "profiles", "r2_tol_parity.json")))

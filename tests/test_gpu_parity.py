@@ -591,14 +591,14 @@ def _ribbon(nx: int, ny: int, seed: int = 5):
 
 
 @pytest.mark.parametrize("m,expect", [(1.0, "truncated"), (40.0, "widened"), (1.0, "partial")])
-def test_zero_level_truncation_bitwise(gpu, port_oracle, m, expect, monkeypatch):
+def test_zero_level_truncation_bitwise(zero_skipping, port_oracle, m, expect, monkeypatch):
     """gs_diffuse on a mesh with far more rings than the heat reaches: only the
     levels below a verified cap are updated, in several launches. u is the oracle's bit for
     bit, equal to the plain launch's (truncation off), for sweep counts that end inside the
     first, a middle and the last launch. "widened": a first cap of 128 levels and a margin of
     8 (the heat reaches ~500 rings in one sweep and ~640 by sweep 71), so the first launch and
     later ones are undone and redone with larger caps."""
-    gh = gpu
+    gh = zero_skipping
     if expect == "widened":
         monkeypatch.setenv("GH_ZERO_LEVELS_FIRST", "128")
         monkeypatch.setenv("GH_ZERO_LEVELS_MARGIN", "8")
@@ -692,11 +692,11 @@ def test_zero_level_truncation_bitwise(gpu, port_oracle, m, expect, monkeypatch)
     assert_same(u1, w1, "warm start")
 
 
-def test_zero_skipping_with_several_sources_and_an_unreachable_part(gpu, port_oracle):
+def test_zero_skipping_with_several_sources_and_an_unreachable_part(zero_skipping, port_oracle):
     """The exact-zero skipping (truncated diffusion, ADMM active sets, partial layout) on a long
     ribbon with sources at both ends and in the middle plus a second, unreachable ribbon: u and the
     distances of both methods are the oracle's bit for bit (unreachable vertices: u = 0, d = inf)."""
-    gh = gpu
+    gh = zero_skipping
     P1, F1 = _ribbon(9000, 10, seed=11)
     P2, F2 = _ribbon(300, 10, seed=12)
     P2 = P2 + np.array([0.0, 50.0, 0.0])

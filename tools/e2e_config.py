@@ -1,5 +1,8 @@
 """End-to-end solve of a BASELINE config through gh_distance_host (host arrays in,
-host distances out), twice, with stage timings and a determinism check."""
+host distances out), twice, with stage timings and a determinism check.
+
+    python tools/e2e_config.py CONFIG [SWEEPS [REPEATS [skip]]]   # "skip": the opt-in exact-zero skipping on
+"""
 import ctypes as C
 import json
 import os
@@ -14,6 +17,8 @@ from paper_1812_06060_b200 import geoheat as G, meshgen  # noqa: E402
 cfg = int(sys.argv[1]) if len(sys.argv) > 1 else 5
 sweeps = int(sys.argv[2]) if len(sys.argv) > 2 else 1000
 repeats = int(sys.argv[3]) if len(sys.argv) > 3 else 2
+skip = len(sys.argv) > 4 and sys.argv[4] == "skip"
+G.set_zero_level_truncation(skip)
 t0 = time.time()
 w = meshgen.config(cfg)
 gen_s = time.time() - t0
@@ -37,7 +42,7 @@ for it in range(repeats):
     d = np.ctypeslib.as_array((C.c_double * P.shape[0]).from_address(pd.value))
     hashes.append(G.field_hash(d))
     fin = np.isfinite(d)
-    out = dict(config=cfg, name=w.name, method=w.method, vertices=int(P.shape[0]), faces=int(F.shape[0]), sweeps=sweeps,
+    out = dict(zero_skipping=skip, config=cfg, name=w.name, method=w.method, vertices=int(P.shape[0]), faces=int(F.shape[0]), sweeps=sweeps,
                iteration=it, wall_s=wall, t=rr.t, build_ms=rr.build_ms, bfs_ms=rr.bfs_ms, diffusion_ms=rr.diffusion_ms,
                normalize_ms=rr.normalize_ms, admm_ms=rr.optimization_ms, integrate_ms=rr.integration_ms,
                admm_iterations=rr.admm_iterations, converged=bool(rr.converged), zero_count=rr.zero_count,

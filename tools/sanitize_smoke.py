@@ -40,6 +40,7 @@ print("sanitize smoke ok", float(d1.max()), float(d2.max()), float(dp.max()), s,
 # first cap and margin, so the truncated launches, the redo path, the layout extension with a
 # carried state and the ADMM active sets (flag screening included) all run
 os.environ.update(GH_PARTIAL_LEVELS="300", GH_ZERO_LEVELS_FIRST="128", GH_ZERO_LEVELS_MARGIN="8")
+g.set_zero_level_truncation(True)  # opt-in
 nx, ny = 1400, 6
 x, y = np.meshgrid(np.arange(nx, dtype=np.float64), np.arange(ny, dtype=np.float64), indexing="ij")
 Pr = np.stack([x, y, 0.05 * np.sin(0.3 * x) * np.cos(0.4 * y)], -1).reshape(-1, 3)
@@ -62,4 +63,5 @@ for method in ("face", "edge"):
     db, _ = g.distance(rl2, method, 40, tr)
     g.set_zero_level_truncation(True)
     assert np.array_equal(da.view(np.uint64), db.view(np.uint64)), method
+g.set_zero_level_truncation(False)
 print("zero skipping ok", st, rl.layout_levels)
